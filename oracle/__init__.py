@@ -1,0 +1,286 @@
+"""ctypes binding of the CPU oracle (liboracle.so, plain C in this directory).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / ``--impl reference`` legs of bench.py - never by the product
+package.  See oracle.h for what each function computes and which passage of
+/root/reference/PAPER.md it follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_SOURCES = ["o64.c", "o16.c"]
+
+ORC_CONVERGED, ORC_MAXIT, ORC_BREAKDOWN, ORC_NONFINITE = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    srcs = [os.path.join(_HERE, s) for s in _SOURCES]
+    hdr = os.path.join(_HERE, "oracle.h")
+    if not force and os.path.exists(_LIB_PATH):
+        newest = max(os.path.getmtime(p) for p in srcs + [hdr])
+        if os.path.getmtime(_LIB_PATH) >= newest:
+            return _LIB_PATH
+    cmd = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-fopenmp",
+           "-ffp-contract=off", "-fno-fast-math", "-Wall", "-o", _LIB_PATH + ".tmp"] + srcs + ["-lm"]
+    subprocess.check_call(cmd, cwd=_HERE)
+    os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _declare(_lib)
+    return _lib
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_U16 = ctypes.c_uint16
+
+
+def _declare(L):
+    L.o64_jacobi_scale.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.o64_apply.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.o64_apply_raw.argtypes = [_I, _I, _I, _P, _P, _P, _P]
+    L.o64_dot.argtypes = [_I64, _P, _P]
+    L.o64_dot.restype = _D
+    L.o64_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
+    L.o64_bicgstab.restype = _I
+    L.o64_true_residual.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.o64_true_residual.restype = _D
+    L.o16_to_double.argtypes = [_U16]
+    L.o16_to_double.restype = _D
+    L.o16_from_double.argtypes = [_D]
+    L.o16_from_double.restype = _U16
+    for f in ("o16_fma",):
+        getattr(L, f).argtypes = [_U16, _U16, _U16]
+        getattr(L, f).restype = _U16
+    for f in ("o16_add", "o16_mul"):
+        getattr(L, f).argtypes = [_U16, _U16]
+        getattr(L, f).restype = _U16
+    L.o16_from_double_array.argtypes = [_I64, _P, _P]
+    L.o16_to_double_array.argtypes = [_I64, _P, _P]
+    L.o16_fma_array.argtypes = [_I64, _P, _P, _P, _P]
+    L.o16_add_array.argtypes = [_I64, _P, _P, _P]
+    L.o16_mul_array.argtypes = [_I64, _P, _P, _P]
+    L.o16_apply_fused.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.o16_apply_unfused.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.o16_dot.argtypes = [_I, _I, _I, _P, _P]
+    L.o16_dot.restype = ctypes.c_float
+    L.o16_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]
+    L.o16_bicgstab.restype = _I
+    L.o32_apply_fma.argtypes = [_I, _I, _I, _P, _P, _P]
+    L.oracle_num_threads.restype = _I
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _arr6(arrs):
+    t = (ctypes.c_void_p * 6)(*[a.ctypes.data for a in arrs])
+    return t
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# ---------------- fp64 ----------------
+
+def jacobi_scale(diag, offs):
+    """Jacobi-scaled couplings c_d = off_d / diag (0 out of mesh). Shapes (nz,ny,nx)."""
+    offs = [_c(o, np.float64) for o in offs]
+    nz, ny, nx = offs[0].shape
+    d = None if diag is None else _c(diag, np.float64)
+    out = [np.empty((nz, ny, nx), np.float64) for _ in range(6)]
+    lib().o64_jacobi_scale(nx, ny, nz, None if d is None else _ptr(d), _arr6(offs), _arr6(out))
+    return out
+
+
+def apply64(c, v):
+    c = [_c(a, np.float64) for a in c]
+    v = _c(v, np.float64)
+    nz, ny, nx = v.shape
+    u = np.empty_like(v)
+    lib().o64_apply(nx, ny, nz, _arr6(c), _ptr(v), _ptr(u))
+    return u
+
+
+def apply_raw64(diag, offs, v):
+    offs = [_c(a, np.float64) for a in offs]
+    diag = _c(diag, np.float64)
+    v = _c(v, np.float64)
+    nz, ny, nx = v.shape
+    u = np.empty_like(v)
+    lib().o64_apply_raw(nx, ny, nz, _ptr(diag), _arr6(offs), _ptr(v), _ptr(u))
+    return u
+
+
+def dot64(a, b):
+    a = _c(a, np.float64).ravel()
+    b = _c(b, np.float64).ravel()
+    return lib().o64_dot(a.size, _ptr(a), _ptr(b))
+
+
+def bicgstab64(c, b, x0=None, tol=0.0, maxit=50):
+    """Returns dict(x, hist, iters, status, event_it, alpha, omega)."""
+    c = [_c(a, np.float64) for a in c]
+    b = _c(b, np.float64)
+    nz, ny, nx = b.shape
+    x = np.empty_like(b)
+    hist = np.full(maxit + 1, np.nan)
+    al = np.full(maxit + 1, np.nan)
+    om = np.full(maxit + 1, np.nan)
+    st = ctypes.c_int(-1)
+    ev = ctypes.c_int(0)
+    x0p = None if x0 is None else _ptr(_c(x0, np.float64))
+    x0keep = None if x0 is None else _c(x0, np.float64)
+    if x0keep is not None:
+        x0p = _ptr(x0keep)
+    it = lib().o64_bicgstab(nx, ny, nz, _arr6(c), _ptr(b), x0p, float(tol), int(maxit),
+                            _ptr(x), _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
+    return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value,
+                alpha=al[1: it + 1], omega=om[1: it + 1])
+
+
+def true_residual64(c, b, x):
+    c = [_c(a, np.float64) for a in c]
+    b = _c(b, np.float64)
+    x = _c(x, np.float64)
+    nz, ny, nx = b.shape
+    return lib().o64_true_residual(nx, ny, nz, _arr6(c), _ptr(b), _ptr(x))
+
+
+# ---------------- fp16 ----------------
+
+def f16_from_double(x):
+    """RNE rounding fp64 -> binary16 bit patterns (uint16)."""
+    x = _c(x, np.float64)
+    h = np.empty(x.shape, np.uint16)
+    lib().o16_from_double_array(x.size, _ptr(x), _ptr(h))
+    return h
+
+
+def f16_to_double(h):
+    h = _c(h, np.uint16)
+    x = np.empty(h.shape, np.float64)
+    lib().o16_to_double_array(h.size, _ptr(h), _ptr(x))
+    return x
+
+
+def fma16(a: int, b: int, c: int) -> int:
+    return lib().o16_fma(a, b, c)
+
+
+def add16(a: int, b: int) -> int:
+    return lib().o16_add(a, b)
+
+
+def mul16(a: int, b: int) -> int:
+    return lib().o16_mul(a, b)
+
+
+def fma16_array(a, b, c):
+    a, b, c = (_c(t, np.uint16) for t in (a, b, c))
+    out = np.empty(a.shape, np.uint16)
+    lib().o16_fma_array(a.size, _ptr(a), _ptr(b), _ptr(c), _ptr(out))
+    return out
+
+
+def add16_array(a, b):
+    a, b = (_c(t, np.uint16) for t in (a, b))
+    out = np.empty(a.shape, np.uint16)
+    lib().o16_add_array(a.size, _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def mul16_array(a, b):
+    a, b = (_c(t, np.uint16) for t in (a, b))
+    out = np.empty(a.shape, np.uint16)
+    lib().o16_mul_array(a.size, _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def apply16(c16, v16, unfused: bool = False):
+    c16 = [_c(a, np.uint16) for a in c16]
+    v16 = _c(v16, np.uint16)
+    nz, ny, nx = v16.shape
+    u = np.empty_like(v16)
+    f = lib().o16_apply_unfused if unfused else lib().o16_apply_fused
+    f(nx, ny, nz, _arr6(c16), _ptr(v16), _ptr(u))
+    return u
+
+
+def dot16(a16, b16):
+    a16 = _c(a16, np.uint16)
+    b16 = _c(b16, np.uint16)
+    nz, ny, nx = a16.shape
+    return float(lib().o16_dot(nx, ny, nz, _ptr(a16), _ptr(b16)))
+
+
+def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False):
+    c16 = [_c(a, np.uint16) for a in c16]
+    b16 = _c(b16, np.uint16)
+    nz, ny, nx = b16.shape
+    x = np.empty_like(b16)
+    hist = np.full(maxit + 1, np.nan)
+    al = np.full(maxit + 1, np.nan, np.float32)
+    om = np.full(maxit + 1, np.nan, np.float32)
+    st = ctypes.c_int(-1)
+    ev = ctypes.c_int(0)
+    x0keep = None if x0 is None else _c(x0, np.uint16)
+    it = lib().o16_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
+                            None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
+                            int(bool(unfused)), _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
+                            ctypes.byref(st), ctypes.byref(ev))
+    return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value,
+                alpha=al[1: it + 1], omega=om[1: it + 1])
+
+
+# ---------------- fp32 mirror ----------------
+
+def apply32_fma(c32, v32):
+    c32 = [_c(a, np.float32) for a in c32]
+    v32 = _c(v32, np.float32)
+    nz, ny, nx = v32.shape
+    u = np.empty_like(v32)
+    lib().o32_apply_fma(nx, ny, nz, _arr6(c32), _ptr(v32), _ptr(u))
+    return u
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+# ---------------- quantisation helpers (R3: RN from the fp64 scaled value) ----
+
+def quantize_coeffs(c64, precision: str):
+    """Round the fp64 Jacobi-scaled couplings to the working precision."""
+    if precision == "fp32":
+        return [np.asarray(a, np.float64).astype(np.float32) for a in c64]
+    return [f16_from_double(a) for a in c64]
+
+
+def scale_rhs(b_work, diag, precision: str):
+    """b_hat = rn_w(b / diag) in fp64 (R3).  b_work holds working-precision values
+    (float32 array or uint16 fp16 bit patterns)."""
+    if precision == "fp32":
+        bd = np.asarray(b_work, np.float32).astype(np.float64)
+        return (bd / np.asarray(diag, np.float64)).astype(np.float32)
+    bd = f16_to_double(b_work)
+    return f16_from_double(bd / np.asarray(diag, np.float64))

@@ -1,0 +1,126 @@
+/*
+ * oracle.h - CPU oracle for BiCGStab on the Jacobi-scaled 7-point stencil.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  The
+ * product (paper_2010_03660_b200, libsten.so) never links, loads or calls it,
+ * and shares no code with it.
+ *
+ * Written from the paper (arXiv 2010.03660, /root/reference/PAPER.md):
+ *   - Algorithm 1 "Standard BiCGStab", PAPER.md:168-189 (Sec. III);
+ *   - unit main diagonal by diagonal (Jacobi) preconditioning, six stored
+ *     off-diagonals, PAPER.md:195 (Sec. IV);
+ *   - SpMV u = A v as the sum of the local iterate and six coefficient-times-
+ *     neighbour products, PAPER.md:198-201, 338-346 (Sec. SpMV(3D));
+ *   - mixed precision: fp16 storage and arithmetic, inner products with fp16
+ *     multiply / fp32 add, AllReduce in fp32.
+ * Readings where the paper is silent are numbered R1..R13 in DESIGN.md.
+ *
+ * Mesh: nx*ny*nz points, linear index P = i + nx*(j + ny*k), x fastest.
+ * Coefficient arrays c[0..5] = (xm, xp, ym, yp, zm, zp): c_d[P] multiplies
+ * v at the -x/+x/-y/+y/-z/+z neighbour of P.  Neighbours outside the mesh
+ * contribute nothing (Dirichlet zero, R5).
+ *
+ * Parity pins: every function is pinned by tests/test_oracle_*.py (see the
+ * "Pins" table in DESIGN.md).  Functions marked "mirror" reproduce one
+ * specific evaluation order of the GPU kernels (bitwise tests); they are
+ * independent re-statements of that order, not shared code.
+ */
+#ifndef STEN_ORACLE_H
+#define STEN_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (same meaning as include/sten.h, restated here) */
+#define ORC_CONVERGED 0
+#define ORC_MAXIT 1
+#define ORC_BREAKDOWN 2
+#define ORC_NONFINITE 3
+
+/* ---------------- fp64 reference (O64) ---------------- */
+
+/* Jacobi scaling: c_d[P] = off_d[P] / diag[P] for in-mesh
+ * neighbours, +0 where the neighbour is outside the mesh (R5). diag==NULL:
+ * the off-diagonals are taken as already scaled (only the zeroing applies). */
+void o64_jacobi_scale(int nx, int ny, int nz, const double *diag,
+                      const double *const off[6], double *const c[6]);
+
+/* u = v + sum_d c_d * v_nb(d)   (unit diagonal) */
+void o64_apply(int nx, int ny, int nz, const double *const c[6],
+               const double *v, double *u);
+
+/* u = diag*v + sum_d off_d * v_nb(d)  (the un-scaled matrix; used to make a
+ * manufactured right-hand side b = A x_true, config 1) */
+void o64_apply_raw(int nx, int ny, int nz, const double *diag,
+                   const double *const off[6], const double *v, double *u);
+
+/* sum_P a[P]*b[P], P ascending, fp64 */
+double o64_dot(int64_t n, const double *a, const double *b);
+
+/* BiCGStab, Alg. 1 in fp64 with the stopping / breakdown
+ * readings R6-R9.  x0 may be NULL (x0 = 0, Alg. 1 line 174 exactly).
+ * hist[0..maxit] receives ||r_i||/||b||; alpha/omega (may be NULL) receive
+ * alpha_i, omega_i at index i (1-based).  Returns the number of completed
+ * iterations; *status one of ORC_*.  *event_it = iteration of the first event
+ * (tol == 0 benchmark mode), 0 if none. */
+int o64_bicgstab(int nx, int ny, int nz, const double *const c[6],
+                 const double *b, const double *x0, double tol, int maxit,
+                 double *x, double *hist, double *alpha, double *omega,
+                 int *status, int *event_it);
+
+/* ||b - A x||_2 / ||b||_2 in fp64 (unit-diagonal operator) */
+double o64_true_residual(int nx, int ny, int nz, const double *const c[6],
+                         const double *b, const double *x);
+
+/* ---------------- IEEE binary16 primitives (exact integer arithmetic) ------ */
+double o16_to_double(uint16_t h);
+uint16_t o16_from_double(double x);              /* round-to-nearest-even */
+uint16_t o16_fma(uint16_t a, uint16_t b, uint16_t c); /* a*b+c, one rounding */
+uint16_t o16_add(uint16_t a, uint16_t b);
+uint16_t o16_mul(uint16_t a, uint16_t b);
+void o16_from_double_array(int64_t n, const double *x, uint16_t *h);
+void o16_to_double_array(int64_t n, const uint16_t *h, double *x);
+void o16_fma_array(int64_t n, const uint16_t *a, const uint16_t *b, const uint16_t *c, uint16_t *out);
+void o16_add_array(int64_t n, const uint16_t *a, const uint16_t *b, uint16_t *out);
+void o16_mul_array(int64_t n, const uint16_t *a, const uint16_t *b, uint16_t *out);
+
+/* ---------------- fp16 "mixed" oracle (O16) ---------------- */
+
+/* mirror: u = v; u = fma16(c_xm, v_xm, u); ... xp, ym, yp, zm, zp (R10);
+ * out-of-mesh neighbour value taken as +0. */
+void o16_apply_fused(int nx, int ny, int nz, const uint16_t *const c[6],
+                     const uint16_t *v, uint16_t *u);
+/* paper-faithful variant: each product rounded to fp16, then an fp16 add
+ * (Table "Operations per meshpoint per iteration": HP x and HP + counted
+ * separately; separate multiply threads + sumtask,
+ * PAPER.md:340-346).  Diagonal term first, then xm..zp. */
+void o16_apply_unfused(int nx, int ny, int nz, const uint16_t *const c[6],
+                       const uint16_t *v, uint16_t *u);
+/* mixed inner product: fp16 x fp16 product exact in fp32,
+ * fp32 accumulation along each z-pencil (one CS-1 core's local dot,
+ * PAPER.md:193-195), then an fp32 sum over pencils (the fp32 AllReduce). */
+float o16_dot(int nx, int ny, int nz, const uint16_t *a, const uint16_t *b);
+
+/* BiCGStab in mixed precision: every vector op in fp16 (fused FMAs, R11),
+ * dots as o16_dot, scalars in fp32 (R12).  unfused != 0 selects
+ * o16_apply_unfused and unfused AXPYs.  Same control flow as o64_bicgstab. */
+int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                 const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                 int unfused, uint16_t *x, double *hist, float *alpha,
+                 float *omega, int *status, int *event_it);
+
+/* ---------------- fp32 mirror of the GPU fp32 kernels ---------------- */
+/* u = v; u = fmaf(c_xm, v_xm, u); ... (same order as o16_apply_fused) */
+void o32_apply_fma(int nx, int ny, int nz, const float *const c[6],
+                   const float *v, float *u);
+
+/* informational */
+int oracle_num_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
