@@ -1,0 +1,168 @@
+/*
+ * sten.h - C ABI of libsten.so: B200-native (sm_100a) BiCGStab for the linear
+ * system of a 7-point finite-difference stencil on a regular 3D mesh, with the
+ * main diagonal Jacobi-scaled to one.
+ *
+ * What is computed (arXiv 2010.03660, /root/reference/PAPER.md):
+ *   - the operator: A x = b from a 7-point stencil; "with
+ *     diagonal preconditioning the main diagonal is all ones.  Therefore, we
+ *     only store six other diagonals" (Sec. IV);
+ *   - stencil_apply: u = A v as the local value plus six coefficient-times-
+ *     neighbour products (Sec. "SpMV (3D)");
+ *   - bicgstab_solve: Algorithm 1 "Standard BiCGStab";
+ *   - precisions: fp32 throughout, or the paper's mixed mode - fp16 storage
+ *     and arithmetic, inner products with fp16 multiply / fp32 accumulate, the
+ *     cross-device reduction in fp32.
+ * Readings of the paper where it is silent (stopping rule, breakdown, x0, the
+ * order of floating-point operations ...) are R1..R13 in DESIGN.md.
+ *
+ * Layout.  A mesh (or a rank's slab of it) of nx*ny*nz points is a dense
+ * array with linear index P = i + nx*(j + ny*k): x fastest, z slowest, so a
+ * z-slab is contiguous.  Every vector argument (b, x0, x_out, x, y) is such a
+ * dense array of this rank's points, in the precision's storage type:
+ * float for STEN_FP32, IEEE binary16 (uint16 bit patterns) for STEN_MIXED.
+ * Vector and coefficient pointers may be device pointers or host pointers
+ * (pinned or pageable); the library classifies each with
+ * cudaPointerGetAttributes and copies host data itself, inside the call.
+ *
+ * Multi-GPU.  With a communicator, rank r of R owns the z-planes directly
+ * above rank r-1's (rank order = z order) and passes only its own planes;
+ * the library exchanges one halo plane per neighbour over NCCL and all-reduces
+ * the 1-2 fp32 dot-product partial sums of each half-iteration.
+ *
+ * Errors.  Every int-returning entry point returns STEN_OK (0) or a negative
+ * STEN_E* code; sten_last_error() then gives a thread-local message.
+ * Numerical breakdown is NOT an error: bicgstab_solve returns STEN_OK and
+ * reports it in *status.
+ *
+ * Threading.  A handle may be used by one host thread at a time.
+ */
+#ifndef STEN_H
+#define STEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STEN_VERSION 1
+
+/* precision of a solve / apply */
+#define STEN_FP32 0   /* fp32 storage, fp32 arithmetic, fp32 dots */
+#define STEN_MIXED 1  /* fp16 storage + arithmetic, fp16*fp16 products summed in fp32 */
+
+/* element type of the coefficient arrays passed to stencil_create */
+#define STEN_DT_F64 0
+#define STEN_DT_F32 1
+
+/* return codes */
+#define STEN_OK 0
+#define STEN_EINVAL (-1)
+#define STEN_ENOMEM (-2)
+#define STEN_ECUDA (-3)
+#define STEN_ENCCL (-4)
+#define STEN_EUNSUPPORTED (-5)
+
+/* solve status (R6-R8) */
+#define STEN_CONVERGED 0 /* ||r_i||/||b|| <= tol, or r_i == 0 exactly        */
+#define STEN_MAXIT 1     /* maxit iterations done without an event             */
+#define STEN_BREAKDOWN 2 /* (rhat, v) == 0, omega == 0 or (rhat, r_new) == 0   */
+#define STEN_NONFINITE 3 /* a dot product or scalar became Inf/NaN             */
+
+typedef struct sten_comm sten_comm;       /* opaque: NCCL communicator wrapper */
+typedef struct sten_stencil sten_stencil; /* opaque: operator + solver workspace */
+
+/* Performance counters of the last bicgstab_solve on a handle. */
+typedef struct sten_stats {
+  double phase_ms[3];     /* summed device time of phases H1, H2, H3 (timing on) */
+  long long phase_launches[3]; /* launches of the H1/H2/H3 kernels timed      */
+  double solve_ms;        /* device time from first to last kernel of the solve */
+  long long kernel_launches; /* kernels of this library launched by the solve  */
+  int event_iter;         /* iteration of the first breakdown event (0: none) */
+  int graph_chunk;        /* iterations per CUDA-graph replay                  */
+} sten_stats;
+
+/* ---------------------------------------------------------------- misc -- */
+int sten_version(void);
+/* Thread-local message describing the last non-OK return on this thread. */
+const char *sten_last_error(void);
+
+/* ---------------------------------------------------------------- comm -- */
+/* Write a fresh ncclUniqueId (128 bytes) into id_out; call on rank 0 and
+ * broadcast the bytes to the other ranks by any means. */
+int sten_comm_unique_id(void *id_out);
+/* Create the communicator of rank `rank` of `nranks` on the CURRENT CUDA
+ * device.  NCCL is loaded at run time (libnccl.so.2).  Errors: STEN_EINVAL
+ * (bad rank/nranks), STEN_ENCCL (NCCL missing or ncclCommInitRank failed). */
+int sten_comm_create(const void *unique_id, int nranks, int rank, sten_comm **out);
+void sten_comm_destroy(sten_comm *comm);
+
+/* ------------------------------------------------------------- stencil -- */
+/* Build the Jacobi-scaled operator of this rank's nx*ny*nz points.
+ *   coeffs[0]   : main diagonal a_P of A, or NULL if A already has a unit
+ *                 diagonal;
+ *   coeffs[1..6]: off-diagonal entries of A coupling P to its -x, +x, -y, +y,
+ *                 -z, +z neighbour (A[P, P-1], A[P, P+1], A[P, P-nx], ...);
+ *   all dense (nz, ny, nx) arrays of coeff_dtype (STEN_DT_F64 or _F32), host
+ *   or device; they are copied, the caller keeps ownership.
+ * The library forms c_d = A_d / a_P in fp64 (c_d = A_d without a diagonal),
+ * drops couplings to points outside the global mesh (Dirichlet zero), and
+ * stores c_d rounded to nearest in fp32 AND in fp16 (R3, R5), plus a_P in fp64
+ * to scale right-hand sides.
+ *   nslabs >= 1: split this rank's planes into nslabs z-slabs with one-plane
+ *                halos exchanged by device copies - the same halo/reduction
+ *                path as multi-GPU, for testing it on one GPU (nz % nslabs
+ *                must be 0; 1 for normal use);
+ *   comm: NULL for a single rank, else this rank's communicator.
+ * Errors: STEN_EINVAL (sizes <= 0, nz % nslabs, NULL coefficient),
+ * STEN_ENOMEM, STEN_ECUDA. */
+int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype,
+                   int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out);
+void stencil_destroy(sten_stencil *st);
+
+/* y = A_hat x, A_hat the Jacobi-scaled operator (unit diagonal), one halo
+ * exchange first when decomposed.  x, y: this rank's points in the storage
+ * type of `precision`; x and y must not overlap.  Enqueued on cuda_stream and
+ * synchronised before return.  Errors: STEN_EINVAL, STEN_ECUDA, STEN_ENCCL. */
+int stencil_apply(sten_stencil *st, int precision, const void *x, void *y, void *cuda_stream);
+
+/* Solve A x = b with BiCGStab (Alg. 1) on the Jacobi-scaled system
+ * A_hat x = b_hat, b_hat = b / a_P rounded to the working precision (R3).
+ *   b      : right-hand side of the ORIGINAL system (of A_hat if no diagonal
+ *            was given), this rank's points;
+ *   x0     : initial guess, or NULL for x0 = 0 (Alg. 1 l.174 exactly, R1);
+ *   tol    : stop when ||r_i||_2 / ||b_hat||_2 <= tol (recurrence residual,
+ *            R4); tol == 0 runs exactly maxit iterations (benchmark mode: a
+ *            breakdown is recorded in sten_stats.event_iter and the scalars
+ *            are guarded so the iteration stays finite, R7);
+ *   maxit  : >= 0;
+ *   x_out  : solution, this rank's points;
+ *   iters  : completed iterations;
+ *   res_hist: host array of >= maxit+1 doubles: ||r_i||/||b_hat||, i = 0..iters;
+ *   status : STEN_CONVERGED / _MAXIT / _BREAKDOWN / _NONFINITE.
+ * All work is enqueued on cuda_stream; returns after x_out, iters, res_hist
+ * and status are final.  Errors: STEN_EINVAL (tol < 0 or NaN, maxit < 0),
+ * STEN_ENOMEM, STEN_ECUDA, STEN_ENCCL. */
+int bicgstab_solve(sten_stencil *st, int precision, const void *b, const void *x0, double tol,
+                   int maxit, void *x_out, int *iters, double *res_hist, int *status,
+                   void *cuda_stream);
+
+/* Per-iteration scalars alpha_i, omega_i (i = 1..n) of the last solve, as
+ * computed on the device (fp32), for parity checks.  n <= iters. */
+int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
+
+/* Record per-phase CUDA events inside the solve's graphs (enable != 0). */
+int sten_set_timing(sten_stencil *st, int enable);
+int sten_get_stats(sten_stencil *st, sten_stats *out);
+
+/* Tile geometry override for tuning (0 = library default).  bx: points per
+ * tile in x (multiple of 8), by: rows per tile, zc: planes per CTA,
+ * stages: TMA pipeline depth (2..8). */
+int sten_set_tiling(sten_stencil *st, int precision, int bx, int by, int zc, int stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STEN_H */

@@ -1,1 +1,252 @@
-"""B200-native BiCGStab for Jacobi-scaled 7-point stencils (arXiv 2010.03660)."""
+"""B200-native BiCGStab for Jacobi-scaled 7-point stencils (arXiv 2010.03660).
+
+Thin ctypes binding of libsten.so (include/sten.h): the same entry points,
+argument marshalling only - every step of the solve runs in the library's
+CUDA kernels.  There is no CPU fallback: if libsten.so is missing or cannot be
+loaded every call raises StenError.
+
+Vectors may be torch tensors (CUDA or CPU) or numpy arrays; their element type
+must match the precision: float32 for FP32, float16 (torch.float16, or numpy
+float16/uint16 bit patterns) for MIXED.  Coefficients are float64 or float32.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import roofline  # noqa: F401  (work/traffic accounting)
+
+FP32 = 0
+MIXED = 1
+DT_F64 = 0
+DT_F32 = 1
+
+CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3
+STATUS_NAMES = {0: "converged", 1: "maxit", 2: "breakdown", 3: "nonfinite"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsten.so")
+
+
+class StenError(RuntimeError):
+    pass
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("phase_ms", ctypes.c_double * 3), ("phase_launches", ctypes.c_longlong * 3),
+                ("solve_ms", ctypes.c_double), ("kernel_launches", ctypes.c_longlong),
+                ("event_iter", ctypes.c_int), ("graph_chunk", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsten.so; raise StenError (never fall back) if it is unavailable."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise StenError(f"{LIB_PATH} not built - run `python -m paper_2010_03660_b200.build` "
+                            "(or __graft_entry__.build())")
+        try:
+            L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        except OSError as e:  # pragma: no cover
+            raise StenError(f"cannot load {LIB_PATH}: {e}") from e
+        P, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        L.sten_version.restype = I
+        L.sten_last_error.restype = ctypes.c_char_p
+        L.sten_comm_unique_id.argtypes = [P]
+        L.sten_comm_create.argtypes = [P, I, I, ctypes.POINTER(P)]
+        L.sten_comm_destroy.argtypes = [P]
+        L.stencil_create.argtypes = [I, I, I, P, I, I, P, P, ctypes.POINTER(P)]
+        L.stencil_destroy.argtypes = [P]
+        L.stencil_apply.argtypes = [P, I, P, P, P]
+        L.bicgstab_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
+        L.sten_scalar_history.argtypes = [P, I, P, P]
+        L.sten_set_timing.argtypes = [P, I]
+        L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
+        L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().sten_last_error().decode(errors="replace")
+        raise StenError(f"libsten error {rc}: {msg}")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise StenError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise StenError("array must be C-contiguous")
+        return ctypes.c_void_p(a.ctypes.data)
+    raise StenError(f"unsupported array type {type(a)}")
+
+
+def _itemsize(a):
+    if hasattr(a, "element_size"):
+        return a.element_size()
+    return a.itemsize
+
+
+def _numel(a):
+    return a.numel() if hasattr(a, "numel") else a.size
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:  # pragma: no cover
+        pass
+    return ctypes.c_void_p(0)
+
+
+def _check_vec(a, precision, n, name):
+    want = 4 if precision == FP32 else 2
+    if _itemsize(a) != want:
+        raise StenError(f"{name}: element size {_itemsize(a)} does not match precision {precision}")
+    if _numel(a) != n:
+        raise StenError(f"{name}: {_numel(a)} elements, expected {n}")
+
+
+def version() -> int:
+    return lib().sten_version()
+
+
+# ------------------------------------------------------------------ comm --
+class Comm:
+    def __init__(self, handle, nranks, rank):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    def close(self):
+        if self.handle:
+            lib().sten_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().sten_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_create(unique_id: bytes, nranks: int, rank: int) -> Comm:
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(lib().sten_comm_create(buf, nranks, rank, ctypes.byref(h)))
+    return Comm(h, nranks, rank)
+
+
+# --------------------------------------------------------------- stencil --
+class Stencil:
+    """Owner of a sten_stencil handle."""
+
+    def __init__(self, handle, nx, ny, nz, comm):
+        self.handle, self.nx, self.ny, self.nz, self.comm = handle, nx, ny, nz, comm
+
+    @property
+    def npoints(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def close(self):
+        if self.handle:
+            lib().stencil_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stencil_create(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
+                   stream=None) -> Stencil:
+    """coeffs = [diag or None, A_xm, A_xp, A_ym, A_yp, A_zm, A_zp], dense (nz,ny,nx) each."""
+    if len(coeffs) != 7:
+        raise StenError("coeffs must have 7 entries (diag, xm, xp, ym, yp, zm, zp)")
+    ref = next(c for c in coeffs[1:] if c is not None)
+    dt = DT_F64 if _itemsize(ref) == 8 else DT_F32
+    n = nx * ny * nz
+    keep = []
+    arr = (ctypes.c_void_p * 7)()
+    for i, c in enumerate(coeffs):
+        if c is None:
+            arr[i] = None
+            continue
+        if _itemsize(c) != _itemsize(ref) or _numel(c) != n:
+            raise StenError(f"coeffs[{i}] has the wrong dtype or size")
+        keep.append(c)
+        arr[i] = _ptr(c).value
+    h = ctypes.c_void_p()
+    _check(lib().stencil_create(nx, ny, nz, arr, dt, nslabs, comm.handle if comm else None,
+                                _stream(stream), ctypes.byref(h)))
+    return Stencil(h, nx, ny, nz, comm)
+
+
+def stencil_destroy(st: Stencil):
+    st.close()
+
+
+def stencil_apply(st: Stencil, precision: int, x, y, stream=None):
+    _check_vec(x, precision, st.npoints, "x")
+    _check_vec(y, precision, st.npoints, "y")
+    _check(lib().stencil_apply(st.handle, precision, _ptr(x), _ptr(y), _stream(stream)))
+    return y
+
+
+def bicgstab_solve(st: Stencil, precision: int, b, x0, tol: float, maxit: int, x_out, stream=None):
+    """Returns (iters, res_hist[0..iters] as numpy fp64, status)."""
+    _check_vec(b, precision, st.npoints, "b")
+    _check_vec(x_out, precision, st.npoints, "x_out")
+    if x0 is not None:
+        _check_vec(x0, precision, st.npoints, "x0")
+    hist = np.zeros(max(maxit, 0) + 1, dtype=np.float64)
+    it = ctypes.c_int(0)
+    status = ctypes.c_int(-1)
+    _check(lib().bicgstab_solve(st.handle, precision, _ptr(b), _ptr(x0), float(tol), int(maxit), _ptr(x_out),
+                                ctypes.byref(it), hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(status),
+                                _stream(stream)))
+    return it.value, hist[: it.value + 1].copy(), status.value
+
+
+def scalar_history(st: Stencil, n: int):
+    a = np.zeros(n, np.float64)
+    w = np.zeros(n, np.float64)
+    _check(lib().sten_scalar_history(st.handle, n, a.ctypes.data_as(ctypes.c_void_p),
+                                     w.ctypes.data_as(ctypes.c_void_p)))
+    return a, w
+
+
+def set_timing(st: Stencil, enable: bool):
+    _check(lib().sten_set_timing(st.handle, int(bool(enable))))
+
+
+def get_stats(st: Stencil) -> dict:
+    s = _Stats()
+    _check(lib().sten_get_stats(st.handle, ctypes.byref(s)))
+    return dict(phase_ms=list(s.phase_ms), phase_launches=list(s.phase_launches), solve_ms=s.solve_ms,
+                kernel_launches=s.kernel_launches, event_iter=s.event_iter, graph_chunk=s.graph_chunk)
+
+
+def set_tiling(st: Stencil, precision: int, bx: int = 0, by: int = 0, zc: int = 0, stages: int = 0):
+    _check(lib().sten_set_tiling(st.handle, precision, bx, by, zc, stages))

@@ -1,0 +1,862 @@
+// api.cu - the C ABI of libsten.so (include/sten.h): operator setup, workspace,
+// TMA descriptors, the BiCGStab driver (CUDA graphs of whole iterations), the
+// z-slab halo exchange and the fp32 scalar all-reduce (NCCL over NVLink).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "sten_internal.cuh"
+
+using namespace sten;
+
+// ------------------------------------------------------------ errors --
+static thread_local std::string g_err;
+static int set_err(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return set_err(STEN_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define RC_TRY(expr)                 \
+  do {                               \
+    int rc_ = (expr);                \
+    if (rc_ != STEN_OK) return rc_;  \
+  } while (0)
+#define KLAUNCH(expr)                                                                              \
+  do {                                                                                             \
+    int e_ = (expr);                                                                               \
+    if (e_ != 0)                                                                                   \
+      return set_err(STEN_ECUDA, "%s:%d launch %s: %s", __FILE__, __LINE__, #expr,                \
+                     cudaGetErrorString((cudaError_t)e_));                                         \
+  } while (0)
+
+// ------------------------------------------------------------- NCCL --
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+static int nccl_load() {
+  if (g_nccl.h) return STEN_OK;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return set_err(STEN_ENCCL, "cannot dlopen libnccl.so.2: %s", dlerror());
+#define SYM(field, name)                                                               \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));             \
+  if (!g_nccl.field) return set_err(STEN_ENCCL, "libnccl.so.2 lacks %s", name);
+  SYM(GetUniqueId, "ncclGetUniqueId");
+  SYM(CommInitRank, "ncclCommInitRank");
+  SYM(CommDestroy, "ncclCommDestroy");
+  SYM(AllReduce, "ncclAllReduce");
+  SYM(Send, "ncclSend");
+  SYM(Recv, "ncclRecv");
+  SYM(GroupStart, "ncclGroupStart");
+  SYM(GroupEnd, "ncclGroupEnd");
+  SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  g_nccl.h = h;
+  return STEN_OK;
+}
+#define NCCL_TRY(expr)                                                                          \
+  do {                                                                                          \
+    ncclResult_t r_ = (expr);                                                                   \
+    if (r_ != ncclSuccess)                                                                      \
+      return set_err(STEN_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+struct sten_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+// -------------------------------------------------- tensor-map encoding --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn g_encode = nullptr;
+static int load_encode() {
+  if (g_encode) return STEN_OK;
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return set_err(STEN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  return STEN_OK;
+}
+// 3D map over an array of `planes` planes of (ny rows x pitch elements), logical width nx.
+static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int planes, int pitch, int boxx, int boxy) {
+  RC_TRY(load_encode());
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)pitch * ny * elem};
+  cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base,
+                        dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(STEN_ECUDA, "cuTensorMapEncodeTiled failed (%d): dims %d %d %d box %d %d", (int)r, nx, ny, planes,
+                   boxx, boxy);
+  return STEN_OK;
+}
+
+// ------------------------------------------------------------ handle --
+struct Tiling {
+  int bx = 0, by = 0, zc = 0, stages = 0, threads = 0;
+};
+
+struct PrecBufs {
+  bool ready = false;
+  void *x = nullptr, *r = nullptr, *rh = nullptr, *p[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr};
+  void *s = nullptr, *t = nullptr, *bw = nullptr;
+  // tensor maps (rebuilt when the tiling changes)
+  bool maps_ok = false;
+  CUtensorMap m_r, m_p[2], m_v[2], m_s, m_x, m_rh, m_c[6];
+};
+
+struct Slab {
+  int nz = 0;                     // planes of this slab
+  long long z_first = 0;          // first plane within this rank's part
+  float *c32[6] = {};
+  __half *c16[6] = {};
+  double *aP = nullptr;
+  PrecBufs pb[2];
+};
+
+struct GraphKey {
+  int prec, chunk, timing;
+  bool operator<(const GraphKey &o) const {
+    return std::tie(prec, chunk, timing) < std::tie(o.prec, o.chunk, o.timing);
+  }
+};
+struct GraphRec {
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0;
+  std::vector<cudaEvent_t> ev;  // [chunk][3][2] when timing
+};
+
+struct sten_stencil {
+  int nx = 0, ny = 0, nz = 0, pitch = 0;
+  long long plane = 0;
+  int nslabs = 1;
+  std::vector<Slab> slabs;
+  sten_comm *comm = nullptr;
+  bool has_diag = false;
+  int sm = 148;
+  Tiling tiling[2];
+  DevState *st = nullptr;       // device
+  DevState *st_host = nullptr;  // pinned mirror
+  float *partials = nullptr;
+  int partials_cap = 0;
+  unsigned *counter = nullptr;
+  float *slab_sums = nullptr;   // [nslabs * kMaxDots]
+  float *red_total = nullptr;   // [kMaxDots] (NCCL path)
+  double *hist = nullptr;
+  float *ahist = nullptr, *whist = nullptr;
+  int hist_cap = 0;
+  cudaStream_t cap = nullptr;   // capture stream
+  std::map<GraphKey, GraphRec> graphs;
+  bool timing = false;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  sten_stats stats{};
+  long long launches = 0;       // kernel launches (direct + graph nodes) of the current call
+};
+
+static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
+static int esize(int prec) { return prec == STEN_FP32 ? 4 : 2; }
+
+static void default_tiling(sten_stencil *st, int prec) {
+  Tiling &t = st->tiling[prec];
+  const int vec = prec == STEN_FP32 ? 4 : 8;
+  int bx = prec == STEN_FP32 ? 64 : 128;
+  int w = (st->nx + vec - 1) / vec * vec;
+  if (w < bx) bx = w;
+  t.bx = bx;
+  t.by = 8;
+  t.stages = 4;
+  int nzs = st->slabs[0].nz;
+  t.zc = nzs < 64 ? nzs : 64;
+  int vpr = bx / vec;
+  int th = (vpr * t.by + 31) / 32 * 32;
+  t.threads = th < 64 ? 64 : (th > 256 ? 256 : th);
+}
+
+static int ensure_maps(sten_stencil *st, int prec) {
+  const Tiling &t = st->tiling[prec];
+  const int e = esize(prec);
+  const int H = prec == STEN_FP32 ? 4 : 8;
+  for (Slab &sl : st->slabs) {
+    PrecBufs &b = sl.pb[prec];
+    if (b.maps_ok) continue;
+    const int planes = sl.nz + 2;
+    const int hx = t.bx + 2 * H, hy = t.by + 2;
+    RC_TRY(make_map(&b.m_r, b.r, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    for (int i = 0; i < 2; ++i) {
+      RC_TRY(make_map(&b.m_p[i], b.p[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
+      RC_TRY(make_map(&b.m_v[i], b.v[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    }
+    RC_TRY(make_map(&b.m_s, b.s, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    RC_TRY(make_map(&b.m_x, b.x, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, planes, st->pitch, t.bx, t.by));
+    for (int d = 0; d < 6; ++d) {
+      void *c = prec == STEN_FP32 ? (void *)sl.c32[d] : (void *)sl.c16[d];
+      RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz, st->pitch, t.bx, t.by));
+    }
+    b.maps_ok = true;
+  }
+  return STEN_OK;
+}
+
+static void drop_graphs(sten_stencil *st);
+static int ensure_bufs(sten_stencil *st, int prec) {
+  const size_t vbytes = (size_t)st->plane * esize(prec);
+  for (Slab &sl : st->slabs) {
+    PrecBufs &b = sl.pb[prec];
+    if (b.ready) continue;
+    const size_t bytes = vbytes * (sl.nz + 2);
+    void **all[] = {&b.x, &b.r, &b.rh, &b.p[0], &b.p[1], &b.v[0], &b.v[1], &b.s, &b.t, &b.bw};
+    for (void **pp : all) {
+      cudaError_t e = cudaMalloc(pp, bytes);
+      if (e != cudaSuccess) return set_err(STEN_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      CUDA_TRY(cudaMemset(*pp, 0, bytes));  // halo planes and row padding stay zero
+    }
+    b.ready = true;
+    b.maps_ok = false;
+  }
+  if (st->tiling[prec].bx == 0) default_tiling(st, prec);
+  RC_TRY(ensure_maps(st, prec));
+  // partial-sum buffer large enough for the largest grid
+  int need = 0;
+  for (Slab &sl : st->slabs) {
+    const Tiling &t = st->tiling[prec];
+    int g = ((st->nx + t.bx - 1) / t.bx) * ((st->ny + t.by - 1) / t.by) * ((sl.nz + t.zc - 1) / t.zc);
+    if (g > need) need = g;
+  }
+  if (need < st->sm * 16) need = st->sm * 16;
+  if (need > st->partials_cap) {
+    if (st->partials) cudaFree(st->partials);
+    CUDA_TRY(cudaMalloc(&st->partials, (size_t)need * kMaxDots * sizeof(float)));
+    st->partials_cap = need;
+    drop_graphs(st);
+  }
+  return STEN_OK;
+}
+
+// --------------------------------------------------------- launch helpers --
+static Reduce make_red(sten_stencil *st, int slab) {
+  Reduce r;
+  r.partials = st->partials;
+  r.counter = st->counter;
+  r.slab_out = decomposed(st) ? st->slab_sums + slab * kMaxDots : nullptr;
+  r.st = st->st;
+  return r;
+}
+
+static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int parity, cudaStream_t s) {
+  Slab &sl = st->slabs[slab];
+  PrecBufs &b = sl.pb[prec];
+  const Tiling &t = st->tiling[prec];
+  StencilArgs a;
+  memset(&a, 0, sizeof a);
+  const int cur = parity, nxt = parity ^ 1;
+  if (mode == MODE_APPLY) {
+    a.tm_in[0] = b.m_s;  // apply reads the s buffer
+    a.out0 = b.t;
+  } else if (mode == MODE_H1) {
+    a.tm_in[0] = b.m_r;
+    a.tm_in[1] = b.m_p[cur];
+    a.tm_in[2] = b.m_v[cur];
+    a.tm_aux = b.m_rh;
+    a.out0 = b.v[nxt];
+    a.out1 = b.p[nxt];
+  } else {
+    a.tm_in[0] = b.m_r;
+    a.tm_in[1] = b.m_v[nxt];
+    a.out0 = b.t;
+    a.out1 = b.s;
+  }
+  for (int d = 0; d < 6; ++d) a.tm_c[d] = b.m_c[d];
+  a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
+  a.bx = t.bx;
+  a.by = t.by;
+  a.zc = t.zc;
+  a.stages = t.stages;
+  a.tiles_x = (st->nx + t.bx - 1) / t.bx;
+  a.tiles_y = (st->ny + t.by - 1) / t.by;
+  a.red = make_red(st, slab);
+  size_t smem = prec == STEN_FP32 ? stencil_smem_bytes<float>(mode, t.bx, t.by, t.stages)
+                                  : stencil_smem_bytes<__half>(mode, t.bx, t.by, t.stages);
+  if (prec == STEN_FP32) KLAUNCH(stencil_launch<float>(mode, a, t.threads, smem, s));
+  else KLAUNCH(stencil_launch<__half>(mode, a, t.threads, smem, s));
+  st->launches++;
+  return STEN_OK;
+}
+
+static int ew_grid(sten_stencil *st) { return st->sm * 8; }
+
+static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStream_t s) {
+  Slab &sl = st->slabs[slab];
+  PrecBufs &b = sl.pb[prec];
+  const int e = esize(prec), vec = prec == STEN_FP32 ? 4 : 8;
+  const size_t off = (size_t)st->plane * e;  // interior starts at plane 1
+  auto in = [&](void *p) { return (const void *)((char *)p + off); };
+  EwArgs a;
+  memset(&a, 0, sizeof a);
+  a.x = in(b.x);
+  a.p = in(b.p[parity ^ 1]);
+  a.s = in(b.s);
+  a.t = in(b.t);
+  a.rhat = in(b.rh);
+  a.xo = (char *)b.x + off;
+  a.ro = (char *)b.r + off;
+  a.nvec = (long long)st->plane * sl.nz / vec;
+  a.red = make_red(st, slab);
+  if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st), 256, s));
+  else KLAUNCH(h3_launch<__half>(a, ew_grid(st), 256, s));
+  st->launches++;
+  return STEN_OK;
+}
+
+static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s) {
+  Slab &sl = st->slabs[slab];
+  PrecBufs &b = sl.pb[prec];
+  const int e = esize(prec), vec = prec == STEN_FP32 ? 4 : 8;
+  const size_t off = (size_t)st->plane * e;
+  EwArgs a;
+  memset(&a, 0, sizeof a);
+  a.bw = (char *)b.bw + off;
+  a.aP = st->has_diag ? sl.aP : nullptr;
+  a.ax = with_ax ? (const void *)((char *)b.t + off) : nullptr;
+  a.r = (char *)b.r + off;
+  a.rh = (char *)b.rh + off;
+  a.p0 = (char *)b.p[0] + off;
+  a.v0 = (char *)b.v[0] + off;
+  a.nvec = (long long)st->plane * sl.nz / vec;
+  a.red = make_red(st, slab);
+  if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st), 256, s));
+  else KLAUNCH(init_launch<__half>(a, ew_grid(st), 256, s));
+  st->launches++;
+  return STEN_OK;
+}
+
+// One halo plane to each z-neighbour, for the array selected by `pick`.
+template <typename Pick>
+static int exchange(sten_stencil *st, int prec, Pick pick, cudaStream_t s) {
+  const size_t pb = (size_t)st->plane * esize(prec);
+  const int ns = (int)st->slabs.size();
+  for (int k = 0; k + 1 < ns; ++k) {  // local neighbours: device copies
+    char *lo = (char *)pick(st->slabs[k].pb[prec]);
+    char *hi = (char *)pick(st->slabs[k + 1].pb[prec]);
+    const int nzl = st->slabs[k].nz;
+    CUDA_TRY(cudaMemcpyAsync(hi, lo + (size_t)nzl * pb, pb, cudaMemcpyDeviceToDevice, s));        // top -> halo 0
+    CUDA_TRY(cudaMemcpyAsync(lo + (size_t)(nzl + 1) * pb, hi + pb, pb, cudaMemcpyDeviceToDevice, s));  // bottom -> halo top
+  }
+  if (st->comm && st->comm->nranks > 1) {
+    const int R = st->comm->nranks, me = st->comm->rank;
+    char *bot = (char *)pick(st->slabs[0].pb[prec]);
+    char *top = (char *)pick(st->slabs[ns - 1].pb[prec]);
+    const int nzt = st->slabs[ns - 1].nz;
+    NCCL_TRY(g_nccl.GroupStart());
+    if (me > 0) {
+      NCCL_TRY(g_nccl.Send(bot + pb, pb, ncclUint8, me - 1, st->comm->comm, s));
+      NCCL_TRY(g_nccl.Recv(bot, pb, ncclUint8, me - 1, st->comm->comm, s));
+    }
+    if (me + 1 < R) {
+      NCCL_TRY(g_nccl.Send(top + (size_t)nzt * pb, pb, ncclUint8, me + 1, st->comm->comm, s));
+      NCCL_TRY(g_nccl.Recv(top + (size_t)(nzt + 1) * pb, pb, ncclUint8, me + 1, st->comm->comm, s));
+    }
+    NCCL_TRY(g_nccl.GroupEnd());
+  }
+  return STEN_OK;
+}
+
+// Decomposed solve: slab sums -> (NCCL fp32 all-reduce) -> scalar step.
+static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s) {
+  if (!decomposed(st)) return STEN_OK;
+  const int ns = (int)st->slabs.size();
+  if (st->comm && st->comm->nranks > 1) {
+    KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
+    NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
+    KLAUNCH(scalars_launch(phase, st->red_total, 1, st->st, s));
+    st->launches += 2;
+  } else {
+    KLAUNCH(scalars_launch(phase, st->slab_sums, ns, st->st, s));
+    st->launches += 1;
+  }
+  return STEN_OK;
+}
+
+// One BiCGStab iteration (Alg. 1 l.176-184); iteration parity selects the
+// ping-pong p/v buffers.  evs: optional [3][2] events around H1, H2, H3.
+static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
+  const int ns = (int)st->slabs.size();
+  const bool dec = decomposed(st);
+  // H1: halos of r (new from H3), p, v (new from the previous H1)
+  if (evs) CUDA_TRY(cudaEventRecord(evs[0], s));
+  if (dec) {
+    RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, s));
+    RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.p[parity]; }, s));
+    RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity]; }, s));
+  }
+  for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H1, k, parity, s));
+  RC_TRY(reduce_scalars(st, PH_H1, s));
+  if (evs) CUDA_TRY(cudaEventRecord(evs[1], s));
+  // H2: halo of the new v
+  if (evs) CUDA_TRY(cudaEventRecord(evs[2], s));
+  if (dec) RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity ^ 1]; }, s));
+  for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H2, k, parity, s));
+  RC_TRY(reduce_scalars(st, PH_H2, s));
+  if (evs) CUDA_TRY(cudaEventRecord(evs[3], s));
+  // H3
+  if (evs) CUDA_TRY(cudaEventRecord(evs[4], s));
+  for (int k = 0; k < ns; ++k) RC_TRY(launch_h3(st, prec, k, parity, s));
+  RC_TRY(reduce_scalars(st, PH_H3, s));
+  if (evs) CUDA_TRY(cudaEventRecord(evs[5], s));
+  return STEN_OK;
+}
+
+static int get_graph(sten_stencil *st, int prec, int chunk, GraphRec **out) {
+  GraphKey key{prec, chunk, st->timing ? 1 : 0};
+  auto it = st->graphs.find(key);
+  if (it != st->graphs.end()) {
+    *out = &it->second;
+    return STEN_OK;
+  }
+  GraphRec rec;
+  if (st->timing) {
+    rec.ev.resize((size_t)chunk * 6);
+    for (auto &e : rec.ev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  const long long l0 = st->launches;
+  CUDA_TRY(cudaStreamBeginCapture(st->cap, cudaStreamCaptureModeThreadLocal));
+  int rc = STEN_OK;
+  for (int j = 0; j < chunk && rc == STEN_OK; ++j)
+    rc = enqueue_iteration(st, prec, j & 1, st->cap, st->timing ? &rec.ev[(size_t)j * 6] : nullptr);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(st->cap, &g);
+  if (rc != STEN_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) return set_err(STEN_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&rec.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return set_err(STEN_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+  rec.kernels = st->launches - l0;
+  st->launches = l0;
+  auto ins = st->graphs.emplace(key, rec);
+  *out = &ins.first->second;
+  return STEN_OK;
+}
+
+static void drop_graphs(sten_stencil *st) {
+  for (auto &kv : st->graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    for (auto e : kv.second.ev) cudaEventDestroy(e);
+  }
+  st->graphs.clear();
+}
+
+// dense (nz,ny,nx) user array <-> pitched internal array with halo planes
+static int copy_in(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), const void *src, cudaStream_t s) {
+  const int e = esize(prec);
+  for (Slab &sl : st->slabs) {
+    char *dst = (char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
+    const char *sp = (const char *)src + (size_t)sl.z_first * st->nx * st->ny * e;
+    CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)st->pitch * e, sp, (size_t)st->nx * e, (size_t)st->nx * e,
+                               (size_t)st->ny * sl.nz, cudaMemcpyDefault, s));
+  }
+  return STEN_OK;
+}
+static int copy_out(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), void *dst, cudaStream_t s) {
+  const int e = esize(prec);
+  for (Slab &sl : st->slabs) {
+    const char *src = (const char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
+    char *dp = (char *)dst + (size_t)sl.z_first * st->nx * st->ny * e;
+    CUDA_TRY(cudaMemcpy2DAsync(dp, (size_t)st->nx * e, src, (size_t)st->pitch * e, (size_t)st->nx * e,
+                               (size_t)st->ny * sl.nz, cudaMemcpyDefault, s));
+  }
+  return STEN_OK;
+}
+static void *sel_x(PrecBufs &b) { return b.x; }
+static void *sel_s(PrecBufs &b) { return b.s; }
+static void *sel_t(PrecBufs &b) { return b.t; }
+static void *sel_bw(PrecBufs &b) { return b.bw; }
+
+// ============================================================== C ABI ==
+extern "C" {
+
+int sten_version(void) { return STEN_VERSION; }
+const char *sten_last_error(void) { return g_err.c_str(); }
+
+int sten_comm_unique_id(void *id_out) {
+  if (!id_out) return set_err(STEN_EINVAL, "id_out is NULL");
+  RC_TRY(nccl_load());
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.GetUniqueId(&id));
+  memcpy(id_out, &id, sizeof id);
+  return STEN_OK;
+}
+
+int sten_comm_create(const void *unique_id, int nranks, int rank, sten_comm **out) {
+  if (!unique_id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return set_err(STEN_EINVAL, "bad comm arguments (nranks=%d rank=%d)", nranks, rank);
+  RC_TRY(nccl_load());
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof id);
+  sten_comm *c = new sten_comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return set_err(STEN_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+  }
+  *out = c;
+  return STEN_OK;
+}
+
+void sten_comm_destroy(sten_comm *c) {
+  if (!c) return;
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  delete c;
+}
+
+static int is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype, int nslabs,
+                   sten_comm *comm, void *cuda_stream, sten_stencil **out) {
+  if (!out) return set_err(STEN_EINVAL, "out is NULL");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return set_err(STEN_EINVAL, "mesh %d x %d x %d must be positive", nx, ny, nz);
+  if (nslabs < 1 || nz % nslabs != 0) return set_err(STEN_EINVAL, "nz=%d not divisible into nslabs=%d", nz, nslabs);
+  if (!coeffs) return set_err(STEN_EINVAL, "coeffs is NULL");
+  for (int d = 1; d < 7; ++d)
+    if (!coeffs[d]) return set_err(STEN_EINVAL, "coeffs[%d] is NULL", d);
+  if (coeff_dtype != STEN_DT_F64 && coeff_dtype != STEN_DT_F32)
+    return set_err(STEN_EINVAL, "coeff_dtype %d unsupported", coeff_dtype);
+  if (nx > (1 << 20) || ny > (1 << 20)) return set_err(STEN_EINVAL, "nx, ny too large");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  sten_stencil *st = new sten_stencil;
+  st->nx = nx;
+  st->ny = ny;
+  st->nz = nz;
+  st->pitch = (nx + 7) / 8 * 8;
+  st->plane = (long long)st->pitch * ny;
+  st->nslabs = nslabs;
+  st->comm = comm;
+  st->has_diag = coeffs[0] != nullptr;
+  st->sm = device_sm_count();
+  st->slabs.resize(nslabs);
+  auto fail = [&](int rc) {
+    stencil_destroy(st);
+    return rc;
+  };
+  const int ein = coeff_dtype == STEN_DT_F64 ? 8 : 4;
+  const size_t nin = (size_t)nx * ny * nz;
+  // stage host inputs on the device
+  std::vector<void *> staged(7, nullptr);
+  const void *dev_in[7];
+  for (int d = 0; d < 7; ++d) {
+    dev_in[d] = coeffs[d];
+    if (coeffs[d] && !is_device_ptr(coeffs[d])) {
+      if (cudaMalloc(&staged[d], nin * ein) != cudaSuccess) {
+        for (void *p : staged) cudaFree(p);
+        return fail(set_err(STEN_ENOMEM, "staging coefficients failed"));
+      }
+      cudaMemcpyAsync(staged[d], coeffs[d], nin * ein, cudaMemcpyHostToDevice, s);
+      dev_in[d] = staged[d];
+    }
+  }
+  int rc = STEN_OK;
+  const int nzs = nz / nslabs;
+  const int R = comm ? comm->nranks : 1, me = comm ? comm->rank : 0;
+  for (int k = 0; k < nslabs && rc == STEN_OK; ++k) {
+    Slab &sl = st->slabs[k];
+    sl.nz = nzs;
+    sl.z_first = (long long)k * nzs;
+    const size_t cb32 = (size_t)st->plane * nzs * 4, cb16 = (size_t)st->plane * nzs * 2;
+    for (int d = 0; d < 6 && rc == STEN_OK; ++d) {
+      if (cudaMalloc(&sl.c32[d], cb32) != cudaSuccess || cudaMalloc(&sl.c16[d], cb16) != cudaSuccess)
+        rc = set_err(STEN_ENOMEM, "coefficient allocation failed");
+    }
+    if (rc == STEN_OK && st->has_diag && cudaMalloc(&sl.aP, (size_t)st->plane * nzs * 8) != cudaSuccess)
+      rc = set_err(STEN_ENOMEM, "diagonal allocation failed");
+    if (rc != STEN_OK) break;
+    const size_t soff = (size_t)sl.z_first * nx * ny * ein;
+    const void *off[6];
+    for (int d = 0; d < 6; ++d) off[d] = (const char *)dev_in[d + 1] + soff;
+    const void *dg = dev_in[0] ? (const char *)dev_in[0] + soff : nullptr;
+    Geom g{nx, ny, nzs, st->pitch, st->plane};
+    const int below = k > 0 || me > 0, above = k + 1 < nslabs || me + 1 < R;
+    int e = create_coeffs_launch(coeff_dtype, dg, off, g, below, above, sl.c32, sl.c16, sl.aP, s);
+    if (e) rc = set_err(STEN_ECUDA, "coefficient kernel: %s", cudaGetErrorString((cudaError_t)e));
+  }
+  if (rc == STEN_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = set_err(STEN_ECUDA, "stencil_create: %s", cudaGetErrorString(e));
+  }
+  for (void *p : staged)
+    if (p) cudaFree(p);
+  if (rc != STEN_OK) return fail(rc);
+  if (cudaMalloc(&st->st, sizeof(DevState)) != cudaSuccess ||
+      cudaMallocHost(&st->st_host, sizeof(DevState)) != cudaSuccess ||
+      cudaMalloc(&st->counter, sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc(&st->slab_sums, sizeof(float) * kMaxDots * nslabs) != cudaSuccess ||
+      cudaMalloc(&st->red_total, sizeof(float) * kMaxDots) != cudaSuccess)
+    return fail(set_err(STEN_ENOMEM, "state allocation failed"));
+  cudaMemset(st->counter, 0, sizeof(unsigned));
+  cudaMemset(st->st, 0, sizeof(DevState));
+  cudaMemset(st->slab_sums, 0, sizeof(float) * kMaxDots * nslabs);
+  cudaMemset(st->red_total, 0, sizeof(float) * kMaxDots);
+  if (cudaStreamCreateWithFlags(&st->cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&st->ev_a) != cudaSuccess || cudaEventCreate(&st->ev_b) != cudaSuccess)
+    return fail(set_err(STEN_ECUDA, "stream/event creation failed"));
+  *out = st;
+  return STEN_OK;
+}
+
+void stencil_destroy(sten_stencil *st) {
+  if (!st) return;
+  drop_graphs(st);
+  for (Slab &sl : st->slabs) {
+    for (int d = 0; d < 6; ++d) {
+      cudaFree(sl.c32[d]);
+      cudaFree(sl.c16[d]);
+    }
+    cudaFree(sl.aP);
+    for (PrecBufs &b : sl.pb) {
+      void *all[] = {b.x, b.r, b.rh, b.p[0], b.p[1], b.v[0], b.v[1], b.s, b.t, b.bw};
+      for (void *p : all) cudaFree(p);
+    }
+  }
+  cudaFree(st->st);
+  if (st->st_host) cudaFreeHost(st->st_host);
+  cudaFree(st->partials);
+  cudaFree(st->counter);
+  cudaFree(st->slab_sums);
+  cudaFree(st->red_total);
+  cudaFree(st->hist);
+  cudaFree(st->ahist);
+  cudaFree(st->whist);
+  if (st->cap) cudaStreamDestroy(st->cap);
+  if (st->ev_a) cudaEventDestroy(st->ev_a);
+  if (st->ev_b) cudaEventDestroy(st->ev_b);
+  delete st;
+}
+
+int sten_set_tiling(sten_stencil *st, int prec, int bx, int by, int zc, int stages) {
+  if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
+  if (st->slabs[0].pb[prec].ready == false && st->tiling[prec].bx == 0) default_tiling(st, prec);
+  Tiling t = st->tiling[prec];
+  const int vec = prec == STEN_FP32 ? 4 : 8, H = vec;
+  if (bx) t.bx = bx;
+  if (by) t.by = by;
+  if (zc) t.zc = zc;
+  if (stages) t.stages = stages;
+  if (t.bx % vec || t.bx <= 0 || t.bx + 2 * H > 256 || t.by <= 0 || t.by + 2 > 256 || t.zc <= 0 ||
+      t.stages < 2 || t.stages > 8)
+    return set_err(STEN_EINVAL, "invalid tiling bx=%d by=%d zc=%d stages=%d", t.bx, t.by, t.zc, t.stages);
+  size_t smem = prec == STEN_FP32 ? stencil_smem_bytes<float>(MODE_H1, t.bx, t.by, t.stages)
+                                  : stencil_smem_bytes<__half>(MODE_H1, t.bx, t.by, t.stages);
+  if (smem > 227 * 1024) return set_err(STEN_EINVAL, "tiling needs %zu B of shared memory", smem);
+  int vpr = t.bx / vec;
+  int th = (vpr * t.by + 31) / 32 * 32;
+  t.threads = th < 64 ? 64 : (th > 256 ? 256 : th);
+  st->tiling[prec] = t;
+  for (Slab &sl : st->slabs) sl.pb[prec].maps_ok = false;
+  drop_graphs(st);
+  if (st->slabs[0].pb[prec].ready) RC_TRY(ensure_bufs(st, prec));
+  return STEN_OK;
+}
+
+int sten_set_timing(sten_stencil *st, int enable) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  st->timing = enable != 0;
+  return STEN_OK;
+}
+
+int sten_get_stats(sten_stencil *st, sten_stats *out) {
+  if (!st || !out) return set_err(STEN_EINVAL, "NULL argument");
+  *out = st->stats;
+  return STEN_OK;
+}
+
+int stencil_apply(sten_stencil *st, int prec, const void *x, void *y, void *cuda_stream) {
+  if (!st || !x || !y) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  RC_TRY(ensure_bufs(st, prec));
+  st->launches = 0;
+  RC_TRY(copy_in(st, prec, sel_s, x, s));
+  if (decomposed(st)) RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.s; }, s));
+  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, prec, MODE_APPLY, k, 0, s));
+  RC_TRY(copy_out(st, prec, sel_t, y, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  return STEN_OK;
+}
+
+int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, double tol, int maxit, void *x_out,
+                   int *iters, double *res_hist, int *status, void *cuda_stream) {
+  if (!st || !b || !x_out || !iters || !res_hist || !status) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (!(tol >= 0.0) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  RC_TRY(ensure_bufs(st, prec));
+  if (maxit + 1 > st->hist_cap) {
+    cudaFree(st->hist);
+    cudaFree(st->ahist);
+    cudaFree(st->whist);
+    st->hist_cap = maxit + 1 < 64 ? 64 : maxit + 1;
+    CUDA_TRY(cudaMalloc(&st->hist, sizeof(double) * st->hist_cap));
+    CUDA_TRY(cudaMalloc(&st->ahist, sizeof(float) * st->hist_cap));
+    CUDA_TRY(cudaMalloc(&st->whist, sizeof(float) * st->hist_cap));
+  }
+  st->launches = 0;
+  memset(&st->stats, 0, sizeof st->stats);
+  CUDA_TRY(cudaEventRecord(st->ev_a, s));
+  // device state
+  DevState h;
+  memset(&h, 0, sizeof h);
+  h.tol = tol;
+  h.maxit = maxit;
+  h.status = -1;
+  h.ev = -1;
+  h.hist = st->hist;
+  h.ahist = st->ahist;
+  h.whist = st->whist;
+  *st->st_host = h;
+  CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
+  // S1: b_hat, r0, rhat, p0 (Alg. 1 l.174; R1, R3)
+  RC_TRY(copy_in(st, prec, sel_bw, b, s));
+  const bool with_x0 = x0 != nullptr;
+  if (with_x0) {
+    RC_TRY(copy_in(st, prec, sel_x, x0, s));
+    // A x0 through the apply path: input buffer s, output t
+    for (Slab &sl : st->slabs) {
+      const size_t vb = (size_t)st->plane * esize(prec);
+      CUDA_TRY(cudaMemcpyAsync((char *)sl.pb[prec].s + vb, (char *)sl.pb[prec].x + vb, vb * sl.nz,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    if (decomposed(st)) RC_TRY(exchange(st, prec, [](PrecBufs &bb) { return bb.s; }, s));
+    for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, prec, MODE_APPLY, k, 0, s));
+  } else {
+    for (Slab &sl : st->slabs) {
+      const size_t vb = (size_t)st->plane * esize(prec);
+      CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
+    }
+  }
+  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_init(st, prec, k, with_x0, s));
+  RC_TRY(reduce_scalars(st, PH_INIT, s));
+  // iterations: CUDA graphs of `chunk` iterations (even, so the ping-pong
+  // parity of p/v is the same at every replay)
+  long long kernels = 0;
+  double ph_ms[3] = {0, 0, 0};
+  long long ph_n[3] = {0, 0, 0};
+  int chunk = 0;
+  if (maxit > 0) {
+    chunk = tol > 0.0 ? 8 : ((maxit + 1) / 2) * 2;
+    if (chunk > 2048) chunk = 2048;
+    GraphRec *gr = nullptr;
+    RC_TRY(get_graph(st, prec, chunk, &gr));
+    const int nrep = (maxit + chunk - 1) / chunk;
+    for (int rep = 0; rep < nrep; ++rep) {
+      CUDA_TRY(cudaGraphLaunch(gr->exec, s));
+      kernels += gr->kernels;
+      const bool poll = tol > 0.0 || st->timing;
+      if (poll) {
+        CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (st->timing) {
+          const int done_it = st->st_host->it;
+          const int first = rep * chunk;
+          for (int j = 0; j < chunk; ++j) {
+            if (first + j >= done_it) break;  // later kernels were no-ops
+            for (int p = 0; p < 3; ++p) {
+              float ms = 0.f;
+              if (cudaEventElapsedTime(&ms, gr->ev[(size_t)j * 6 + 2 * p], gr->ev[(size_t)j * 6 + 2 * p + 1]) ==
+                  cudaSuccess) {
+                ph_ms[p] += ms;
+                ph_n[p] += 1;
+              }
+            }
+          }
+        }
+        if (st->st_host->stop || st->st_host->it >= maxit) break;
+      }
+    }
+  }
+  CUDA_TRY(cudaEventRecord(st->ev_b, s));
+  // results
+  CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  DevState fin = *st->st_host;
+  if (fin.zero_x)
+    for (Slab &sl : st->slabs) {
+      const size_t vb = (size_t)st->plane * esize(prec);
+      CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
+    }
+  RC_TRY(copy_out(st, prec, sel_x, x_out, s));
+  CUDA_TRY(cudaMemcpyAsync(res_hist, st->hist, sizeof(double) * (fin.it + 1), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  *iters = fin.it;
+  *status = fin.stop ? fin.status : (fin.ev >= 0 ? fin.ev : STEN_MAXIT);
+  float solve_ms = 0.f;
+  cudaEventElapsedTime(&solve_ms, st->ev_a, st->ev_b);
+  st->stats.solve_ms = solve_ms;
+  for (int p = 0; p < 3; ++p) {
+    st->stats.phase_ms[p] = ph_ms[p];
+    st->stats.phase_launches[p] = ph_n[p];
+  }
+  st->stats.kernel_launches = st->launches + kernels;
+  st->stats.event_iter = fin.ev >= 0 ? fin.ev_it : 0;
+  st->stats.graph_chunk = chunk;
+  return STEN_OK;
+}
+
+int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega) {
+  if (!st || n < 0 || (n > 0 && (!alpha || !omega))) return set_err(STEN_EINVAL, "bad arguments");
+  if (n + 1 > st->hist_cap) return set_err(STEN_EINVAL, "n=%d exceeds the last solve", n);
+  std::vector<float> a(n + 1), w(n + 1);
+  CUDA_TRY(cudaMemcpy(a.data(), st->ahist, sizeof(float) * (n + 1), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(w.data(), st->whist, sizeof(float) * (n + 1), cudaMemcpyDeviceToHost));
+  for (int i = 1; i <= n; ++i) {
+    alpha[i - 1] = a[i];
+    omega[i - 1] = w[i];
+  }
+  return STEN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,415 @@
+// kernels.cu - sm_100a kernels of the BiCGStab hot path.
+//
+//  k_stencil<T, MODE>: the matrix-free 7-point SpMV u = A v with unit diagonal
+//    (PAPER.md:198-201, 338-346), z-marching over a CTA's xy tile.  Each z-plane
+//    of every operand arrives in shared memory by TMA (cp.async.bulk.tensor,
+//    zero-filled outside the mesh) through an S-stage mbarrier ring; the SpMV
+//    input is formed in shared memory from the staged operands (fused AXPYs),
+//    the three planes k-1, k, k+1 of it are kept in a shared ring, and the
+//    result is written with 16-byte stores while the dot products that follow
+//    it in Algorithm 1 are accumulated in registers:
+//      MODE_APPLY: y = A x
+//      MODE_H1   : p' = r + beta (p - omega v)  (l.184), v' = A p' (l.176),
+//                  sigma = (rhat, v')                      (l.177)
+//      MODE_H2   : s = r - alpha v (l.178), t = A s (l.179), (t,s), (t,t) (l.180)
+//  k_h3<T>: x += alpha p + omega s (l.181), r = s - omega t (l.182),
+//           (rhat, r), (r, r) (l.183 and the stopping rule R4)
+//  k_init<T>: b_hat = b / a_P (R3), r0 = b_hat - A x0 (R1), rhat = p = r0, v = 0
+//  k_create_coeffs: Jacobi scaling c_d = A_d / a_P in fp64, rounded to fp32 and
+//    fp16 (R3, R5).
+#include "sten_internal.cuh"
+
+namespace sten {
+
+static __host__ __device__ __forceinline__ int align128(int b) { return (b + 127) & ~127; }
+
+template <typename T>
+struct TileLayout {
+  static constexpr int VEC = Pack<T>::VEC;
+  static constexpr int H = VEC;  // x halo pad, keeps every 16-byte vector aligned
+  int hw, hbox, ibox, hbytes, ibytes, stage_bytes;
+  __host__ __device__ TileLayout(int mode, int bx, int by) {
+    const int nin = mode == MODE_H1 ? 3 : (mode == MODE_H2 ? 2 : 1);
+    const int nint = 6 + (mode == MODE_H1 ? 1 : 0);
+    hw = bx + 2 * H;
+    hbox = hw * (by + 2);
+    ibox = bx * by;
+    hbytes = align128(hbox * (int)sizeof(T));
+    ibytes = align128(ibox * (int)sizeof(T));
+    stage_bytes = nin * hbytes + nint * ibytes;
+  }
+};
+
+template <typename T>
+size_t stencil_smem_bytes(int mode, int bx, int by, int stages) {
+  TileLayout<T> L(mode, bx, by);
+  return 128 /* mbarriers */ + (size_t)stages * L.stage_bytes + 3 * (size_t)L.hbytes + 32 * kMaxDots * 4;
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ StencilArgs a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  constexpr int H = VEC;
+  constexpr int NIN = MODE == MODE_H1 ? 3 : (MODE == MODE_H2 ? 2 : 1);
+  constexpr int NINT = 6 + (MODE == MODE_H1 ? 1 : 0);
+  constexpr int ND = MODE == MODE_H1 ? 1 : (MODE == MODE_H2 ? 2 : 1);
+
+  if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
+
+  const TileLayout<T> L(MODE, a.bx, a.by);
+  const int S = a.stages;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);
+  unsigned char *stage0 = smem + 128;
+  T *U = reinterpret_cast<T *>(stage0 + S * L.stage_bytes);
+  const int ustride = L.hbytes / (int)sizeof(T);
+  float *scratch = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(U) + 3 * L.hbytes);
+
+  int b = blockIdx.x;
+  const int tx = b % a.tiles_x;
+  b /= a.tiles_x;
+  const int ty = b % a.tiles_y;
+  const int ch = b / a.tiles_y;
+  const int x0 = tx * a.bx, y0 = ty * a.by;
+  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int np = z1 - z0 + 2;  // planes z0-1 .. z1 (halo planes included)
+  const int tid = threadIdx.x, nthr = blockDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+    for (int i = 0; i < NIN; ++i) prefetch_tmap(&a.tm_in[i]);
+  }
+  __syncthreads();
+
+  // ---- producer: one thread issues every TMA of a plane ----
+  auto issue = [&](int q) {
+    const int s = q % S, p = z0 - 1 + q;
+    unsigned char *base = stage0 + s * L.stage_bytes;
+    const bool interior = (p >= z0 && p < z1);
+    uint32_t bytes = NIN * L.hbox * (uint32_t)sizeof(T) + (interior ? NINT * L.ibox * (uint32_t)sizeof(T) : 0u);
+    mbar_expect_tx(&mbar[s], bytes);
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) tma_load_3d(base + i * L.hbytes, &a.tm_in[i], x0 - H, y0 - 1, p + 1, &mbar[s]);
+    if (interior) {
+#pragma unroll
+      for (int d = 0; d < 6; ++d)
+        tma_load_3d(base + NIN * L.hbytes + d * L.ibytes, &a.tm_c[d], x0, y0, p, &mbar[s]);
+      if (MODE == MODE_H1) tma_load_3d(base + NIN * L.hbytes + 6 * L.ibytes, &a.tm_aux, x0, y0, p + 1, &mbar[s]);
+    }
+  };
+  auto wait = [&](int q) { mbar_wait(&mbar[q % S], (uint32_t)((q / S) & 1)); };
+
+  // scalars of the fused AXPYs (fp16: rounded to nearest, R11)
+  typename P::S beta_s{}, momega_s{}, malpha_s{};
+  if (MODE == MODE_H1) {
+    beta_s = P::scalar(a.red.st->beta);
+    momega_s = P::neg(P::scalar(a.red.st->omega));
+  } else if (MODE == MODE_H2) {
+    malpha_s = P::neg(P::scalar(a.red.st->alpha));
+  }
+
+  // ---- SpMV input of plane q over the whole halo box, into the U ring ----
+  auto compute_u = [&](int q) {
+    const T *in = reinterpret_cast<const T *>(stage0 + (q % S) * L.stage_bytes);
+    const int istr = L.hbytes / (int)sizeof(T);
+    T *u = U + (q % 3) * ustride;
+    const int nvec = L.hbox / VEC;
+    for (int v = tid; v < nvec; v += nthr) {
+      const int off = v * VEC;
+      P out = P::ld(in + off);
+      if (MODE == MODE_H1) {  // p' = r + beta (p - omega v)
+        P pp = P::ld(in + istr + off), vv = P::ld(in + 2 * istr + off);
+        out = P::fmas(beta_s, P::fmas(momega_s, vv, pp), out);
+      } else if (MODE == MODE_H2) {  // s = r - alpha v
+        P vv = P::ld(in + istr + off);
+        out = P::fmas(malpha_s, vv, out);
+      }
+      out.st(u + off);
+    }
+  };
+
+  if (tid == 0)
+    for (int q = 0; q < min(S, np); ++q) issue(q);
+  wait(0);
+  compute_u(0);
+  wait(1);
+  compute_u(1);
+  __syncthreads();
+  if (tid == 0 && S < np) issue(S);  // slot of plane z0-1 is free
+
+  float dacc[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) dacc[d] = 0.0f;
+  const int vpr = a.bx / VEC;
+  const int nout = vpr * a.by;
+  const int istride = L.ibytes / (int)sizeof(T);
+
+  for (int k = z0; k < z1; ++k) {
+    const int qk = k - z0 + 1, qn = qk + 1;
+    wait(qn);
+    compute_u(qn);
+    __syncthreads();
+    const T *cb = reinterpret_cast<const T *>(stage0 + (qk % S) * L.stage_bytes + NIN * L.hbytes);
+    const T *Um = U + ((qk - 1) % 3) * ustride;
+    const T *Uc = U + (qk % 3) * ustride;
+    const T *Up = U + (qn % 3) * ustride;
+    for (int o = tid; o < nout; o += nthr) {
+      const int ry = o / vpr, cx = o - ry * vpr;
+      const int h = (ry + 1) * L.hw + H + cx * VEC;
+      const int io = ry * a.bx + cx * VEC;
+      const P c = P::ld(Uc + h);
+      P acc = c;  // unit diagonal: no multiply
+      acc = P::fma(P::ld(cb + 0 * istride + io), P::shl(P::ld(Uc + h - VEC), c), acc);  // xm
+      acc = P::fma(P::ld(cb + 1 * istride + io), P::shr(c, P::ld(Uc + h + VEC)), acc);  // xp
+      acc = P::fma(P::ld(cb + 2 * istride + io), P::ld(Uc + h - L.hw), acc);            // ym
+      acc = P::fma(P::ld(cb + 3 * istride + io), P::ld(Uc + h + L.hw), acc);            // yp
+      acc = P::fma(P::ld(cb + 4 * istride + io), P::ld(Um + h), acc);                   // zm
+      acc = P::fma(P::ld(cb + 5 * istride + io), P::ld(Up + h), acc);                   // zp
+      const int gy = y0 + ry, gx = x0 + cx * VEC;
+      if (gy < a.g.ny && gx < a.g.pitch) {
+        const long long gi = (long long)(k + 1) * a.g.plane + (long long)gy * a.g.pitch + gx;
+        acc.st(reinterpret_cast<T *>(a.out0) + gi);
+        if (MODE != MODE_APPLY) c.st(reinterpret_cast<T *>(a.out1) + gi);
+      }
+      if (MODE == MODE_H1) {
+        dacc[0] = P::ld(cb + 6 * istride + io).dot(acc, dacc[0]);  // (rhat, v')
+      } else if (MODE == MODE_H2) {
+        dacc[0] = acc.dot(c, dacc[0]);                          // (t, s)
+        dacc[ND - 1] = acc.dot(acc, dacc[ND - 1]);              // (t, t)
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && qk + S < np) issue(qk + S);
+  }
+
+  if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(dacc, a.red, scratch);
+  else if (MODE == MODE_H2) grid_reduce_finalize<ND, PH_H2>(dacc, a.red, scratch);
+}
+
+template <typename T>
+int stencil_launch(int mode, const StencilArgs &a, int threads, size_t smem, cudaStream_t s) {
+  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  void (*fn)(StencilArgs) = mode == MODE_H1 ? k_stencil<T, MODE_H1>
+                            : mode == MODE_H2 ? k_stencil<T, MODE_H2>
+                                              : k_stencil<T, MODE_APPLY>;
+  static size_t configured[3] = {0, 0, 0};
+  if (configured[mode] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured[mode] = smem;
+  }
+  fn<<<grid, threads, smem, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ H3 --
+template <typename T>
+__global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  __shared__ float scratch[32 * kMaxDots];
+  if (st_idle(a.red.st)) return;
+  const typename P::S as = P::scalar(a.red.st->alpha);
+  const typename P::S ws = P::scalar(a.red.st->omega);
+  const typename P::S mws = P::neg(ws);
+  const T *__restrict__ X = reinterpret_cast<const T *>(a.x);
+  const T *__restrict__ Pp = reinterpret_cast<const T *>(a.p);
+  const T *__restrict__ Sv = reinterpret_cast<const T *>(a.s);
+  const T *__restrict__ Tv = reinterpret_cast<const T *>(a.t);
+  const T *__restrict__ Rh = reinterpret_cast<const T *>(a.rhat);
+  T *__restrict__ XO = reinterpret_cast<T *>(a.xo);
+  T *__restrict__ RO = reinterpret_cast<T *>(a.ro);
+  float d[2] = {0.0f, 0.0f};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // two vectors per thread per trip: all ten loads issued before any math
+  for (; v + stride < a.nvec; v += 2 * stride) {
+    const long long o0 = v * VEC, o1 = (v + stride) * VEC;
+    P x0 = P::ldg(X + o0), p0 = P::ldg(Pp + o0), s0 = P::ldg(Sv + o0), t0 = P::ldg(Tv + o0), r0 = P::ldg(Rh + o0);
+    P x1 = P::ldg(X + o1), p1 = P::ldg(Pp + o1), s1 = P::ldg(Sv + o1), t1 = P::ldg(Tv + o1), r1 = P::ldg(Rh + o1);
+    P xn0 = P::fmas(ws, s0, P::fmas(as, p0, x0)), rn0 = P::fmas(mws, t0, s0);
+    P xn1 = P::fmas(ws, s1, P::fmas(as, p1, x1)), rn1 = P::fmas(mws, t1, s1);
+    xn0.st(XO + o0);
+    rn0.st(RO + o0);
+    xn1.st(XO + o1);
+    rn1.st(RO + o1);
+    d[0] = r0.dot(rn0, d[0]);
+    d[1] = rn0.dot(rn0, d[1]);
+    d[0] = r1.dot(rn1, d[0]);
+    d[1] = rn1.dot(rn1, d[1]);
+  }
+  if (v < a.nvec) {
+    const long long o0 = v * VEC;
+    P x0 = P::ldg(X + o0), p0 = P::ldg(Pp + o0), s0 = P::ldg(Sv + o0), t0 = P::ldg(Tv + o0), r0 = P::ldg(Rh + o0);
+    P xn0 = P::fmas(ws, s0, P::fmas(as, p0, x0)), rn0 = P::fmas(mws, t0, s0);
+    xn0.st(XO + o0);
+    rn0.st(RO + o0);
+    d[0] = r0.dot(rn0, d[0]);
+    d[1] = rn0.dot(rn0, d[1]);
+  }
+  grid_reduce_finalize<2, PH_H3>(d, a.red, scratch);
+}
+
+template <typename T>
+int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
+  k_h3<T><<<grid, threads, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- INIT --
+template <typename T> __device__ __forceinline__ T round_from_double(double x);
+template <> __device__ __forceinline__ float round_from_double<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ __half round_from_double<__half>(double x) { return __double2half(x); }
+template <typename T> __device__ __forceinline__ double widen(T x);
+template <> __device__ __forceinline__ double widen<float>(float x) { return (double)x; }
+template <> __device__ __forceinline__ double widen<__half>(__half x) { return (double)__half2float(x); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_init(const __grid_constant__ EwArgs a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  __shared__ float scratch[32 * kMaxDots];
+  const T *__restrict__ B = reinterpret_cast<const T *>(a.bw);
+  const T *__restrict__ AX = reinterpret_cast<const T *>(a.ax);
+  T *R = reinterpret_cast<T *>(a.r);
+  T *RH = reinterpret_cast<T *>(a.rh);
+  T *P0 = reinterpret_cast<T *>(a.p0);
+  T *V0 = reinterpret_cast<T *>(a.v0);
+  float d[3] = {0.0f, 0.0f, 0.0f};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.nvec; v += stride) {
+    const long long o = v * VEC;
+    P bh = P::ld(B + o);
+    if (a.aP) {  // b_hat = rn(b / a_P) in fp64 (R3)
+      T e[VEC];
+      *reinterpret_cast<P *>(e) = bh;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) e[i] = round_from_double<T>(widen<T>(e[i]) / a.aP[o + i]);
+      bh = *reinterpret_cast<P *>(e);
+    }
+    P r = AX ? P::sub(bh, P::ld(AX + o)) : bh;
+    r.st(R + o);
+    r.st(RH + o);
+    r.st(P0 + o);
+    P::zero().st(V0 + o);
+    d[0] = r.dot(r, d[0]);    // rho = (rhat, r0), rhat = r0
+    d[1] = bh.dot(bh, d[1]);  // (b_hat, b_hat)
+    d[2] = r.dot(r, d[2]);    // (r0, r0)
+  }
+  grid_reduce_finalize<3, PH_INIT>(d, a.red, scratch);
+}
+
+template <typename T>
+int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
+  k_init<T><<<grid, threads, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------- cross-slab scalar step --
+__global__ void k_scalars(int phase, const float *__restrict__ slab_sums, int nslabs, DevState *st) {
+  if (phase != PH_INIT && st_idle(st)) return;
+  float s[kMaxDots] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < nslabs; ++k)  // fixed slab order: deterministic
+    for (int d = 0; d < kMaxDots; ++d) s[d] += slab_sums[k * kMaxDots + d];
+  switch (phase) {
+    case PH_INIT: finalize_phase<PH_INIT>(st, s); break;
+    case PH_H1: finalize_phase<PH_H1>(st, s); break;
+    case PH_H2: finalize_phase<PH_H2>(st, s); break;
+    default: finalize_phase<PH_H3>(st, s); break;
+  }
+}
+
+__global__ void k_slabsum(const float *__restrict__ slab_sums, int nslabs, float *out) {
+  float s[kMaxDots] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < nslabs; ++k)
+    for (int d = 0; d < kMaxDots; ++d) s[d] += slab_sums[k * kMaxDots + d];
+  for (int d = 0; d < kMaxDots; ++d) out[d] = s[d];
+}
+
+int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s) {
+  k_scalars<<<1, 1, 0, s>>>(phase, slab_sums, nslabs, st);
+  return (int)cudaGetLastError();
+}
+int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s) {
+  k_slabsum<<<1, 1, 0, s>>>(slab_sums, nslabs, out);
+  return (int)cudaGetLastError();
+}
+
+// -------------------------------------------------- Jacobi scaling (S0) --
+template <typename TIN>
+__global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, const TIN *o1, const TIN *o2,
+                                const TIN *o3, const TIN *o4, const TIN *o5, Geom g, int has_below,
+                                int has_above, float *c32_0, float *c32_1, float *c32_2, float *c32_3,
+                                float *c32_4, float *c32_5, __half *c16_0, __half *c16_1, __half *c16_2,
+                                __half *c16_3, __half *c16_4, __half *c16_5, double *aP) {
+  const TIN *off[6] = {o0, o1, o2, o3, o4, o5};
+  float *c32[6] = {c32_0, c32_1, c32_2, c32_3, c32_4, c32_5};
+  __half *c16[6] = {c16_0, c16_1, c16_2, c16_3, c16_4, c16_5};
+  const long long total = (long long)g.pitch * g.ny * g.nz;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(q % g.pitch);
+    const long long rest = q / g.pitch;
+    const int y = (int)(rest % g.ny), z = (int)(rest / g.ny);
+    if (x >= g.nx) {  // row padding: zero couplings, unit diagonal
+      for (int d = 0; d < 6; ++d) {
+        c32[d][q] = 0.0f;
+        c16[d][q] = __float2half(0.0f);
+      }
+      if (aP) aP[q] = 1.0;
+      continue;
+    }
+    const long long P = x + (long long)g.nx * (y + (long long)g.ny * z);
+    const bool inside[6] = {x > 0, x + 1 < g.nx, y > 0, y + 1 < g.ny, z > 0 || has_below != 0,
+                            z + 1 < g.nz || has_above != 0};
+    const double dP = diag ? (double)diag[P] : 1.0;
+    for (int d = 0; d < 6; ++d) {
+      double c = 0.0;  // R5: couplings leaving the mesh are dropped
+      if (inside[d]) c = diag ? __ddiv_rn((double)off[d][P], dP) : (double)off[d][P];
+      c32[d][q] = __double2float_rn(c);
+      c16[d][q] = __double2half(c);
+    }
+    if (aP) aP[q] = dP;
+  }
+}
+
+int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g, int has_below,
+                         int has_above, float *const c32[6], __half *const c16[6], double *aP,
+                         cudaStream_t s) {
+  const long long total = (long long)g.pitch * g.ny * g.nz;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 32) grid = 148 * 32;
+  if (grid < 1) grid = 1;
+  if (in_dtype == STEN_DT_F64) {
+    const double *const *o = reinterpret_cast<const double *const *>(off);
+    k_create_coeffs<double><<<grid, 256, 0, s>>>((const double *)diag, o[0], o[1], o[2], o[3], o[4], o[5], g,
+                                                 has_below, has_above, c32[0], c32[1], c32[2], c32[3], c32[4],
+                                                 c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP);
+  } else {
+    const float *const *o = reinterpret_cast<const float *const *>(off);
+    k_create_coeffs<float><<<grid, 256, 0, s>>>((const float *)diag, o[0], o[1], o[2], o[3], o[4], o[5], g,
+                                                has_below, has_above, c32[0], c32[1], c32[2], c32[3], c32[4],
+                                                c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP);
+  }
+  return (int)cudaGetLastError();
+}
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+template int stencil_launch<float>(int, const StencilArgs &, int, size_t, cudaStream_t);
+template int stencil_launch<__half>(int, const StencilArgs &, int, size_t, cudaStream_t);
+template size_t stencil_smem_bytes<float>(int, int, int, int);
+template size_t stencil_smem_bytes<__half>(int, int, int, int);
+template int h3_launch<float>(const EwArgs &, int, int, cudaStream_t);
+template int h3_launch<__half>(const EwArgs &, int, int, cudaStream_t);
+template int init_launch<float>(const EwArgs &, int, int, cudaStream_t);
+template int init_launch<__half>(const EwArgs &, int, int, cudaStream_t);
+
+}  // namespace sten

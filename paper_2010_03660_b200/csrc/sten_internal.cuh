@@ -1,0 +1,396 @@
+// sten_internal.cuh - shared definitions of libsten.so (B200 / sm_100a).
+//
+// Device-side solver state, packed fp32x4 / fp16x8 vectors, TMA + mbarrier
+// PTX wrappers, block/grid reductions and the scalar steps of Algorithm 1
+// (PAPER.md:176-184).  Nothing here is shared with oracle/ (R13 in DESIGN.md).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sten.h"
+
+namespace sten {
+
+// ----------------------------------------------------------------------------
+// Solver state living in device memory.  Written only by single-thread
+// finalize code (last CTA of a reduction or the scalar kernel), read by every
+// kernel of the next phase in stream order.
+struct DevState {
+  float rho, alpha, omega, beta;   // current BiCGStab scalars (fp32, R12)
+  double nb;                       // ||b_hat||_2
+  double tol;                      // stopping tolerance (0 = benchmark mode)
+  int it;                          // completed iterations
+  int maxit;
+  int stop;                        // 1: later phases are no-ops
+  int status;                      // STEN_* status when stop == 1
+  int ev;                          // first event code (-1: none)
+  int ev_it;                       // iteration of the first event
+  int zero_x;                      // b_hat == 0: x must be returned as 0
+  int pad_;
+  double *hist;                    // [maxit+1] ||r_i|| / ||b_hat||
+  float *ahist, *whist;            // [maxit+1] alpha_i, omega_i
+};
+
+enum Phase { PH_INIT = 0, PH_H1 = 1, PH_H2 = 2, PH_H3 = 3 };
+enum Mode { MODE_APPLY = 0, MODE_H1 = 1, MODE_H2 = 2 };
+constexpr int kMaxDots = 3;
+
+// Grid reduction plumbing of one kernel launch.
+struct Reduce {
+  float *partials;      // [gridDim.x * kMaxDots]
+  unsigned *counter;    // zero between launches (reset by the last CTA)
+  float *slab_out;      // decomposed solve: write the slab's sums here ...
+  DevState *st;         // ... else finalize the scalars directly
+};
+
+// Geometry of one z-slab in the internal layout: planes 0 and nz+1 are the
+// halo planes, rows have `pitch` elements (pitch % 8 == 0, x >= nx padded
+// with zeros).  Coefficient arrays use the same rows but no halo planes.
+struct Geom {
+  int nx, ny, nz, pitch;
+  long long plane;      // pitch * ny elements
+};
+
+// Arguments of the TMA z-march stencil kernel.
+struct alignas(64) StencilArgs {
+  CUtensorMap tm_in[3];   // halo'd inputs: box (bx+2H) x (by+2) x 1
+  CUtensorMap tm_c[6];    // coefficients xm,xp,ym,yp,zm,zp: box bx x by x 1
+  CUtensorMap tm_aux;     // rhat (H1): box bx x by x 1
+  void *out0;             // APPLY: y   H1: v_new   H2: t
+  void *out1;             // H1: p_new  H2: s
+  Geom g;
+  int bx, by, zc, tiles_x, tiles_y, stages;
+  Reduce red;
+};
+
+struct EwArgs {           // element-wise kernels (H3, INIT)
+  const void *x, *p, *s, *t, *rhat;   // H3 inputs
+  void *xo, *ro;                       // H3 outputs
+  const void *bw; const double *aP; const void *ax; // INIT inputs (ax = A x0 or null)
+  void *r, *rh, *p0, *v0;              // INIT outputs
+  long long nvec;                      // vectors of VEC elements (interior range)
+  Reduce red;
+};
+
+// ---------------------------------------------------------------- packs --
+template <typename T> struct Pack;
+
+template <> struct Pack<float> {
+  static constexpr int VEC = 4;
+  float v[4];
+  using S = float;
+  static __device__ __forceinline__ Pack ld(const float *p) {
+    float4 q = *reinterpret_cast<const float4 *>(p);
+    return Pack{{q.x, q.y, q.z, q.w}};
+  }
+  static __device__ __forceinline__ Pack ldg(const float *p) {
+    float4 q = __ldcs(reinterpret_cast<const float4 *>(p));
+    return Pack{{q.x, q.y, q.z, q.w}};
+  }
+  __device__ __forceinline__ void st(float *p) const {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  static __device__ __forceinline__ Pack zero() { return Pack{{0.f, 0.f, 0.f, 0.f}}; }
+  // neighbour at x-1 of each lane: (l3, c0, c1, c2); at x+1: (c1, c2, c3, r0)
+  static __device__ __forceinline__ Pack shl(const Pack &l, const Pack &c) {
+    return Pack{{l.v[3], c.v[0], c.v[1], c.v[2]}};
+  }
+  static __device__ __forceinline__ Pack shr(const Pack &c, const Pack &r) {
+    return Pack{{c.v[1], c.v[2], c.v[3], r.v[0]}};
+  }
+  static __device__ __forceinline__ Pack fma(const Pack &a, const Pack &b, const Pack &c) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.v[i] = __fmaf_rn(a.v[i], b.v[i], c.v[i]);
+    return o;
+  }
+  static __device__ __forceinline__ S scalar(float a) { return a; }
+  static __device__ __forceinline__ S neg(S a) { return -a; }
+  static __device__ __forceinline__ Pack fmas(S a, const Pack &b, const Pack &c) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.v[i] = __fmaf_rn(a, b.v[i], c.v[i]);
+    return o;
+  }
+  static __device__ __forceinline__ Pack sub(const Pack &a, const Pack &b) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.v[i] = __fsub_rn(a.v[i], b.v[i]);
+    return o;
+  }
+  // acc += a_i * b_i in lane order, fp32 FMA
+  __device__ __forceinline__ float dot(const Pack &b, float acc) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc = __fmaf_rn(v[i], b.v[i], acc);
+    return acc;
+  }
+};
+
+template <> struct Pack<__half> {
+  static constexpr int VEC = 8;
+  uint32_t w[4];  // 4 x half2, lane 2i in the low half of w[i]
+  using S = __half2;
+  static __device__ __forceinline__ Pack ld(const __half *p) {
+    uint4 q = *reinterpret_cast<const uint4 *>(p);
+    return Pack{{q.x, q.y, q.z, q.w}};
+  }
+  static __device__ __forceinline__ Pack ldg(const __half *p) {
+    uint4 q = __ldcs(reinterpret_cast<const uint4 *>(p));
+    return Pack{{q.x, q.y, q.z, q.w}};
+  }
+  __device__ __forceinline__ void st(__half *p) const {
+    *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  static __device__ __forceinline__ Pack zero() { return Pack{{0u, 0u, 0u, 0u}}; }
+  // x-1 neighbour of lanes (2i, 2i+1) = (lane 2i-1, lane 2i): low <- prev.hi, high <- cur.lo
+  static __device__ __forceinline__ Pack shl(const Pack &l, const Pack &c) {
+    return Pack{{__byte_perm(l.w[3], c.w[0], 0x5432), __byte_perm(c.w[0], c.w[1], 0x5432),
+                 __byte_perm(c.w[1], c.w[2], 0x5432), __byte_perm(c.w[2], c.w[3], 0x5432)}};
+  }
+  static __device__ __forceinline__ Pack shr(const Pack &c, const Pack &r) {
+    return Pack{{__byte_perm(c.w[0], c.w[1], 0x5432), __byte_perm(c.w[1], c.w[2], 0x5432),
+                 __byte_perm(c.w[2], c.w[3], 0x5432), __byte_perm(c.w[3], r.w[0], 0x5432)}};
+  }
+  static __device__ __forceinline__ __half2 h2(uint32_t u) { return *reinterpret_cast<const __half2 *>(&u); }
+  static __device__ __forceinline__ uint32_t u32(__half2 h) { return *reinterpret_cast<const uint32_t *>(&h); }
+  static __device__ __forceinline__ Pack fma(const Pack &a, const Pack &b, const Pack &c) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.w[i] = u32(__hfma2(h2(a.w[i]), h2(b.w[i]), h2(c.w[i])));
+    return o;
+  }
+  static __device__ __forceinline__ S scalar(float a) { return __float2half2_rn(a); }
+  static __device__ __forceinline__ S neg(S a) { return __hneg2(a); }
+  static __device__ __forceinline__ Pack fmas(S a, const Pack &b, const Pack &c) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.w[i] = u32(__hfma2(a, h2(b.w[i]), h2(c.w[i])));
+    return o;
+  }
+  static __device__ __forceinline__ Pack sub(const Pack &a, const Pack &b) {
+    Pack o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.w[i] = u32(__hsub2(h2(a.w[i]), h2(b.w[i])));
+    return o;
+  }
+  // fp16 x fp16 products are exact in fp32; accumulate in fp32
+  __device__ __forceinline__ float dot(const Pack &b, float acc) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 x = __half22float2(h2(w[i])), y = __half22float2(h2(b.w[i]));
+      acc = __fmaf_rn(x.x, y.x, acc);
+      acc = __fmaf_rn(x.y, y.y, acc);
+    }
+    return acc;
+  }
+};
+
+// ------------------------------------------------------------- PTX: TMA --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ------------------------------------------------------------ reductions --
+// Deterministic: fixed shuffle tree, fixed warp order.  Result valid in thread 0.
+template <int ND>
+__device__ __forceinline__ void block_sum(float (&v)[ND], float *scratch) {
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[d] += __shfl_xor_sync(0xffffffffu, v[d], o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();  // scratch may still be read by a previous call
+  if (lane == 0)
+#pragma unroll
+    for (int d = 0; d < ND; ++d) scratch[warp * ND + d] = v[d];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      float x = lane < nw ? scratch[lane * ND + d] : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      v[d] = x;
+    }
+  }
+}
+
+// ------------------------------------------------ Algorithm 1 scalar steps --
+// R6-R8 of DESIGN.md.  Run by ONE thread.
+__device__ __forceinline__ void st_event(DevState *st, int code, int i, bool before_update) {
+  if (st->ev < 0) {
+    st->ev = code;
+    st->ev_it = i;
+  }
+  if (st->tol > 0.0) {
+    st->stop = 1;
+    st->status = code;
+    (void)before_update;  // `it` is only advanced by the H3 step
+  }
+}
+
+// S1: rho = (rhat, r0), ||b_hat||, hist[0]  (Alg. 1 l.174)
+__device__ __forceinline__ void fin_init(DevState *st, float rho, float bb, float rr) {
+  st->rho = rho;
+  st->alpha = 0.f;
+  st->omega = 0.f;
+  st->beta = 0.f;  // first H1 then computes p = r exactly (p_0 := r_0)
+  double nb = sqrt((double)bb);
+  st->nb = nb;
+  if (nb == 0.0) {
+    st->hist[0] = 0.0;
+    st->zero_x = 1;
+    st->stop = 1;
+    st->status = STEN_CONVERGED;
+    return;
+  }
+  double h0 = sqrt((double)rr) / nb;
+  st->hist[0] = h0;
+  if (st->tol > 0.0 && h0 <= st->tol) {
+    st->stop = 1;
+    st->status = STEN_CONVERGED;
+  }
+}
+
+// H1: alpha_i = rho_i / (rhat, s_i)   (l.177)
+__device__ __forceinline__ void fin_h1(DevState *st, float sigma) {
+  int i = st->it + 1;
+  float alpha = st->rho / sigma;
+  if (sigma == 0.0f || !isfinite(alpha)) {
+    alpha = 0.0f;
+    st_event(st, isfinite(sigma) ? STEN_BREAKDOWN : STEN_NONFINITE, i, true);
+  }
+  st->alpha = alpha;
+  st->ahist[i] = alpha;
+}
+
+// H2: omega_i = (q_i, y_i) / (y_i, y_i)   (l.180)
+__device__ __forceinline__ void fin_h2(DevState *st, float ts, float tt) {
+  int i = st->it + 1;
+  float omega = 0.0f;  // tt == 0: s == 0, x += alpha p is exact (R8)
+  if (tt != 0.0f) {
+    omega = ts / tt;
+    if (!isfinite(omega)) {
+      omega = 0.0f;
+      st_event(st, STEN_NONFINITE, i, true);
+    }
+  }
+  st->omega = omega;
+  st->whist[i] = omega;
+}
+
+// H3: residual history, beta_i = (alpha/omega) (rhat,r_{i+1})/(rhat,r_i)  (l.183)
+__device__ __forceinline__ void fin_h3(DevState *st, float rhon, float rr) {
+  int i = st->it + 1;
+  double h = sqrt((double)rr) / st->nb;
+  st->hist[i] = h;
+  st->it = i;
+  int code = -1;
+  if (!isfinite(rr) || !isfinite(rhon)) code = STEN_NONFINITE;
+  else if (rr == 0.0f || (st->tol > 0.0 && h <= st->tol)) code = STEN_CONVERGED;
+  else if (st->omega == 0.0f || rhon == 0.0f) code = STEN_BREAKDOWN;
+  float beta = (rhon / st->rho) * (st->alpha / st->omega);
+  if (!isfinite(beta)) beta = 0.0f;
+  st->beta = beta;
+  st->rho = rhon;
+  if (code >= 0) st_event(st, code, i, false);
+}
+
+template <int PH>
+__device__ __forceinline__ void finalize_phase(DevState *st, const float *s) {
+  if (PH == PH_INIT) fin_init(st, s[0], s[1], s[2]);
+  else if (PH == PH_H1) fin_h1(st, s[0]);
+  else if (PH == PH_H2) fin_h2(st, s[0], s[1]);
+  else fin_h3(st, s[0], s[1]);
+}
+
+__device__ __forceinline__ bool st_idle(const DevState *st) { return st->stop || st->it >= st->maxit; }
+
+// Grid-level end of a reduction: every CTA deposits its block sum; the last
+// CTA to arrive sums the deposits in CTA order (deterministic) and either
+// finalizes the phase or writes the slab's sums for the cross-slab step.
+template <int ND, int PH>
+__device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduce &red, float *scratch) {
+  block_sum<ND>(v, scratch);
+  __shared__ int am_last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d = 0; d < ND; ++d) red.partials[blockIdx.x * kMaxDots + d] = v[d];
+    __threadfence();
+    unsigned t = atomicAdd(red.counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  float s[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) s[d] = 0.0f;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int d = 0; d < ND; ++d) s[d] += __ldcg(&red.partials[b * kMaxDots + d]);
+  block_sum<ND>(s, scratch);
+  if (threadIdx.x == 0) {
+    *red.counter = 0u;
+    if (red.slab_out) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) red.slab_out[d] = s[d];
+    } else {
+      float full[kMaxDots] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int d = 0; d < ND; ++d) full[d] = s[d];
+      finalize_phase<PH>(red.st, full);
+    }
+  }
+}
+
+// ----------------------------------------------------------- host side --
+// kernels.cu
+template <typename T> int stencil_launch(int mode, const StencilArgs &a, int threads, size_t smem,
+                                         cudaStream_t s);
+template <typename T> size_t stencil_smem_bytes(int mode, int bx, int by, int stages);
+template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
+template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
+int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);
+int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s);
+int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g,
+                         int has_below, int has_above, float *const c32[6], __half *const c16[6],
+                         double *aP, cudaStream_t s);
+int device_sm_count();
+
+}  // namespace sten
