@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark: BiCGStab Gpoint-iter/s and % of the HBM roofline (BASELINE.json metric).
+
+One "step" = one bicgstab_solve of the whole hot path (S1 init, then H1, H2, H3
+for `maxit` iterations, tol = 0 so exactly maxit iterations run) on a synthetic
+problem with the shape of the paper's run:
+  N = 1 : config 3  - 600x595x1536, convection-diffusion (delta = 0.1), mixed fp16
+  N > 1 : config 5  - weak scaling, 600x595x(1536*N), one 1536-plane z-slab per
+          GPU, halo planes + fp32 scalar all-reduce over NCCL
+  (`--workload` overrides; fp32 with --precision fp32).
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + device
+sync, CUDA events on the solve's stream, max over ranks.  The working set
+(16.5 GB) is > 100x the 126 MB L2, so no flush is needed between steps.
+
+`--impl reference` times the CPU oracle (oracle/, O16 for mixed, O64 for fp32)
+on a bounded z-slab sample of the same workload, on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NX, NY, NZ = 600, 595, 1536
+PAPER_GPT_ITER_S = 548_352_000 / 28.1e-6 / 1e9  # CS-1: 19514 Gpt-iter/s
+FALLBACK_HBM_GBS = 6650.0
+METRIC = "BiCGStab Gpoint-iter/s & % HBM roofline, 600×595×1536 mixed fp16, 1–8 GPU"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="sten", choices=["sten", "reference"])
+    p.add_argument("--precision", default="mixed", choices=["mixed", "fp32"])
+    p.add_argument("--maxit", type=int, default=100)
+    p.add_argument("--workload", default="auto", choices=["auto", "cfg3", "cfg5"])
+    p.add_argument("--nz", type=int, default=NZ, help="planes per GPU (debug / profiling)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--tiling", default="", help="bx,by,zc,stages override")
+    p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 6 and parts[0].isdigit():
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [int(r[0]) for r in rows]
+        mx = max(int(r[1]) for r in rows)
+        under = [s for s in sm if s > 0.5 * mx] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(statistics.median(under)), "sm_max_mhz": float(mx), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------- oracle --
+def oracle_sample(precision: str, workload: str, planes: int, iters: int, z0: int = 0):
+    """Time the oracle as it stands on a z-slab sample [z0, z0+planes) of the workload."""
+    import inputs
+    import oracle as orc
+    kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
+    kz = inputs.weak_kz_table(NZ) if kind == inputs.KIND_CD_WEAK else None
+    diag, offs = inputs.problem_fields(kind, NX, NY, planes, z0=z0, seed=1, delta=0.1, kz_table=kz)
+    b64 = inputs.rhs_uniform(NX, NY, planes, z0=z0, seed=1)
+    c64 = orc.jacobi_scale(diag, offs)
+    t0 = time.perf_counter()
+    if precision == "mixed":
+        c16 = orc.quantize_coeffs(c64, "mixed")
+        bh = orc.scale_rhs(orc.f16_from_double(b64), diag, "mixed")
+        t0 = time.perf_counter()
+        orc.bicgstab16(c16, bh, tol=0.0, maxit=iters)
+    else:
+        c32 = [c.astype(np.float32).astype(np.float64) for c in c64]
+        bh = orc.scale_rhs(b64.astype(np.float32), diag, "fp32").astype(np.float64)
+        t0 = time.perf_counter()
+        orc.bicgstab64(c32, bh, tol=0.0, maxit=iters)
+    dt = time.perf_counter() - t0
+    pts = NX * NY * planes
+    return dict(value=pts * iters / dt / 1e9, unit="Gpoint-iter/s", cores=orc.num_threads(), kind="oracle",
+                sample=f"{'O16' if precision == 'mixed' else 'O64'} BiCGStab, {iters} iterations on a "
+                       f"{NX}x{NY}x{planes} z-slab of {workload} ({pts} points), {dt:.1f} s"), dt
+
+
+def cpu_baseline_auto(precision, workload, planes_override=0):
+    # size the sample to ~10-30 s of oracle work
+    planes = planes_override or (16 if precision == "mixed" else 64)
+    iters = 3
+    res, dt = oracle_sample(precision, workload, planes, iters)
+    return res
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    workload = args.workload if args.workload != "auto" else ("cfg3" if args.gpus == 1 else "cfg5")
+    planes = args.cpu_planes or (2 if args.precision == "mixed" else 8)
+    iters = 2
+    for _ in range(args.warmup):
+        oracle_sample(args.precision, workload, planes, 1)
+    vals, dts = [], []
+    for _ in range(args.steps):
+        res, dt = oracle_sample(args.precision, workload, planes, iters)
+        vals.append(res["value"])
+        dts.append(dt)
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(dts)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PAPER_GPT_ITER_S,
+            "dtype": "f16" if args.precision == "mixed" else "f64", "data": "synthetic",
+            "config": {"workload": workload, "mesh": [NX, NY, NZ], "precision": args.precision,
+                       "sample_planes": planes, "iters_per_step": iters},
+            "cpu_baseline": res,
+            "e2e": {"value": value, "unit": "Gpoint-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU --
+def run_sten(args):
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import inputs.cuda as icuda
+    import paper_2010_03660_b200 as sten
+    from paper_2010_03660_b200 import roofline
+
+    rank, world, local = dist_env()
+    n = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    workload = args.workload if args.workload != "auto" else ("cfg3" if n == 1 else "cfg5")
+    prec = sten.MIXED if args.precision == "mixed" else sten.FP32
+    tdt = torch.float16 if prec == sten.MIXED else torch.float32
+    nzl = args.nz
+    z0 = rank * nzl
+
+    comm = None
+    if world > 1:
+        uid = [sten.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sten.comm_create(uid[0], world, rank)
+
+    # problem: fields of this rank's slab generated on the device (inputs/gen_cuda.cu)
+    kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
+    kz = inputs.weak_kz_table(nzl * n) if kind == inputs.KIND_CD_WEAK else None
+    diag, offs = icuda.fields_device(kind, NX, NY, nzl, z0=z0, seed=1, delta=0.1, kz_table=kz)
+    st = sten.stencil_create(NX, NY, nzl, [diag] + offs, nslabs=1, comm=comm)
+    del diag, offs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    if args.tiling:
+        bx, by, zc, stg = (int(v) for v in args.tiling.split(","))
+        sten.set_tiling(st, prec, bx, by, zc, stg)
+    b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)
+    x = torch.empty_like(b)
+    maxit = args.maxit
+    npts_local = NX * NY * nzl
+    npts = npts_local * n
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    sten.set_timing(st, True)
+    for _ in range(args.warmup):
+        sten.bicgstab_solve(st, prec, b, None, 0.0, maxit, x)
+    torch.cuda.synchronize()
+    barrier()
+
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    launches = 0
+    h1_ms, h1_n = 0.0, 0
+    ph_ms = [0.0, 0.0, 0.0]
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    last = None
+    for _ in range(args.steps):
+        last = sten.bicgstab_solve(st, prec, b, None, 0.0, maxit, x)
+        s = sten.get_stats(st)
+        launches += s["kernel_launches"]
+        for p in range(3):
+            ph_ms[p] += s["phase_ms"][p]
+        h1_ms += s["phase_ms"][0]
+        h1_n += s["phase_launches"][0]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    it, hist, status = last
+    value = npts * maxit * args.steps / (t_ms / 1e3) / 1e9
+
+    # end to end through the same C-ABI call with pinned HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        bh = b.cpu().pin_memory()
+        xh = torch.empty_like(bh).pin_memory()
+        sten.set_timing(st, False)
+        sten.bicgstab_solve(st, prec, bh, None, 0.0, maxit, xh)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, hh, _ = sten.bicgstab_solve(st, prec, bh, None, 0.0, maxit, xh)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        esz = b.element_size()
+        e2e = {"value": npts * maxit * args.steps / te / 1e9, "unit": "Gpoint-iter/s",
+               "h2d_bytes_per_step": npts_local * esz, "d2h_bytes_per_step": npts_local * esz + 8 * (maxit + 1)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = measured_peak()
+    pname = "mixed" if prec == sten.MIXED else "fp32"
+    h1_avg_ms = h1_ms / max(h1_n, 1)
+    h1_bytes = roofline.phase_bytes("H1", pname, npts_local)
+    achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
+    bpi = roofline.bytes_per_point_iter(pname)
+    whole_gbs = npts_local * maxit * args.steps * bpi / (t_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / PAPER_GPT_ITER_S,
+        "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
+        "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
+                   "precision": pname, "maxit": maxit, "tol": 0.0, "parallelism": f"zslab{n}",
+                   "l2": "no flush: 16.5 GB working set per GPU >> 126 MB L2",
+                   "gflops": value * roofline.FLOPS_PER_POINT_ITER,
+                   "hbm_frac_whole_step": whole_gbs / peak, "bytes_per_point_iter": bpi,
+                   "status": sten.STATUS_NAMES.get(status, status), "final_rel_residual": float(hist[-1])},
+        "roofline": {"bound": "hbm", "kernel": "k_stencil<half,H1>" if prec == sten.MIXED else "k_stencil<float,H1>",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": h1_bytes, "avg_launch_ms": h1_avg_ms,
+                     "phase_ms_per_iter": [p / max(h1_n, 1) for p in ph_ms]},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_auto(pname, workload, args.cpu_planes)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_sten(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

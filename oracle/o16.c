@@ -183,6 +183,11 @@ static int on_event(int code, int i, double tol, int *ev, int *ev_it) {
   return tol > 0.0;
 }
 
+/* R7 (mixed): the scalars enter fp16 FMACs, so a scalar whose fp16 rounding is
+ * +-Inf (|s| >= 65520, the midpoint above the largest finite 65504) is as
+ * unusable as an fp32 Inf/NaN. */
+static int usable16(float s) { return isfinite(s) && finite16(rn16f(s)); }
+
 int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
                  const uint16_t *b, const uint16_t *x0, double tol, int maxit,
                  int unfused, uint16_t *x, double *hist, float *alpha_out,
@@ -232,7 +237,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     apply(nx, ny, nz, c, p, v);                       /* l.176 */
     float sigma = o16_dot(nx, ny, nz, rh, v);         /* l.177 */
     alpha = rho / sigma;
-    if (sigma == 0.0f || !isfinite(alpha)) {
+    if (sigma == 0.0f || !usable16(alpha)) {
       alpha = 0.0f;
       if (on_event(isfinite(sigma) ? ORC_BREAKDOWN : ORC_NONFINITE, i, tol, &ev, &ev_it)) {
         it = i - 1;
@@ -247,7 +252,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
       omega = 0.0f;
     } else {
       omega = ts / tt;                                /* l.180 */
-      if (!isfinite(omega)) {
+      if (!usable16(omega)) {
         omega = 0.0f;
         if (on_event(ORC_NONFINITE, i, tol, &ev, &ev_it)) {
           it = i - 1;
@@ -268,7 +273,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     else if (rr == 0.0f || (tol > 0.0 && hist[i] <= tol)) code = ORC_CONVERGED;
     else if (omega == 0.0f || rhon == 0.0f) code = ORC_BREAKDOWN;
     beta = (rhon / rho) * (alpha / omega);            /* l.183, fp32 */
-    if (!isfinite(beta)) beta = 0.0f;
+    if (!usable16(beta)) beta = 0.0f;
     rho = rhon;
     if (code >= 0 && on_event(code, i, tol, &ev, &ev_it)) break;
   }

@@ -416,7 +416,7 @@ static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_
   const int ns = (int)st->slabs.size();
   const bool dec = decomposed(st);
   // H1: halos of r (new from H3), p, v (new from the previous H1)
-  if (evs) CUDA_TRY(cudaEventRecord(evs[0], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
   if (dec) {
     RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, s));
     RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.p[parity]; }, s));
@@ -424,18 +424,18 @@ static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_
   }
   for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H1, k, parity, s));
   RC_TRY(reduce_scalars(st, PH_H1, s));
-  if (evs) CUDA_TRY(cudaEventRecord(evs[1], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
   // H2: halo of the new v
-  if (evs) CUDA_TRY(cudaEventRecord(evs[2], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
   if (dec) RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity ^ 1]; }, s));
   for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H2, k, parity, s));
   RC_TRY(reduce_scalars(st, PH_H2, s));
-  if (evs) CUDA_TRY(cudaEventRecord(evs[3], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
   // H3
-  if (evs) CUDA_TRY(cudaEventRecord(evs[4], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[4], s, cudaEventRecordExternal));
   for (int k = 0; k < ns; ++k) RC_TRY(launch_h3(st, prec, k, parity, s));
   RC_TRY(reduce_scalars(st, PH_H3, s));
-  if (evs) CUDA_TRY(cudaEventRecord(evs[5], s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[5], s, cudaEventRecordExternal));
   return STEN_OK;
 }
 
@@ -753,6 +753,7 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   h.maxit = maxit;
   h.status = -1;
   h.ev = -1;
+  h.half = prec == STEN_MIXED;
   h.hist = st->hist;
   h.ahist = st->ahist;
   h.whist = st->whist;
@@ -805,11 +806,13 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
             if (first + j >= done_it) break;  // later kernels were no-ops
             for (int p = 0; p < 3; ++p) {
               float ms = 0.f;
-              if (cudaEventElapsedTime(&ms, gr->ev[(size_t)j * 6 + 2 * p], gr->ev[(size_t)j * 6 + 2 * p + 1]) ==
-                  cudaSuccess) {
-                ph_ms[p] += ms;
-                ph_n[p] += 1;
-              }
+              cudaError_t te =
+                  cudaEventElapsedTime(&ms, gr->ev[(size_t)j * 6 + 2 * p], gr->ev[(size_t)j * 6 + 2 * p + 1]);
+              if (te != cudaSuccess)
+                return set_err(STEN_ECUDA, "cudaEventElapsedTime(iter %d, phase %d): %s", j, p,
+                               cudaGetErrorString(te));
+              ph_ms[p] += ms;
+              ph_n[p] += 1;
             }
           }
         }

@@ -29,7 +29,7 @@ struct DevState {
   int ev;                          // first event code (-1: none)
   int ev_it;                       // iteration of the first event
   int zero_x;                      // b_hat == 0: x must be returned as 0
-  int pad_;
+  int half;                        // mixed mode: scalars must be finite in fp16 (R7)
   double *hist;                    // [maxit+1] ||r_i|| / ||b_hat||
   float *ahist, *whist;            // [maxit+1] alpha_i, omega_i
 };
@@ -287,11 +287,17 @@ __device__ __forceinline__ void fin_init(DevState *st, float rho, float bb, floa
   }
 }
 
+// A scalar is usable if finite in the working precision: in mixed mode it is
+// rounded to fp16 before the AXPYs, and |s| >= 65520 rounds to Inf (R7).
+__device__ __forceinline__ bool usable(const DevState *st, float s) {
+  return isfinite(s) && (!st->half || fabsf(s) < 65520.0f);
+}
+
 // H1: alpha_i = rho_i / (rhat, s_i)   (l.177)
 __device__ __forceinline__ void fin_h1(DevState *st, float sigma) {
   int i = st->it + 1;
   float alpha = st->rho / sigma;
-  if (sigma == 0.0f || !isfinite(alpha)) {
+  if (sigma == 0.0f || !usable(st, alpha)) {
     alpha = 0.0f;
     st_event(st, isfinite(sigma) ? STEN_BREAKDOWN : STEN_NONFINITE, i, true);
   }
@@ -305,7 +311,7 @@ __device__ __forceinline__ void fin_h2(DevState *st, float ts, float tt) {
   float omega = 0.0f;  // tt == 0: s == 0, x += alpha p is exact (R8)
   if (tt != 0.0f) {
     omega = ts / tt;
-    if (!isfinite(omega)) {
+    if (!usable(st, omega)) {
       omega = 0.0f;
       st_event(st, STEN_NONFINITE, i, true);
     }
@@ -325,7 +331,7 @@ __device__ __forceinline__ void fin_h3(DevState *st, float rhon, float rr) {
   else if (rr == 0.0f || (st->tol > 0.0 && h <= st->tol)) code = STEN_CONVERGED;
   else if (st->omega == 0.0f || rhon == 0.0f) code = STEN_BREAKDOWN;
   float beta = (rhon / st->rho) * (st->alpha / st->omega);
-  if (!isfinite(beta)) beta = 0.0f;
+  if (!usable(st, beta)) beta = 0.0f;
   st->beta = beta;
   st->rho = rhon;
   if (code >= 0) st_event(st, code, i, false);
