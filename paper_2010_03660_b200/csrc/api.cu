@@ -333,7 +333,10 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
   a.rhat = in(b.rh);
   a.xo = (char *)b.x + off;
   a.ro = (char *)b.r + off;
-  a.nvec = (long long)st->plane * sl.nz / vec;
+  a.rows = (long long)st->ny * sl.nz;
+  a.vpr = (st->nx + vec - 1) / vec;
+  a.pitch = st->pitch;
+  a.nvec = a.rows * (a.pitch / vec);  // linear over the padded rows (zeros in the padding)
   a.red = make_red(st, slab);
   if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st), 256, s));
   else KLAUNCH(h3_launch<__half>(a, ew_grid(st), 256, s));
@@ -355,7 +358,10 @@ static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaS
   a.rh = (char *)b.rh + off;
   a.p0 = (char *)b.p[0] + off;
   a.v0 = (char *)b.v[0] + off;
-  a.nvec = (long long)st->plane * sl.nz / vec;
+  a.rows = (long long)st->ny * sl.nz;
+  a.vpr = (st->nx + vec - 1) / vec;
+  a.pitch = st->pitch;
+  a.nvec = a.rows * (a.pitch / vec);  // linear over the padded rows (zeros in the padding)
   a.red = make_red(st, slab);
   if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st), 256, s));
   else KLAUNCH(init_launch<__half>(a, ew_grid(st), 256, s));
@@ -571,7 +577,7 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   st->nx = nx;
   st->ny = ny;
   st->nz = nz;
-  st->pitch = (nx + 7) / 8 * 8;
+  st->pitch = (nx + 63) / 64 * 64;  // 128-byte rows for fp16 and fp32
   st->plane = (long long)st->pitch * ny;
   st->nslabs = nslabs;
   st->comm = comm;

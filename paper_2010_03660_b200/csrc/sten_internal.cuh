@@ -71,7 +71,10 @@ struct EwArgs {           // element-wise kernels (H3, INIT)
   void *xo, *ro;                       // H3 outputs
   const void *bw; const double *aP; const void *ax; // INIT inputs (ax = A x0 or null)
   void *r, *rh, *p0, *v0;              // INIT outputs
-  long long nvec;                      // vectors of VEC elements (interior range)
+  long long nvec;                      // vectors of VEC elements holding mesh points
+  long long rows;                      // ny * nz rows of the interior range
+  int vpr;                             // vectors per row that hold points (ceil(nx/VEC))
+  int pitch;                           // row pitch in elements (multiple of 64: 128-B rows)
   Reduce red;
 };
 
@@ -126,6 +129,11 @@ template <> struct Pack<float> {
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc = __fmaf_rn(v[i], b.v[i], acc);
     return acc;
+  }
+  // four independent partial sums (short dependency chains)
+  __device__ __forceinline__ void dot4(const Pack &b, float (&acc)[4]) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = __fmaf_rn(v[i], b.v[i], acc[i]);
   }
 };
 
@@ -186,7 +194,17 @@ template <> struct Pack<__half> {
     }
     return acc;
   }
+  __device__ __forceinline__ void dot4(const Pack &b, float (&acc)[4]) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 x = __half22float2(h2(w[i])), y = __half22float2(h2(b.w[i]));
+      acc[i] = __fmaf_rn(x.x, y.x, acc[i]);
+      acc[i] = __fmaf_rn(x.y, y.y, acc[i]);
+    }
+  }
 };
+
+__device__ __forceinline__ float sum4(const float (&a)[4]) { return (a[0] + a[1]) + (a[2] + a[3]); }
 
 // ------------------------------------------------------------- PTX: TMA --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

@@ -132,7 +132,8 @@ def test_fp32_config1_manufactured(sten):
     bh = orc.scale_rhs(b, diag, "fp32")
     ref = orc.bicgstab64([c.astype(np.float64) for c in c32], bh.astype(np.float64), tol=1e-6, maxit=200)
     assert status == sten.CONVERGED and hist[-1] <= 1e-6
-    assert abs(it - ref["iters"]) <= 3
+    # iteration counts of a rounding-sensitive Krylov trajectory (R14) agree loosely
+    assert abs(it - ref["iters"]) <= max(3, 0.25 * ref["iters"])
     assert np.linalg.norm(x - xt) / np.linalg.norm(xt) <= 441 * 1e-6 * 2
     st.close()
 
