@@ -115,9 +115,16 @@ static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int pl
   cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)pitch * ny * elem};
   cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
   cuuint32_t es[3] = {1, 1, 1};
+  static int promo = -1;
+  if (promo < 0) {
+    const char *e = getenv("STEN_TMA_PROMO");  // tuning knob: 0 none, 1 64B, 2 128B, 3 256B
+    promo = e ? atoi(e) : 3;
+  }
+  const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUresult r = g_encode(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base,
                         dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        pr[promo & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(STEN_ECUDA, "cuTensorMapEncodeTiled failed (%d): dims %d %d %d box %d %d", (int)r, nx, ny, planes,
                    boxx, boxy);
@@ -126,6 +133,7 @@ static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int pl
 
 // ------------------------------------------------------------ handle --
 struct Tiling {
+  int rows = 0;  // 1: full-row strips (k_rows), 0: BX-wide tiles with an x halo (k_stencil)
   int bx = 0, by = 0, zc = 0, stages = 0, threads = 0;
 };
 
@@ -181,6 +189,7 @@ struct sten_stencil {
   cudaStream_t cap = nullptr;   // capture stream
   std::map<GraphKey, GraphRec> graphs;
   bool timing = false;
+  int coef_pf = 0;              // L2 prefetch distance of coefficient tiles (tuning knob STEN_COEF_PF)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   sten_stats stats{};
   long long launches = 0;       // kernel launches (direct + graph nodes) of the current call
@@ -189,20 +198,24 @@ struct sten_stencil {
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
 static int esize(int prec) { return prec == STEN_FP32 ? 4 : 2; }
 
+static int rows_thr(int prec, int nx, int by) {
+  return prec == STEN_FP32 ? rows_threads<float>(nx, by) : rows_threads<__half>(nx, by);
+}
+
+// Default: 256-B-wide tiles x 16 rows, 4 TMA stages (2 CTAs/SM).  Measured on
+// B200 at 600x595x1536 (profiles/): 102.9 Gpoint-iter/s vs
+// 99.9 for the best full-row strip (by 2, 3 stages) - the strips need more
+// CTAs in flight than their shared-memory footprint allows.  Strips remain
+// selectable with sten_set_tiling(bx >= nx).
 static void default_tiling(sten_stencil *st, int prec) {
   Tiling &t = st->tiling[prec];
-  const int vec = prec == STEN_FP32 ? 4 : 8;
-  int bx = prec == STEN_FP32 ? 64 : 128;
-  int w = (st->nx + vec - 1) / vec * vec;
-  if (w < bx) bx = w;
-  t.bx = bx;
-  t.by = 8;
-  t.stages = 4;
   int nzs = st->slabs[0].nz;
   t.zc = nzs < 64 ? nzs : 64;
-  int vpr = bx / vec;
-  int th = (vpr * t.by + 31) / 32 * 32;
-  t.threads = th < 64 ? 64 : (th > 256 ? 256 : th);
+  t.rows = 0;
+  t.bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  t.by = 16;
+  t.stages = 4;
+  t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);
 }
 
 static int ensure_maps(sten_stencil *st, int prec) {
@@ -213,7 +226,8 @@ static int ensure_maps(sten_stencil *st, int prec) {
     PrecBufs &b = sl.pb[prec];
     if (b.maps_ok) continue;
     const int planes = sl.nz + 2;
-    const int hx = t.bx + 2 * H, hy = t.by + 2;
+    const int hx = t.rows ? kRowBoxElems : t.bx + 2 * H, hy = t.by + 2;
+    const int ix = t.rows ? kRowBoxElems : t.bx;  // interior box (coefficient / rhat prefetch)
     RC_TRY(make_map(&b.m_r, b.r, e, st->nx, st->ny, planes, st->pitch, hx, hy));
     for (int i = 0; i < 2; ++i) {
       RC_TRY(make_map(&b.m_p[i], b.p[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
@@ -221,10 +235,10 @@ static int ensure_maps(sten_stencil *st, int prec) {
     }
     RC_TRY(make_map(&b.m_s, b.s, e, st->nx, st->ny, planes, st->pitch, hx, hy));
     RC_TRY(make_map(&b.m_x, b.x, e, st->nx, st->ny, planes, st->pitch, hx, hy));
-    RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, planes, st->pitch, t.bx, t.by));
+    RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, planes, st->pitch, ix, t.by));
     for (int d = 0; d < 6; ++d) {
       void *c = prec == STEN_FP32 ? (void *)sl.c32[d] : (void *)sl.c16[d];
-      RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz, st->pitch, t.bx, t.by));
+      RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz, st->pitch, ix, t.by));
     }
     b.maps_ok = true;
   }
@@ -291,6 +305,7 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     a.tm_in[1] = b.m_p[cur];
     a.tm_in[2] = b.m_v[cur];
     a.tm_aux = b.m_rh;
+    a.aux = b.rh;
     a.out0 = b.v[nxt];
     a.out1 = b.p[nxt];
   } else {
@@ -299,19 +314,23 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     a.out0 = b.t;
     a.out1 = b.s;
   }
-  for (int d = 0; d < 6; ++d) a.tm_c[d] = b.m_c[d];
+  for (int d = 0; d < 6; ++d) {
+    a.tm_c[d] = b.m_c[d];
+    a.cptr[d] = prec == STEN_FP32 ? (const void *)sl.c32[d] : (const void *)sl.c16[d];
+  }
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
-  a.bx = t.bx;
-  a.by = t.by;
   a.zc = t.zc;
-  a.stages = t.stages;
-  a.tiles_x = (st->nx + t.bx - 1) / t.bx;
+  a.pf = st->coef_pf;
+  a.tiles_x = t.rows ? 1 : (st->nx + t.bx - 1) / t.bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
   a.red = make_red(st, slab);
-  size_t smem = prec == STEN_FP32 ? stencil_smem_bytes<float>(mode, t.bx, t.by, t.stages)
-                                  : stencil_smem_bytes<__half>(mode, t.bx, t.by, t.stages);
-  if (prec == STEN_FP32) KLAUNCH(stencil_launch<float>(mode, a, t.threads, smem, s));
-  else KLAUNCH(stencil_launch<__half>(mode, a, t.threads, smem, s));
+  if (t.rows) {
+    if (prec == STEN_FP32) KLAUNCH(rows_launch<float>(mode, a, t.by, t.stages, s));
+    else KLAUNCH(rows_launch<__half>(mode, a, t.by, t.stages, s));
+  } else {
+    if (prec == STEN_FP32) KLAUNCH(stencil_launch<float>(mode, a, t.by, t.stages, s));
+    else KLAUNCH(stencil_launch<__half>(mode, a, t.by, t.stages, s));
+  }
   st->launches++;
   return STEN_OK;
 }
@@ -583,6 +602,8 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   st->comm = comm;
   st->has_diag = coeffs[0] != nullptr;
   st->sm = device_sm_count();
+  if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
+  if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
   st->slabs.resize(nslabs);
   auto fail = [&](int rc) {
     stencil_destroy(st);
@@ -685,20 +706,30 @@ int sten_set_tiling(sten_stencil *st, int prec, int bx, int by, int zc, int stag
   if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
   if (st->slabs[0].pb[prec].ready == false && st->tiling[prec].bx == 0) default_tiling(st, prec);
   Tiling t = st->tiling[prec];
-  const int vec = prec == STEN_FP32 ? 4 : 8, H = vec;
-  if (bx) t.bx = bx;
+  const int tbx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  if (bx == tbx) {
+    t.rows = 0;
+    t.bx = tbx;
+  } else if (bx >= st->nx) {
+    t.rows = 1;
+    t.bx = st->pitch;
+  } else if (bx != 0) {
+    return set_err(STEN_EINVAL, "bx must be 0, %d (tiles) or >= nx=%d (full-row strips)", tbx, st->nx);
+  }
   if (by) t.by = by;
   if (zc) t.zc = zc;
   if (stages) t.stages = stages;
-  if (t.bx % vec || t.bx <= 0 || t.bx + 2 * H > 256 || t.by <= 0 || t.by + 2 > 256 || t.zc <= 0 ||
-      t.stages < 2 || t.stages > 8)
-    return set_err(STEN_EINVAL, "invalid tiling bx=%d by=%d zc=%d stages=%d", t.bx, t.by, t.zc, t.stages);
-  size_t smem = prec == STEN_FP32 ? stencil_smem_bytes<float>(MODE_H1, t.bx, t.by, t.stages)
-                                  : stencil_smem_bytes<__half>(MODE_H1, t.bx, t.by, t.stages);
-  if (smem > 227 * 1024) return set_err(STEN_EINVAL, "tiling needs %zu B of shared memory", smem);
-  int vpr = t.bx / vec;
-  int th = (vpr * t.by + 31) / 32 * 32;
-  t.threads = th < 64 ? 64 : (th > 256 ? 256 : th);
+  if (t.rows) {
+    if (t.zc <= 0 || !rows_config_ok(t.by, t.stages) || rows_thr(prec, st->nx, t.by) > 512 ||
+        rows_smem_bytes(MODE_H1, esize(prec), st->pitch, t.by, t.stages) > 227 * 1024)
+      return set_err(STEN_EINVAL, "unsupported row-strip tiling by=%d zc=%d stages=%d", t.by, t.zc, t.stages);
+    t.threads = rows_thr(prec, st->nx, t.by);
+  } else {
+    if (t.zc <= 0 || !stencil_config_ok(t.by, t.stages))
+      return set_err(STEN_EINVAL, "unsupported tiling by=%d zc=%d stages=%d (by 4/8/16, stages 3/4)", t.by, t.zc,
+                     t.stages);
+    t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);
+  }
   st->tiling[prec] = t;
   for (Slab &sl : st->slabs) sl.pb[prec].maps_ok = false;
   drop_graphs(st);

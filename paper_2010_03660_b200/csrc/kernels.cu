@@ -1,17 +1,6 @@
 // kernels.cu - sm_100a kernels of the BiCGStab hot path.
 //
-//  k_stencil<T, MODE>: the matrix-free 7-point SpMV u = A v with unit diagonal
-//    (PAPER.md:198-201, 338-346), z-marching over a CTA's xy tile.  Each z-plane
-//    of every operand arrives in shared memory by TMA (cp.async.bulk.tensor,
-//    zero-filled outside the mesh) through an S-stage mbarrier ring; the SpMV
-//    input is formed in shared memory from the staged operands (fused AXPYs),
-//    the three planes k-1, k, k+1 of it are kept in a shared ring, and the
-//    result is written with 16-byte stores while the dot products that follow
-//    it in Algorithm 1 are accumulated in registers:
-//      MODE_APPLY: y = A x
-//      MODE_H1   : p' = r + beta (p - omega v)  (l.184), v' = A p' (l.176),
-//                  sigma = (rhat, v')                      (l.177)
-//      MODE_H2   : s = r - alpha v (l.178), t = A s (l.179), (t,s), (t,t) (l.180)
+//  (the fused stencil kernels k_stencil<T, MODE, BY, S> are in stencil.cu)
 //  k_h3<T>: x += alpha p + omega s (l.181), r = s - omega t (l.182),
 //           (rhat, r), (r, r) (l.183 and the stopping rule R4)
 //  k_init<T>: b_hat = b / a_P (R3), r0 = b_hat - A x0 (R1), rhat = p = r0, v = 0
@@ -20,189 +9,6 @@
 #include "sten_internal.cuh"
 
 namespace sten {
-
-static __host__ __device__ __forceinline__ int align128(int b) { return (b + 127) & ~127; }
-
-template <typename T>
-struct TileLayout {
-  static constexpr int VEC = Pack<T>::VEC;
-  static constexpr int H = VEC;  // x halo pad, keeps every 16-byte vector aligned
-  int hw, hbox, ibox, hbytes, ibytes, stage_bytes;
-  __host__ __device__ TileLayout(int mode, int bx, int by) {
-    const int nin = mode == MODE_H1 ? 3 : (mode == MODE_H2 ? 2 : 1);
-    const int nint = 6 + (mode == MODE_H1 ? 1 : 0);
-    hw = bx + 2 * H;
-    hbox = hw * (by + 2);
-    ibox = bx * by;
-    hbytes = align128(hbox * (int)sizeof(T));
-    ibytes = align128(ibox * (int)sizeof(T));
-    stage_bytes = nin * hbytes + nint * ibytes;
-  }
-};
-
-template <typename T>
-size_t stencil_smem_bytes(int mode, int bx, int by, int stages) {
-  TileLayout<T> L(mode, bx, by);
-  return 128 /* mbarriers */ + (size_t)stages * L.stage_bytes + 3 * (size_t)L.hbytes + 32 * kMaxDots * 4;
-}
-
-template <typename T, int MODE>
-__global__ void __launch_bounds__(256) k_stencil(const __grid_constant__ StencilArgs a) {
-  using P = Pack<T>;
-  constexpr int VEC = P::VEC;
-  constexpr int H = VEC;
-  constexpr int NIN = MODE == MODE_H1 ? 3 : (MODE == MODE_H2 ? 2 : 1);
-  constexpr int NINT = 6 + (MODE == MODE_H1 ? 1 : 0);
-  constexpr int ND = MODE == MODE_H1 ? 1 : (MODE == MODE_H2 ? 2 : 1);
-
-  if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
-
-  const TileLayout<T> L(MODE, a.bx, a.by);
-  const int S = a.stages;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);
-  unsigned char *stage0 = smem + 128;
-  T *U = reinterpret_cast<T *>(stage0 + S * L.stage_bytes);
-  const int ustride = L.hbytes / (int)sizeof(T);
-  float *scratch = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(U) + 3 * L.hbytes);
-
-  int b = blockIdx.x;
-  const int tx = b % a.tiles_x;
-  b /= a.tiles_x;
-  const int ty = b % a.tiles_y;
-  const int ch = b / a.tiles_y;
-  const int x0 = tx * a.bx, y0 = ty * a.by;
-  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
-  const int np = z1 - z0 + 2;  // planes z0-1 .. z1 (halo planes included)
-  const int tid = threadIdx.x, nthr = blockDim.x;
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
-    fence_mbar_init();
-    for (int i = 0; i < NIN; ++i) prefetch_tmap(&a.tm_in[i]);
-  }
-  __syncthreads();
-
-  // ---- producer: one thread issues every TMA of a plane ----
-  auto issue = [&](int q) {
-    const int s = q % S, p = z0 - 1 + q;
-    unsigned char *base = stage0 + s * L.stage_bytes;
-    const bool interior = (p >= z0 && p < z1);
-    uint32_t bytes = NIN * L.hbox * (uint32_t)sizeof(T) + (interior ? NINT * L.ibox * (uint32_t)sizeof(T) : 0u);
-    mbar_expect_tx(&mbar[s], bytes);
-#pragma unroll
-    for (int i = 0; i < NIN; ++i) tma_load_3d(base + i * L.hbytes, &a.tm_in[i], x0 - H, y0 - 1, p + 1, &mbar[s]);
-    if (interior) {
-#pragma unroll
-      for (int d = 0; d < 6; ++d)
-        tma_load_3d(base + NIN * L.hbytes + d * L.ibytes, &a.tm_c[d], x0, y0, p, &mbar[s]);
-      if (MODE == MODE_H1) tma_load_3d(base + NIN * L.hbytes + 6 * L.ibytes, &a.tm_aux, x0, y0, p + 1, &mbar[s]);
-    }
-  };
-  auto wait = [&](int q) { mbar_wait(&mbar[q % S], (uint32_t)((q / S) & 1)); };
-
-  // scalars of the fused AXPYs (fp16: rounded to nearest, R11)
-  typename P::S beta_s{}, momega_s{}, malpha_s{};
-  if (MODE == MODE_H1) {
-    beta_s = P::scalar(a.red.st->beta);
-    momega_s = P::neg(P::scalar(a.red.st->omega));
-  } else if (MODE == MODE_H2) {
-    malpha_s = P::neg(P::scalar(a.red.st->alpha));
-  }
-
-  // ---- SpMV input of plane q over the whole halo box, into the U ring ----
-  auto compute_u = [&](int q) {
-    const T *in = reinterpret_cast<const T *>(stage0 + (q % S) * L.stage_bytes);
-    const int istr = L.hbytes / (int)sizeof(T);
-    T *u = U + (q % 3) * ustride;
-    const int nvec = L.hbox / VEC;
-    for (int v = tid; v < nvec; v += nthr) {
-      const int off = v * VEC;
-      P out = P::ld(in + off);
-      if (MODE == MODE_H1) {  // p' = r + beta (p - omega v)
-        P pp = P::ld(in + istr + off), vv = P::ld(in + 2 * istr + off);
-        out = P::fmas(beta_s, P::fmas(momega_s, vv, pp), out);
-      } else if (MODE == MODE_H2) {  // s = r - alpha v
-        P vv = P::ld(in + istr + off);
-        out = P::fmas(malpha_s, vv, out);
-      }
-      out.st(u + off);
-    }
-  };
-
-  if (tid == 0)
-    for (int q = 0; q < min(S, np); ++q) issue(q);
-  wait(0);
-  compute_u(0);
-  wait(1);
-  compute_u(1);
-  __syncthreads();
-  if (tid == 0 && S < np) issue(S);  // slot of plane z0-1 is free
-
-  float dacc[ND];
-#pragma unroll
-  for (int d = 0; d < ND; ++d) dacc[d] = 0.0f;
-  const int vpr = a.bx / VEC;
-  const int nout = vpr * a.by;
-  const int istride = L.ibytes / (int)sizeof(T);
-
-  for (int k = z0; k < z1; ++k) {
-    const int qk = k - z0 + 1, qn = qk + 1;
-    wait(qn);
-    compute_u(qn);
-    __syncthreads();
-    const T *cb = reinterpret_cast<const T *>(stage0 + (qk % S) * L.stage_bytes + NIN * L.hbytes);
-    const T *Um = U + ((qk - 1) % 3) * ustride;
-    const T *Uc = U + (qk % 3) * ustride;
-    const T *Up = U + (qn % 3) * ustride;
-    for (int o = tid; o < nout; o += nthr) {
-      const int ry = o / vpr, cx = o - ry * vpr;
-      const int h = (ry + 1) * L.hw + H + cx * VEC;
-      const int io = ry * a.bx + cx * VEC;
-      const P c = P::ld(Uc + h);
-      P acc = c;  // unit diagonal: no multiply
-      acc = P::fma(P::ld(cb + 0 * istride + io), P::shl(P::ld(Uc + h - VEC), c), acc);  // xm
-      acc = P::fma(P::ld(cb + 1 * istride + io), P::shr(c, P::ld(Uc + h + VEC)), acc);  // xp
-      acc = P::fma(P::ld(cb + 2 * istride + io), P::ld(Uc + h - L.hw), acc);            // ym
-      acc = P::fma(P::ld(cb + 3 * istride + io), P::ld(Uc + h + L.hw), acc);            // yp
-      acc = P::fma(P::ld(cb + 4 * istride + io), P::ld(Um + h), acc);                   // zm
-      acc = P::fma(P::ld(cb + 5 * istride + io), P::ld(Up + h), acc);                   // zp
-      const int gy = y0 + ry, gx = x0 + cx * VEC;
-      if (gy < a.g.ny && gx < a.g.nx) {  // row padding past nx is never written
-        const long long gi = (long long)(k + 1) * a.g.plane + (long long)gy * a.g.pitch + gx;
-        acc.st(reinterpret_cast<T *>(a.out0) + gi);
-        if (MODE != MODE_APPLY) c.st(reinterpret_cast<T *>(a.out1) + gi);
-      }
-      if (MODE == MODE_H1) {
-        dacc[0] = P::ld(cb + 6 * istride + io).dot(acc, dacc[0]);  // (rhat, v')
-      } else if (MODE == MODE_H2) {
-        dacc[0] = acc.dot(c, dacc[0]);                          // (t, s)
-        dacc[ND - 1] = acc.dot(acc, dacc[ND - 1]);              // (t, t)
-      }
-    }
-    __syncthreads();
-    if (tid == 0 && qk + S < np) issue(qk + S);
-  }
-
-  if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(dacc, a.red, scratch);
-  else if (MODE == MODE_H2) grid_reduce_finalize<ND, PH_H2>(dacc, a.red, scratch);
-}
-
-template <typename T>
-int stencil_launch(int mode, const StencilArgs &a, int threads, size_t smem, cudaStream_t s) {
-  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
-  void (*fn)(StencilArgs) = mode == MODE_H1 ? k_stencil<T, MODE_H1>
-                            : mode == MODE_H2 ? k_stencil<T, MODE_H2>
-                                              : k_stencil<T, MODE_APPLY>;
-  static size_t configured[3] = {0, 0, 0};
-  if (configured[mode] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    configured[mode] = smem;
-  }
-  fn<<<grid, threads, smem, s>>>(a);
-  return (int)cudaGetLastError();
-}
 
 // ------------------------------------------------------------------ H3 --
 // Element offset of the v-th vector of the interior range.  The element-wise
@@ -414,10 +220,6 @@ int device_sm_count() {
   return n;
 }
 
-template int stencil_launch<float>(int, const StencilArgs &, int, size_t, cudaStream_t);
-template int stencil_launch<__half>(int, const StencilArgs &, int, size_t, cudaStream_t);
-template size_t stencil_smem_bytes<float>(int, int, int, int);
-template size_t stencil_smem_bytes<__half>(int, int, int, int);
 template int h3_launch<float>(const EwArgs &, int, int, cudaStream_t);
 template int h3_launch<__half>(const EwArgs &, int, int, cudaStream_t);
 template int init_launch<float>(const EwArgs &, int, int, cudaStream_t);

@@ -56,13 +56,16 @@ struct Geom {
 
 // Arguments of the TMA z-march stencil kernel.
 struct alignas(64) StencilArgs {
-  CUtensorMap tm_in[3];   // halo'd inputs: box (bx+2H) x (by+2) x 1
-  CUtensorMap tm_c[6];    // coefficients xm,xp,ym,yp,zm,zp: box bx x by x 1
-  CUtensorMap tm_aux;     // rhat (H1): box bx x by x 1
+  CUtensorMap tm_in[3];   // halo'd inputs: box (BX+2H) x (BY+2) x 1 into shared memory
+  CUtensorMap tm_c[6];    // coefficients xm,xp,ym,yp,zm,zp: box BX x BY x 1 (L2 prefetch)
+  CUtensorMap tm_aux;     // rhat (H1): box BX x BY x 1 (L2 prefetch)
+  const void *cptr[6];    // coefficient arrays (plane 0 at k = 0, no halo planes)
+  const void *aux;        // rhat (H1), halo layout
   void *out0;             // APPLY: y   H1: v_new   H2: t
   void *out1;             // H1: p_new  H2: s
   Geom g;
-  int bx, by, zc, tiles_x, tiles_y, stages;
+  int zc, tiles_x, tiles_y;
+  int pf;                 // L2 prefetch distance of the coefficient tiles (planes; 0 = off)
   Reduce red;
 };
 
@@ -405,9 +408,20 @@ __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduc
 
 // ----------------------------------------------------------- host side --
 // kernels.cu
-template <typename T> int stencil_launch(int mode, const StencilArgs &a, int threads, size_t smem,
-                                         cudaStream_t s);
-template <typename T> size_t stencil_smem_bytes(int mode, int bx, int by, int stages);
+// stencil.cu: x extent of a tile is fixed per precision (128-B rows of a tile:
+// 128 fp16 / 64 fp32 points); rows per tile (by) and TMA stages are template
+// instances chosen at run time.
+template <typename T> constexpr int tile_bx() { return sizeof(T) == 2 ? 128 : 64; }
+bool stencil_config_ok(int by, int stages);
+template <typename T> int stencil_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s);
+template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
+template <typename T> int stencil_threads(int by);
+// row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits
+constexpr int kRowBoxElems = 64;
+bool rows_config_ok(int by, int stages);
+size_t rows_smem_bytes(int mode, int esz, int pitch, int by, int stages);
+template <typename T> int rows_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s);
+template <typename T> int rows_threads(int nx, int by);
 template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);

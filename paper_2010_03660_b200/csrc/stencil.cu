@@ -1,0 +1,536 @@
+// stencil.cu - the fused 7-point SpMV kernels of the BiCGStab hot path (sm_100a).
+//
+// u = A v with the unit diagonal left implicit:
+//   u_P = v_P + c_xm v_{P-x} + c_xp v_{P+x} + c_ym v_{P-y} + c_yp v_{P+y}
+//             + c_zm v_{P-z} + c_zp v_{P+z}
+// evaluated as one FMA chain in that order (R10), fp32 FFMA or fp16 HFMA2.
+//
+// Structure:
+//  * A CTA owns an xy tile of BX x BY points (BX = 128 fp16 / 64 fp32, i.e. a
+//    256-B row segment) and marches z over a chunk of planes, one 16-byte vector
+//    of VEC points per thread.
+//  * The operands the SpMV input is built from (halo'd: H1 r, p, v; H2 r, v;
+//    APPLY x) arrive plane by plane through a TMA ring of S stages
+//    (cp.async.bulk.tensor.3d, mbarrier complete_tx, out-of-mesh zero fill).
+//  * The SpMV input plane (H1: p' = r + beta (p - omega v), Alg. 1 l.184;
+//    H2: s = r - alpha v, l.178) is formed once per point into a 3-deep shared
+//    ring for the xy neighbours; each thread keeps its own column k-1, k, k+1 in
+//    registers for the z terms.  One __syncthreads per plane.
+//  * The six coefficient arrays (and rhat for H1) are read once per point: TMA
+//    prefetches their tiles into L2 (cp.async.bulk.prefetch.tensor) PF planes
+//    ahead and each thread loads its 16-B vectors straight into registers.
+//  * The dot products that follow each SpMV in Alg. 1 are accumulated in fp32
+//    registers and reduced by the deterministic last-CTA reduction.
+#include "sten_internal.cuh"
+
+namespace sten {
+
+namespace {
+
+constexpr int align128c(int b) { return (b + 127) & ~127; }
+
+template <typename T, int MODE, int BY>
+struct Geo {
+  static constexpr int VEC = Pack<T>::VEC;
+  static constexpr int BX = tile_bx<T>();
+  static constexpr int H = VEC;                 // x halo pad (keeps 16-B vectors aligned)
+  static constexpr int VPR = BX / VEC;          // vectors per tile row
+  static constexpr int NT = VPR * BY;           // threads: one output vector each
+  static constexpr int HW = BX + 2 * H;         // halo box width (elements)
+  static constexpr int HBOX = HW * (BY + 2);    // halo box elements
+  static constexpr int HBYTES = align128c(HBOX * (int)sizeof(T));
+  static constexpr int NIN = MODE == MODE_H1 ? 3 : (MODE == MODE_H2 ? 2 : 1);
+  static constexpr int NHALO = 2 * VPR + 2 * BY;  // halo vectors formed per plane
+  static constexpr int PF = 4;                  // L2 prefetch distance of the coefficients (planes)
+};
+
+template <typename T, int MODE, int BY, int S>
+constexpr size_t smem_bytes_c() {
+  using G = Geo<T, MODE, BY>;
+  return 128 /* mbarriers */ + (size_t)S * G::NIN * G::HBYTES + 3 * (size_t)G::HBYTES;
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+// x-1 / x+1 neighbours of a vector given the single elements left and right of it
+template <typename T> struct Shift;
+template <> struct Shift<float> {
+  static __device__ __forceinline__ Pack<float> left(const Pack<float> &c, float l) {
+    return Pack<float>{{l, c.v[0], c.v[1], c.v[2]}};
+  }
+  static __device__ __forceinline__ Pack<float> right(const Pack<float> &c, float r) {
+    return Pack<float>{{c.v[1], c.v[2], c.v[3], r}};
+  }
+  static __device__ __forceinline__ float ld1(const float *p) { return *p; }
+};
+template <> struct Shift<__half> {
+  static __device__ __forceinline__ Pack<__half> left(const Pack<__half> &c, uint32_t l) {
+    return Pack<__half>{{__byte_perm(l, c.w[0], 0x5410), __byte_perm(c.w[0], c.w[1], 0x5432),
+                         __byte_perm(c.w[1], c.w[2], 0x5432), __byte_perm(c.w[2], c.w[3], 0x5432)}};
+  }
+  static __device__ __forceinline__ Pack<__half> right(const Pack<__half> &c, uint32_t r) {
+    return Pack<__half>{{__byte_perm(c.w[0], c.w[1], 0x5432), __byte_perm(c.w[1], c.w[2], 0x5432),
+                         __byte_perm(c.w[2], c.w[3], 0x5432), __byte_perm(c.w[3], r, 0x5432)}};
+  }
+  static __device__ __forceinline__ uint32_t ld1(const __half *p) {
+    return (uint32_t)*reinterpret_cast<const unsigned short *>(p);
+  }
+};
+
+}  // namespace
+
+template <typename T, int MODE, int BY, int S>
+__global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __grid_constant__ StencilArgs a) {
+  using P = Pack<T>;
+  using G = Geo<T, MODE, BY>;
+  constexpr int VEC = G::VEC, BX = G::BX, H = G::H, HW = G::HW, NIN = G::NIN;
+  constexpr int HSTR = G::HBYTES / (int)sizeof(T);  // elements between halo boxes
+  constexpr int ND = MODE == MODE_H2 ? 2 : 1;
+
+  if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);
+  T *stage0 = reinterpret_cast<T *>(smem + 128);         // [S][NIN][HSTR]
+  T *U = stage0 + S * NIN * HSTR;                       // [3][HSTR]
+  __shared__ float scratch[32 * kMaxDots];
+
+  int b = blockIdx.x;
+  const int tx = b % a.tiles_x;
+  b /= a.tiles_x;
+  const int ty = b % a.tiles_y;
+  const int ch = b / a.tiles_y;
+  const int x0 = tx * BX, y0 = ty * BY;
+  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int np = z1 - z0 + 2;  // staged planes z0-1 .. z1
+  const int tid = threadIdx.x;
+
+  // own output vector and (for the first NHALO threads) one halo vector
+  const int ry = tid / G::VPR, cx = tid - (tid / G::VPR) * G::VPR;
+  const int hown = (ry + 1) * HW + H + cx * VEC;
+  int hhalo = -1;
+  if (tid < G::VPR) hhalo = H + tid * VEC;                                     // row y0-1
+  else if (tid < 2 * G::VPR) hhalo = (BY + 1) * HW + H + (tid - G::VPR) * VEC;  // row y0+BY
+  else if (tid < 2 * G::VPR + BY) hhalo = (tid - 2 * G::VPR + 1) * HW;          // x0-H .. x0-1
+  else if (tid < G::NHALO) hhalo = (tid - 2 * G::VPR - BY + 1) * HW + H + BX;   // x0+BX ..
+  const int gx = x0 + cx * VEC, gy = y0 + ry;
+  const bool inside = gy < a.g.ny && gx < a.g.nx;
+  const long long gofs = (long long)gy * a.g.pitch + gx;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int q) {  // planes z0-1+q of every halo'd operand, one thread
+    const int s = q % S, p = z0 - 1 + q;
+    mbar_expect_tx(&mbar[s], NIN * G::HBOX * (uint32_t)sizeof(T));
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) tma_load_3d(stage0 + (s * NIN + i) * HSTR, &a.tm_in[i], x0 - H, y0 - 1, p + 1, &mbar[s]);
+  };
+  auto prefetch = [&](int k) {  // coefficient (+ rhat) tiles of plane k into L2
+    if (k < z1) {
+#pragma unroll
+      for (int d = 0; d < 6; ++d) tma_prefetch_3d(&a.tm_c[d], x0, y0, k);
+      if (MODE == MODE_H1) tma_prefetch_3d(&a.tm_aux, x0, y0, k + 1);
+    }
+  };
+  if (tid == 0) {
+    for (int q = 0; q < min(S, np); ++q) issue(q);
+    for (int k = z0; k < z0 + a.pf; ++k) prefetch(k);
+  }
+  // coefficients (+ rhat) of a plane straight into registers, one plane ahead
+  const T *const *cp = reinterpret_cast<const T *const *>(a.cptr);
+  P cn[6], rhn;
+  auto load_coefs = [&](int k) {
+    if (inside && k < z1) {
+      const long long o = (long long)k * a.g.plane + gofs;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) cn[d] = P::ldg(cp[d] + o);
+      if (MODE == MODE_H1) rhn = P::ldg(reinterpret_cast<const T *>(a.aux) + o + a.g.plane);
+    } else {
+#pragma unroll
+      for (int d = 0; d < 6; ++d) cn[d] = P::zero();
+      rhn = P::zero();
+    }
+  };
+  load_coefs(z0);
+
+  typename P::S beta_s{}, momega_s{}, malpha_s{};
+  if (MODE == MODE_H1) {
+    beta_s = P::scalar(a.red.st->beta);
+    momega_s = P::neg(P::scalar(a.red.st->omega));
+  } else if (MODE == MODE_H2) {
+    malpha_s = P::neg(P::scalar(a.red.st->alpha));
+  }
+  // SpMV input at box offset h of staged plane q
+  auto form = [&](int q, int h) -> P {
+    const T *in = stage0 + (q % S) * NIN * HSTR;
+    P o = P::ld(in + h);
+    if (MODE == MODE_H1) o = P::fmas(beta_s, P::fmas(momega_s, P::ld(in + 2 * HSTR + h), P::ld(in + HSTR + h)), o);
+    else if (MODE == MODE_H2) o = P::fmas(malpha_s, P::ld(in + HSTR + h), o);
+    return o;
+  };
+  auto wait = [&](int q) { mbar_wait(&mbar[q % S], (uint32_t)((q / S) & 1)); };
+
+  // prologue: planes z0-1 (own column only) and z0 (own + halo into U ring)
+  wait(0);
+  P um = form(0, hown);
+  wait(1);
+  P uc = form(1, hown);
+  uc.st(U + 1 * HSTR + hown);
+  if (hhalo >= 0) form(1, hhalo).st(U + 1 * HSTR + hhalo);
+  __syncthreads();
+  if (tid == 0) {
+    if (S < np) issue(S);
+    if (S + 1 < np) issue(S + 1);
+  }
+
+  float dacc[ND][4];
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dacc[d][i] = 0.0f;
+
+  for (int k = z0; k < z1; ++k) {
+    const int qc = k - z0 + 1, qn = qc + 1;
+    P c[6], rh;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) c[d] = cn[d];
+    rh = rhn;
+    load_coefs(k + 1);  // in flight during this plane's work
+    if (tid == 0 && a.pf > 0) prefetch(k + a.pf);
+    // SpMV input of plane k+1
+    wait(qn);
+    T *Un = U + (qn % 3) * HSTR;
+    const P up = form(qn, hown);
+    up.st(Un + hown);
+    if (hhalo >= 0) form(qn, hhalo).st(Un + hhalo);
+    __syncthreads();
+    if (tid == 0 && qn + S < np) issue(qn + S);  // stage of plane k+1 is consumed
+    // u_k = v_k + sum of the six products (order xm, xp, ym, yp, zm, zp)
+    const T *Uc = U + (qc % 3) * HSTR;
+    P acc = uc;
+    acc = P::fma(c[0], Shift<T>::left(uc, Shift<T>::ld1(Uc + hown - 1)), acc);
+    acc = P::fma(c[1], Shift<T>::right(uc, Shift<T>::ld1(Uc + hown + VEC)), acc);
+    acc = P::fma(c[2], P::ld(Uc + hown - HW), acc);
+    acc = P::fma(c[3], P::ld(Uc + hown + HW), acc);
+    acc = P::fma(c[4], um, acc);
+    acc = P::fma(c[5], up, acc);
+    if (inside) {
+      const long long o = (long long)(k + 1) * a.g.plane + gofs;
+      acc.st(reinterpret_cast<T *>(a.out0) + o);
+      if (MODE != MODE_APPLY) uc.st(reinterpret_cast<T *>(a.out1) + o);
+    }
+    if (MODE == MODE_H1) {
+      rh.dot4(acc, dacc[0]);  // (rhat, v')
+    } else if (MODE == MODE_H2) {
+      acc.dot4(uc, dacc[0]);        // (t, s)
+      acc.dot4(acc, dacc[ND - 1]);  // (t, t)
+    }
+    um = uc;
+    uc = up;
+  }
+
+  if (MODE != MODE_APPLY) {
+    float v[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) v[d] = sum4(dacc[d]);
+    if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(v, a.red, scratch);
+    else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch);
+  }
+}
+
+// ============================================================ row strips ==
+// k_rows: a CTA owns BY complete mesh rows (all of x) and marches z.  With no x
+// halo every TMA box row is whole 128-B lines of this CTA's own rows, and the
+// only re-read data are the two y-halo rows, which the y-neighbour CTAs (next
+// blockIdx) read at about the same time (L2 hits).  A strip plane of one
+// operand arrives as pitch/64 TMA boxes of 64 x (BY+2) elements; shared memory
+// holds them box-major, element (row r, x) at (x/64)*(BY+2)*64 + r*64 + x%64.
+constexpr int kRowBox = 64;  // elements per TMA box row (128 B fp16, 256 B fp32)
+
+template <typename T, int MODE, int BY, int S>
+__global__ void __launch_bounds__(512, 1) k_rows(const __grid_constant__ StencilArgs a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC, W = kRowBox, RB = BY + 2;
+  constexpr int NIN = MODE == MODE_H1 ? 3 : (MODE == MODE_H2 ? 2 : 1);
+  constexpr int ND = MODE == MODE_H2 ? 2 : 1;
+
+  if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
+
+  const int pitch = a.g.pitch;
+  const int nb = pitch / W;                 // boxes per strip row
+  const int astr = nb * RB * W;             // elements per staged operand (128-B multiple)
+  const int vpr = (a.g.nx + VEC - 1) / VEC; // point-holding vectors per row
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);
+  T *stage0 = reinterpret_cast<T *>(smem + 128);  // [S][NIN][astr]
+  T *U = stage0 + S * NIN * astr;                 // [3][astr]
+  __shared__ float scratch[32 * kMaxDots];
+
+  const int ty = blockIdx.x % a.tiles_y;  // y-neighbours are consecutive CTAs
+  const int ch = blockIdx.x / a.tiles_y;
+  const int y0 = ty * BY;
+  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int np = z1 - z0 + 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  auto sidx = [&](int r, int x) { return (x / W) * (RB * W) + r * W + (x % W); };
+  const int ry = tid / vpr, cx = tid - (tid / vpr) * vpr;
+  const int x = cx * VEC;
+  const bool active = ry < BY;  // blockDim may be rounded up to whole warps
+  const int hown = active ? sidx(ry + 1, x) : 0;
+  const int hleft = (active && x > 0) ? sidx(ry + 1, x - 1) : -1;
+  // U columns >= vpr*VEC are never formed: a right neighbour at x+VEC >= nx is
+  // outside the mesh and must be an exact zero (0 * stale data could be NaN)
+  const int hright = (active && x + VEC < a.g.nx) ? sidx(ry + 1, x + VEC) : -1;
+  int hhalo = -1;
+  if (tid < 2 * vpr) hhalo = sidx(tid < vpr ? 0 : RB - 1, (tid % vpr) * VEC);
+  const int gy = y0 + ry;
+  const bool inside = active && gy < a.g.ny;
+  const long long gofs = (long long)gy * pitch + x;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int q) {  // warp 0: lane j issues box j of every operand
+    const int s = q % S, p = z0 - 1 + q;
+    if (lane == 0) mbar_expect_tx(&mbar[s], (uint32_t)(NIN * nb * RB * W * (int)sizeof(T)));
+    __syncwarp();
+    for (int j = lane; j < nb; j += 32)
+#pragma unroll
+      for (int i = 0; i < NIN; ++i)
+        tma_load_3d(stage0 + (s * NIN + i) * astr + j * RB * W, &a.tm_in[i], j * W, y0 - 1, p + 1, &mbar[s]);
+  };
+  if (warp == 0)
+    for (int q = 0; q < min(S, np); ++q) issue(q);
+
+  const T *const *cp = reinterpret_cast<const T *const *>(a.cptr);
+  P cn[6], rhn;
+  auto load_coefs = [&](int k) {
+    if (inside && k < z1) {
+      const long long o = (long long)k * a.g.plane + gofs;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) cn[d] = P::ldg(cp[d] + o);
+      if (MODE == MODE_H1) rhn = P::ldg(reinterpret_cast<const T *>(a.aux) + o + a.g.plane);
+    } else {
+#pragma unroll
+      for (int d = 0; d < 6; ++d) cn[d] = P::zero();
+      rhn = P::zero();
+    }
+  };
+  load_coefs(z0);
+
+  typename P::S beta_s{}, momega_s{}, malpha_s{};
+  if (MODE == MODE_H1) {
+    beta_s = P::scalar(a.red.st->beta);
+    momega_s = P::neg(P::scalar(a.red.st->omega));
+  } else if (MODE == MODE_H2) {
+    malpha_s = P::neg(P::scalar(a.red.st->alpha));
+  }
+  auto form = [&](int q, int h) -> P {
+    const T *in = stage0 + (q % S) * NIN * astr;
+    P o = P::ld(in + h);
+    if (MODE == MODE_H1) o = P::fmas(beta_s, P::fmas(momega_s, P::ld(in + 2 * astr + h), P::ld(in + astr + h)), o);
+    else if (MODE == MODE_H2) o = P::fmas(malpha_s, P::ld(in + astr + h), o);
+    return o;
+  };
+  auto wait = [&](int q) { mbar_wait(&mbar[q % S], (uint32_t)((q / S) & 1)); };
+
+  wait(0);
+  P um = form(0, hown);
+  wait(1);
+  P uc = form(1, hown);
+  if (active) uc.st(U + 1 * astr + hown);
+  if (hhalo >= 0) form(1, hhalo).st(U + 1 * astr + hhalo);
+  __syncthreads();
+  if (warp == 0) {
+    if (S < np) issue(S);
+    if (S + 1 < np) issue(S + 1);
+  }
+
+  float dacc[ND][4];
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dacc[d][i] = 0.0f;
+
+  for (int k = z0; k < z1; ++k) {
+    const int qc = k - z0 + 1, qn = qc + 1;
+    P c[6], rh;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) c[d] = cn[d];
+    rh = rhn;
+    load_coefs(k + 1);
+    wait(qn);
+    T *Un = U + (qn % 3) * astr;
+    const P up = form(qn, hown);
+    if (active) up.st(Un + hown);
+    if (hhalo >= 0) form(qn, hhalo).st(Un + hhalo);
+    __syncthreads();
+    if (warp == 0 && qn + S < np) issue(qn + S);
+    const T *Uc = U + (qc % 3) * astr;
+    P acc = uc;
+    const auto zl = Shift<T>::ld1(Uc + (hleft >= 0 ? hleft : hown)), zr = Shift<T>::ld1(Uc + (hright >= 0 ? hright : hown));
+    acc = P::fma(c[0], Shift<T>::left(uc, hleft >= 0 ? zl : decltype(zl)(0)), acc);
+    acc = P::fma(c[1], Shift<T>::right(uc, hright >= 0 ? zr : decltype(zr)(0)), acc);
+    acc = P::fma(c[2], P::ld(Uc + hown - W), acc);
+    acc = P::fma(c[3], P::ld(Uc + hown + W), acc);
+    acc = P::fma(c[4], um, acc);
+    acc = P::fma(c[5], up, acc);
+    if (inside) {
+      const long long o = (long long)(k + 1) * a.g.plane + gofs;
+      acc.st(reinterpret_cast<T *>(a.out0) + o);
+      if (MODE != MODE_APPLY) uc.st(reinterpret_cast<T *>(a.out1) + o);
+    }
+    if (MODE == MODE_H1 && active) {
+      rh.dot4(acc, dacc[0]);
+    } else if (MODE == MODE_H2 && active) {
+      acc.dot4(uc, dacc[0]);
+      acc.dot4(acc, dacc[ND - 1]);
+    }
+    um = uc;
+    uc = up;
+  }
+
+  if (MODE != MODE_APPLY) {
+    float v[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) v[d] = sum4(dacc[d]);
+    if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(v, a.red, scratch);
+    else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch);
+  }
+}
+
+size_t rows_smem_bytes(int mode, int esz, int pitch, int by, int stages) {
+  const int nin = mode == MODE_H1 ? 3 : (mode == MODE_H2 ? 2 : 1);
+  const size_t astr = (size_t)(pitch / kRowBox) * (by + 2) * kRowBox * esz;
+  return 128 + (size_t)stages * nin * astr + 3 * astr;
+}
+
+template <typename T>
+int rows_threads(int nx, int by) {
+  const int vpr = (nx + Pack<T>::VEC - 1) / Pack<T>::VEC;
+  return (vpr * by + 31) / 32 * 32;
+}
+
+// ------------------------------------------------------------ host side --
+namespace {
+template <typename T, int MODE, int BY, int S>
+int launch_rows(const StencilArgs &a, cudaStream_t s) {
+  const size_t smem = rows_smem_bytes(MODE, (int)sizeof(T), a.g.pitch, BY, S);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_rows<T, MODE, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = smem;
+  }
+  const int grid = a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  k_rows<T, MODE, BY, S><<<grid, rows_threads<T>(a.g.nx, BY), smem, s>>>(a);
+  return (int)cudaGetLastError();
+}
+template <typename T, int MODE>
+int launch_rows_mode(const StencilArgs &a, int by, int stages, cudaStream_t s) {
+  if (by == 2 && stages == 3) return launch_rows<T, MODE, 2, 3>(a, s);
+  if (by == 2 && stages == 4) return launch_rows<T, MODE, 2, 4>(a, s);
+  if (by == 4 && stages == 3) return launch_rows<T, MODE, 4, 3>(a, s);
+  if (by == 4 && stages == 4) return launch_rows<T, MODE, 4, 4>(a, s);
+  if (by == 8 && stages == 3) return launch_rows<T, MODE, 8, 3>(a, s);
+  return (int)cudaErrorInvalidValue;
+}
+}  // namespace
+
+bool rows_config_ok(int by, int stages) {
+  return ((by == 2 || by == 4) && (stages == 3 || stages == 4)) || (by == 8 && stages == 3);
+}
+
+template <typename T>
+int rows_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s) {
+  if (mode == MODE_H1) return launch_rows_mode<T, MODE_H1>(a, by, stages, s);
+  if (mode == MODE_H2) return launch_rows_mode<T, MODE_H2>(a, by, stages, s);
+  return launch_rows_mode<T, MODE_APPLY>(a, by, stages, s);
+}
+template int rows_launch<float>(int, const StencilArgs &, int, int, cudaStream_t);
+template int rows_launch<__half>(int, const StencilArgs &, int, int, cudaStream_t);
+template int rows_threads<float>(int, int);
+template int rows_threads<__half>(int, int);
+
+// ------------------------------------------------------------ host side --
+namespace {
+template <typename T, int MODE, int BY, int S>
+int launch_one(const StencilArgs &a, cudaStream_t s) {
+  using G = Geo<T, MODE, BY>;
+  constexpr size_t smem = smem_bytes_c<T, MODE, BY, S>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  k_stencil<T, MODE, BY, S><<<grid, G::NT, smem, s>>>(a);
+  return (int)cudaGetLastError();
+}
+template <typename T, int MODE>
+int launch_mode(const StencilArgs &a, int by, int stages, cudaStream_t s) {
+  if (by == 8 && stages == 3) return launch_one<T, MODE, 8, 3>(a, s);
+  if (by == 8 && stages == 4) return launch_one<T, MODE, 8, 4>(a, s);
+  if (by == 16 && stages == 3) return launch_one<T, MODE, 16, 3>(a, s);
+  if (by == 16 && stages == 4) return launch_one<T, MODE, 16, 4>(a, s);
+  if (by == 4 && stages == 4) return launch_one<T, MODE, 4, 4>(a, s);
+  return (int)cudaErrorInvalidValue;
+}
+template <typename T, int MODE>
+size_t smem_mode(int by, int stages) {
+  if (by == 8 && stages == 3) return smem_bytes_c<T, MODE, 8, 3>();
+  if (by == 8 && stages == 4) return smem_bytes_c<T, MODE, 8, 4>();
+  if (by == 16 && stages == 3) return smem_bytes_c<T, MODE, 16, 3>();
+  if (by == 16 && stages == 4) return smem_bytes_c<T, MODE, 16, 4>();
+  if (by == 4 && stages == 4) return smem_bytes_c<T, MODE, 4, 4>();
+  return 0;
+}
+}  // namespace
+
+bool stencil_config_ok(int by, int stages) {
+  return (by == 8 && (stages == 3 || stages == 4)) || (by == 16 && (stages == 3 || stages == 4)) ||
+         (by == 4 && stages == 4);
+}
+
+template <typename T>
+int stencil_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s) {
+  if (mode == MODE_H1) return launch_mode<T, MODE_H1>(a, by, stages, s);
+  if (mode == MODE_H2) return launch_mode<T, MODE_H2>(a, by, stages, s);
+  return launch_mode<T, MODE_APPLY>(a, by, stages, s);
+}
+template <typename T>
+size_t stencil_smem_bytes(int mode, int by, int stages) {
+  if (mode == MODE_H1) return smem_mode<T, MODE_H1>(by, stages);
+  if (mode == MODE_H2) return smem_mode<T, MODE_H2>(by, stages);
+  return smem_mode<T, MODE_APPLY>(by, stages);
+}
+template <typename T>
+int stencil_threads(int by) {
+  return (tile_bx<T>() / Pack<T>::VEC) * by;
+}
+
+template int stencil_launch<float>(int, const StencilArgs &, int, int, cudaStream_t);
+template int stencil_launch<__half>(int, const StencilArgs &, int, int, cudaStream_t);
+template size_t stencil_smem_bytes<float>(int, int, int);
+template size_t stencil_smem_bytes<__half>(int, int, int);
+template int stencil_threads<float>(int);
+template int stencil_threads<__half>(int);
+
+}  // namespace sten

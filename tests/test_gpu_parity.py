@@ -72,17 +72,27 @@ def test_spmv_bitwise_vs_mirror_and_tolerance_vs_o64(sten, mesh, prec):
     st.close()
 
 
-@pytest.mark.parametrize("tiling", [(8, 1, 1, 2), (16, 3, 5, 3), (32, 16, 7, 8), (0, 5, 64, 6)])
+ROWS = 1 << 20  # bx >= nx selects the full-row strip kernel
+TILE = {"fp32": 64, "mixed": 128}  # bx = tile width selects the x-halo tile kernel
+
+
+@pytest.mark.parametrize("tiling", [("tile", 16, 5, 3), ("tile", 8, 7, 4), ("tile", 4, 64, 4), ("tile", 16, 2, 4),
+                                    ("rows", 2, 3, 4), ("rows", 4, 5, 3), ("rows", 2, 64, 3), ("rows", 8, 1, 3)])
+@pytest.mark.parametrize("mesh", [(45, 23, 17), (136, 9, 11), (256, 12, 6)])
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-def test_spmv_tilings_and_pipeline_depths(sten, tiling, prec):
+def test_spmv_tilings_and_pipeline_depths(sten, tiling, mesh, prec):
     torch = torch_cuda()
-    nx, ny, nz = 45, 23, 17
+    nx, ny, nz = mesh
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=3)
     st = gpu_stencil(diag, offs)
-    bx, by, zc, stages = tiling
-    if prec == "fp32" and bx == 0:
-        bx = 4 * 5
-    sten.set_tiling(st, PREC[prec], bx, by, zc, stages)
+    kind, by, zc, stages = tiling
+    bx = ROWS if kind == "rows" else TILE[prec]
+    try:
+        sten.set_tiling(st, PREC[prec], bx, by, zc, stages)
+    except sten.StenError:
+        assert kind == "rows" and by == 8  # a strip wider than one CTA is refused
+        st.close()
+        return
     cq = oracle_coeffs(diag, offs, prec)
     v = quantize_vec(np.random.default_rng(1).uniform(-1, 1, (nz, ny, nx)), prec)
     vt = to_gpu_vec(v, prec)
