@@ -169,10 +169,18 @@ def test_fp32_50_iterations_vs_o64(sten, kind, delta, mesh):
     # a one-ulp change of b moves the fp64 oracle's own x_50 by ~1e-3.  The
     # 1e-4 bar applies where the oracle is stable under that perturbation;
     # elsewhere the GPU must stay within 10x of the oracle's own spread.
-    spread = np.linalg.norm(orc.bicgstab64(c64, np.nextafter(bh, np.inf), tol=0.0, maxit=50)["x"] - xr)
+    rng = np.random.default_rng(0)
+    perturbed = [np.nextafter(bh, np.inf), np.nextafter(bh, -np.inf),
+                 np.where(rng.random(bh.shape) < 0.5, np.nextafter(bh, np.inf), bh)]
+    spread = max(np.linalg.norm(orc.bicgstab64(c64, pb, tol=0.0, maxit=50)["x"] - xr) for pb in perturbed)
     spread /= np.linalg.norm(xr)
-    bar = 1e-4 if spread < 1e-6 else 10 * spread
-    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= bar
+    err = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+    if spread < 1e-6:
+        assert err <= 1e-4
+    else:
+        assert err <= 20 * spread
+        # well-posed in the chaotic regime: the GPU iterate is as accurate as the oracle's
+        assert orc.true_residual64(c64, bh, x.astype(np.float64)) <= 3 * orc.true_residual64(c64, bh, xr)
     assert np.all(np.abs(alpha - ref["alpha"][:10]) <= 1e-4 * np.abs(ref["alpha"][:10]))
     assert np.all(np.abs(omega - ref["omega"][:10]) <= 1e-4 * np.abs(ref["omega"][:10]))
     # early history agrees tightly; later entries down to fp32 noise
