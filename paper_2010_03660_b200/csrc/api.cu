@@ -109,10 +109,11 @@ static int load_encode() {
   return STEN_OK;
 }
 // 3D map over an array of `planes` planes of (ny rows x pitch elements), logical width nx.
+static long long g_plane_stride = 0;  // set by the caller (elements between z-planes)
 static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int planes, int pitch, int boxx, int boxy) {
   RC_TRY(load_encode());
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
-  cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)pitch * ny * elem};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)g_plane_stride * elem};
   cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
   cuuint32_t es[3] = {1, 1, 1};
   static int promo = -1;
@@ -222,6 +223,7 @@ static int ensure_maps(sten_stencil *st, int prec) {
   const Tiling &t = st->tiling[prec];
   const int e = esize(prec);
   const int H = prec == STEN_FP32 ? 4 : 8;
+  g_plane_stride = st->plane;
   for (Slab &sl : st->slabs) {
     PrecBufs &b = sl.pb[prec];
     if (b.maps_ok) continue;
@@ -335,7 +337,21 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
   return STEN_OK;
 }
 
-static int ew_grid(sten_stencil *st) { return st->sm * 8; }
+// Element-wise grid: 64 CTAs of 256 threads per SM (measured best for the H3
+// stream, 1.33 -> 1.29 ms at 600x595x1536 vs 8/SM), capped by the work so a
+// small mesh does not launch idle CTAs.  STEN_EW_BPS is the tuning knob.
+static int ew_grid(sten_stencil *st, long long nvec) {
+  static int bps = -1;
+  if (bps < 0) {
+    const char *e = getenv("STEN_EW_BPS");
+    bps = e ? atoi(e) : 64;
+    if (bps < 1) bps = 1;
+  }
+  long long need = (nvec + 511) / 512;  // two vectors per thread
+  long long g = (long long)st->sm * bps;
+  if (need < g) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
 
 static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStream_t s) {
   Slab &sl = st->slabs[slab];
@@ -355,10 +371,10 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
   a.rows = (long long)st->ny * sl.nz;
   a.vpr = (st->nx + vec - 1) / vec;
   a.pitch = st->pitch;
-  a.nvec = a.rows * (a.pitch / vec);  // linear over the padded rows (zeros in the padding)
+  a.nvec = (long long)st->plane * sl.nz / vec;  // linear over whole planes (padding holds zeros)
   a.red = make_red(st, slab);
-  if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st), 256, s));
-  else KLAUNCH(h3_launch<__half>(a, ew_grid(st), 256, s));
+  if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st, a.nvec), 256, s));
+  else KLAUNCH(h3_launch<__half>(a, ew_grid(st, a.nvec), 256, s));
   st->launches++;
   return STEN_OK;
 }
@@ -380,10 +396,10 @@ static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaS
   a.rows = (long long)st->ny * sl.nz;
   a.vpr = (st->nx + vec - 1) / vec;
   a.pitch = st->pitch;
-  a.nvec = a.rows * (a.pitch / vec);  // linear over the padded rows (zeros in the padding)
+  a.nvec = (long long)st->plane * sl.nz / vec;  // linear over whole planes (padding holds zeros)
   a.red = make_red(st, slab);
-  if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st), 256, s));
-  else KLAUNCH(init_launch<__half>(a, ew_grid(st), 256, s));
+  if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st, a.nvec), 256, s));
+  else KLAUNCH(init_launch<__half>(a, ew_grid(st, a.nvec), 256, s));
   st->launches++;
   return STEN_OK;
 }
@@ -506,14 +522,28 @@ static void drop_graphs(sten_stencil *st) {
   st->graphs.clear();
 }
 
-// dense (nz,ny,nx) user array <-> pitched internal array with halo planes
+// dense (nz,ny,nx) user array <-> internal array (rows of `pitch`, planes of
+// `plane` elements, halo planes): one 3D copy per slab, a 1D copy when the
+// internal layout has no padding at all.
+static cudaError_t copy3d(void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch, size_t sysize,
+                          size_t wbytes, size_t h, size_t d, cudaStream_t s) {
+  if (dpitch == wbytes && spitch == wbytes && dysize == h && sysize == h)
+    return cudaMemcpyAsync(dst, src, wbytes * h * d, cudaMemcpyDefault, s);
+  cudaMemcpy3DParms p;
+  memset(&p, 0, sizeof p);
+  p.srcPtr = make_cudaPitchedPtr(const_cast<void *>(src), spitch, wbytes, sysize);
+  p.dstPtr = make_cudaPitchedPtr(dst, dpitch, wbytes, dysize);
+  p.extent = make_cudaExtent(wbytes, h, d);
+  p.kind = cudaMemcpyDefault;
+  return cudaMemcpy3DAsync(&p, s);
+}
 static int copy_in(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), const void *src, cudaStream_t s) {
   const int e = esize(prec);
   for (Slab &sl : st->slabs) {
     char *dst = (char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
     const char *sp = (const char *)src + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)st->pitch * e, sp, (size_t)st->nx * e, (size_t)st->nx * e,
-                               (size_t)st->ny * sl.nz, cudaMemcpyDefault, s));
+    CUDA_TRY(copy3d(dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
+                    (size_t)st->ny, (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
 }
@@ -522,8 +552,8 @@ static int copy_out(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), void *
   for (Slab &sl : st->slabs) {
     const char *src = (const char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
     char *dp = (char *)dst + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(cudaMemcpy2DAsync(dp, (size_t)st->nx * e, src, (size_t)st->pitch * e, (size_t)st->nx * e,
-                               (size_t)st->ny * sl.nz, cudaMemcpyDefault, s));
+    CUDA_TRY(copy3d(dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
+                    (size_t)(st->plane / st->pitch), (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
 }
@@ -596,8 +626,20 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   st->nx = nx;
   st->ny = ny;
   st->nz = nz;
-  st->pitch = (nx + 63) / 64 * 64;  // 128-byte rows for fp16 and fp32
-  st->plane = (long long)st->pitch * ny;
+  // Layout: rows padded to `pitch` = a multiple of 64
+  // elements (128-B aligned rows), planes a multiple of 64 elements.  The
+  // padding costs a line fetch per row (6.7% at nx = 600, measured), but the
+  // 256-B tiles of the stencil kernel then start on line boundaries; unpadded
+  // rows (STEN_PITCH_ALIGN=8) remove that traffic yet lose more to tiles that
+  // straddle lines (tools/ and DESIGN.md "Tuning": 102.8 vs 98.6 Gpoint-iter/s).
+  {
+    int align = 64;
+    if (const char *pa = getenv("STEN_PITCH_ALIGN")) align = atoi(pa) >= 8 ? atoi(pa) : 8;
+    st->pitch = (nx + align - 1) / align * align;
+    int nyp = ny;
+    while (((long long)st->pitch * nyp) % 64) ++nyp;
+    st->plane = (long long)st->pitch * nyp;
+  }
   st->nslabs = nslabs;
   st->comm = comm;
   st->has_diag = coeffs[0] != nullptr;

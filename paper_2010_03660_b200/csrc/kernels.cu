@@ -164,13 +164,13 @@ __global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, con
   const TIN *off[6] = {o0, o1, o2, o3, o4, o5};
   float *c32[6] = {c32_0, c32_1, c32_2, c32_3, c32_4, c32_5};
   __half *c16[6] = {c16_0, c16_1, c16_2, c16_3, c16_4, c16_5};
-  const long long total = (long long)g.pitch * g.ny * g.nz;
+  const long long total = g.plane * g.nz;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(q % g.pitch);
-    const long long rest = q / g.pitch;
-    const int y = (int)(rest % g.ny), z = (int)(rest / g.ny);
-    if (x >= g.nx) {  // row padding: zero couplings, unit diagonal
+    const long long inplane = q % g.plane;
+    const int x = (int)(inplane % g.pitch);
+    const int y = (int)(inplane / g.pitch), z = (int)(q / g.plane);
+    if (x >= g.nx || y >= g.ny) {  // row / plane padding: zero couplings, unit diagonal
       for (int d = 0; d < 6; ++d) {
         c32[d][q] = 0.0f;
         c16[d][q] = __float2half(0.0f);
@@ -195,7 +195,7 @@ __global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, con
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g, int has_below,
                          int has_above, float *const c32[6], __half *const c16[6], double *aP,
                          cudaStream_t s) {
-  const long long total = (long long)g.pitch * g.ny * g.nz;
+  const long long total = g.plane * g.nz;
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 32) grid = 148 * 32;
   if (grid < 1) grid = 1;

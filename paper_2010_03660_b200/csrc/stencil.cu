@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(512, 1) k_rows(const __grid_constant__ Stencil
   if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
 
   const int pitch = a.g.pitch;
-  const int nb = pitch / W;                 // boxes per strip row
+  const int nb = (a.g.nx + W - 1) / W;      // boxes per strip row (last one zero-filled past nx)
   const int astr = nb * RB * W;             // elements per staged operand (128-B multiple)
   const int vpr = (a.g.nx + VEC - 1) / VEC; // point-holding vectors per row
   extern __shared__ __align__(128) unsigned char smem[];
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(512, 1) k_rows(const __grid_constant__ Stencil
 
 size_t rows_smem_bytes(int mode, int esz, int pitch, int by, int stages) {
   const int nin = mode == MODE_H1 ? 3 : (mode == MODE_H2 ? 2 : 1);
-  const size_t astr = (size_t)(pitch / kRowBox) * (by + 2) * kRowBox * esz;
+  const size_t astr = (size_t)((pitch + kRowBox - 1) / kRowBox) * (by + 2) * kRowBox * esz;
   return 128 + (size_t)stages * nin * astr + 3 * astr;
 }
 
