@@ -67,6 +67,23 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def measured_traffic(kernel_prefix: str):
+    """DRAM bytes per launch of the dominant kernel from the latest committed ncu
+    capture (profiles/<round>_traffic.json, full-size cfg3 launches)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for path in reversed(files):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        for k, launches in d.get("kernels", {}).items():
+            if k.startswith(kernel_prefix) and launches:
+                return (float(np.mean([x["traffic_bytes"] for x in launches])),
+                        os.path.relpath(path, ROOT))
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -191,14 +208,13 @@ def run_sten(args):
     workload = args.workload if args.workload != "auto" else ("cfg3" if n == 1 else "cfg5")
     prec = sten.MIXED if args.precision == "mixed" else sten.FP32
     tdt = torch.float16 if prec == sten.MIXED else torch.float32
-    nzl = args.nz
-    z0 = rank * nzl
+    from paper_2010_03660_b200 import dist as sdist
+    # weak scaling (config 5): every rank owns one args.nz-plane slab of the global mesh
+    z0, nzl = sdist.slab_of(rank, world, args.nz * world)
 
     comm = None
     if world > 1:
-        uid = [sten.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = sten.comm_create(uid[0], world, rank)
+        comm = sdist.bootstrap_comm(sten, rank, world)
 
     # problem: fields of this rank's slab generated on the device (inputs/gen_cuda.cu)
     kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
@@ -249,11 +265,7 @@ def run_sten(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    t_ms = sdist.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     it, hist, status = last
     value = npts * maxit * args.steps / (t_ms / 1e3) / 1e9
 
@@ -270,11 +282,7 @@ def run_sten(args):
         for _ in range(args.steps):
             _, hh, _ = sten.bicgstab_solve(st, prec, bh, None, 0.0, maxit, xh)
         torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+        te = sdist.max_over_ranks(time.perf_counter() - t0, device="cuda")
         esz = b.element_size()
         e2e = {"value": npts * maxit * args.steps / te / 1e9, "unit": "Gpoint-iter/s",
                "h2d_bytes_per_step": npts_local * esz, "d2h_bytes_per_step": npts_local * esz + 8 * (maxit + 1)}
@@ -292,6 +300,9 @@ def run_sten(args):
     achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
     bpi = roofline.bytes_per_point_iter(pname)
     whole_gbs = npts_local * maxit * args.steps * bpi / (t_ms / 1e3) / 1e9
+    traffic, traffic_src = (None, None)
+    if prec == sten.MIXED and nzl == NZ and not args.tiling:
+        traffic, traffic_src = measured_traffic("k_stencil<__half, 1")
     line = {
         "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -305,7 +316,7 @@ def run_sten(args):
                    "status": sten.STATUS_NAMES.get(status, status), "final_rel_residual": float(hist[-1])},
         "roofline": {"bound": "hbm", "kernel": "k_stencil<half,H1>" if prec == sten.MIXED else "k_stencil<float,H1>",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": h1_bytes, "avg_launch_ms": h1_avg_ms,
                      "phase_ms_per_iter": [p / max(h1_n, 1) for p in ph_ms]},
         "gpu_launches": int(launches),
