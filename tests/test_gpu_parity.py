@@ -325,6 +325,32 @@ def test_deterministic_repeat(sten, prec):
     st.close()
 
 
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_nccl_single_rank_path_is_bitwise_identical(sten, prec):
+    # The multi-rank path (slab sums -> ncclAllReduce fp32 -> scalar kernel, all
+    # captured in the solve's CUDA graph) run on a 1-rank NCCL communicator must
+    # reproduce the single-GPU path exactly: a 1-rank all-reduce is the identity.
+    torch = torch_cuda()
+    nx, ny, nz = 40, 21, 16
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=9)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=9), prec)
+    st1 = gpu_stencil(diag, offs)
+    x1, it1, h1, _ = _solve(sten, st1, prec, b, 0.0, 20)
+    comm = sten.comm_create(sten.comm_unique_id(), 1, 0)
+    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+    stc = sten.stencil_create(nx, ny, nz, coeffs, nslabs=2, comm=comm)
+    xc, itc, hc, _ = _solve(sten, stc, prec, b, 0.0, 20)
+    stn = gpu_stencil(diag, offs, nslabs=2)
+    xn, itn, hn, _ = _solve(sten, stn, prec, b, 0.0, 20)
+    assert itc == it1 == 20
+    assert np.array_equal(hc, hn) and np.array_equal(xc, xn)  # comm path == loopback path, bitwise
+    assert np.all(np.abs(hc[:8] - h1[:8]) <= (1e-5 if prec == "fp32" else 5e-2) * h1[:8])
+    stc.close()
+    stn.close()
+    st1.close()
+    comm.close()
+
+
 def test_host_buffers_roundtrip(sten):
     # e2e path: host (pinned) b and x_out through the same C-ABI call
     torch = torch_cuda()
