@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--impl", default="sten", choices=["sten", "reference"])
     p.add_argument("--precision", default="mixed", choices=["mixed", "fp32"])
     p.add_argument("--maxit", type=int, default=100)
+    p.add_argument("--tol", type=float, default=0.0, help="0: exactly maxit iterations (config 3a)")
     p.add_argument("--workload", default="auto", choices=["auto", "cfg3", "cfg5"])
     p.add_argument("--nz", type=int, default=NZ, help="planes per GPU (debug / profiling)")
     p.add_argument("--no-e2e", action="store_true")
@@ -237,9 +238,10 @@ def run_sten(args):
         if world > 1:
             dist.barrier()
 
+    tol = args.tol
     sten.set_timing(st, True)
     for _ in range(args.warmup):
-        sten.bicgstab_solve(st, prec, b, None, 0.0, maxit, x)
+        sten.bicgstab_solve(st, prec, b, None, tol, maxit, x)
     torch.cuda.synchronize()
     barrier()
 
@@ -249,12 +251,14 @@ def run_sten(args):
     launches = 0
     h1_ms, h1_n = 0.0, 0
     ph_ms = [0.0, 0.0, 0.0]
+    iters_done = 0
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
     last = None
     for _ in range(args.steps):
-        last = sten.bicgstab_solve(st, prec, b, None, 0.0, maxit, x)
+        last = sten.bicgstab_solve(st, prec, b, None, tol, maxit, x)
+        iters_done += last[0]
         s = sten.get_stats(st)
         launches += s["kernel_launches"]
         for p in range(3):
@@ -267,7 +271,7 @@ def run_sten(args):
     clk = clocks.stop()
     t_ms = sdist.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     it, hist, status = last
-    value = npts * maxit * args.steps / (t_ms / 1e3) / 1e9
+    value = npts * iters_done / (t_ms / 1e3) / 1e9
 
     # end to end through the same C-ABI call with pinned HOST buffers
     e2e = None
@@ -275,17 +279,20 @@ def run_sten(args):
         bh = b.cpu().pin_memory()
         xh = torch.empty_like(bh).pin_memory()
         sten.set_timing(st, False)
-        sten.bicgstab_solve(st, prec, bh, None, 0.0, maxit, xh)
+        sten.bicgstab_solve(st, prec, bh, None, tol, maxit, xh)
         barrier()
         torch.cuda.synchronize()
+        e_iters = 0
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            _, hh, _ = sten.bicgstab_solve(st, prec, bh, None, 0.0, maxit, xh)
+            e_it, hh, _ = sten.bicgstab_solve(st, prec, bh, None, tol, maxit, xh)
+            e_iters += e_it
         torch.cuda.synchronize()
         te = sdist.max_over_ranks(time.perf_counter() - t0, device="cuda")
         esz = b.element_size()
-        e2e = {"value": npts * maxit * args.steps / te / 1e9, "unit": "Gpoint-iter/s",
-               "h2d_bytes_per_step": npts_local * esz, "d2h_bytes_per_step": npts_local * esz + 8 * (maxit + 1)}
+        e2e = {"value": npts * e_iters / te / 1e9, "unit": "Gpoint-iter/s",
+               "h2d_bytes_per_step": npts_local * esz,
+               "d2h_bytes_per_step": npts_local * esz + 8 * (e_iters // max(args.steps, 1) + 1)}
 
     if rank != 0:
         if world > 1:
@@ -299,7 +306,7 @@ def run_sten(args):
     h1_bytes = roofline.phase_bytes("H1", pname, npts_local)
     achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
     bpi = roofline.bytes_per_point_iter(pname)
-    whole_gbs = npts_local * maxit * args.steps * bpi / (t_ms / 1e3) / 1e9
+    whole_gbs = npts_local * iters_done * bpi / (t_ms / 1e3) / 1e9
     traffic, traffic_src = (None, None)
     if prec == sten.MIXED and nzl == NZ and not args.tiling:
         traffic, traffic_src = measured_traffic("k_stencil<__half, 1")
@@ -309,7 +316,8 @@ def run_sten(args):
         "vs_baseline": value / PAPER_GPT_ITER_S,
         "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
         "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
-                   "precision": pname, "maxit": maxit, "tol": 0.0, "parallelism": f"zslab{n}",
+                   "precision": pname, "maxit": maxit, "tol": tol, "iters_per_solve": iters_done / args.steps,
+                   "parallelism": f"zslab{n}",
                    "l2": "no flush: 16.5 GB working set per GPU >> 126 MB L2",
                    "gflops": value * roofline.FLOPS_PER_POINT_ITER,
                    "hbm_frac_whole_step": whole_gbs / peak, "bytes_per_point_iter": bpi,
