@@ -248,6 +248,7 @@ static int ensure_maps(sten_stencil *st, int prec) {
 }
 
 static void drop_graphs(sten_stencil *st);
+static int ew_grid(sten_stencil *st, long long nvec);
 static int ensure_bufs(sten_stencil *st, int prec) {
   const size_t vbytes = (size_t)st->plane * esize(prec);
   for (Slab &sl : st->slabs) {
@@ -265,12 +266,15 @@ static int ensure_bufs(sten_stencil *st, int prec) {
   }
   if (st->tiling[prec].bx == 0) default_tiling(st, prec);
   RC_TRY(ensure_maps(st, prec));
-  // partial-sum buffer large enough for the largest grid
+  // partial-sum buffer: one slot per CTA of the largest grid of ANY reducing
+  // kernel - stencil tiles and the element-wise kernels (checked at launch too)
   int need = 0;
   for (Slab &sl : st->slabs) {
     const Tiling &t = st->tiling[prec];
     int g = ((st->nx + t.bx - 1) / t.bx) * ((st->ny + t.by - 1) / t.by) * ((sl.nz + t.zc - 1) / t.zc);
     if (g > need) need = g;
+    const int ge = ew_grid(st, (long long)st->plane * sl.nz / 4);  // vec = 4 gives the larger grid
+    if (ge > need) need = ge;
   }
   if (need < st->sm * 16) need = st->sm * 16;
   if (need > st->partials_cap) {
@@ -325,6 +329,8 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
   a.pf = st->coef_pf;
   a.tiles_x = t.rows ? 1 : (st->nx + t.bx - 1) / t.bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
+  if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + t.zc - 1) / t.zc) > st->partials_cap)
+    return set_err(STEN_ECUDA, "internal: stencil grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (t.rows) {
     if (prec == STEN_FP32) KLAUNCH(rows_launch<float>(mode, a, t.by, t.stages, s));
@@ -373,6 +379,8 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
   a.pitch = st->pitch;
   a.nvec = (long long)st->plane * sl.nz / vec;  // linear over whole planes (padding holds zeros)
   a.red = make_red(st, slab);
+  if (ew_grid(st, a.nvec) > st->partials_cap)
+    return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
   if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st, a.nvec), 256, s));
   else KLAUNCH(h3_launch<__half>(a, ew_grid(st, a.nvec), 256, s));
   st->launches++;
@@ -398,6 +406,8 @@ static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaS
   a.pitch = st->pitch;
   a.nvec = (long long)st->plane * sl.nz / vec;  // linear over whole planes (padding holds zeros)
   a.red = make_red(st, slab);
+  if (ew_grid(st, a.nvec) > st->partials_cap)
+    return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
   if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st, a.nvec), 256, s));
   else KLAUNCH(init_launch<__half>(a, ew_grid(st, a.nvec), 256, s));
   st->launches++;
