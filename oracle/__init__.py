@@ -15,7 +15,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["o64.c", "o16.c"]
+_SOURCES = ["o64.c", "o16.c", "osr.c"]
 
 ORC_CONVERGED, ORC_MAXIT, ORC_BREAKDOWN, ORC_NONFINITE = 0, 1, 2, 3
 
@@ -85,6 +85,15 @@ def _declare(L):
     L.o16_bicgstab.restype = _I
     L.o32_apply_fma.argtypes = [_I, _I, _I, _P, _P, _P]
     L.oracle_num_threads.restype = _I
+    L.o64_sr_sweep.argtypes = [_I, _I, _I, _P, _D, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P]
+    L.o16_sr_sweep.argtypes = [_I, _I, _I, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                               _P, _P, _P, _P, _P, _P, _P, _P]
+    L.o32_sr_sweep.argtypes = [_I, _I, _I, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                               _P, _P, _P, _P, _P, _P, _P, _P]
+    L.o64_sr_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
+    L.o64_sr_bicgstab.restype = _I
+    L.o16_sr_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
+    L.o16_sr_bicgstab.restype = _I
 
 
 def _ptr(a: np.ndarray):
@@ -137,8 +146,9 @@ def dot64(a, b):
     return lib().o64_dot(a.size, _ptr(a), _ptr(b))
 
 
-def bicgstab64(c, b, x0=None, tol=0.0, maxit=50):
-    """Returns dict(x, hist, iters, status, event_it, alpha, omega)."""
+def bicgstab64(c, b, x0=None, tol=0.0, maxit=50, schedule="classic"):
+    """Returns dict(x, hist, iters, status, event_it, alpha, omega).
+    schedule "classic": Alg. 1 as printed; "sr": the single-reduction schedule (osr.c)."""
     c = [_c(a, np.float64) for a in c]
     b = _c(b, np.float64)
     nz, ny, nx = b.shape
@@ -152,7 +162,8 @@ def bicgstab64(c, b, x0=None, tol=0.0, maxit=50):
     x0keep = None if x0 is None else _c(x0, np.float64)
     if x0keep is not None:
         x0p = _ptr(x0keep)
-    it = lib().o64_bicgstab(nx, ny, nz, _arr6(c), _ptr(b), x0p, float(tol), int(maxit),
+    fn = lib().o64_sr_bicgstab if schedule == "sr" else lib().o64_bicgstab
+    it = fn(nx, ny, nz, _arr6(c), _ptr(b), x0p, float(tol), int(maxit),
                             _ptr(x), _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
     return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value,
                 alpha=al[1: it + 1], omega=om[1: it + 1])
@@ -233,7 +244,7 @@ def dot16(a16, b16):
     return float(lib().o16_dot(nx, ny, nz, _ptr(a16), _ptr(b16)))
 
 
-def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False):
+def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False, schedule="classic"):
     c16 = [_c(a, np.uint16) for a in c16]
     b16 = _c(b16, np.uint16)
     nz, ny, nx = b16.shape
@@ -244,12 +255,58 @@ def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False):
     st = ctypes.c_int(-1)
     ev = ctypes.c_int(0)
     x0keep = None if x0 is None else _c(x0, np.uint16)
-    it = lib().o16_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
-                            None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
-                            int(bool(unfused)), _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
-                            ctypes.byref(st), ctypes.byref(ev))
+    if schedule == "sr":
+        if unfused:
+            raise ValueError("the SR schedule has only the fused (GPU-mirroring) variant")
+        it = lib().o16_sr_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
+                                   None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
+                                   _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
+                                   ctypes.byref(st), ctypes.byref(ev))
+    else:
+        it = lib().o16_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
+                                None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
+                                int(bool(unfused)), _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
+                                ctypes.byref(st), ctypes.byref(ev))
     return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value,
                 alpha=al[1: it + 1], omega=om[1: it + 1])
+
+
+# ---------------- single-reduction sweeps (osr.c) ----------------
+
+def sr_sweep64(c, scalars, rh, x, r, p, v, q, y):
+    """One SR sweep in fp64.  Returns (x, r, p, v, q, y, dots[12]) (new arrays)."""
+    c = [_c(a, np.float64) for a in c]
+    vecs = [_c(a, np.float64).copy() for a in (x, r, p, v, q, y)]
+    rh = _c(rh, np.float64)
+    nz, ny, nx = rh.shape
+    dots = np.zeros(12, np.float64)
+    a, w, b = (float(s) for s in scalars)
+    lib().o64_sr_sweep(nx, ny, nz, _arr6(c), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], _ptr(dots))
+    return (*vecs, dots)
+
+
+def sr_sweep16(c16, scalars, rh, x, r, p, v, q, y):
+    """One SR sweep, fp16 mirror (uint16 bit patterns; fp32 scalars and dots)."""
+    c16 = [_c(a, np.uint16) for a in c16]
+    vecs = [_c(a, np.uint16).copy() for a in (x, r, p, v, q, y)]
+    rh = _c(rh, np.uint16)
+    nz, ny, nx = rh.shape
+    dots = np.zeros(12, np.float32)
+    a, w, b = (float(np.float32(s)) for s in scalars)
+    lib().o16_sr_sweep(nx, ny, nz, _arr6(c16), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], _ptr(dots))
+    return (*vecs, dots)
+
+
+def sr_sweep32(c32, scalars, rh, x, r, p, v, q, y):
+    """One SR sweep, fp32 mirror of the GPU's element-wise order (dots in fp64)."""
+    c32 = [_c(a, np.float32) for a in c32]
+    vecs = [_c(a, np.float32).copy() for a in (x, r, p, v, q, y)]
+    rh = _c(rh, np.float32)
+    nz, ny, nx = rh.shape
+    dots = np.zeros(12, np.float64)
+    a, w, b = (float(np.float32(s)) for s in scalars)
+    lib().o32_sr_sweep(nx, ny, nz, _arr6(c32), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], _ptr(dots))
+    return (*vecs, dots)
 
 
 # ---------------- fp32 mirror ----------------

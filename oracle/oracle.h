@@ -117,6 +117,33 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
 void o32_apply_fma(int nx, int ny, int nz, const float *const c[6],
                    const float *v, float *u);
 
+/* ---------------- single-reduction schedule (osr.c, R19) -------- */
+/* One sweep: with scalars (alpha, omega, beta) of the previous iteration,
+ * update x, r, p in place, then v = A p, q = A r, y = A v, and the twelve
+ * inner products dots[] = (rh,v) (rh,r) (rh,q) (rh,y) (q,r) (q,v) (y,r) (y,v)
+ * (q,q) (q,y) (y,y) (r,r).  See osr.c for the derivation from Alg. 1. */
+void o64_sr_sweep(int nx, int ny, int nz, const double *const c[6], double alpha,
+                  double omega, double beta, const double *rh, double *x,
+                  double *r, double *p, double *v, double *q, double *y,
+                  double dots[12]);
+void o16_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alpha,
+                  float omega, float beta, const uint16_t *rh, uint16_t *x,
+                  uint16_t *r, uint16_t *p, uint16_t *v, uint16_t *q, uint16_t *y,
+                  float dots[12]);
+void o32_sr_sweep(int nx, int ny, int nz, const float *const c[6], float alpha,
+                  float omega, float beta, const float *rh, float *x, float *r,
+                  float *p, float *v, float *q, float *y, double dots[12]);
+/* Whole solves with the SR schedule; same arguments, outputs and control flow
+ * (stopping, events) as o64_bicgstab / o16_bicgstab. */
+int o64_sr_bicgstab(int nx, int ny, int nz, const double *const c[6],
+                    const double *b, const double *x0, double tol, int maxit,
+                    double *x, double *hist, double *alpha, double *omega,
+                    int *status, int *event_it);
+int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                    const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                    uint16_t *x, double *hist, float *alpha, float *omega,
+                    int *status, int *event_it);
+
 /* informational */
 int oracle_num_threads(void);
 

@@ -1,0 +1,255 @@
+"""Pins for the single-reduction (SR) BiCGStab oracle (oracle/osr.c, R19).
+
+The SR schedule is Alg. 1 rearranged so one sweep and one
+reduction serve an iteration.  It is pinned against references that do not
+share its arithmetic:
+  * the classic oracle o64_bicgstab (Alg. 1 as printed; pinned separately in
+    test_oracle_o64.py): in exact arithmetic the two produce the same iterates;
+  * numpy.linalg.solve (LAPACK) on a dense matrix assembled here;
+  * the algebraic identities the schedule relies on, evaluated with the
+    separately pinned SpMV (t = A s = q - alpha y, and the bilinear expansions
+    of (t,s), (t,t), (rhat, r_{i+1}) against direct inner products);
+  * closed forms: Krylov termination on Poisson eigenvectors, A = I, the
+    2-unknown triangular system.
+"""
+import numpy as np
+import pytest
+
+import inputs
+from test_oracle_o64 import dense_scaled, lam, phi, poisson_scaled
+
+
+def cd(orc, n, seed=1, delta=0.1, shape=None):
+    nx, ny, nz = shape or (n, n, n)
+    diag, offs = inputs.problem_fields(inputs.KIND_CD, nx, ny, nz, seed=seed, delta=delta)
+    return diag, offs, orc.jacobi_scale(diag, offs), inputs.rhs_uniform(nx, ny, nz, seed=seed)
+
+
+@pytest.mark.parametrize("kind,delta", [(inputs.KIND_CD, 0.1), (inputs.KIND_CD, 0.0), (inputs.KIND_POISSON, 0.0)])
+def test_sr_iterates_equal_classic(orc, kind, delta):
+    """Same Krylov iterates as Alg. 1 while rounding is negligible (first 8 iterations)."""
+    nx, ny, nz = 9, 8, 7
+    diag, offs = inputs.problem_fields(kind, nx, ny, nz, seed=3, delta=delta)
+    c = orc.jacobi_scale(diag, offs)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=3)
+    it = 8
+    a = orc.bicgstab64(c, b, tol=0.0, maxit=it)
+    s = orc.bicgstab64(c, b, tol=0.0, maxit=it, schedule="sr")
+    assert s["iters"] == a["iters"] == it
+    assert np.allclose(s["hist"], a["hist"], rtol=1e-8, atol=0)
+    assert np.allclose(s["alpha"], a["alpha"], rtol=1e-8, atol=0)
+    assert np.allclose(s["omega"], a["omega"], rtol=1e-8, atol=0)
+    assert np.linalg.norm(s["x"] - a["x"]) <= 1e-8 * np.linalg.norm(a["x"])
+
+
+@pytest.mark.parametrize("kind,delta", [(inputs.KIND_POISSON, 0.0), (inputs.KIND_CD, 0.1), (inputs.KIND_CD, 0.0)])
+def test_sr_solve_matches_dense_lu(orc, kind, delta):
+    nx = ny = nz = 6
+    diag, offs = inputs.problem_fields(kind, nx, ny, nz, seed=2, delta=delta)
+    c = orc.jacobi_scale(diag, offs)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=2)
+    x_lu = np.linalg.solve(dense_scaled(diag, offs), b.ravel())
+    res = orc.bicgstab64(c, b, tol=1e-13, maxit=500, schedule="sr")
+    assert res["status"] == orc.ORC_CONVERGED
+    assert np.linalg.norm(res["x"].ravel() - x_lu) / np.linalg.norm(x_lu) <= 1e-10
+
+
+def test_sweep_identities(orc):
+    """One sweep from a genuine mid-solve state: every vector the sweep returns
+    obeys its defining relation, checked with the pinned SpMV and numpy dots."""
+    nx, ny, nz = 7, 6, 5
+    _, _, c, b = cd(orc, 0, seed=5, shape=(nx, ny, nz))
+    rng = np.random.default_rng(1)
+    rh = b.copy()
+    x = rng.uniform(-1, 1, b.shape)
+    r = rng.uniform(-1, 1, b.shape)
+    p = rng.uniform(-1, 1, b.shape)
+    v = orc.apply64(c, p)
+    q = orc.apply64(c, r)
+    y = orc.apply64(c, v)
+    al, om, be = 0.37, 0.81, -0.45
+    x1, r1, p1, v1, q1, y1, dots = orc.sr_sweep64(c, (al, om, be), rh, x, r, p, v, q, y)
+    s = r - al * v
+    t_direct = orc.apply64(c, s)                       # Alg. 1 l.179 computed directly
+    assert np.allclose(q - al * y, t_direct, rtol=0, atol=1e-14)
+    assert np.allclose(r1, s - om * t_direct, rtol=0, atol=1e-14)
+    assert np.allclose(x1, x + al * p + om * s, rtol=0, atol=1e-14)
+    assert np.allclose(p1, r1 + be * (p - om * v), rtol=0, atol=1e-14)
+    assert np.array_equal(v1, orc.apply64(c, p1))
+    assert np.array_equal(q1, orc.apply64(c, r1))
+    assert np.array_equal(y1, orc.apply64(c, v1))
+    pairs = [(rh, v1), (rh, r1), (rh, q1), (rh, y1), (q1, r1), (q1, v1), (y1, r1), (y1, v1),
+             (q1, q1), (q1, y1), (y1, y1), (r1, r1)]
+    assert np.allclose(dots, [np.vdot(a_, b_) for a_, b_ in pairs], rtol=1e-13, atol=0)
+    # the bilinear expansions used by the scalar step, against formed vectors
+    a2 = dots[1] / dots[0]
+    s2 = r1 - a2 * v1
+    t2 = orc.apply64(c, s2)
+    ts = dots[4] - a2 * dots[5] - a2 * dots[6] + a2 * a2 * dots[7]
+    tt = dots[8] - 2 * a2 * dots[9] + a2 * a2 * dots[10]
+    assert np.isclose(ts, np.vdot(t2, s2), rtol=1e-10)
+    assert np.isclose(tt, np.vdot(t2, t2), rtol=1e-10)
+    w2 = ts / tt
+    rn = dots[1] - a2 * dots[0] - w2 * (dots[2] - a2 * dots[3])
+    assert np.isclose(rn, np.vdot(rh, s2 - w2 * t2), rtol=1e-9)
+
+
+def test_sr_krylov_termination_one_eigenvector(orc):
+    nx, ny, nz = 7, 6, 5
+    c = poisson_scaled(orc, nx, ny, nz)
+    f = phi(nx, ny, nz, 1, 1, 1)
+    res = orc.bicgstab64(c, f, tol=0.0, maxit=1, schedule="sr")
+    assert res["hist"][1] <= 1e-14
+    assert np.max(np.abs(res["x"] - f / lam(nx, ny, nz, 1, 1, 1))) <= 1e-13
+
+
+def test_sr_krylov_termination_two_eigenvectors(orc):
+    nx, ny, nz = 7, 6, 5
+    c = poisson_scaled(orc, nx, ny, nz)
+    f = phi(nx, ny, nz, 1, 1, 1) + 0.7 * phi(nx, ny, nz, 2, 1, 3)
+    res = orc.bicgstab64(c, f, tol=0.0, maxit=2, schedule="sr")
+    assert res["hist"][2] <= 1e-13 and res["hist"][1] > 1e-6
+
+
+def test_sr_identity_lucky_exit(orc):
+    rng = np.random.default_rng(11)
+    c = [np.zeros((3, 4, 5)) for _ in range(6)]
+    b = rng.uniform(-1, 1, (3, 4, 5))
+    res = orc.bicgstab64(c, b, tol=1e-12, maxit=10, schedule="sr")
+    assert res["iters"] == 1 and res["status"] == orc.ORC_CONVERGED
+    assert np.array_equal(res["x"], b) and res["hist"][1] == 0.0
+    # fp16: x = b bitwise as well
+    c16 = [np.zeros((3, 4, 5), np.uint16) for _ in range(6)]
+    b16 = orc.f16_from_double(b)
+    r16 = orc.bicgstab16(c16, b16, tol=1e-3, maxit=10, schedule="sr")
+    assert r16["iters"] == 1 and r16["status"] == orc.ORC_CONVERGED
+    assert np.array_equal(r16["x"], b16)
+
+
+def test_sr_two_unknown_upper_triangular(orc):
+    c = [np.zeros((2, 1, 1)) for _ in range(6)]
+    c[5][0, 0, 0] = 0.5
+    res = orc.bicgstab64(c, np.ones((2, 1, 1)), tol=1e-14, maxit=10, schedule="sr")
+    assert res["status"] == orc.ORC_CONVERGED
+    assert np.allclose(res["x"].ravel(), [0.5, 1.0], rtol=0, atol=1e-14)
+
+
+def test_sr_zero_rhs_and_maxit_zero(orc):
+    _, _, c, b = cd(orc, 5)
+    z = orc.bicgstab64(c, np.zeros_like(b), tol=1e-6, maxit=5, schedule="sr")
+    assert z["status"] == orc.ORC_CONVERGED and z["iters"] == 0 and not np.any(z["x"])
+    m = orc.bicgstab64(c, b, tol=0.0, maxit=0, schedule="sr")
+    assert m["iters"] == 0 and m["hist"][0] == 1.0 and not np.any(m["x"])
+
+
+def test_sr_x0_and_true_residual_invariant(orc):
+    nx, ny, nz = 10, 9, 8
+    _, _, c, b = cd(orc, 0, seed=7, delta=0.0, shape=(nx, ny, nz))
+    for it in (1, 5, 20, 35):
+        res = orc.bicgstab64(c, b, tol=0.0, maxit=it, schedule="sr")
+        assert abs(orc.true_residual64(c, b, res["x"]) - res["hist"][it]) <= 1e-10
+    x0 = inputs.rhs_uniform(nx, ny, nz, seed=8)
+    r1 = orc.bicgstab64(c, b, tol=1e-12, maxit=400, schedule="sr")
+    r2 = orc.bicgstab64(c, b, x0=x0, tol=1e-12, maxit=400, schedule="sr")
+    assert r1["status"] == r2["status"] == orc.ORC_CONVERGED
+    assert np.allclose(r1["x"], r2["x"], rtol=0, atol=1e-9)
+    assert abs(r2["hist"][0] - orc.true_residual64(c, b, x0)) <= 1e-14
+
+
+def test_sr_many_seeds_converge(orc):
+    for seed in range(1, 11):
+        _, _, c, b = cd(orc, 0, seed=seed, shape=(8, 7, 6))
+        res = orc.bicgstab64(c, b, tol=1e-8, maxit=100, schedule="sr")
+        assert res["status"] == orc.ORC_CONVERGED, seed
+        assert orc.true_residual64(c, b, res["x"]) <= 1e-7
+
+
+# ---------------------------------------------------------------- fp16 / fp32 mirrors
+
+def _state16(orc, c16, rng, shape):
+    def rnd(scale=1.0):
+        return orc.f16_from_double(rng.uniform(-scale, scale, shape))
+    rh, x, r, p = rnd(), rnd(), rnd(), rnd()
+    v = orc.apply16(c16, p)
+    q = orc.apply16(c16, r)
+    y = orc.apply16(c16, v)
+    return rh, x, r, p, v, q, y
+
+
+def test_sr_sweep16_composes_pinned_primitives(orc):
+    """The fp16 sweep is exactly the composition of the pinned binary16 FMA
+    (test_oracle_fp16.py) and fused SpMV (test_oracle_o16.py) in the stated order."""
+    nx, ny, nz = 9, 5, 4
+    _, _, c, _ = cd(orc, 0, seed=2, shape=(nx, ny, nz))
+    c16 = orc.quantize_coeffs(c, "mixed")
+    rng = np.random.default_rng(4)
+    rh, x, r, p, v, q, y = _state16(orc, c16, rng, (nz, ny, nx))
+    al, om, be = np.float32(0.6), np.float32(0.9), np.float32(-0.3)
+    x1, r1, p1, v1, q1, y1, dots = orc.sr_sweep16(c16, (al, om, be), rh, x, r, p, v, q, y)
+    h = lambda f: np.full((nz, ny, nx), orc.f16_from_double(np.array(float(f)))[()], np.uint16)
+    ah, wh, bh = h(al), h(om), h(be)
+    neg = lambda a: a ^ np.uint16(0x8000)
+    s = orc.fma16_array(neg(ah), v, r)
+    t = orc.fma16_array(neg(ah), y, q)
+    assert np.array_equal(x1, orc.fma16_array(wh, s, orc.fma16_array(ah, p, x)))
+    assert np.array_equal(r1, orc.fma16_array(neg(wh), t, s))
+    assert np.array_equal(p1, orc.fma16_array(bh, orc.fma16_array(neg(wh), v, p), r1))
+    assert np.array_equal(v1, orc.apply16(c16, p1))
+    assert np.array_equal(q1, orc.apply16(c16, r1))
+    assert np.array_equal(y1, orc.apply16(c16, v1))
+    assert np.isclose(dots[11], orc.dot16(r1, r1), rtol=0, atol=0)
+    assert np.isclose(dots[5], orc.dot16(q1, v1), rtol=0, atol=0)
+
+
+def test_sr_sweep32_matches_fp32_mirror(orc):
+    nx, ny, nz = 9, 5, 4
+    _, _, c, _ = cd(orc, 0, seed=2, shape=(nx, ny, nz))
+    c32 = orc.quantize_coeffs(c, "fp32")
+    rng = np.random.default_rng(6)
+    f = lambda: rng.uniform(-1, 1, (nz, ny, nx)).astype(np.float32)
+    rh, x, r, p = f(), f(), f(), f()
+    v = orc.apply32_fma(c32, p)
+    q = orc.apply32_fma(c32, r)
+    y = orc.apply32_fma(c32, v)
+    al, om, be = np.float32(0.6), np.float32(0.9), np.float32(-0.3)
+    x1, r1, p1, v1, q1, y1, dots = orc.sr_sweep32(c32, (al, om, be), rh, x, r, p, v, q, y)
+    # element-wise ops are single-rounding fmas: fp64 product+sum rounded once to fp32
+    # (exact for fp32 inputs since 24+24+1 < 53 bits holds for the product)
+    fma32 = lambda a, b, cc: (a.astype(np.float64) * b.astype(np.float64) + cc.astype(np.float64)).astype(np.float32)
+    s = fma32(-al * np.ones_like(v), v, r)
+    t = fma32(-al * np.ones_like(y), y, q)
+    assert np.array_equal(r1, fma32(-om * np.ones_like(t), t, s))
+    assert np.array_equal(v1, orc.apply32_fma(c32, p1))
+    assert np.array_equal(y1, orc.apply32_fma(c32, v1))
+    assert np.isclose(dots[11], np.vdot(r1.astype(np.float64), r1.astype(np.float64)), rtol=1e-14)
+
+
+def test_sr16_tracks_sr64_then_plateaus(orc):
+    """Mixed SR follows the fp64 SR history early and then reaches the mixed
+    target 1e-3 (north_star) on the delta = 0.1 class; its true residual
+    plateaus near fp16 resolution."""
+    n = 16
+    diag, offs, c, b = cd(orc, n, seed=1)
+    c16 = orc.quantize_coeffs(c, "mixed")
+    b16 = orc.f16_from_double(b)
+    r64 = orc.bicgstab64([orc.f16_to_double(a) for a in c16], orc.f16_to_double(b16), tol=0.0,
+                         maxit=4, schedule="sr")
+    r16 = orc.bicgstab16(c16, b16, tol=0.0, maxit=4, schedule="sr")
+    assert np.allclose(r16["hist"][:4], r64["hist"][:4], rtol=2e-2)
+    conv = orc.bicgstab16(c16, b16, tol=1e-3, maxit=60, schedule="sr")
+    assert conv["status"] == orc.ORC_CONVERGED and conv["iters"] <= 20
+    tr = orc.true_residual64([orc.f16_to_double(a) for a in c16], orc.f16_to_double(b16),
+                             orc.f16_to_double(conv["x"]))
+    assert 1e-4 <= tr <= 1e-2
+
+
+def test_sr16_matches_classic16_early(orc):
+    """Both fp16 schedules compute the same Krylov iteration: their histories agree
+    to fp16 accuracy for the first iterations."""
+    n = 16
+    _, _, c, b = cd(orc, n, seed=3)
+    c16 = orc.quantize_coeffs(c, "mixed")
+    b16 = orc.f16_from_double(b)
+    a = orc.bicgstab16(c16, b16, tol=0.0, maxit=4)
+    s = orc.bicgstab16(c16, b16, tol=0.0, maxit=4, schedule="sr")
+    assert np.allclose(s["hist"], a["hist"], rtol=5e-2)
