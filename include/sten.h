@@ -47,11 +47,15 @@
 extern "C" {
 #endif
 
-#define STEN_VERSION 1
+#define STEN_VERSION 2
 
 /* precision of a solve / apply */
 #define STEN_FP32 0   /* fp32 storage, fp32 arithmetic, fp32 dots */
 #define STEN_MIXED 1  /* fp16 storage + arithmetic, fp16*fp16 products summed in fp32 */
+
+/* iteration schedule of bicgstab_solve (sten_set_schedule) */
+#define STEN_SCHED_CLASSIC 0 /* Alg. 1 as printed: 3 kernels, 3 reductions, 29 array passes / iteration */
+#define STEN_SCHED_SR 1      /* single reduction: 1 sweep, 1 reduction, 19 array passes / iteration (R19) */
 
 /* element type of the coefficient arrays passed to stencil_create */
 #define STEN_DT_F64 0
@@ -156,6 +160,39 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
 /* Record per-phase CUDA events inside the solve's graphs (enable != 0). */
 int sten_set_timing(sten_stencil *st, int enable);
 int sten_get_stats(sten_stencil *st, sten_stats *out);
+
+/* Select the iteration schedule of later bicgstab_solve calls on this handle.
+ *   STEN_SCHED_CLASSIC: Algorithm 1 exactly as printed:
+ *     three fused kernels per iteration, one global reduction after each
+ *     (alpha l.177, omega l.180, beta l.183).
+ *   STEN_SCHED_SR: the same iteration rearranged so ONE sweep and ONE
+ *     reduction serve it (R19; the paper notes it did not use a
+ *     communication-hiding variant): with q = A r and y = A v the
+ *     second product is t = A s = q - alpha y, and (t,s), (t,t), (rhat, r_new)
+ *     expand into twelve inner products of one sweep.  Identical iterates in
+ *     exact arithmetic; the rounding differs (oracle/osr.c is its oracle).
+ *     Per iteration it moves 19 instead of 29 arrays through HBM.  Needs two
+ *     halo planes per z-neighbour (exchanged once per iteration).
+ * Errors: STEN_EINVAL. */
+int sten_set_schedule(sten_stencil *st, int schedule);
+
+/* One SR sweep on caller vectors, for parity tests (oracle/osr.c
+ * o16_sr_sweep / o32_sr_sweep).  With the scalars (alpha, omega, beta) of
+ * the previous iteration (rounded to fp32, then to the working precision):
+ *   s = r - alpha v; t = q - alpha y; x += alpha p + omega s (as
+ *   fma(omega, s, fma(alpha, p, x))); r = s - omega t; p = r + beta (p - omega v);
+ *   v = A p; q = A r; y = A v;
+ * x, r, p, v, q, y are updated in place (this rank's points, dense layout,
+ * storage type of `precision`; host or device); rh is read.  dots (host,
+ * 12 floats) receives the fp32 sums (rh,v) (rh,r) (rh,q) (rh,y) (q,r) (q,v)
+ * (y,r) (y,v) (q,q) (q,y) (y,y) (r,r) over this rank (all ranks when
+ * decomposed).  Synchronises cuda_stream.  Errors: STEN_EINVAL, STEN_ECUDA. */
+int sten_sr_sweep(sten_stencil *st, int precision, double alpha, double omega, double beta, const void *rh,
+                  void *x, void *r, void *p, void *v, void *q, void *y, float *dots, void *cuda_stream);
+
+/* SR kernel geometry for tuning (0 = default): by rows per tile (8 or 16),
+ * stages input TMA stages, cstages coefficient stages, zc planes per CTA. */
+int sten_set_sr_tiling(sten_stencil *st, int precision, int by, int stages, int cstages, int zc);
 
 /* Tile geometry override for tuning (0 = library default).  bx: points per
  * tile in x (multiple of 8), by: rows per tile, zc: planes per CTA,

@@ -20,6 +20,8 @@ from . import roofline  # noqa: F401  (work/traffic accounting)
 
 FP32 = 0
 MIXED = 1
+SCHED_CLASSIC = 0
+SCHED_SR = 1
 DT_F64 = 0
 DT_F32 = 1
 
@@ -68,6 +70,9 @@ def lib():
         L.sten_set_timing.argtypes = [P, I]
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
+        L.sten_set_schedule.argtypes = [P, I]
+        L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I]
+        L.sten_sr_sweep.argtypes = [P, I, D, D, D, P, P, P, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -250,3 +255,23 @@ def get_stats(st: Stencil) -> dict:
 
 def set_tiling(st: Stencil, precision: int, bx: int = 0, by: int = 0, zc: int = 0, stages: int = 0):
     _check(lib().sten_set_tiling(st.handle, precision, bx, by, zc, stages))
+
+
+def set_schedule(st: Stencil, schedule: int):
+    """SCHED_CLASSIC (Alg. 1 as printed) or SCHED_SR (single reduction, R19)."""
+    _check(lib().sten_set_schedule(st.handle, int(schedule)))
+
+
+def set_sr_tiling(st: Stencil, precision: int, by: int = 0, stages: int = 0, cstages: int = 0, zc: int = 0):
+    _check(lib().sten_set_sr_tiling(st.handle, precision, by, stages, cstages, zc))
+
+
+def sr_sweep(st: Stencil, precision: int, scalars, rh, x, r, p, v, q, y, stream=None):
+    """One SR sweep in place on (x, r, p, v, q, y); returns the 12 fp32 dot sums."""
+    for name, a in (("rh", rh), ("x", x), ("r", r), ("p", p), ("v", v), ("q", q), ("y", y)):
+        _check_vec(a, precision, st.npoints, name)
+    dots = np.zeros(12, np.float32)
+    al, om, be = (float(t) for t in scalars)
+    _check(lib().sten_sr_sweep(st.handle, precision, al, om, be, _ptr(rh), _ptr(x), _ptr(r), _ptr(p), _ptr(v),
+                               _ptr(q), _ptr(y), dots.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+    return dots

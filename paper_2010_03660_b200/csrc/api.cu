@@ -138,6 +138,16 @@ struct Tiling {
   int bx = 0, by = 0, zc = 0, stages = 0, threads = 0;
 };
 
+// SR schedule buffers (R19): two halo planes per side, because the
+// sweep's y' = A(A p') reaches two planes into the z-neighbour's data.
+constexpr int kSrHalo = 2;
+struct SrBufs {
+  bool ready = false, maps_ok = false;
+  void *x = nullptr, *rh = nullptr;
+  void *vec[2][5] = {};           // ping-pong sets of r, p, v, q, y
+  CUtensorMap m_vec[2][5], m_c[6];
+};
+
 struct PrecBufs {
   bool ready = false;
   void *x = nullptr, *r = nullptr, *rh = nullptr, *p[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr};
@@ -150,17 +160,23 @@ struct PrecBufs {
 struct Slab {
   int nz = 0;                     // planes of this slab
   long long z_first = 0;          // first plane within this rank's part
-  float *c32[6] = {};
+  float *c32[6] = {};             // interior plane 0 (one halo plane below it: c32b)
   __half *c16[6] = {};
+  float *c32b[6] = {};            // allocations: nz + 2 planes, halo planes 0 and nz+1
+  __half *c16b[6] = {};
   double *aP = nullptr;
   PrecBufs pb[2];
+  SrBufs sr[2];
 };
 
 struct GraphKey {
-  int prec, chunk, timing;
+  int prec, chunk, timing, sched;
   bool operator<(const GraphKey &o) const {
-    return std::tie(prec, chunk, timing) < std::tie(o.prec, o.chunk, o.timing);
+    return std::tie(prec, chunk, timing, sched) < std::tie(o.prec, o.chunk, o.timing, o.sched);
   }
+};
+struct SrTiling {
+  int by = 0, stages = 0, cstages = 0, zc = 0;
 };
 struct GraphRec {
   cudaGraphExec_t exec = nullptr;
@@ -177,6 +193,8 @@ struct sten_stencil {
   bool has_diag = false;
   int sm = 148;
   Tiling tiling[2];
+  SrTiling srt[2];
+  int schedule = STEN_SCHED_CLASSIC;
   DevState *st = nullptr;       // device
   DevState *st_host = nullptr;  // pinned mirror
   float *partials = nullptr;
@@ -490,8 +508,189 @@ static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_
   return STEN_OK;
 }
 
+// ============================================== SR schedule (R19) ==
+// Coefficient halo planes: the z-neighbour slab's boundary plane of each of
+// the 12 coefficient arrays (6 x fp32, 6 x fp16).  Device copies between the
+// slabs of this rank, NCCL send/recv between ranks; once, at create.
+static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
+  const int ns = (int)st->slabs.size();
+  for (int pr = 0; pr < 2; ++pr) {
+    const size_t pb = (size_t)st->plane * (pr == 0 ? 4 : 2);
+    auto base = [&](Slab &sl, int d) -> char * { return pr == 0 ? (char *)sl.c32b[d] : (char *)sl.c16b[d]; };
+    for (int k = 0; k + 1 < ns; ++k) {
+      Slab &lo = st->slabs[k], &hi = st->slabs[k + 1];
+      for (int d = 0; d < 6; ++d) {
+        CUDA_TRY(cudaMemcpyAsync(base(hi, d), base(lo, d) + (size_t)lo.nz * pb, pb, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(base(lo, d) + (size_t)(lo.nz + 1) * pb, base(hi, d) + pb, pb, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    if (st->comm && st->comm->nranks > 1) {
+      const int R = st->comm->nranks, me = st->comm->rank;
+      Slab &bot = st->slabs[0], &top = st->slabs[ns - 1];
+      NCCL_TRY(g_nccl.GroupStart());
+      for (int d = 0; d < 6; ++d) {
+        if (me > 0) {
+          NCCL_TRY(g_nccl.Send(base(bot, d) + pb, pb, ncclUint8, me - 1, st->comm->comm, s));
+          NCCL_TRY(g_nccl.Recv(base(bot, d), pb, ncclUint8, me - 1, st->comm->comm, s));
+        }
+        if (me + 1 < R) {
+          NCCL_TRY(g_nccl.Send(base(top, d) + (size_t)top.nz * pb, pb, ncclUint8, me + 1, st->comm->comm, s));
+          NCCL_TRY(g_nccl.Recv(base(top, d) + (size_t)(top.nz + 1) * pb, pb, ncclUint8, me + 1, st->comm->comm, s));
+        }
+      }
+      NCCL_TRY(g_nccl.GroupEnd());
+    }
+  }
+  return STEN_OK;
+}
+
+// Default SR geometry: 16-row tiles, 3 input stages, 2 coefficient stages
+// (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
+static void default_sr_tiling(sten_stencil *st, int prec) {
+  SrTiling &t = st->srt[prec];
+  int by = 16, stg = 3, cst = 2, zc = 64;
+  if (const char *e = getenv("STEN_SR_TILING")) sscanf(e, "%d,%d,%d,%d", &by, &stg, &cst, &zc);
+  t.by = by;
+  t.stages = stg;
+  t.cstages = cst;
+  const int nzs = st->slabs[0].nz;
+  t.zc = zc < nzs ? zc : nzs;
+}
+
+static int sr_grid(const sten_stencil *st, int prec, int nzs) {
+  const SrTiling &t = st->srt[prec];
+  const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  return ((st->nx + bx - 1) / bx) * ((st->ny + t.by - 1) / t.by) * ((nzs + t.zc - 1) / t.zc);
+}
+
+static int ensure_sr(sten_stencil *st, int prec) {
+  if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
+  const SrTiling &t = st->srt[prec];
+  if (!sr_config_ok(t.by, t.stages, t.cstages) || t.zc <= 0)
+    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d", t.by, t.stages, t.cstages, t.zc);
+  const int e = esize(prec);
+  const size_t vb = (size_t)st->plane * e;
+  const int H = prec == STEN_FP32 ? 4 : 8, bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  g_plane_stride = st->plane;
+  for (Slab &sl : st->slabs) {
+    SrBufs &b = sl.sr[prec];
+    if (!b.ready) {
+      const size_t bytes = vb * (sl.nz + 2 * kSrHalo);
+      void **all[12] = {&b.x, &b.rh};
+      int n = 2;
+      for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < 5; ++i) all[n++] = &b.vec[k][i];
+      for (void **pp : all) {
+        cudaError_t ce = cudaMalloc(pp, bytes);
+        if (ce != cudaSuccess) return set_err(STEN_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(ce));
+        CUDA_TRY(cudaMemset(*pp, 0, bytes));  // halo planes and row padding stay zero
+      }
+      b.ready = true;
+      b.maps_ok = false;
+    }
+    if (!b.maps_ok) {
+      for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < 5; ++i)
+          RC_TRY(make_map(&b.m_vec[k][i], b.vec[k][i], e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx + 2 * H,
+                          t.by + 4));
+      for (int d = 0; d < 6; ++d) {
+        void *c = prec == STEN_FP32 ? (void *)sl.c32b[d] : (void *)sl.c16b[d];
+        RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + 2 * H, t.by + 2));
+      }
+      b.maps_ok = true;
+    }
+    const int g = sr_grid(st, prec, sl.nz);
+    if (g > st->partials_cap) {
+      if (st->partials) cudaFree(st->partials);
+      CUDA_TRY(cudaMalloc(&st->partials, (size_t)g * kMaxDots * sizeof(float)));
+      st->partials_cap = g;
+      drop_graphs(st);
+    }
+  }
+  return STEN_OK;
+}
+
+static char *sr_interior(void *base, const sten_stencil *st, int prec) {
+  return (char *)base + (size_t)kSrHalo * st->plane * esize(prec);
+}
+
+// one sweep of slab `slab`: reads set `set`, writes set `set ^ 1`.
+// capture: deposit the raw sums in slab_sums instead of finalising.
+static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture, cudaStream_t s) {
+  Slab &sl = st->slabs[slab];
+  SrBufs &b = sl.sr[prec];
+  const SrTiling &t = st->srt[prec];
+  SrArgs a;
+  memset(&a, 0, sizeof a);
+  for (int i = 0; i < 5; ++i) {
+    a.tm_in[i] = b.m_vec[set][i];
+    a.out[i] = sr_interior(b.vec[set ^ 1][i], st, prec);
+  }
+  for (int d = 0; d < 6; ++d) a.tm_c[d] = b.m_c[d];
+  a.x = sr_interior(b.x, st, prec);
+  a.rh = sr_interior(b.rh, st, prec);
+  a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
+  a.zc = t.zc;
+  const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  a.tiles_x = (st->nx + bx - 1) / bx;
+  a.tiles_y = (st->ny + t.by - 1) / t.by;
+  if (sr_grid(st, prec, sl.nz) > st->partials_cap)
+    return set_err(STEN_ECUDA, "internal: SR grid exceeds the partial-sum buffer");
+  a.red = make_red(st, slab);
+  if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;
+  if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, s));
+  else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, s));
+  st->launches++;
+  return STEN_OK;
+}
+
+// two halo planes of r, p, v, q, y (set `set`) to each z-neighbour
+static int sr_exchange(sten_stencil *st, int prec, int set, cudaStream_t s) {
+  const size_t pb = (size_t)st->plane * esize(prec), hb = pb * kSrHalo;
+  const int ns = (int)st->slabs.size();
+  for (int i = 0; i < 5; ++i) {
+    for (int k = 0; k + 1 < ns; ++k) {
+      char *lo = (char *)st->slabs[k].sr[prec].vec[set][i];
+      char *hi = (char *)st->slabs[k + 1].sr[prec].vec[set][i];
+      const int nzl = st->slabs[k].nz;
+      CUDA_TRY(cudaMemcpyAsync(hi, lo + (size_t)nzl * pb, hb, cudaMemcpyDeviceToDevice, s));  // top 2 -> low halo
+      CUDA_TRY(cudaMemcpyAsync(lo + (size_t)(nzl + kSrHalo) * pb, hi + hb, hb, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  if (st->comm && st->comm->nranks > 1) {
+    const int R = st->comm->nranks, me = st->comm->rank;
+    NCCL_TRY(g_nccl.GroupStart());
+    for (int i = 0; i < 5; ++i) {
+      char *bot = (char *)st->slabs[0].sr[prec].vec[set][i];
+      char *top = (char *)st->slabs[ns - 1].sr[prec].vec[set][i];
+      const int nzt = st->slabs[ns - 1].nz;
+      if (me > 0) {
+        NCCL_TRY(g_nccl.Send(bot + hb, hb, ncclUint8, me - 1, st->comm->comm, s));
+        NCCL_TRY(g_nccl.Recv(bot, hb, ncclUint8, me - 1, st->comm->comm, s));
+      }
+      if (me + 1 < R) {
+        NCCL_TRY(g_nccl.Send(top + (size_t)nzt * pb, hb, ncclUint8, me + 1, st->comm->comm, s));
+        NCCL_TRY(g_nccl.Recv(top + (size_t)(nzt + kSrHalo) * pb, hb, ncclUint8, me + 1, st->comm->comm, s));
+      }
+    }
+    NCCL_TRY(g_nccl.GroupEnd());
+  }
+  return STEN_OK;
+}
+
+// one SR iteration: halos of the input set, the sweep of every slab, the
+// cross-slab / cross-rank scalar step.  evs: optional [2] events.
+static int enqueue_sr_sweep(sten_stencil *st, int prec, int set, cudaStream_t s, cudaEvent_t *evs) {
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
+  if (decomposed(st)) RC_TRY(sr_exchange(st, prec, set, s));
+  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_sr(st, prec, k, set, false, s));
+  RC_TRY(reduce_scalars(st, PH_SR, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
+  return STEN_OK;
+}
+
 static int get_graph(sten_stencil *st, int prec, int chunk, GraphRec **out) {
-  GraphKey key{prec, chunk, st->timing ? 1 : 0};
+  GraphKey key{prec, chunk, st->timing ? 1 : 0, st->schedule};
   auto it = st->graphs.find(key);
   if (it != st->graphs.end()) {
     *out = &it->second;
@@ -506,7 +705,9 @@ static int get_graph(sten_stencil *st, int prec, int chunk, GraphRec **out) {
   CUDA_TRY(cudaStreamBeginCapture(st->cap, cudaStreamCaptureModeThreadLocal));
   int rc = STEN_OK;
   for (int j = 0; j < chunk && rc == STEN_OK; ++j)
-    rc = enqueue_iteration(st, prec, j & 1, st->cap, st->timing ? &rec.ev[(size_t)j * 6] : nullptr);
+    rc = st->schedule == STEN_SCHED_SR
+             ? enqueue_sr_sweep(st, prec, j & 1, st->cap, st->timing ? &rec.ev[(size_t)j * 6] : nullptr)
+             : enqueue_iteration(st, prec, j & 1, st->cap, st->timing ? &rec.ev[(size_t)j * 6] : nullptr);
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(st->cap, &g);
   if (rc != STEN_OK) {
@@ -567,6 +768,63 @@ static int copy_out(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), void *
   }
   return STEN_OK;
 }
+// the same for SR buffers (kSrHalo halo planes); base(slab) -> allocation
+template <typename Base>
+static int sr_copy_in(sten_stencil *st, int prec, Base base, const void *src, cudaStream_t s) {
+  const int e = esize(prec);
+  for (Slab &sl : st->slabs) {
+    char *dst = sr_interior(base(sl), st, prec);
+    const char *sp = (const char *)src + (size_t)sl.z_first * st->nx * st->ny * e;
+    CUDA_TRY(copy3d(dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
+                    (size_t)st->ny, (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
+  }
+  return STEN_OK;
+}
+template <typename Base>
+static int sr_copy_out(sten_stencil *st, int prec, Base base, void *dst, cudaStream_t s) {
+  const int e = esize(prec);
+  for (Slab &sl : st->slabs) {
+    const char *src = sr_interior(base(sl), st, prec);
+    char *dp = (char *)dst + (size_t)sl.z_first * st->nx * st->ny * e;
+    CUDA_TRY(copy3d(dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
+                    (size_t)(st->plane / st->pitch), (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
+  }
+  return STEN_OK;
+}
+
+// S1 for the SR schedule: b_hat, r0 = b_hat - A x0, rhat = p = r0, v = 0 into
+// SR set 0 (k_init), q = y = 0.
+static int launch_init_sr(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s) {
+  Slab &sl = st->slabs[slab];
+  PrecBufs &b = sl.pb[prec];
+  SrBufs &r = sl.sr[prec];
+  const int e = esize(prec), vec = prec == STEN_FP32 ? 4 : 8;
+  const size_t off = (size_t)st->plane * e;
+  EwArgs a;
+  memset(&a, 0, sizeof a);
+  a.bw = (char *)b.bw + off;
+  a.aP = st->has_diag ? sl.aP : nullptr;
+  a.ax = with_ax ? (const void *)((char *)b.t + off) : nullptr;
+  a.r = sr_interior(r.vec[0][0], st, prec);
+  a.rh = sr_interior(r.rh, st, prec);
+  a.p0 = sr_interior(r.vec[0][1], st, prec);
+  a.v0 = sr_interior(r.vec[0][2], st, prec);
+  a.rows = (long long)st->ny * sl.nz;
+  a.vpr = (st->nx + vec - 1) / vec;
+  a.pitch = st->pitch;
+  a.nvec = (long long)st->plane * sl.nz / vec;
+  a.red = make_red(st, slab);
+  if (ew_grid(st, a.nvec) > st->partials_cap)
+    return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
+  const size_t all = (size_t)st->plane * e * (sl.nz + 2 * kSrHalo);
+  CUDA_TRY(cudaMemsetAsync(r.vec[0][3], 0, all, s));
+  CUDA_TRY(cudaMemsetAsync(r.vec[0][4], 0, all, s));
+  if (prec == STEN_FP32) KLAUNCH(init_launch<float>(a, ew_grid(st, a.nvec), 256, s));
+  else KLAUNCH(init_launch<__half>(a, ew_grid(st, a.nvec), 256, s));
+  st->launches++;
+  return STEN_OK;
+}
+
 static void *sel_x(PrecBufs &b) { return b.x; }
 static void *sel_s(PrecBufs &b) { return b.s; }
 static void *sel_t(PrecBufs &b) { return b.t; }
@@ -684,10 +942,18 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
     Slab &sl = st->slabs[k];
     sl.nz = nzs;
     sl.z_first = (long long)k * nzs;
-    const size_t cb32 = (size_t)st->plane * nzs * 4, cb16 = (size_t)st->plane * nzs * 2;
+    // one halo plane below and above (zero at the global mesh boundary, the
+    // z-neighbour's plane at slab interfaces; read only by the SR sweep)
+    const size_t cb32 = (size_t)st->plane * (nzs + 2) * 4, cb16 = (size_t)st->plane * (nzs + 2) * 2;
     for (int d = 0; d < 6 && rc == STEN_OK; ++d) {
-      if (cudaMalloc(&sl.c32[d], cb32) != cudaSuccess || cudaMalloc(&sl.c16[d], cb16) != cudaSuccess)
+      if (cudaMalloc(&sl.c32b[d], cb32) != cudaSuccess || cudaMalloc(&sl.c16b[d], cb16) != cudaSuccess) {
         rc = set_err(STEN_ENOMEM, "coefficient allocation failed");
+        break;
+      }
+      cudaMemsetAsync(sl.c32b[d], 0, cb32, s);
+      cudaMemsetAsync(sl.c16b[d], 0, cb16, s);
+      sl.c32[d] = sl.c32b[d] + st->plane;
+      sl.c16[d] = sl.c16b[d] + st->plane;
     }
     if (rc == STEN_OK && st->has_diag && cudaMalloc(&sl.aP, (size_t)st->plane * nzs * 8) != cudaSuccess)
       rc = set_err(STEN_ENOMEM, "diagonal allocation failed");
@@ -701,6 +967,7 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
     int e = create_coeffs_launch(coeff_dtype, dg, off, g, below, above, sl.c32, sl.c16, sl.aP, s);
     if (e) rc = set_err(STEN_ECUDA, "coefficient kernel: %s", cudaGetErrorString((cudaError_t)e));
   }
+  if (rc == STEN_OK) rc = fill_coef_halos(st, s);
   if (rc == STEN_OK) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = set_err(STEN_ECUDA, "stencil_create: %s", cudaGetErrorString(e));
@@ -730,13 +997,19 @@ void stencil_destroy(sten_stencil *st) {
   drop_graphs(st);
   for (Slab &sl : st->slabs) {
     for (int d = 0; d < 6; ++d) {
-      cudaFree(sl.c32[d]);
-      cudaFree(sl.c16[d]);
+      cudaFree(sl.c32b[d]);
+      cudaFree(sl.c16b[d]);
     }
     cudaFree(sl.aP);
     for (PrecBufs &b : sl.pb) {
       void *all[] = {b.x, b.r, b.rh, b.p[0], b.p[1], b.v[0], b.v[1], b.s, b.t, b.bw};
       for (void *p : all) cudaFree(p);
+    }
+    for (SrBufs &b : sl.sr) {
+      cudaFree(b.x);
+      cudaFree(b.rh);
+      for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < 5; ++i) cudaFree(b.vec[k][i]);
     }
   }
   cudaFree(st->st);
@@ -822,12 +1095,14 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
   if (!(tol >= 0.0) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  const bool sr = st->schedule == STEN_SCHED_SR;
   RC_TRY(ensure_bufs(st, prec));
-  if (maxit + 1 > st->hist_cap) {
+  if (sr) RC_TRY(ensure_sr(st, prec));
+  if (maxit + 2 > st->hist_cap) {
     cudaFree(st->hist);
     cudaFree(st->ahist);
     cudaFree(st->whist);
-    st->hist_cap = maxit + 1 < 64 ? 64 : maxit + 1;
+    st->hist_cap = maxit + 2 < 64 ? 64 : maxit + 2;
     CUDA_TRY(cudaMalloc(&st->hist, sizeof(double) * st->hist_cap));
     CUDA_TRY(cudaMalloc(&st->ahist, sizeof(float) * st->hist_cap));
     CUDA_TRY(cudaMalloc(&st->whist, sizeof(float) * st->hist_cap));
@@ -861,13 +1136,21 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
     }
     if (decomposed(st)) RC_TRY(exchange(st, prec, [](PrecBufs &bb) { return bb.s; }, s));
     for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, prec, MODE_APPLY, k, 0, s));
+    if (sr)
+      for (Slab &sl : st->slabs) {
+        const size_t vb = (size_t)st->plane * esize(prec);
+        CUDA_TRY(cudaMemcpyAsync(sr_interior(sl.sr[prec].x, st, prec), (char *)sl.pb[prec].x + vb, vb * sl.nz,
+                                 cudaMemcpyDeviceToDevice, s));
+      }
   } else {
     for (Slab &sl : st->slabs) {
       const size_t vb = (size_t)st->plane * esize(prec);
-      CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
+      if (sr) CUDA_TRY(cudaMemsetAsync(sr_interior(sl.sr[prec].x, st, prec), 0, vb * sl.nz, s));
+      else CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
     }
   }
-  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_init(st, prec, k, with_x0, s));
+  for (int k = 0; k < (int)st->slabs.size(); ++k)
+    RC_TRY(sr ? launch_init_sr(st, prec, k, with_x0, s) : launch_init(st, prec, k, with_x0, s));
   RC_TRY(reduce_scalars(st, PH_INIT, s));
   // iterations: CUDA graphs of `chunk` iterations (even, so the ping-pong
   // parity of p/v is the same at every replay)
@@ -875,12 +1158,13 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   double ph_ms[3] = {0, 0, 0};
   long long ph_n[3] = {0, 0, 0};
   int chunk = 0;
-  if (maxit > 0) {
-    chunk = tol > 0.0 ? 8 : ((maxit + 1) / 2) * 2;
+  const int nsteps = sr ? maxit + 1 : maxit;  // SR: sweep i computes x_i, r_i (i = 0..maxit)
+  if (nsteps > 0) {
+    chunk = tol > 0.0 ? 8 : ((nsteps + 1) / 2) * 2;
     if (chunk > 2048) chunk = 2048;
     GraphRec *gr = nullptr;
     RC_TRY(get_graph(st, prec, chunk, &gr));
-    const int nrep = (maxit + chunk - 1) / chunk;
+    const int nrep = (nsteps + chunk - 1) / chunk;
     for (int rep = 0; rep < nrep; ++rep) {
       CUDA_TRY(cudaGraphLaunch(gr->exec, s));
       kernels += gr->kernels;
@@ -892,8 +1176,8 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
           const int done_it = st->st_host->it;
           const int first = rep * chunk;
           for (int j = 0; j < chunk; ++j) {
-            if (first + j >= done_it) break;  // later kernels were no-ops
-            for (int p = 0; p < 3; ++p) {
+            if (sr ? first + j > done_it : first + j >= done_it) break;  // later kernels were no-ops
+            for (int p = 0; p < (sr ? 1 : 3); ++p) {
               float ms = 0.f;
               cudaError_t te =
                   cudaEventElapsedTime(&ms, gr->ev[(size_t)j * 6 + 2 * p], gr->ev[(size_t)j * 6 + 2 * p + 1]);
@@ -917,9 +1201,11 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   if (fin.zero_x)
     for (Slab &sl : st->slabs) {
       const size_t vb = (size_t)st->plane * esize(prec);
-      CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
+      if (sr) CUDA_TRY(cudaMemsetAsync(sr_interior(sl.sr[prec].x, st, prec), 0, vb * sl.nz, s));
+      else CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
     }
-  RC_TRY(copy_out(st, prec, sel_x, x_out, s));
+  if (sr) RC_TRY(sr_copy_out(st, prec, [prec](Slab &sl) { return sl.sr[prec].x; }, x_out, s));
+  else RC_TRY(copy_out(st, prec, sel_x, x_out, s));
   CUDA_TRY(cudaMemcpyAsync(res_hist, st->hist, sizeof(double) * (fin.it + 1), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
@@ -948,6 +1234,75 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega) {
     alpha[i - 1] = a[i];
     omega[i - 1] = w[i];
   }
+  return STEN_OK;
+}
+
+int sten_set_schedule(sten_stencil *st, int schedule) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  if (schedule != STEN_SCHED_CLASSIC && schedule != STEN_SCHED_SR)
+    return set_err(STEN_EINVAL, "unknown schedule %d", schedule);
+  st->schedule = schedule;
+  return STEN_OK;
+}
+
+int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstages, int zc) {
+  if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
+  if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
+  SrTiling t = st->srt[prec];
+  if (by) t.by = by;
+  if (stages) t.stages = stages;
+  if (cstages) t.cstages = cstages;
+  if (zc) t.zc = zc;
+  if (!sr_config_ok(t.by, t.stages, t.cstages) || t.zc <= 0)
+    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d", t.by, t.stages, t.cstages,
+                   t.zc);
+  st->srt[prec] = t;
+  for (Slab &sl : st->slabs) sl.sr[prec].maps_ok = false;
+  drop_graphs(st);
+  return STEN_OK;
+}
+
+int sten_sr_sweep(sten_stencil *st, int prec, double alpha, double omega, double beta, const void *rh, void *x,
+                  void *r, void *p, void *v, void *q, void *y, float *dots, void *cuda_stream) {
+  if (!st || !rh || !x || !r || !p || !v || !q || !y || !dots) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  RC_TRY(ensure_bufs(st, prec));
+  RC_TRY(ensure_sr(st, prec));
+  st->launches = 0;
+  DevState h;
+  memset(&h, 0, sizeof h);
+  h.alpha = (float)alpha;
+  h.omega = (float)omega;
+  h.beta = (float)beta;
+  h.maxit = 1;
+  h.ev = -1;
+  h.half = prec == STEN_MIXED;
+  *st->st_host = h;
+  CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
+  void *user[5] = {r, p, v, q, y};
+  for (int i = 0; i < 5; ++i)
+    RC_TRY(sr_copy_in(st, prec, [prec, i](Slab &sl) { return sl.sr[prec].vec[0][i]; }, user[i], s));
+  RC_TRY(sr_copy_in(st, prec, [prec](Slab &sl) { return sl.sr[prec].x; }, x, s));
+  RC_TRY(sr_copy_in(st, prec, [prec](Slab &sl) { return sl.sr[prec].rh; }, rh, s));
+  if (decomposed(st)) RC_TRY(sr_exchange(st, prec, 0, s));
+  const int ns = (int)st->slabs.size();
+  for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, 0, true, s));
+  float *sums = st->slab_sums;
+  if (st->comm && st->comm->nranks > 1) {
+    KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
+    NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
+    sums = st->red_total;
+  } else if (ns > 1) {
+    KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
+    sums = st->red_total;
+  }
+  for (int i = 0; i < 5; ++i)
+    RC_TRY(sr_copy_out(st, prec, [prec, i](Slab &sl) { return sl.sr[prec].vec[1][i]; }, user[i], s));
+  RC_TRY(sr_copy_out(st, prec, [prec](Slab &sl) { return sl.sr[prec].x; }, x, s));
+  CUDA_TRY(cudaMemcpyAsync(dots, sums, sizeof(float) * 12, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
   return STEN_OK;
 }
 

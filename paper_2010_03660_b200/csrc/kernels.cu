@@ -126,20 +126,24 @@ int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
 
 // ------------------------------------------------- cross-slab scalar step --
 __global__ void k_scalars(int phase, const float *__restrict__ slab_sums, int nslabs, DevState *st) {
-  if (phase != PH_INIT && st_idle(st)) return;
-  float s[kMaxDots] = {0.f, 0.f, 0.f};
+  if (phase != PH_INIT && phase != PH_SR && st_idle(st)) return;
+  if (phase == PH_SR && sr_idle(st)) return;
+  float s[kMaxDots];
+  for (int d = 0; d < kMaxDots; ++d) s[d] = 0.0f;
   for (int k = 0; k < nslabs; ++k)  // fixed slab order: deterministic
     for (int d = 0; d < kMaxDots; ++d) s[d] += slab_sums[k * kMaxDots + d];
   switch (phase) {
     case PH_INIT: finalize_phase<PH_INIT>(st, s); break;
     case PH_H1: finalize_phase<PH_H1>(st, s); break;
     case PH_H2: finalize_phase<PH_H2>(st, s); break;
-    default: finalize_phase<PH_H3>(st, s); break;
+    case PH_H3: finalize_phase<PH_H3>(st, s); break;
+    default: finalize_phase<PH_SR>(st, s); break;
   }
 }
 
 __global__ void k_slabsum(const float *__restrict__ slab_sums, int nslabs, float *out) {
-  float s[kMaxDots] = {0.f, 0.f, 0.f};
+  float s[kMaxDots];
+  for (int d = 0; d < kMaxDots; ++d) s[d] = 0.0f;
   for (int k = 0; k < nslabs; ++k)
     for (int d = 0; d < kMaxDots; ++d) s[d] += slab_sums[k * kMaxDots + d];
   for (int d = 0; d < kMaxDots; ++d) out[d] = s[d];

@@ -29,14 +29,15 @@ struct DevState {
   int ev;                          // first event code (-1: none)
   int ev_it;                       // iteration of the first event
   int zero_x;                      // b_hat == 0: x must be returned as 0
+  int sweep;                       // SR schedule: index of the next sweep
   int half;                        // mixed mode: scalars must be finite in fp16 (R7)
   double *hist;                    // [maxit+1] ||r_i|| / ||b_hat||
   float *ahist, *whist;            // [maxit+1] alpha_i, omega_i
 };
 
-enum Phase { PH_INIT = 0, PH_H1 = 1, PH_H2 = 2, PH_H3 = 3 };
+enum Phase { PH_INIT = 0, PH_H1 = 1, PH_H2 = 2, PH_H3 = 3, PH_SR = 4 };
 enum Mode { MODE_APPLY = 0, MODE_H1 = 1, MODE_H2 = 2 };
-constexpr int kMaxDots = 3;
+constexpr int kMaxDots = 12;  // SR sweep: 12 inner products (classic phases use 1-3)
 
 // Grid reduction plumbing of one kernel launch.
 struct Reduce {
@@ -138,6 +139,7 @@ template <> struct Pack<float> {
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] = __fmaf_rn(v[i], b.v[i], acc[i]);
   }
+  __device__ __forceinline__ float mdot(const Pack &b, float acc) const { return dot(b, acc); }
 };
 
 template <> struct Pack<__half> {
@@ -204,6 +206,18 @@ template <> struct Pack<__half> {
       acc[i] = __fmaf_rn(x.x, y.x, acc[i]);
       acc[i] = __fmaf_rn(x.y, y.y, acc[i]);
     }
+  }
+  // acc += a_i * b_i in lane order with the sm_100 mixed FMA (fma.rn.f32.f16:
+  // fp16 x fp16 product, exact, added to fp32 with one rounding) - the same
+  // value as dot(), one instruction per element
+  __device__ __forceinline__ float mdot(const Pack &b, float acc) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm("{\n .reg .b16 al, ah, bl, bh;\n mov.b32 {al, ah}, %1;\n mov.b32 {bl, bh}, %2;\n"
+          " fma.rn.f32.f16 %0, al, bl, %0;\n fma.rn.f32.f16 %0, ah, bh, %0;\n}"
+          : "+f"(acc)
+          : "r"(w[i]), "r"(b.w[i]));
+    return acc;
   }
 };
 
@@ -358,15 +372,61 @@ __device__ __forceinline__ void fin_h3(DevState *st, float rhon, float rr) {
   if (code >= 0) st_event(st, code, i, false);
 }
 
+// SR schedule (R19, oracle/osr.c): the scalar step after sweep i,
+// from its twelve inner products d = (rh,v) (rh,r) (rh,q) (rh,y) (q,r) (q,v)
+// (y,r) (y,v) (q,q) (q,y) (y,y) (r,r).  fp32 arithmetic, no contraction, in
+// the oracle's operation order.
+__device__ __forceinline__ void fin_sr(DevState *st, const float *d) {
+  const int i = st->sweep;
+  const float sigma = d[0], rho = d[1], phi = d[2], psi = d[3];
+  const float qr = d[4], qv = d[5], yr = d[6], yv = d[7], qq = d[8], qy = d[9], yy = d[10], rr = d[11];
+  const double h = sqrt((double)rr) / st->nb;
+  st->hist[i] = h;  // ||r_i|| / ||b_hat||, R4
+  st->it = i;
+  st->sweep = i + 1;
+  int code = -1;
+  if (!isfinite(rr) || !isfinite(rho)) code = STEN_NONFINITE;
+  else if (rr == 0.0f || (st->tol > 0.0 && h <= st->tol)) code = STEN_CONVERGED;
+  else if (i > 0 && (st->omega == 0.0f || rho == 0.0f)) code = STEN_BREAKDOWN;
+  if (code >= 0) st_event(st, code, i, false);
+  if (st->stop || i >= st->maxit) return;
+  float alpha = __fdiv_rn(rho, sigma);  // l.177
+  if (sigma == 0.0f || !usable(st, alpha)) {
+    alpha = 0.0f;
+    st_event(st, isfinite(sigma) ? STEN_BREAKDOWN : STEN_NONFINITE, i + 1, true);
+  }
+  const float a2 = __fmul_rn(alpha, alpha);
+  const float ts = __fadd_rn(__fsub_rn(__fsub_rn(qr, __fmul_rn(alpha, qv)), __fmul_rn(alpha, yr)), __fmul_rn(a2, yv));
+  const float tt = __fadd_rn(__fsub_rn(qq, __fmul_rn(__fmul_rn(2.0f, alpha), qy)), __fmul_rn(a2, yy));
+  float omega = 0.0f;  // tt <= 0: t = A s = 0, s = 0 (R8)
+  bool nf = !isfinite(tt);
+  if (tt > 0.0f) omega = __fdiv_rn(ts, tt);  // l.180
+  if (nf || !usable(st, omega)) {
+    omega = 0.0f;
+    st_event(st, STEN_NONFINITE, i + 1, true);
+  }
+  const float rhon = __fsub_rn(__fsub_rn(rho, __fmul_rn(alpha, sigma)), __fmul_rn(omega, __fsub_rn(phi, __fmul_rn(alpha, psi))));
+  float beta = __fmul_rn(__fdiv_rn(rhon, rho), __fdiv_rn(alpha, omega));  // l.183
+  if (!usable(st, beta)) beta = 0.0f;
+  st->alpha = alpha;
+  st->omega = omega;
+  st->beta = beta;
+  st->rho = rho;
+  st->ahist[i + 1] = alpha;
+  st->whist[i + 1] = omega;
+}
+
 template <int PH>
 __device__ __forceinline__ void finalize_phase(DevState *st, const float *s) {
   if (PH == PH_INIT) fin_init(st, s[0], s[1], s[2]);
   else if (PH == PH_H1) fin_h1(st, s[0]);
   else if (PH == PH_H2) fin_h2(st, s[0], s[1]);
-  else fin_h3(st, s[0], s[1]);
+  else if (PH == PH_H3) fin_h3(st, s[0], s[1]);
+  else fin_sr(st, s);
 }
 
 __device__ __forceinline__ bool st_idle(const DevState *st) { return st->stop || st->it >= st->maxit; }
+__device__ __forceinline__ bool sr_idle(const DevState *st) { return st->stop || st->sweep > st->maxit; }
 
 // Grid-level end of a reduction: every CTA deposits its block sum; the last
 // CTA to arrive sums the deposits in CTA order (deterministic) and either
@@ -398,9 +458,9 @@ __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduc
 #pragma unroll
       for (int d = 0; d < ND; ++d) red.slab_out[d] = s[d];
     } else {
-      float full[kMaxDots] = {0.f, 0.f, 0.f};
+      float full[kMaxDots];
 #pragma unroll
-      for (int d = 0; d < ND; ++d) full[d] = s[d];
+      for (int d = 0; d < kMaxDots; ++d) full[d] = d < ND ? s[d] : 0.0f;
       finalize_phase<PH>(red.st, full);
     }
   }
@@ -426,6 +486,22 @@ template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cuda
 template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);
 int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s);
+// sr.cu: the single-reduction sweep kernel (one launch per iteration)
+struct alignas(64) SrArgs {
+  CUtensorMap tm_in[5];   // r, p, v, q, y of the previous sweep: box (BX+2H) x (BY+4), 2 halo planes
+  CUtensorMap tm_c[6];    // coefficients with one halo plane: box (BX+2H) x (BY+2)
+  void *x;                // in place (own points only), interior plane 0
+  const void *rh;         // shadow residual, interior plane 0
+  void *out[5];           // r, p, v, q, y of this sweep, interior plane 0
+  Geom g;
+  int zc, tiles_x, tiles_y;
+  Reduce red;
+};
+bool sr_config_ok(int by, int stages, int cstages);
+template <typename T> int sr_launch(const SrArgs &a, int by, int stages, int cstages, cudaStream_t s);
+template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages);
+template <typename T> int sr_threads(int by);
+
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g,
                          int has_below, int has_above, float *const c32[6], __half *const c16[6],
                          double *aP, cudaStream_t s);

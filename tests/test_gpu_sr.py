@@ -1,0 +1,261 @@
+"""GPU parity of the single-reduction (SR) schedule against its oracle (oracle/osr.c).
+
+  one sweep   : x, r, p, v, q, y BITWISE equal to o16_sr_sweep / o32_sr_sweep
+                (same scalars, same inputs), on meshes with several tiles, ragged
+                tails, 1x1x1, every kernel geometry, z-chunks down to one plane and
+                slab decomposition; the twelve fp32 sums within the reordering bound
+                |d| <= 1e-5 * sum|a_i b_i| (R13)
+  solves      : the north_star tolerances, against O64-SR / O16-SR (as for the
+                classic schedule in test_gpu_parity.py: fp32 x_50 with the R14 rule,
+                mixed history within 5e-2 for 20 iterations, targets 1e-6 / 1e-3)
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle as orc
+from gpu_util import (fields, from_gpu_vec, gpu_stencil, oracle_coeffs, quantize_vec, to_gpu_vec, torch_cuda,
+                      widen)
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"fp32": 0, "mixed": 1}
+
+
+@pytest.fixture(scope="module")
+def sten():
+    torch_cuda()
+    import paper_2010_03660_b200 as s
+    return s
+
+
+def _pairs(rh, r, v, q, y):
+    return [(rh, v), (rh, r), (rh, q), (rh, y), (q, r), (q, v), (y, r), (y, v), (q, q), (q, y), (y, y), (r, r)]
+
+
+def _sweep_case(sten, prec, mesh, tiling=None, nslabs=1, scalars=(0.61, 0.93, -0.27), seed=1):
+    nx, ny, nz = mesh
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.0, seed=seed)
+    st = gpu_stencil(diag, offs, nslabs=nslabs)
+    if tiling:
+        sten.set_sr_tiling(st, PREC[prec], *tiling)
+    cq = oracle_coeffs(diag, offs, prec)
+    rng = np.random.default_rng(seed + 17)
+    vec = lambda: quantize_vec(rng.uniform(-1, 1, (nz, ny, nx)), prec)
+    rh, x, r, p = vec(), vec(), vec(), vec()
+    if prec == "fp32":
+        v = orc.apply32_fma(cq, p)
+        q = orc.apply32_fma(cq, r)
+        y = orc.apply32_fma(cq, v)
+    else:
+        v = orc.apply16(cq, p)
+        q = orc.apply16(cq, r)
+        y = orc.apply16(cq, v)
+    ts = [to_gpu_vec(a, prec) for a in (rh, x, r, p, v, q, y)]
+    dots = sten.sr_sweep(st, PREC[prec], scalars, *ts)
+    got = [from_gpu_vec(t, prec) for t in ts[1:]]
+    fn = orc.sr_sweep32 if prec == "fp32" else orc.sr_sweep16
+    ref = fn(cq, scalars, rh, x, r, p, v, q, y)
+    st.close()
+    return got, dots, ref, rh
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("mesh", [(37, 29, 19), (1, 1, 1), (5, 3, 2), (130, 17, 9), (264, 20, 11), (8, 40, 4)])
+def test_sr_sweep_bitwise(sten, prec, mesh):
+    got, dots, ref, rh = _sweep_case(sten, prec, mesh)
+    names = ["x", "r", "p", "v", "q", "y"]
+    for name, g, w in zip(names, got, ref[:6]):
+        assert np.array_equal(widen(g, prec), widen(w, prec)), name
+    wide = [widen(a, prec) for a in (rh, got[1], got[3], got[4], got[5])]
+    for d, (a, b) in enumerate(_pairs(*wide)):
+        exact = float(np.vdot(a, b))
+        assert abs(float(dots[d]) - exact) <= 1e-5 * float(np.vdot(np.abs(a), np.abs(b))) + 1e-30, d
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("tiling", [(16, 3, 2, 64), (16, 2, 2, 5), (8, 2, 2, 3), (8, 3, 2, 1), (8, 4, 3, 7),
+                                    (16, 3, 2, 1)])
+def test_sr_sweep_geometries(sten, prec, tiling):
+    got, dots, ref, _ = _sweep_case(sten, prec, (141, 37, 23), tiling=tiling, seed=4)
+    for g, w in zip(got, ref[:6]):
+        assert np.array_equal(widen(g, prec), widen(w, prec))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_sr_sweep_slab_decomposition(sten, prec, nslabs):
+    # two-plane vector halos and one-plane coefficient halos across the slab seams
+    got, dots, ref, _ = _sweep_case(sten, prec, (45, 19, 12), nslabs=nslabs, tiling=(8, 2, 2, 3), seed=6)
+    for g, w in zip(got, ref[:6]):
+        assert np.array_equal(widen(g, prec), widen(w, prec))
+
+
+def _solve(sten, st, prec, b, tol, maxit, x0=None):
+    torch = torch_cuda()
+    sten.set_schedule(st, sten.SCHED_SR)
+    bt = to_gpu_vec(b, prec)
+    xt = torch.empty_like(bt)
+    x0t = None if x0 is None else to_gpu_vec(x0, prec)
+    it, hist, status = sten.bicgstab_solve(st, PREC[prec], bt, x0t, tol, maxit, xt)
+    return from_gpu_vec(xt, prec), it, hist, status
+
+
+@pytest.mark.parametrize("kind,delta,mesh", [(inputs.KIND_POISSON, 0.0, (32, 32, 32)),
+                                             (inputs.KIND_CD, 0.1, (128, 128, 128)),
+                                             (inputs.KIND_CD, 0.0, (37, 29, 19))])
+def test_sr_fp32_50_iterations_vs_o64sr(sten, kind, delta, mesh):
+    nx, ny, nz = mesh
+    diag, offs = fields(kind, nx, ny, nz, delta=delta, seed=2)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=2).astype(np.float32)
+    st = gpu_stencil(diag, offs)
+    x, it, hist, status = _solve(sten, st, "fp32", b, 0.0, 50)
+    assert it == 50
+    alpha, omega = sten.scalar_history(st, 10)
+    c64 = [c.astype(np.float64) for c in oracle_coeffs(diag, offs, "fp32")]
+    bh = orc.scale_rhs(b, diag, "fp32").astype(np.float64)
+    ref = orc.bicgstab64(c64, bh, tol=0.0, maxit=50, schedule="sr")
+    xr = ref["x"]
+    rng = np.random.default_rng(0)  # R14: the oracle's own sensitivity to one ulp of b
+    perturbed = [np.nextafter(bh, np.inf), np.nextafter(bh, -np.inf),
+                 np.where(rng.random(bh.shape) < 0.5, np.nextafter(bh, np.inf), bh)]
+    spread = max(np.linalg.norm(orc.bicgstab64(c64, pb, tol=0.0, maxit=50, schedule="sr")["x"] - xr)
+                 for pb in perturbed) / np.linalg.norm(xr)
+    err = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+    if spread < 1e-6:
+        assert err <= 1e-4
+    else:
+        assert err <= 20 * spread
+        assert orc.true_residual64(c64, bh, x.astype(np.float64)) <= 3 * orc.true_residual64(c64, bh, xr)
+    assert np.all(np.abs(alpha - ref["alpha"][:10]) <= 1e-4 * np.abs(ref["alpha"][:10]))
+    assert np.all(np.abs(omega - ref["omega"][:10]) <= 1e-4 * np.abs(ref["omega"][:10]))
+    assert np.all(np.abs(hist[:11] - ref["hist"][:11]) <= 1e-4 * ref["hist"][:11])
+    st.close()
+
+
+def test_sr_fp32_reaches_1e6(sten):
+    n = 128
+    diag, offs = fields(inputs.KIND_CD, n, n, n, delta=0.1, seed=1)
+    b = inputs.rhs_uniform(n, n, n, seed=1).astype(np.float32)
+    st = gpu_stencil(diag, offs)
+    x, it, hist, status = _solve(sten, st, "fp32", b, 1e-6, 2000)
+    assert status == sten.CONVERGED and hist[-1] <= 1e-6 and it < 60
+    c64 = [c.astype(np.float64) for c in oracle_coeffs(diag, offs, "fp32")]
+    bh = orc.scale_rhs(b, diag, "fp32").astype(np.float64)
+    assert orc.true_residual64(c64, bh, x.astype(np.float64)) <= 5e-6
+    st.close()
+
+
+@pytest.mark.parametrize("mesh,delta,nhist", [((20, 40, 20), 0.0, 20), ((32, 32, 32), 0.1, 12),
+                                              ((45, 23, 17), 0.0, 20)])
+def test_sr_mixed_history_vs_o16sr(sten, mesh, delta, nhist):
+    nx, ny, nz = mesh
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=delta, seed=1)
+    b16 = orc.f16_from_double(inputs.rhs_uniform(nx, ny, nz, seed=1))
+    st = gpu_stencil(diag, offs)
+    x, it, hist, status = _solve(sten, st, "mixed", b16, 0.0, nhist)
+    c16 = oracle_coeffs(diag, offs, "mixed")
+    ref = orc.bicgstab16(c16, orc.scale_rhs(b16, diag, "mixed"), tol=0.0, maxit=nhist, schedule="sr")
+    assert len(hist) == len(ref["hist"]) == nhist + 1
+    assert np.all(np.abs(hist - ref["hist"]) <= 5e-2 * ref["hist"])
+    st.close()
+
+
+def test_sr_mixed_reaches_1e3(sten):
+    n = 32
+    diag, offs = fields(inputs.KIND_CD, n, n, n, delta=0.1, seed=1)
+    b16 = orc.f16_from_double(inputs.rhs_uniform(n, n, n, seed=1))
+    st = gpu_stencil(diag, offs)
+    x, it, hist, status = _solve(sten, st, "mixed", b16, 1e-3, 200)
+    assert status == sten.CONVERGED and hist[-1] <= 1e-3 and it <= 15
+    st.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_sr_slab_decomposed_solve(sten, prec):
+    nx, ny, nz = 33, 21, 32
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.0, seed=6)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=6), prec)
+    st1 = gpu_stencil(diag, offs)
+    _, it1, h1, _ = _solve(sten, st1, prec, b, 0.0, 30)
+    for ns in (2, 4):
+        stn = gpu_stencil(diag, offs, nslabs=ns)
+        _, itn, hn, _ = _solve(sten, stn, prec, b, 0.0, 30)
+        assert itn == it1 == 30
+        tol, k = (1e-5, 10) if prec == "fp32" else (5e-2, 15)
+        assert np.all(np.abs(hn[:k] - h1[:k]) <= tol * h1[:k])
+        stn.close()
+    st1.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_sr_edge_cases(sten, prec):
+    nx, ny, nz = 9, 4, 3
+    offs = [np.zeros((nz, ny, nx)) for _ in range(6)]
+    st = gpu_stencil(None, offs, unit_diag=True)
+    b = quantize_vec(np.random.default_rng(3).uniform(-1, 1, (nz, ny, nx)), prec)
+    x, it, hist, status = _solve(sten, st, prec, b, 1e-3, 10)
+    assert it == 1 and status == sten.CONVERGED and hist[1] == 0.0
+    assert np.array_equal(widen(x, prec), widen(b, prec))
+    x, it, hist, status = _solve(sten, st, prec, b, 0.0, 6)  # benchmark mode keeps going, finite
+    ref = (orc.bicgstab64([np.zeros((nz, ny, nx))] * 6, widen(b, prec), tol=0.0, maxit=6, schedule="sr")
+           if prec == "fp32" else
+           orc.bicgstab16([np.zeros((nz, ny, nx), np.uint16)] * 6, b, tol=0.0, maxit=6, schedule="sr"))
+    assert it == ref["iters"] == 6 and status == ref["status"]
+    assert sten.get_stats(st)["event_iter"] == ref["event_it"]
+    assert np.all(np.isfinite(hist))
+    st.close()
+    diag, offs = fields(inputs.KIND_CD, 6, 5, 4)
+    st = gpu_stencil(diag, offs)
+    b = quantize_vec(inputs.rhs_uniform(6, 5, 4), prec)
+    x, it, hist, status = _solve(sten, st, prec, b, 0.0, 0)
+    assert it == 0 and len(hist) == 1 and hist[0] == 1.0 and status == sten.MAXIT
+    assert np.all(widen(x, prec) == 0)
+    z = quantize_vec(np.zeros((4, 5, 6)), prec)
+    x, it, hist, status = _solve(sten, st, prec, z, 1e-6, 10)
+    assert it == 0 and status == sten.CONVERGED and np.all(widen(x, prec) == 0)
+    st.close()
+
+
+def test_sr_x0_tolerance_stop_and_determinism(sten):
+    nx, ny, nz = 24, 20, 16
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.0, seed=8)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=8).astype(np.float32)
+    x0 = inputs.rhs_uniform(nx, ny, nz, seed=9).astype(np.float32)
+    st = gpu_stencil(diag, offs)
+    x, it, hist, status = _solve(sten, st, "fp32", b, 1e-5, 500, x0=x0)
+    c64 = [c.astype(np.float64) for c in oracle_coeffs(diag, offs, "fp32")]
+    bh = orc.scale_rhs(b, diag, "fp32").astype(np.float64)
+    ref = orc.bicgstab64(c64, bh, x0=x0.astype(np.float64), tol=1e-5, maxit=500, schedule="sr")
+    assert status == sten.CONVERGED and hist[-1] <= 1e-5 < hist[-2]
+    assert abs(hist[0] - ref["hist"][0]) <= 1e-5 * ref["hist"][0]
+    # R14: on this delta = 0 class the oracle's own count moves by several
+    # iterations under a one-ulp change of b; the GPU must fall inside that range
+    counts = [ref["iters"]] + [orc.bicgstab64(c64, pb, x0=x0.astype(np.float64), tol=1e-5, maxit=500,
+                                              schedule="sr")["iters"]
+                               for pb in (np.nextafter(bh, np.inf), np.nextafter(bh, -np.inf))]
+    assert min(counts) - 3 <= it <= max(counts) + 3, (it, counts)
+    assert orc.true_residual64(c64, bh, x.astype(np.float64)) <= 2e-5
+    xa, ita, ha, _ = _solve(sten, st, "fp32", b, 0.0, 25)
+    xb, itb, hb, _ = _solve(sten, st, "fp32", b, 0.0, 25)
+    assert np.array_equal(xa, xb) and np.array_equal(ha, hb)
+    st.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_sr_nccl_single_rank_path_is_bitwise_identical(sten, prec):
+    torch = torch_cuda()
+    nx, ny, nz = 40, 21, 16
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=9)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=9), prec)
+    comm = sten.comm_create(sten.comm_unique_id(), 1, 0)
+    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+    stc = sten.stencil_create(nx, ny, nz, coeffs, nslabs=2, comm=comm)
+    xc, itc, hc, _ = _solve(sten, stc, prec, b, 0.0, 20)
+    stn = gpu_stencil(diag, offs, nslabs=2)
+    xn, itn, hn, _ = _solve(sten, stn, prec, b, 0.0, 20)
+    assert itc == itn == 20
+    assert np.array_equal(hc, hn) and np.array_equal(xc, xn)
+    stc.close()
+    stn.close()
+    comm.close()
