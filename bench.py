@@ -50,7 +50,10 @@ def parse():
     p.add_argument("--nz", type=int, default=NZ, help="planes per GPU (debug / profiling)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--tiling", default="", help="bx,by,zc,stages override")
+    p.add_argument("--schedule", default="sr", choices=["sr", "classic"],
+                   help="sr: single-reduction sweep (19 passes, DESIGN.md R19); classic: Alg. 1 as printed (29)")
+    p.add_argument("--tiling", default="", help="bx,by,zc,stages override (classic)")
+    p.add_argument("--sr-tiling", default="", help="by,stages,cstages,zc override (sr)")
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
     return p.parse_args()
 
@@ -228,6 +231,10 @@ def run_sten(args):
     if args.tiling:
         bx, by, zc, stg = (int(v) for v in args.tiling.split(","))
         sten.set_tiling(st, prec, bx, by, zc, stg)
+    sr = args.schedule == "sr"
+    sten.set_schedule(st, sten.SCHED_SR if sr else sten.SCHED_CLASSIC)
+    if args.sr_tiling:
+        sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
     b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)
     x = torch.empty_like(b)
     maxit = args.maxit
@@ -303,30 +310,34 @@ def run_sten(args):
     peak, peak_kind = measured_peak()
     pname = "mixed" if prec == sten.MIXED else "fp32"
     h1_avg_ms = h1_ms / max(h1_n, 1)
-    h1_bytes = roofline.phase_bytes("H1", pname, npts_local)
+    # dominant kernel: the SR sweep (one per iteration) or the classic H1 stencil
+    h1_bytes = roofline.sweep_bytes(pname, npts_local) if sr else roofline.phase_bytes("H1", pname, npts_local)
     achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
-    bpi = roofline.bytes_per_point_iter(pname)
+    bpi = roofline.bytes_per_point_iter(pname, args.schedule)
     whole_gbs = npts_local * iters_done * bpi / (t_ms / 1e3) / 1e9
+    tname = "half" if prec == sten.MIXED else "float"
+    kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
     traffic, traffic_src = (None, None)
-    if prec == sten.MIXED and nzl == NZ and not args.tiling:
-        traffic, traffic_src = measured_traffic("k_stencil<__half, 1")
+    if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling:
+        traffic, traffic_src = measured_traffic("k_sr<__half" if sr else "k_stencil<__half, 1")
     line = {
         "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / PAPER_GPT_ITER_S,
         "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
         "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
-                   "precision": pname, "maxit": maxit, "tol": tol, "iters_per_solve": iters_done / args.steps,
+                   "precision": pname, "schedule": args.schedule, "maxit": maxit, "tol": tol,
+                   "iters_per_solve": iters_done / args.steps,
                    "parallelism": f"zslab{n}",
                    "l2": "no flush: 16.5 GB working set per GPU >> 126 MB L2",
                    "gflops": value * roofline.FLOPS_PER_POINT_ITER,
                    "hbm_frac_whole_step": whole_gbs / peak, "bytes_per_point_iter": bpi,
                    "status": sten.STATUS_NAMES.get(status, status), "final_rel_residual": float(hist[-1])},
-        "roofline": {"bound": "hbm", "kernel": "k_stencil<half,H1>" if prec == sten.MIXED else "k_stencil<float,H1>",
+        "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": h1_bytes, "avg_launch_ms": h1_avg_ms,
-                     "phase_ms_per_iter": [p / max(h1_n, 1) for p in ph_ms]},
+                     "phase_ms_per_iter": [p / max(h1_n, 1) for p in ph_ms][:1 if sr else 3]},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

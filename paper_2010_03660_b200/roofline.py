@@ -23,9 +23,21 @@ PASSES_PER_ITER = sum(PASSES.values())  # 29
 
 ELEM_BYTES = {"fp32": 4, "mixed": 2}
 
+# Single-reduction schedule (R19): one sweep per iteration reads
+# x, r, p, v, q, y, rhat + 6 coefficients and writes x, r, p, v, q, y.
+PASSES_SR = 19
 
-def bytes_per_point_iter(precision: str) -> int:
-    return PASSES_PER_ITER * ELEM_BYTES[precision]
+
+def passes_per_iter(schedule: str = "classic") -> int:
+    return PASSES_SR if schedule == "sr" else PASSES_PER_ITER
+
+
+def bytes_per_point_iter(precision: str, schedule: str = "classic") -> int:
+    return passes_per_iter(schedule) * ELEM_BYTES[precision]
+
+
+def sweep_bytes(precision: str, npoints: int) -> int:
+    return PASSES_SR * ELEM_BYTES[precision] * npoints
 
 
 def phase_bytes(phase: str, precision: str, npoints: int) -> int:
