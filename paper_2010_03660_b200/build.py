@@ -17,6 +17,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
+# experiment switches only (e.g. -DSTEN_EXP_...); never set for the product build
+FLAGS += os.environ.get("STEN_NVCC_EXTRA", "").split()
 
 
 def _stale(out: str, deps) -> bool:

@@ -38,6 +38,43 @@ namespace {
 
 constexpr int a128(int b) { return (b + 127) & ~127; }
 
+#ifndef STEN_SR_MMA
+#define STEN_SR_MMA 1  // 0: fp16 dots on the FMA pipe (fma.rn.f32.f16), for comparison
+#endif
+
+// Gram of (rh, r', v', q', y') over one tile row of BX points on the tensor
+// cores.  ldmatrix.x2 at `row` + 16 i gives rows = vectors (lanes 0-7: points
+// 16i..16i+7, lanes 8-15: 16i+8..16i+15): at once the A fragment (rows 0-7;
+// rows 8-15 zero) and the B fragment of mma.m16n8k16 (fp16 x fp16 products,
+// fp32 sums).  D[a][b] = sum_k U[a][k] U[b][k] lands in lane
+// 4a + b/2.  Every mma starts from C = 0 and its D is added to the running
+// sums with round-to-nearest fp32 adds: the tensor core's internal 16-term sum
+// truncates, so the accumulator is never carried through it (R20).
+template <int NB>
+__device__ __forceinline__ void gram_row(uint32_t row_addr, float (&acc)[2]) {
+  uint32_t m0[NB], m1[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(m0[i]), "=r"(m1[i])
+                 : "r"(row_addr + 32u * i));
+  float d0[NB], d1[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    float d2, d3;
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%10, %10, %10, %10};"
+        : "=f"(d0[i]), "=f"(d1[i]), "=f"(d2), "=f"(d3)
+        : "r"(m0[i]), "r"(0u), "r"(m1[i]), "r"(0u), "r"(m0[i]), "r"(m1[i]), "f"(0.0f));
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    acc[0] = __fadd_rn(acc[0], d0[i]);
+    acc[1] = __fadd_rn(acc[1], d1[i]);
+  }
+}
+
 template <typename T, int BY>
 struct SrGeo {
   static constexpr int VEC = Pack<T>::VEC;
@@ -54,12 +91,19 @@ struct SrGeo {
   static constexpr int NHF = RI * VW - NT;       // formed vectors outside the own tile
   static constexpr int NHV = RC * VW - NT;       // v' vectors outside the own tile
   static_assert(NHF <= NT && NHV <= NT, "halo work must fit one extra item per thread");
+  // tensor-core Gram (fp16): rh, v', q', y' of one plane staged as 4 dense
+  // BY x BX arrays (16-B staggered to spread ldmatrix rows over banks) + one
+  // zero row; r' is read from its ring
+  static constexpr bool MMA = sizeof(T) == 2 && STEN_SR_MMA;
+  static constexpr int GSV = BX * BY + 8;        // elements between staged vectors
+  static constexpr int GSE = MMA ? 4 * GSV + BX + 8 : 0;  // staging elements (+ a zero row of BX+8)
 };
 
 template <typename T, int BY, int S, int SC>
 constexpr size_t sr_smem_c() {
   using G = SrGeo<T, BY>;
-  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (size_t)SC * 6 * G::CE + 7 * (size_t)G::IE + 2 * (size_t)G::CE);
+  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (size_t)SC * 6 * G::CE + 7 * (size_t)G::IE +
+                                    2 * (size_t)G::CE + (size_t)G::GSE);
 }
 
 template <typename T> struct SrShift;
@@ -122,6 +166,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   T *const PR = CF + SC * 6 * CE;                                // p' ring [3][IE]
   T *const RR = PR + 3 * IE;                                     // r' ring [4][IE]
   T *const VR = RR + 4 * IE;                                     // v' ring [2][CE]
+  T *const GS = VR + 2 * CE;                                     // Gram staging (MMA): [4][GSV] + zero row
   __shared__ float scratch[32 * kMaxDots];
 
   int b = blockIdx.x;
@@ -216,7 +261,26 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   float dacc[12];
 #pragma unroll
   for (int d = 0; d < 12; ++d) dacc[d] = 0.0f;
-
+  float gacc[2] = {0.f, 0.f};  // MMA path: this lane's part (row g, cols 2c, 2c+1) of the warp's Gram
+  if (G::MMA) {
+    for (int e = tid; e < G::BX + 8; e += blockDim.x) GS[4 * G::GSV + e] = T(0.0f);
+  }
+  // MMA path: warp w reduces rows 2w, 2w+1 of the staged plane (16 points per
+  // mma), r' of that plane from ring slot `rslot`.  Lane l (< 16) points at
+  // row l%8 (rh r' v' q' y' 0 0 0) of the 8 points starting at 8*(l/8).
+  auto gram_plane = [&](int rslot) {
+    const int lane = tid & 31, w = tid >> 5, vrow = lane & 7, half = (lane >> 3) & 1;
+#pragma unroll
+    for (int rr2 = 0; rr2 < 2; ++rr2) {
+      const int row = 2 * w + rr2;
+      const T *addr;
+      if (vrow == 1) addr = RR + rslot * IE + (row + 2) * HW + H + 8 * half;
+      else if (vrow == 0) addr = GS + row * G::BX + 8 * half;
+      else if (vrow < 5) addr = GS + (vrow - 1) * G::GSV + row * G::BX + 8 * half;
+      else addr = GS + 4 * G::GSV;
+      gram_row<G::BX / 16>(smem_u32(addr), gacc);  // rows 5-7 walk the zero row
+    }
+  };
   for (int j = 0; j < npi; ++j) {
     const int k = z0 - 4 + j;  // step k: form plane k+2, v' of plane k+1, q'/y'/dots of plane k
     // ---------------- (A) form p', r' of plane k+2; update own x, r, p ----------------
@@ -288,6 +352,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
                 P::ld(p0 + hp), P::ld(p2 + hp))
             .st(vr + hv);
       }
+      if (G::MMA && j >= 5) gram_plane((j + 1) & 3);  // plane k-1, staged in C(k-1)
       __syncthreads();
       if (tid == 0 && qc + SC < npc) issue_c(qc + SC);
     }
@@ -306,6 +371,14 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
         const long long o = (long long)k * plane + gofs;
         qn.st(Og[3] + o);
         yn.st(Og[4] + o);
+      }
+      if (G::MMA) {  // stage rh, v', q', y' of plane k for the tensor-core Gram (read in B(k+1))
+        T *g = GS + ry * G::BX + cx * VEC;
+        (inside ? rh : P::zero()).st(g);
+        (inside ? vw1 : P::zero()).st(g + G::GSV);
+        (inside ? qn : P::zero()).st(g + 2 * G::GSV);
+        (inside ? yn : P::zero()).st(g + 3 * G::GSV);
+      } else if (inside) {
         dacc[0] = rh.mdot(vw1, dacc[0]);   // (rh, v)
         dacc[1] = rh.mdot(rw1, dacc[1]);   // (rh, r)
         dacc[2] = rh.mdot(qn, dacc[2]);    // (rh, q)
@@ -329,6 +402,17 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     vw1 = vw2;
 #pragma unroll
     for (int d = 0; d < 6; ++d) cc[d] = cn[d];
+  }
+  if (G::MMA) {
+    __syncthreads();
+    gram_plane((npi + 1) & 3);  // the last plane, staged in C of the last step
+    // G[a][b] sits in lane 4a + b/2, register b%2 (a, b: 0 rh, 1 r, 2 v, 3 q, 4 y)
+    constexpr int A_[12] = {0, 0, 0, 0, 3, 3, 4, 4, 3, 3, 4, 1};
+    constexpr int B_[12] = {2, 1, 3, 4, 1, 2, 1, 2, 3, 4, 4, 1};
+    const int lane = tid & 31;
+#pragma unroll
+    for (int d = 0; d < 12; ++d)
+      dacc[d] = (lane == 4 * A_[d] + B_[d] / 2) ? gacc[B_[d] & 1] : 0.0f;
   }
   grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
 }
