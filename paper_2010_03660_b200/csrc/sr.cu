@@ -30,6 +30,10 @@
 //    keeps its own z column of p', r', v' and its coefficients in registers.
 //  * Two __syncthreads per plane.  Operation order of every element-wise op
 //    and SpMV is the one oracle/osr.c mirrors (bitwise test).
+//  * The z loop is unrolled by 6 (the period of every ring and window: input
+//    stages 2|3, coefficient stages 2|3, p' ring 3, r' ring 6, v' ring 2), so
+//    every shared-memory slot and register window is a compile-time name: no
+//    modulo arithmetic and no register rotation per plane.
 #include "sten_internal.cuh"
 
 namespace sten {
@@ -38,41 +42,14 @@ namespace {
 
 constexpr int a128(int b) { return (b + 127) & ~127; }
 
-#ifndef STEN_SR_MMA
-#define STEN_SR_MMA 1  // 0: fp16 dots on the FMA pipe (fma.rn.f32.f16), for comparison
-#endif
 
-// Gram of (rh, r', v', q', y') over one tile row of BX points on the tensor
-// cores.  ldmatrix.x2 at `row` + 16 i gives rows = vectors (lanes 0-7: points
-// 16i..16i+7, lanes 8-15: 16i+8..16i+15): at once the A fragment (rows 0-7;
-// rows 8-15 zero) and the B fragment of mma.m16n8k16 (fp16 x fp16 products,
-// fp32 sums).  D[a][b] = sum_k U[a][k] U[b][k] lands in lane
-// 4a + b/2.  Every mma starts from C = 0 and its D is added to the running
-// sums with round-to-nearest fp32 adds: the tensor core's internal 16-term sum
-// truncates, so the accumulator is never carried through it (R20).
-template <int NB>
-__device__ __forceinline__ void gram_row(uint32_t row_addr, float (&acc)[2]) {
-  uint32_t m0[NB], m1[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i)
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
-                 : "=r"(m0[i]), "=r"(m1[i])
-                 : "r"(row_addr + 32u * i));
-  float d0[NB], d1[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    float d2, d3;
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-        "{%10, %10, %10, %10};"
-        : "=f"(d0[i]), "=f"(d1[i]), "=f"(d2), "=f"(d3)
-        : "r"(m0[i]), "r"(0u), "r"(m1[i]), "r"(0u), "r"(m0[i]), "r"(m1[i]), "f"(0.0f));
-  }
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    acc[0] = __fadd_rn(acc[0], d0[i]);
-    acc[1] = __fadd_rn(acc[1], d1[i]);
-  }
+template <int V> struct IC { static constexpr int value = V; };
+
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 
 template <typename T, int BY>
@@ -90,20 +67,15 @@ struct SrGeo {
   static constexpr int CE = a128(HW * RC * (int)sizeof(T)) / (int)sizeof(T);  // elements per coef box
   static constexpr int NHF = RI * VW - NT;       // formed vectors outside the own tile
   static constexpr int NHV = RC * VW - NT;       // v' vectors outside the own tile
+  static constexpr int NR = 6;                   // r' ring slots (= unroll period)
   static_assert(NHF <= NT && NHV <= NT, "halo work must fit one extra item per thread");
-  // tensor-core Gram (fp16): rh, v', q', y' of one plane staged as 4 dense
-  // BY x BX arrays (16-B staggered to spread ldmatrix rows over banks) + one
-  // zero row; r' is read from its ring
-  static constexpr bool MMA = sizeof(T) == 2 && STEN_SR_MMA;
-  static constexpr int GSV = BX * BY + 8;        // elements between staged vectors
-  static constexpr int GSE = MMA ? 4 * GSV + BX + 8 : 0;  // staging elements (+ a zero row of BX+8)
 };
 
 template <typename T, int BY, int S, int SC>
 constexpr size_t sr_smem_c() {
   using G = SrGeo<T, BY>;
-  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (size_t)SC * 6 * G::CE + 7 * (size_t)G::IE +
-                                    2 * (size_t)G::CE + (size_t)G::GSE);
+  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (size_t)SC * 6 * G::CE + (3 + G::NR) * (size_t)G::IE +
+                                    2 * (size_t)G::CE);
 }
 
 template <typename T> struct SrShift;
@@ -132,7 +104,7 @@ template <> struct SrShift<__half> {
   }
 };
 
-// u = c0 l + ... in the fixed order: u = m; fma xm, xp, ym, yp, zm, zp (R10)
+// u = m; u = fma(c_xm, x-1, u); ... xp, ym, yp, zm, zp (R10, oracle o16/o32 mirrors)
 template <typename T>
 __device__ __forceinline__ Pack<T> spmv(const Pack<T> (&c)[6], const Pack<T> &m, const Pack<T> &xl,
                                         const Pack<T> &xr, const Pack<T> &ym, const Pack<T> &yp,
@@ -156,6 +128,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   using G = SrGeo<T, BY>;
   using SH = SrShift<T>;
   constexpr int VEC = G::VEC, H = G::H, HW = G::HW, VW = G::VW, VPR = G::VPR, IE = G::IE, CE = G::CE;
+  static_assert(6 % S == 0 && 6 % SC == 0, "stage counts must divide the unroll period");
 
   if (sr_idle(a.red.st)) return;
 
@@ -164,9 +137,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   T *const IN = reinterpret_cast<T *>(smem + 128);               // [S][5][IE]
   T *const CF = IN + S * 5 * IE;                                 // [SC][6][CE]
   T *const PR = CF + SC * 6 * CE;                                // p' ring [3][IE]
-  T *const RR = PR + 3 * IE;                                     // r' ring [4][IE]
-  T *const VR = RR + 4 * IE;                                     // v' ring [2][CE]
-  T *const GS = VR + 2 * CE;                                     // Gram staging (MMA): [4][GSV] + zero row
+  T *const RR = PR + 3 * IE;                                     // r' ring [6][IE]
+  T *const VR = RR + G::NR * IE;                                 // v' ring [2][CE]
   __shared__ float scratch[32 * kMaxDots];
 
   int b = blockIdx.x;
@@ -176,7 +148,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   const int ch = b / a.tiles_y;
   const int x0 = tx * G::BX, y0 = ty * BY;
   const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
-  const int npi = z1 - z0 + 4;  // staged input planes z0-2 .. z1+1
+  const int npi = z1 - z0 + 4;  // steps = staged input planes z0-2 .. z1+1
   const int npc = z1 - z0 + 2;  // staged coefficient planes z0-1 .. z1
   const int tid = threadIdx.x;
 
@@ -232,114 +204,104 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     for (int q = 0; q < min(SC, npc); ++q) issue_c(q);
   }
 
-  typename P::S al_s = P::scalar(a.red.st->alpha), mal_s = P::neg(al_s);
-  typename P::S om_s = P::scalar(a.red.st->omega), mom_s = P::neg(om_s);
-  typename P::S be_s = P::scalar(a.red.st->beta);
+  const typename P::S al_s = P::scalar(a.red.st->alpha), mal_s = P::neg(al_s);
+  const typename P::S om_s = P::scalar(a.red.st->omega), mom_s = P::neg(om_s);
+  const typename P::S be_s = P::scalar(a.red.st->beta);
 
   T *const Xg = reinterpret_cast<T *>(a.x);
   const T *const RHg = reinterpret_cast<const T *>(a.rh);
   T *const Og[5] = {reinterpret_cast<T *>(a.out[0]), reinterpret_cast<T *>(a.out[1]), reinterpret_cast<T *>(a.out[2]),
                     reinterpret_cast<T *>(a.out[3]), reinterpret_cast<T *>(a.out[4])};
-
-  // own x of the plane formed at the next step, r_hat of the plane of the next dots
-  P xn = P::zero(), rhn = P::zero();
-  auto load_x = [&](int m) {
-    if (inside && m >= z0 && m < z1) xn = P::ldg(Xg + (long long)m * plane + gofs);
+  // own x / r_hat arrive by plain 16-B loads three planes ahead of their use
+  // (x at the step that forms its plane, r_hat at the dots of its plane)
+  auto ld_x = [&](int m) {
+    P v = P::zero();
+    if (inside && m >= z0 && m < z1) v = P::ldg(Xg + (long long)m * plane + gofs);
+    return v;
   };
-  auto load_rh = [&](int k) {
-    if (inside && k < z1) rhn = P::ldg(RHg + (long long)k * plane + gofs);
+  auto ld_rh = [&](int k) {
+    P v = P::zero();
+    if (inside && k < z1) v = P::ldg(RHg + (long long)k * plane + gofs);
+    return v;
   };
-  load_x(z0 - 2);
-  load_rh(z0);
 
-  P pw0 = P::zero(), pw1 = P::zero(), pw2 = P::zero();                   // own p' at k, k+1, k+2
-  P rw0 = P::zero(), rw1 = P::zero(), rw2 = P::zero(), rw3 = P::zero();  // own r' at k-1 .. k+2
-  P vw0 = P::zero(), vw1 = P::zero(), vw2 = P::zero();                   // own v' at k-1, k, k+1
-  P cc[6], cn[6];                                                        // own coefficients at k, k+1
+  // register windows, named by step mod 6 (or mod 3 / mod 2)
+  P pw[3], rw[6], vw[3], cw[2][6], xq[3], rq[3];
 #pragma unroll
-  for (int d = 0; d < 6; ++d) cc[d] = cn[d] = P::zero();
+  for (int i = 0; i < 3; ++i) {
+    pw[i] = vw[i] = P::zero();
+    xq[i] = ld_x(z0 - 2 + i);  // x of the plane formed at step i
+    rq[i] = ld_rh(z0 + i);     // r_hat of the plane of the dots at step 4 + i
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    rw[i] = P::zero();
+    cw[0][i] = cw[1][i] = P::zero();
+  }
   float dacc[12];
 #pragma unroll
   for (int d = 0; d < 12; ++d) dacc[d] = 0.0f;
-  float gacc[2] = {0.f, 0.f};  // MMA path: this lane's part (row g, cols 2c, 2c+1) of the warp's Gram
-  if (G::MMA) {
-    for (int e = tid; e < G::BX + 8; e += blockDim.x) GS[4 * G::GSV + e] = T(0.0f);
-  }
-  // MMA path: warp w reduces rows 2w, 2w+1 of the staged plane (16 points per
-  // mma), r' of that plane from ring slot `rslot`.  Lane l (< 16) points at
-  // row l%8 (rh r' v' q' y' 0 0 0) of the 8 points starting at 8*(l/8).
-  auto gram_plane = [&](int rslot) {
-    const int lane = tid & 31, w = tid >> 5, vrow = lane & 7, half = (lane >> 3) & 1;
-#pragma unroll
-    for (int rr2 = 0; rr2 < 2; ++rr2) {
-      const int row = 2 * w + rr2;
-      const T *addr;
-      if (vrow == 1) addr = RR + rslot * IE + (row + 2) * HW + H + 8 * half;
-      else if (vrow == 0) addr = GS + row * G::BX + 8 * half;
-      else if (vrow < 5) addr = GS + (vrow - 1) * G::GSV + row * G::BX + 8 * half;
-      else addr = GS + 4 * G::GSV;
-      gram_row<G::BX / 16>(smem_u32(addr), gacc);  // rows 5-7 walk the zero row
-    }
-  };
-  for (int j = 0; j < npi; ++j) {
-    const int k = z0 - 4 + j;  // step k: form plane k+2, v' of plane k+1, q'/y'/dots of plane k
-    // ---------------- (A) form p', r' of plane k+2; update own x, r, p ----------------
-    mbar_wait(&mbar[j % S], (uint32_t)((j / S) & 1));
+
+  // one step j (= J mod 6): (A) form p', r' of plane m = k+2 and update the own
+  // x, r, p; (B) v' = A p' on plane k+1; (C) q' = A r', y' = A v' and the
+  // twelve inner products on plane k.  k = z0 - 4 + j.
+  auto step = [&](auto JC, int j) {
+    constexpr int J = decltype(JC)::value;
+    const int k = z0 - 4 + j, m = k + 2;
+    // ---------------- (A) ----------------
+    mbar_wait(&mbar[J % S], (uint32_t)((j / S) & 1));
     {
-      const T *st = IN + (j % S) * 5 * IE;
-      T *pr = PR + (j % 3) * IE;
-      T *rr = RR + (j & 3) * IE;
-      const int m = k + 2;
-      {
-        const P r = P::ld(st + ei), p = P::ld(st + IE + ei), v = P::ld(st + 2 * IE + ei);
-        const P q = P::ld(st + 3 * IE + ei), y = P::ld(st + 4 * IE + ei);
-        const P s = P::fmas(mal_s, v, r);
-        const P t = P::fmas(mal_s, y, q);
-        const P rn = P::fmas(mom_s, t, s);
-        const P pn = P::fmas(be_s, P::fmas(mom_s, v, p), rn);
-        rn.st(rr + ei);
-        pn.st(pr + ei);
-        pw2 = pn;
-        rw3 = rn;
-        if (inside && m >= z0 && m < z1) {
-          const long long o = (long long)m * plane + gofs;
-          P::fmas(om_s, s, P::fmas(al_s, p, xn)).st(Xg + o);
-          rn.st(Og[0] + o);
-          pn.st(Og[1] + o);
-        }
+      const T *st = IN + (J % S) * 5 * IE;
+      T *pr = PR + (J % 3) * IE;
+      T *rr = RR + J * IE;
+      const P r = P::ld(st + ei), p = P::ld(st + IE + ei), v = P::ld(st + 2 * IE + ei);
+      const P q = P::ld(st + 3 * IE + ei), y = P::ld(st + 4 * IE + ei);
+      const P s = P::fmas(mal_s, v, r);
+      const P t = P::fmas(mal_s, y, q);
+      const P rn = P::fmas(mom_s, t, s);
+      const P pn = P::fmas(be_s, P::fmas(mom_s, v, p), rn);
+      rn.st(rr + ei);
+      pn.st(pr + ei);
+      pw[J % 3] = pn;
+      rw[J] = rn;
+      if (inside && m >= z0 && m < z1) {
+        const long long o = (long long)m * plane + gofs;
+        P::fmas(om_s, s, P::fmas(al_s, p, xq[J % 3])).st(Xg + o);
+        rn.st(Og[0] + o);
+        pn.st(Og[1] + o);
       }
+      xq[J % 3] = ld_x(m + 3);
       if (hf >= 0) {
-        const P r = P::ld(st + hf), p = P::ld(st + IE + hf), v = P::ld(st + 2 * IE + hf);
-        const P q = P::ld(st + 3 * IE + hf), y = P::ld(st + 4 * IE + hf);
-        const P s = P::fmas(mal_s, v, r);
-        const P t = P::fmas(mal_s, y, q);
-        const P rn = P::fmas(mom_s, t, s);
-        P::fmas(be_s, P::fmas(mom_s, v, p), rn).st(pr + hf);
-        rn.st(rr + hf);
+        const P hr = P::ld(st + hf), hp = P::ld(st + IE + hf), hv_ = P::ld(st + 2 * IE + hf);
+        const P hq = P::ld(st + 3 * IE + hf), hy = P::ld(st + 4 * IE + hf);
+        const P hs = P::fmas(mal_s, hv_, hr);
+        const P ht = P::fmas(mal_s, hy, hq);
+        const P hrn = P::fmas(mom_s, ht, hs);
+        P::fmas(be_s, P::fmas(mom_s, hv_, hp), hrn).st(pr + hf);
+        hrn.st(rr + hf);
       }
-      load_x(m + 1);
     }
     __syncthreads();
     if (tid == 0 && j + S < npi) issue_in(j + S);
 
-    // ---------------- (B) v' = A p' on plane k+1 (own tile + one-point ring) ----------------
+    // ---------------- (B) ----------------
     if (j >= 2) {
-      const int qc = j - 2;  // coefficient plane k+1
-      mbar_wait(&mbar[S + qc % SC], (uint32_t)((qc / SC) & 1));
-      const T *cf = CF + (qc % SC) * 6 * CE;
-      const T *p0 = PR + ((j + 1) % 3) * IE;  // plane k
-      const T *p1 = PR + ((j + 2) % 3) * IE;  // plane k+1
-      const T *p2 = PR + (j % 3) * IE;        // plane k+2
-      T *vr = VR + ((j + 1) & 1) * CE;
-      {
+      constexpr int CS = (J + 6 - 2) % SC;  // coefficient slot of plane k+1 (ordinal j-2)
+      mbar_wait(&mbar[S + CS], (uint32_t)(((j - 2) / SC) & 1));
+      const T *cf = CF + CS * 6 * CE;
+      const T *p0 = PR + ((J + 1) % 3) * IE;  // plane k
+      const T *p1 = PR + ((J + 2) % 3) * IE;  // plane k+1
+      const T *p2 = PR + (J % 3) * IE;        // plane k+2
+      T *vr = VR + ((J + 1) & 1) * CE;
+      P (&cn)[6] = cw[J & 1];
 #pragma unroll
-        for (int d = 0; d < 6; ++d) cn[d] = P::ld(cf + d * CE + ec);
-        const P xl = SH::left(pw1, SH::ld1(p1 + ei - 1)), xr = SH::right(pw1, SH::ld1(p1 + ei + VEC));
-        const P vn = spmv<T>(cn, pw1, xl, xr, P::ld(p1 + ei - HW), P::ld(p1 + ei + HW), pw0, pw2);
-        vn.st(vr + ec);
-        vw2 = vn;
-        if (inside && k + 1 >= z0 && k + 1 < z1) vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
-      }
+      for (int d = 0; d < 6; ++d) cn[d] = P::ld(cf + d * CE + ec);
+      const P &c1 = pw[(J + 2) % 3];
+      const P xl = SH::left(c1, SH::ld1(p1 + ei - 1)), xr = SH::right(c1, SH::ld1(p1 + ei + VEC));
+      const P vn = spmv<T>(cn, c1, xl, xr, P::ld(p1 + ei - HW), P::ld(p1 + ei + HW), pw[(J + 1) % 3], pw[J % 3]);
+      vn.st(vr + ec);
+      vw[J % 3] = vn;
+      if (inside && k + 1 >= z0 && k + 1 < z1) vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
       if (hv >= 0) {
         const int hp = hv + HW;  // same point in the input-box layout
         P c[6];
@@ -352,67 +314,50 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
                 P::ld(p0 + hp), P::ld(p2 + hp))
             .st(vr + hv);
       }
-      if (G::MMA && j >= 5) gram_plane((j + 1) & 3);  // plane k-1, staged in C(k-1)
       __syncthreads();
-      if (tid == 0 && qc + SC < npc) issue_c(qc + SC);
+      if (tid == 0 && j - 2 + SC < npc) issue_c(j - 2 + SC);
     }
 
-    // ---------------- (C) q' = A r', y' = A v' on plane k; the twelve dots ----------------
+    // ---------------- (C) ----------------
     if (j >= 4) {
-      const T *r1 = RR + ((j + 2) & 3) * IE;  // r' plane k
-      const T *v1 = VR + (j & 1) * CE;        // v' plane k
-      const P qn = spmv<T>(cc, rw1, SH::left(rw1, SH::ld1(r1 + ei - 1)), SH::right(rw1, SH::ld1(r1 + ei + VEC)),
-                           P::ld(r1 + ei - HW), P::ld(r1 + ei + HW), rw0, rw2);
-      const P yn = spmv<T>(cc, vw1, SH::left(vw1, SH::ld1(v1 + ec - 1)), SH::right(vw1, SH::ld1(v1 + ec + VEC)),
-                           P::ld(v1 + ec - HW), P::ld(v1 + ec + HW), vw0, vw2);
-      const P rh = rhn;
-      load_rh(k + 1);
+      const T *r1 = RR + ((J + 4) % 6) * IE;  // r' plane k
+      const T *v1 = VR + (J & 1) * CE;        // v' plane k
+      const P (&cc)[6] = cw[(J + 1) & 1];     // coefficients of plane k (loaded at step j-1)
+      const P &rm = rw[(J + 3) % 6], &rc = rw[(J + 4) % 6], &rp = rw[(J + 5) % 6];
+      const P &vm = vw[(J + 1) % 3], &vc = vw[(J + 2) % 3], &vp = vw[J % 3];
+      const P qn = spmv<T>(cc, rc, SH::left(rc, SH::ld1(r1 + ei - 1)), SH::right(rc, SH::ld1(r1 + ei + VEC)),
+                           P::ld(r1 + ei - HW), P::ld(r1 + ei + HW), rm, rp);
+      const P yn = spmv<T>(cc, vc, SH::left(vc, SH::ld1(v1 + ec - 1)), SH::right(vc, SH::ld1(v1 + ec + VEC)),
+                           P::ld(v1 + ec - HW), P::ld(v1 + ec + HW), vm, vp);
+      const P rh = rq[(J + 2) % 3];  // r_hat of plane k (loaded three steps ago)
+      rq[(J + 2) % 3] = ld_rh(k + 3);
       if (inside) {
         const long long o = (long long)k * plane + gofs;
         qn.st(Og[3] + o);
         yn.st(Og[4] + o);
-      }
-      if (G::MMA) {  // stage rh, v', q', y' of plane k for the tensor-core Gram (read in B(k+1))
-        T *g = GS + ry * G::BX + cx * VEC;
-        (inside ? rh : P::zero()).st(g);
-        (inside ? vw1 : P::zero()).st(g + G::GSV);
-        (inside ? qn : P::zero()).st(g + 2 * G::GSV);
-        (inside ? yn : P::zero()).st(g + 3 * G::GSV);
-      } else if (inside) {
-        dacc[0] = rh.mdot(vw1, dacc[0]);   // (rh, v)
-        dacc[1] = rh.mdot(rw1, dacc[1]);   // (rh, r)
+        dacc[0] = rh.mdot(vc, dacc[0]);    // (rh, v)
+        dacc[1] = rh.mdot(rc, dacc[1]);    // (rh, r)
         dacc[2] = rh.mdot(qn, dacc[2]);    // (rh, q)
         dacc[3] = rh.mdot(yn, dacc[3]);    // (rh, y)
-        dacc[4] = qn.mdot(rw1, dacc[4]);   // (q, r)
-        dacc[5] = qn.mdot(vw1, dacc[5]);   // (q, v)
-        dacc[6] = yn.mdot(rw1, dacc[6]);   // (y, r)
-        dacc[7] = yn.mdot(vw1, dacc[7]);   // (y, v)
+        dacc[4] = qn.mdot(rc, dacc[4]);    // (q, r)
+        dacc[5] = qn.mdot(vc, dacc[5]);    // (q, v)
+        dacc[6] = yn.mdot(rc, dacc[6]);    // (y, r)
+        dacc[7] = yn.mdot(vc, dacc[7]);    // (y, v)
         dacc[8] = qn.mdot(qn, dacc[8]);    // (q, q)
         dacc[9] = qn.mdot(yn, dacc[9]);    // (q, y)
         dacc[10] = yn.mdot(yn, dacc[10]);  // (y, y)
-        dacc[11] = rw1.mdot(rw1, dacc[11]);  // (r, r)
+        dacc[11] = rc.mdot(rc, dacc[11]);  // (r, r)
       }
     }
-    pw0 = pw1;
-    pw1 = pw2;
-    rw0 = rw1;
-    rw1 = rw2;
-    rw2 = rw3;
-    vw0 = vw1;
-    vw1 = vw2;
-#pragma unroll
-    for (int d = 0; d < 6; ++d) cc[d] = cn[d];
-  }
-  if (G::MMA) {
-    __syncthreads();
-    gram_plane((npi + 1) & 3);  // the last plane, staged in C of the last step
-    // G[a][b] sits in lane 4a + b/2, register b%2 (a, b: 0 rh, 1 r, 2 v, 3 q, 4 y)
-    constexpr int A_[12] = {0, 0, 0, 0, 3, 3, 4, 4, 3, 3, 4, 1};
-    constexpr int B_[12] = {2, 1, 3, 4, 1, 2, 1, 2, 3, 4, 4, 1};
-    const int lane = tid & 31;
-#pragma unroll
-    for (int d = 0; d < 12; ++d)
-      dacc[d] = (lane == 4 * A_[d] + B_[d] / 2) ? gacc[B_[d] & 1] : 0.0f;
+  };
+
+  for (int j = 0; j < npi; j += 6) {
+    step(IC<0>{}, j);
+    if (j + 1 < npi) step(IC<1>{}, j + 1);
+    if (j + 2 < npi) step(IC<2>{}, j + 2);
+    if (j + 3 < npi) step(IC<3>{}, j + 3);
+    if (j + 4 < npi) step(IC<4>{}, j + 4);
+    if (j + 5 < npi) step(IC<5>{}, j + 5);
   }
   grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
 }
@@ -435,7 +380,7 @@ int launch_sr_one(const SrArgs &a, cudaStream_t s) {
 }
 }  // namespace
 
-#define STEN_SR_CONFIGS(X) X(16, 3, 2) X(16, 2, 2) X(8, 2, 2) X(8, 3, 2) X(8, 4, 3)
+#define STEN_SR_CONFIGS(X) X(16, 3, 2) X(16, 2, 2) X(16, 2, 3) X(8, 2, 2) X(8, 3, 2) X(8, 3, 3)
 
 bool sr_config_ok(int by, int stages, int cstages) {
 #define X(B, S_, C_) if (by == B && stages == S_ && cstages == C_) return true;

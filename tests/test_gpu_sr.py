@@ -74,7 +74,7 @@ def test_sr_sweep_bitwise(sten, prec, mesh):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-@pytest.mark.parametrize("tiling", [(16, 3, 2, 64), (16, 2, 2, 5), (8, 2, 2, 3), (8, 3, 2, 1), (8, 4, 3, 7),
+@pytest.mark.parametrize("tiling", [(16, 3, 2, 64), (16, 2, 2, 5), (8, 2, 2, 3), (8, 3, 2, 1), (8, 3, 3, 7), (16, 2, 3, 9),
                                     (16, 3, 2, 1)])
 def test_sr_sweep_geometries(sten, prec, tiling):
     got, dots, ref, _ = _sweep_case(sten, prec, (141, 37, 23), tiling=tiling, seed=4)
