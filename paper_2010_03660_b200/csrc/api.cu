@@ -212,6 +212,8 @@ struct sten_stencil {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   sten_stats stats{};
   long long launches = 0;       // kernel launches (direct + graph nodes) of the current call
+  void *stage = nullptr;        // contiguous device staging for pitched host copies
+  size_t stage_bytes = 0;
 };
 
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
@@ -736,10 +738,47 @@ static void drop_graphs(sten_stencil *st) {
 // dense (nz,ny,nx) user array <-> internal array (rows of `pitch`, planes of
 // `plane` elements, halo planes): one 3D copy per slab, a 1D copy when the
 // internal layout has no padding at all.
-static cudaError_t copy3d(void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch, size_t sysize,
-                          size_t wbytes, size_t h, size_t d, cudaStream_t s) {
+static int ptr_on_device(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+// Host <-> device copies of a pitched layout go through a contiguous device
+// staging buffer: one full-speed linear PCIe transfer, then the pitched copy
+// on the device (a pitched host transfer runs at a fraction of the link rate).
+static cudaError_t stage_buffer(sten_stencil *st, size_t bytes, void **out) {
+  if (bytes > st->stage_bytes) {
+    if (st->stage) cudaFree(st->stage);
+    st->stage = nullptr;
+    st->stage_bytes = 0;
+    cudaError_t e = cudaMalloc(&st->stage, bytes);
+    if (e != cudaSuccess) return e;
+    st->stage_bytes = bytes;
+  }
+  *out = st->stage;
+  return cudaSuccess;
+}
+static cudaError_t copy3d(sten_stencil *st, void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch,
+                          size_t sysize, size_t wbytes, size_t h, size_t d, cudaStream_t s) {
   if (dpitch == wbytes && spitch == wbytes && dysize == h && sysize == h)
     return cudaMemcpyAsync(dst, src, wbytes * h * d, cudaMemcpyDefault, s);
+  const bool dev_src = ptr_on_device(src), dev_dst = ptr_on_device(dst);
+  if (dev_src != dev_dst) {
+    void *stg = nullptr;
+    cudaError_t e = stage_buffer(st, wbytes * h * d, &stg);
+    if (e != cudaSuccess) return e;
+    if (!dev_src) {  // host (dense rows) -> staging -> pitched device
+      e = cudaMemcpyAsync(stg, src, wbytes * h * d, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return e;
+      return copy3d(st, dst, dpitch, dysize, stg, wbytes, h, wbytes, h, d, s);
+    }
+    e = copy3d(st, stg, wbytes, h, src, spitch, sysize, wbytes, h, d, s);  // pitched device -> staging
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(dst, stg, wbytes * h * d, cudaMemcpyDeviceToHost, s);
+  }
   cudaMemcpy3DParms p;
   memset(&p, 0, sizeof p);
   p.srcPtr = make_cudaPitchedPtr(const_cast<void *>(src), spitch, wbytes, sysize);
@@ -753,7 +792,7 @@ static int copy_in(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), const v
   for (Slab &sl : st->slabs) {
     char *dst = (char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
     const char *sp = (const char *)src + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(copy3d(dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
+    CUDA_TRY(copy3d(st, dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
                     (size_t)st->ny, (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
@@ -763,7 +802,7 @@ static int copy_out(sten_stencil *st, int prec, void *(*sel)(PrecBufs &), void *
   for (Slab &sl : st->slabs) {
     const char *src = (const char *)sel(sl.pb[prec]) + (size_t)st->plane * e;
     char *dp = (char *)dst + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(copy3d(dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
+    CUDA_TRY(copy3d(st, dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
                     (size_t)(st->plane / st->pitch), (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
@@ -775,7 +814,7 @@ static int sr_copy_in(sten_stencil *st, int prec, Base base, const void *src, cu
   for (Slab &sl : st->slabs) {
     char *dst = sr_interior(base(sl), st, prec);
     const char *sp = (const char *)src + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(copy3d(dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
+    CUDA_TRY(copy3d(st, dst, (size_t)st->pitch * e, (size_t)(st->plane / st->pitch), sp, (size_t)st->nx * e,
                     (size_t)st->ny, (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
@@ -786,7 +825,7 @@ static int sr_copy_out(sten_stencil *st, int prec, Base base, void *dst, cudaStr
   for (Slab &sl : st->slabs) {
     const char *src = sr_interior(base(sl), st, prec);
     char *dp = (char *)dst + (size_t)sl.z_first * st->nx * st->ny * e;
-    CUDA_TRY(copy3d(dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
+    CUDA_TRY(copy3d(st, dp, (size_t)st->nx * e, (size_t)st->ny, src, (size_t)st->pitch * e,
                     (size_t)(st->plane / st->pitch), (size_t)st->nx * e, (size_t)st->ny, (size_t)sl.nz, s));
   }
   return STEN_OK;
@@ -1021,6 +1060,7 @@ void stencil_destroy(sten_stencil *st) {
   cudaFree(st->hist);
   cudaFree(st->ahist);
   cudaFree(st->whist);
+  cudaFree(st->stage);
   if (st->cap) cudaStreamDestroy(st->cap);
   if (st->ev_a) cudaEventDestroy(st->ev_a);
   if (st->ev_b) cudaEventDestroy(st->ev_b);

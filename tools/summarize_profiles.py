@@ -31,6 +31,20 @@ def read_ncu_csv(path):
     return out
 
 
+CMDS = {
+    "r1": {"traffic": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                      "--clock-control none -k regex:'k_stencil|k_h3|k_init' -s 30 -c 6 "
+                      "python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu",
+           "full": "ncu --set full --clock-control none --import-source on -k regex:'k_stencil|k_h3' -s 0 -c 3 "
+                   "python bench.py --steps 1 --warmup 1 --maxit 2 --nz 384 --no-e2e --no-cpu"},
+    "r1_sr": {"traffic": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                         "--clock-control none -k regex:'k_sr|k_init' -s 20 -c 4 "
+                         "python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu",
+              "full": "ncu --set full --clock-control none --import-source on -k regex:k_sr -s 2 -c 1 "
+                      "python bench.py --steps 1 --warmup 1 --maxit 4 --nz 384 --no-e2e --no-cpu"},
+}
+
+
 def short(name):
     return name.split("(")[0].replace("void ", "").replace("sten::", "").replace("<unnamed>::", "")
 
@@ -50,7 +64,7 @@ def main(tag):
         for (i, k, g, b), m in data.items():
             agg[short(k)].append(m["gpu__time_duration.sum"])
         tot = sum(sum(v) for v in agg.values())
-        hot = sum(sum(v) for k, v in agg.items() if k.startswith(("k_stencil", "k_h3", "k_rows")))
+        hot = sum(sum(v) for k, v in agg.items() if k.startswith(("k_stencil", "k_h3", "k_rows", "k_sr")))
         with open(os.path.join(PROF, f"{tag}_launch_shares.md"), "w") as f:
             f.write(f"# {tag}: ncu launch list of `python bench.py` (first {len(data)} launches)\n\n")
             f.write("`ncu --metrics gpu__time_duration.sum --clock-control none -c 700` - per-launch times are cold-cache and\n"
@@ -58,13 +72,14 @@ def main(tag):
             f.write("| kernel | launches | avg ms | share of profiled time |\n|---|---|---|---|\n")
             for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
                 f.write(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e6:.3f} | {sum(v) / tot * 100:.1f}% |\n")
-            f.write(f"\nHot path (stencil + H3) share: {hot / tot * 100:.1f}%; the rest is one-time setup "
+            f.write(f"\nHot path (SR sweep / stencil + H3) share: {hot / tot * 100:.1f}%; the rest is one-time setup "
                     f"(field generation, Jacobi scaling, fp16 conversion) and the per-solve init.\n")
     # 2. full-size traffic per hot kernel
     tpath = os.path.join(OUT, f"{tag}_traffic_full.csv")
     if os.path.exists(tpath):
         data = read_ncu_csv(tpath)
-        alg_passes = {"k_stencil<__half, 1": 12, "k_stencil<__half, 2": 10, "k_h3<__half>": 7, "k_init<__half>": 5}
+        alg_passes = {"k_stencil<__half, 1": 12, "k_stencil<__half, 2": 10, "k_h3<__half>": 7, "k_init<__half>": 5,
+                      "k_sr<__half": 19}
         res = {}
         for (i, k, g, b), m in data.items():
             sk = short(k)
@@ -79,9 +94,7 @@ def main(tag):
                 dram_write_bytes=m["dram__bytes_write.sum"], traffic_bytes=tr, algorithmic_bytes=alg,
                 traffic_over_algorithmic=tr / alg, dram_tbs=tr / t / 1e12, algorithmic_tbs=alg / t / 1e12))
         json.dump({"workload": "cfg3 600x595x1536 mixed fp16, steady-state launches of bench.py",
-                   "command": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                              "--clock-control none -k regex:'k_stencil|k_h3|k_init' -s 30 -c 6 "
-                              "python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu",
+                   "command": CMDS.get(tag, {}).get("traffic", ""),
                    "kernels": res}, open(os.path.join(PROF, f"{tag}_traffic.json"), "w"), indent=1)
     # 3. --set full report of the hot kernels (reduced z for cheap replay)
     rpath = os.path.join(OUT, f"{tag}_full.ncu-rep")
@@ -102,14 +115,14 @@ def main(tag):
         idx = {h: i for i, h in enumerate(hdr)}
         with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as f:
             f.write(f"# {tag}: `ncu --set full` of the hot kernels (600x595x384 slab, same kernels/tiling as the bench)\n\n")
-            f.write("Command: `ncu --set full --clock-control none --import-source on -k regex:'k_stencil|k_h3' -s 0 -c 3 "
-                    "python bench.py --steps 1 --warmup 1 --maxit 2 --nz 384 --no-e2e --no-cpu`\n\n")
+            f.write(f"Command: `{CMDS.get(tag, {}).get('full', '')}`\n\n")
             f.write("| metric | unit | " + " | ".join(short(r[idx["Kernel Name"]]) for r in data) + " |\n")
             f.write("|---|---|" + "---|" * len(data) + "\n")
             for w in want[1:]:
                 if w in idx:
                     f.write(f"| {w} | {units[idx[w]]} | " + " | ".join(r[idx[w]] for r in data) + " |\n")
-            f.write("\nTensor pipes are idle by design (not a contraction); the kernels are HBM-bound.\n")
+            f.write("\nTensor pipes are idle: the Gram of the SR sweep runs on the FMA pipe (fma.rn.f32.f16), "
+                    "which measured faster than mma.sync for it (DESIGN.md); the kernels are HBM/latency-bound.\n")
     print("written", os.listdir(PROF))
 
 
