@@ -153,6 +153,30 @@ int bicgstab_solve(sten_stencil *st, int precision, const void *b, const void *x
                    int maxit, void *x_out, int *iters, double *res_hist, int *status,
                    void *cuda_stream);
 
+/* Mixed-precision iterative refinement (the remedy the paper names for the
+ * fp16 plateau; R21).  Solves A x = b to an fp32
+ * accuracy while the iterations run in the mixed mode:
+ *   b_hat = rn32(b / a_P) (R3); x = x0 or 0 (fp32);
+ *   for k = 0, 1, ...:
+ *     r = b_hat - A_hat x in fp32 (fp32 coefficients, the FMA-chain SpMV of R10);
+ *     res_hist[k] = ||r||_2 / ||b_hat||_2 (fp32 sums);
+ *     stop: res <= tol -> STEN_CONVERGED; res not below the previous step's ->
+ *           STEN_BREAKDOWN (stagnation); k == outer_maxit -> STEN_MAXIT;
+ *           non-finite -> STEN_NONFINITE;
+ *     sigma = 2^e, the power of two with max|r| <= sigma; r16 = rn16(r / sigma);
+ *     d = the mixed-precision solve of A_hat d = r16 (the handle's schedule,
+ *         relative tolerance inner_tol, at most inner_maxit iterations, x0 = 0);
+ *     x = fma(sigma, d, x) in fp32.
+ *   b, x0, x_out: fp32, this rank's points (dense layout, host or device);
+ *   outer_iters: refinement steps taken (k at exit); inner_iters: total
+ *   mixed iterations; res_hist: host array of >= outer_maxit + 1 doubles.
+ * b == 0 gives x = 0, CONVERGED, outer_iters = 0.  Errors: STEN_EINVAL (tol
+ * <= 0, inner_tol < 0, outer_maxit < 0, inner_maxit < 1), STEN_ENOMEM,
+ * STEN_ECUDA, STEN_ENCCL. */
+int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol, int outer_maxit, double inner_tol,
+                    int inner_maxit, void *x_out, int *outer_iters, int *inner_iters, double *res_hist,
+                    int *status, void *cuda_stream);
+
 /* Per-iteration scalars alpha_i, omega_i (i = 1..n) of the last solve, as
  * computed on the device (fp32), for parity checks.  n <= iters. */
 int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);

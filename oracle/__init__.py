@@ -309,6 +309,48 @@ def sr_sweep32(c32, scalars, rh, x, r, p, v, q, y):
     return (*vecs, dots)
 
 
+# ---------------- iterative refinement (R21) ----------------
+
+def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inner_maxit=100, schedule="classic"):
+    """Mixed-precision iterative refinement, step by step as R21 states it
+    (PAPER.md:591, 598 name iterative refinement as the remedy for the fp16
+    plateau).  Composes the pinned pieces: the fp32 FMA-chain SpMV mirror
+    (apply32_fma), fp32 element-wise arithmetic (numpy float32), binary16
+    rounding (f16_from_double) and the O16 solver (bicgstab16).
+    bhat32: the scaled right-hand side b_hat (float32).  Returns dict(x (float32),
+    hist (outer residuals), outer, inner, status)."""
+    c32 = quantize_coeffs(c64, "fp32")
+    c16 = quantize_coeffs(c64, "mixed")
+    b = np.asarray(bhat32, np.float32)
+    nb = float(np.sqrt(np.sum(b.astype(np.float64) ** 2)))
+    x = np.zeros_like(b) if x0 is None else np.asarray(x0, np.float32).copy()
+    if nb == 0.0:
+        return dict(x=np.zeros_like(b), hist=np.array([0.0]), outer=0, inner=0, status=ORC_CONVERGED)
+    hist, inner, status, prev = [], 0, ORC_MAXIT, None
+    for k in range(outer_maxit + 1):
+        r = b - apply32_fma(c32, x)                      # fp32: one rounding per element
+        res = float(np.sqrt(np.sum(r.astype(np.float64) ** 2))) / nb
+        hist.append(res)
+        if not np.isfinite(res):
+            status = ORC_NONFINITE
+            break
+        if res <= tol:
+            status = ORC_CONVERGED
+            break
+        if prev is not None and res >= prev:
+            status = ORC_BREAKDOWN                       # stagnation
+            break
+        if k == outer_maxit:
+            break
+        prev = res
+        sigma = 2.0 ** np.frexp(float(np.max(np.abs(r))))[1]  # power of two >= max|r|
+        r16 = f16_from_double(r.astype(np.float64) / sigma)
+        d = bicgstab16(c16, r16, tol=inner_tol, maxit=inner_maxit, schedule=schedule)
+        inner += d["iters"]
+        x = (x.astype(np.float64) + sigma * f16_to_double(d["x"])).astype(np.float32)
+    return dict(x=x, hist=np.array(hist), outer=len(hist) - 1, inner=inner, status=status)
+
+
 # ---------------- fp32 mirror ----------------
 
 def apply32_fma(c32, v32):

@@ -73,6 +73,8 @@ def lib():
         L.sten_set_schedule.argtypes = [P, I]
         L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I]
         L.sten_sr_sweep.argtypes = [P, I, D, D, D, P, P, P, P, P, P, P, P, P]
+        L.bicgstab_refine.argtypes = [P, P, P, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(I), P,
+                                      ctypes.POINTER(I), P]
         _lib = L
     return _lib
 
@@ -275,3 +277,19 @@ def sr_sweep(st: Stencil, precision: int, scalars, rh, x, r, p, v, q, y, stream=
     _check(lib().sten_sr_sweep(st.handle, precision, al, om, be, _ptr(rh), _ptr(x), _ptr(r), _ptr(p), _ptr(v),
                                _ptr(q), _ptr(y), dots.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
     return dots
+
+
+def bicgstab_refine(st: Stencil, b, x0, tol: float, outer_maxit: int, inner_tol: float, inner_maxit: int, x_out,
+                    stream=None):
+    """Mixed-precision iterative refinement (fp32 b, x0, x_out).
+    Returns (outer_iters, inner_iters, res_hist[0..outer_iters], status)."""
+    _check_vec(b, FP32, st.npoints, "b")
+    _check_vec(x_out, FP32, st.npoints, "x_out")
+    if x0 is not None:
+        _check_vec(x0, FP32, st.npoints, "x0")
+    hist = np.zeros(max(outer_maxit, 0) + 1, dtype=np.float64)
+    ko, ki, status = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(-1)
+    _check(lib().bicgstab_refine(st.handle, _ptr(b), _ptr(x0), float(tol), int(outer_maxit), float(inner_tol),
+                                 int(inner_maxit), _ptr(x_out), ctypes.byref(ko), ctypes.byref(ki),
+                                 hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(status), _stream(stream)))
+    return ko.value, ki.value, hist[: ko.value + 1].copy(), status.value

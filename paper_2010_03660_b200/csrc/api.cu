@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -214,6 +215,8 @@ struct sten_stencil {
   long long launches = 0;       // kernel launches (direct + graph nodes) of the current call
   void *stage = nullptr;        // contiguous device staging for pitched host copies
   size_t stage_bytes = 0;
+  unsigned *ir_amax = nullptr;  // refinement: max|r| (float bits), sigma
+  float *ir_sigma = nullptr;
 };
 
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
@@ -407,7 +410,7 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
   return STEN_OK;
 }
 
-static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s) {
+static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s, bool scale = true) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   const int e = esize(prec), vec = prec == STEN_FP32 ? 4 : 8;
@@ -415,7 +418,7 @@ static int launch_init(sten_stencil *st, int prec, int slab, bool with_ax, cudaS
   EwArgs a;
   memset(&a, 0, sizeof a);
   a.bw = (char *)b.bw + off;
-  a.aP = st->has_diag ? sl.aP : nullptr;
+  a.aP = (scale && st->has_diag) ? sl.aP : nullptr;
   a.ax = with_ax ? (const void *)((char *)b.t + off) : nullptr;
   a.r = (char *)b.r + off;
   a.rh = (char *)b.rh + off;
@@ -833,7 +836,7 @@ static int sr_copy_out(sten_stencil *st, int prec, Base base, void *dst, cudaStr
 
 // S1 for the SR schedule: b_hat, r0 = b_hat - A x0, rhat = p = r0, v = 0 into
 // SR set 0 (k_init), q = y = 0.
-static int launch_init_sr(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s) {
+static int launch_init_sr(sten_stencil *st, int prec, int slab, bool with_ax, cudaStream_t s, bool scale = true) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   SrBufs &r = sl.sr[prec];
@@ -842,7 +845,7 @@ static int launch_init_sr(sten_stencil *st, int prec, int slab, bool with_ax, cu
   EwArgs a;
   memset(&a, 0, sizeof a);
   a.bw = (char *)b.bw + off;
-  a.aP = st->has_diag ? sl.aP : nullptr;
+  a.aP = (scale && st->has_diag) ? sl.aP : nullptr;
   a.ax = with_ax ? (const void *)((char *)b.t + off) : nullptr;
   a.r = sr_interior(r.vec[0][0], st, prec);
   a.rh = sr_interior(r.rh, st, prec);
@@ -1061,6 +1064,8 @@ void stencil_destroy(sten_stencil *st) {
   cudaFree(st->ahist);
   cudaFree(st->whist);
   cudaFree(st->stage);
+  cudaFree(st->ir_amax);
+  cudaFree(st->ir_sigma);
   if (st->cap) cudaStreamDestroy(st->cap);
   if (st->ev_a) cudaEventDestroy(st->ev_a);
   if (st->ev_b) cudaEventDestroy(st->ev_b);
@@ -1129,12 +1134,19 @@ int stencil_apply(sten_stencil *st, int prec, const void *x, void *y, void *cuda
   return STEN_OK;
 }
 
-int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, double tol, int maxit, void *x_out,
-                   int *iters, double *res_hist, int *status, void *cuda_stream) {
-  if (!st || !b || !x_out || !iters || !res_hist || !status) return set_err(STEN_EINVAL, "NULL argument");
-  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
-  if (!(tol >= 0.0) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
-  cudaStream_t s = (cudaStream_t)cuda_stream;
+// The solve proper (Alg. 1 / SR) on a right-hand side already in the working
+// precision's bw buffer and (with_x0) an initial guess in the classic x
+// buffer.  scale_rhs: b_hat = b / a_P (R3) - off for the refinement's inner
+// solves, whose right-hand side is already a residual of the scaled system.
+struct SolveOut {
+  DevState fin;
+  int chunk = 0;
+  long long kernels = 0;
+  double ph_ms[3] = {0, 0, 0};
+  long long ph_n[3] = {0, 0, 0};
+};
+static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, double tol, int maxit, cudaStream_t s,
+                      SolveOut *out) {
   const bool sr = st->schedule == STEN_SCHED_SR;
   RC_TRY(ensure_bufs(st, prec));
   if (sr) RC_TRY(ensure_sr(st, prec));
@@ -1147,9 +1159,6 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
     CUDA_TRY(cudaMalloc(&st->ahist, sizeof(float) * st->hist_cap));
     CUDA_TRY(cudaMalloc(&st->whist, sizeof(float) * st->hist_cap));
   }
-  st->launches = 0;
-  memset(&st->stats, 0, sizeof st->stats);
-  CUDA_TRY(cudaEventRecord(st->ev_a, s));
   // device state
   DevState h;
   memset(&h, 0, sizeof h);
@@ -1164,10 +1173,7 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   *st->st_host = h;
   CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
   // S1: b_hat, r0, rhat, p0 (Alg. 1 l.174; R1, R3)
-  RC_TRY(copy_in(st, prec, sel_bw, b, s));
-  const bool with_x0 = x0 != nullptr;
   if (with_x0) {
-    RC_TRY(copy_in(st, prec, sel_x, x0, s));
     // A x0 through the apply path: input buffer s, output t
     for (Slab &sl : st->slabs) {
       const size_t vb = (size_t)st->plane * esize(prec);
@@ -1190,24 +1196,21 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
     }
   }
   for (int k = 0; k < (int)st->slabs.size(); ++k)
-    RC_TRY(sr ? launch_init_sr(st, prec, k, with_x0, s) : launch_init(st, prec, k, with_x0, s));
+    RC_TRY(sr ? launch_init_sr(st, prec, k, with_x0, s, scale_rhs) : launch_init(st, prec, k, with_x0, s, scale_rhs));
   RC_TRY(reduce_scalars(st, PH_INIT, s));
   // iterations: CUDA graphs of `chunk` iterations (even, so the ping-pong
   // parity of p/v is the same at every replay)
-  long long kernels = 0;
-  double ph_ms[3] = {0, 0, 0};
-  long long ph_n[3] = {0, 0, 0};
-  int chunk = 0;
   const int nsteps = sr ? maxit + 1 : maxit;  // SR: sweep i computes x_i, r_i (i = 0..maxit)
   if (nsteps > 0) {
-    chunk = tol > 0.0 ? 8 : ((nsteps + 1) / 2) * 2;
+    int chunk = tol > 0.0 ? 8 : ((nsteps + 1) / 2) * 2;
     if (chunk > 2048) chunk = 2048;
+    out->chunk = chunk;
     GraphRec *gr = nullptr;
     RC_TRY(get_graph(st, prec, chunk, &gr));
     const int nrep = (nsteps + chunk - 1) / chunk;
     for (int rep = 0; rep < nrep; ++rep) {
       CUDA_TRY(cudaGraphLaunch(gr->exec, s));
-      kernels += gr->kernels;
+      out->kernels += gr->kernels;
       const bool poll = tol > 0.0 || st->timing;
       if (poll) {
         CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -1224,8 +1227,8 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
               if (te != cudaSuccess)
                 return set_err(STEN_ECUDA, "cudaEventElapsedTime(iter %d, phase %d): %s", j, p,
                                cudaGetErrorString(te));
-              ph_ms[p] += ms;
-              ph_n[p] += 1;
+              out->ph_ms[p] += ms;
+              out->ph_n[p] += 1;
             }
           }
         }
@@ -1233,17 +1236,42 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
       }
     }
   }
-  CUDA_TRY(cudaEventRecord(st->ev_b, s));
-  // results
   CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  DevState fin = *st->st_host;
-  if (fin.zero_x)
+  out->fin = *st->st_host;
+  if (out->fin.zero_x)
     for (Slab &sl : st->slabs) {
       const size_t vb = (size_t)st->plane * esize(prec);
       if (sr) CUDA_TRY(cudaMemsetAsync(sr_interior(sl.sr[prec].x, st, prec), 0, vb * sl.nz, s));
       else CUDA_TRY(cudaMemsetAsync((char *)sl.pb[prec].x + vb, 0, vb * sl.nz, s));
     }
+  return STEN_OK;
+}
+
+// device pointer of slab `k`'s solution (interior plane 0) after solve_core
+static char *solution_ptr(sten_stencil *st, int prec, Slab &sl) {
+  if (st->schedule == STEN_SCHED_SR) return sr_interior(sl.sr[prec].x, st, prec);
+  return (char *)sl.pb[prec].x + (size_t)st->plane * esize(prec);
+}
+
+int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, double tol, int maxit, void *x_out,
+                   int *iters, double *res_hist, int *status, void *cuda_stream) {
+  if (!st || !b || !x_out || !iters || !res_hist || !status) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (!(tol >= 0.0) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const bool sr = st->schedule == STEN_SCHED_SR;
+  RC_TRY(ensure_bufs(st, prec));
+  if (sr) RC_TRY(ensure_sr(st, prec));
+  st->launches = 0;
+  memset(&st->stats, 0, sizeof st->stats);
+  CUDA_TRY(cudaEventRecord(st->ev_a, s));
+  RC_TRY(copy_in(st, prec, sel_bw, b, s));
+  if (x0) RC_TRY(copy_in(st, prec, sel_x, x0, s));
+  SolveOut so;
+  RC_TRY(solve_core(st, prec, x0 != nullptr, true, tol, maxit, s, &so));
+  CUDA_TRY(cudaEventRecord(st->ev_b, s));
+  const DevState &fin = so.fin;
   if (sr) RC_TRY(sr_copy_out(st, prec, [prec](Slab &sl) { return sl.sr[prec].x; }, x_out, s));
   else RC_TRY(copy_out(st, prec, sel_x, x_out, s));
   CUDA_TRY(cudaMemcpyAsync(res_hist, st->hist, sizeof(double) * (fin.it + 1), cudaMemcpyDeviceToHost, s));
@@ -1255,12 +1283,154 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   cudaEventElapsedTime(&solve_ms, st->ev_a, st->ev_b);
   st->stats.solve_ms = solve_ms;
   for (int p = 0; p < 3; ++p) {
-    st->stats.phase_ms[p] = ph_ms[p];
-    st->stats.phase_launches[p] = ph_n[p];
+    st->stats.phase_ms[p] = so.ph_ms[p];
+    st->stats.phase_launches[p] = so.ph_n[p];
   }
-  st->stats.kernel_launches = st->launches + kernels;
+  st->stats.kernel_launches = st->launches + so.kernels;
   st->stats.event_iter = fin.ev >= 0 ? fin.ev_it : 0;
-  st->stats.graph_chunk = chunk;
+  st->stats.graph_chunk = so.chunk;
+  return STEN_OK;
+}
+
+// ------------------------------------------ iterative refinement (R21) --
+static int ir_grid(sten_stencil *st, long long n) {
+  long long g = (n + 255) / 256;
+  if (g > (long long)st->sm * 8) g = st->sm * 8;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// r = b_hat - A x (fp32) on every slab; returns ||r||^2 (all slabs / ranks) and
+// leaves max|r| in ir_amax
+static int ir_residual(sten_stencil *st, cudaStream_t s, double *rr) {
+  const int F = STEN_FP32;
+  const size_t vb = (size_t)st->plane * 4;
+  if (decomposed(st)) RC_TRY(exchange(st, F, [](PrecBufs &bb) { return bb.s; }, s));
+  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, F, MODE_APPLY, k, 0, s));
+  CUDA_TRY(cudaMemsetAsync(st->ir_amax, 0, sizeof(unsigned), s));
+  for (int k = 0; k < (int)st->slabs.size(); ++k) {
+    Slab &sl = st->slabs[k];
+    PrecBufs &b = sl.pb[F];
+    IrArgs a;
+    memset(&a, 0, sizeof a);
+    a.b = (const float *)((char *)b.rh + vb);  // b_hat
+    a.ax = (const float *)((char *)b.t + vb);
+    a.r = (float *)((char *)b.r + vb);
+    a.amax = st->ir_amax;
+    a.n = (long long)st->plane * sl.nz;
+    a.red = make_red(st, k);
+    a.red.slab_out = st->slab_sums + k * kMaxDots;
+    const int g = ir_grid(st, a.n);
+    if (g > st->partials_cap) return set_err(STEN_ECUDA, "internal: refinement grid exceeds the partial-sum buffer");
+    KLAUNCH(ir_launch(IR_RESID, a, g, s));
+    st->launches++;
+  }
+  KLAUNCH(slabsum_launch(st->slab_sums, (int)st->slabs.size(), st->red_total, s));
+  if (st->comm && st->comm->nranks > 1) {
+    NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, 1, ncclFloat32, ncclSum, st->comm->comm, s));
+    NCCL_TRY(g_nccl.AllReduce(st->ir_amax, st->ir_amax, 1, ncclUint32, ncclMax, st->comm->comm, s));
+  }
+  float h = 0.f;
+  CUDA_TRY(cudaMemcpyAsync(&h, st->red_total, sizeof h, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *rr = (double)h;
+  return STEN_OK;
+}
+
+int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol, int outer_maxit, double inner_tol,
+                    int inner_maxit, void *x_out, int *outer_iters, int *inner_iters, double *res_hist, int *status,
+                    void *cuda_stream) {
+  if (!st || !b || !x_out || !outer_iters || !inner_iters || !res_hist || !status)
+    return set_err(STEN_EINVAL, "NULL argument");
+  if (!(tol > 0.0) || !(inner_tol >= 0.0) || outer_maxit < 0 || inner_maxit < 1)
+    return set_err(STEN_EINVAL, "tol=%g inner_tol=%g outer_maxit=%d inner_maxit=%d invalid", tol, inner_tol,
+                   outer_maxit, inner_maxit);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int F = STEN_FP32, M = STEN_MIXED;
+  RC_TRY(ensure_bufs(st, F));
+  RC_TRY(ensure_bufs(st, M));
+  if (st->schedule == STEN_SCHED_SR) RC_TRY(ensure_sr(st, M));
+  if (!st->ir_amax) {
+    CUDA_TRY(cudaMalloc(&st->ir_amax, sizeof(unsigned)));
+    CUDA_TRY(cudaMalloc(&st->ir_sigma, sizeof(float)));
+  }
+  st->launches = 0;
+  memset(&st->stats, 0, sizeof st->stats);
+  CUDA_TRY(cudaEventRecord(st->ev_a, s));
+  const size_t v4 = (size_t)st->plane * 4, v2 = (size_t)st->plane * 2;
+  // b_hat (fp32, R3) into the fp32 rh buffer; the iterate x lives in the fp32 s buffer
+  RC_TRY(copy_in(st, F, sel_bw, b, s));
+  for (Slab &sl : st->slabs) {
+    PrecBufs &pb = sl.pb[F];
+    IrArgs a;
+    memset(&a, 0, sizeof a);
+    a.b = (const float *)((char *)pb.bw + v4);
+    a.aP = st->has_diag ? sl.aP : nullptr;
+    a.r = (float *)((char *)pb.rh + v4);
+    a.n = (long long)st->plane * sl.nz;
+    KLAUNCH(ir_launch(IR_BHAT, a, ir_grid(st, a.n), s));
+    st->launches++;
+    CUDA_TRY(cudaMemsetAsync((char *)pb.s + v4, 0, v4 * sl.nz, s));
+  }
+  double bb = 0.0;
+  RC_TRY(ir_residual(st, s, &bb));  // x = 0: r = b_hat
+  const double nb = sqrt(bb);
+  const bool zero_b = nb == 0.0;  // b = 0: x = 0 is exact, whatever x0 is
+  if (x0 && !zero_b) RC_TRY(copy_in(st, F, sel_s, x0, s));
+  int k = 0, inner = 0, stat = STEN_MAXIT;
+  double prev = 0.0;
+  for (;; ++k) {
+    if (zero_b) {
+      res_hist[0] = 0.0;
+      stat = STEN_CONVERGED;
+      break;
+    }
+    double rr = bb;
+    if (x0 || k > 0) RC_TRY(ir_residual(st, s, &rr));
+    const double res = sqrt(rr) / nb;
+    res_hist[k] = res;
+    if (!std::isfinite(res)) { stat = STEN_NONFINITE; break; }
+    if (res <= tol) { stat = STEN_CONVERGED; break; }
+    if (k > 0 && res >= prev) { stat = STEN_BREAKDOWN; break; }  // stagnation (R21)
+    if (k == outer_maxit) { stat = STEN_MAXIT; break; }
+    prev = res;
+    // inner right-hand side: r / sigma in fp16 (sigma = 2^e >= max|r|)
+    for (Slab &sl : st->slabs) {
+      IrArgs a;
+      memset(&a, 0, sizeof a);
+      a.r = (float *)((char *)sl.pb[F].r + v4);
+      a.r16 = (__half *)((char *)sl.pb[M].bw + v2);
+      a.amax = st->ir_amax;
+      a.sigma = st->ir_sigma;
+      a.n = (long long)st->plane * sl.nz;
+      KLAUNCH(ir_launch(IR_SCALE, a, ir_grid(st, a.n), s));
+      st->launches++;
+    }
+    SolveOut so;
+    RC_TRY(solve_core(st, M, false, false, inner_tol, inner_maxit, s, &so));
+    inner += so.fin.it;
+    st->launches += so.kernels;
+    for (Slab &sl : st->slabs) {
+      IrArgs a;
+      memset(&a, 0, sizeof a);
+      a.d16 = (const __half *)solution_ptr(st, M, sl);
+      a.x = (float *)((char *)sl.pb[F].s + v4);
+      a.sigma = st->ir_sigma;
+      a.n = (long long)st->plane * sl.nz;
+      KLAUNCH(ir_launch(IR_UPDATE, a, ir_grid(st, a.n), s));
+      st->launches++;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(st->ev_b, s));
+  RC_TRY(copy_out(st, F, sel_s, x_out, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  *outer_iters = k;
+  *inner_iters = inner;
+  *status = stat;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, st->ev_a, st->ev_b);
+  st->stats.solve_ms = ms;
+  st->stats.kernel_launches = st->launches;
   return STEN_OK;
 }
 

@@ -124,6 +124,56 @@ int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
   return (int)cudaGetLastError();
 }
 
+// ------------------------------------------- iterative refinement (R21) --
+// b_hat = rn32(b / a_P) in fp64 (R3); the refinement's fp32 right-hand side
+__global__ void k_ir_bhat(const IrArgs a) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
+    a.r[i] = a.aP ? __double2float_rn((double)a.b[i] / a.aP[i]) : a.b[i];
+}
+// r = b_hat - A x in fp32; (r, r) by the deterministic grid reduction; max|r|
+__global__ void __launch_bounds__(256) k_ir_resid(const IrArgs a) {
+  __shared__ float scratch[32 * kMaxDots];
+  float d[1] = {0.0f};
+  float m = 0.0f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
+    const float r = __fsub_rn(a.b[i], a.ax[i]);
+    a.r[i] = r;
+    d[0] = __fmaf_rn(r, r, d[0]);
+    m = fmaxf(m, fabsf(r));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(a.amax, __float_as_uint(m));  // |r| >= 0: bits order as floats
+  grid_reduce_finalize<1, PH_INIT>(d, a.red, scratch);
+}
+// r16 = rn16(r / sigma), sigma = 2^e the power of two with max|r| <= sigma
+// (an exact scaling: the inner right-hand side uses the whole fp16 range)
+__global__ void k_ir_scale(const IrArgs a) {
+  const float m = __uint_as_float(*a.amax);
+  int e = 0;
+  frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
+  const float inv = ldexpf(1.0f, -e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.sigma = ldexpf(1.0f, e);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
+    a.r16[i] = __float2half_rn(a.r[i] * inv);
+}
+// x = fma(sigma, d, x) in fp32
+__global__ void k_ir_update(const IrArgs a) {
+  const float sg = *a.sigma;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
+    a.x[i] = __fmaf_rn(sg, __half2float(a.d16[i]), a.x[i]);
+}
+
+int ir_launch(int which, const IrArgs &a, int grid, cudaStream_t s) {
+  switch (which) {
+    case IR_BHAT: k_ir_bhat<<<grid, 256, 0, s>>>(a); break;
+    case IR_RESID: k_ir_resid<<<grid, 256, 0, s>>>(a); break;
+    case IR_SCALE: k_ir_scale<<<grid, 256, 0, s>>>(a); break;
+    default: k_ir_update<<<grid, 256, 0, s>>>(a); break;
+  }
+  return (int)cudaGetLastError();
+}
+
 // ------------------------------------------------- cross-slab scalar step --
 __global__ void k_scalars(int phase, const float *__restrict__ slab_sums, int nslabs, DevState *st) {
   if (phase != PH_INIT && phase != PH_SR && st_idle(st)) return;

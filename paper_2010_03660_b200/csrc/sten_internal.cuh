@@ -486,6 +486,24 @@ template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cuda
 template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);
 int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s);
+// Iterative refinement (bicgstab_refine, R21): fp32 outer steps
+// around the mixed inner solve.  All pointers at interior plane 0.
+struct IrArgs {
+  const float *b;        // ir_bhat: user b (fp32)      ir_resid: b_hat (fp32)
+  const double *aP;      // ir_bhat: a_P or null
+  const float *ax;       // ir_resid: A x (fp32)
+  float *r;              // ir_bhat: b_hat out        ir_resid: r = b_hat - A x   ir_scale: r in
+  __half *r16;           // ir_scale: r / sigma in fp16
+  const __half *d16;     // ir_update: inner solution
+  float *x;              // ir_update: x += sigma d
+  unsigned *amax;        // ir_resid: atomicMax of |r| (float bits)
+  float *sigma;          // ir_scale writes, ir_update reads: 2^e >= max|r|
+  long long n;           // elements of the interior range (linear, padding holds zeros)
+  Reduce red;            // ir_resid: (r, r) deposited in red.slab_out
+};
+int ir_launch(int which, const IrArgs &a, int grid, cudaStream_t s);
+enum { IR_BHAT = 0, IR_RESID = 1, IR_SCALE = 2, IR_UPDATE = 3 };
+
 // sr.cu: the single-reduction sweep kernel (one launch per iteration)
 struct alignas(64) SrArgs {
   CUtensorMap tm_in[5];   // r, p, v, q, y of the previous sweep: box (BX+2H) x (BY+4), 2 halo planes
