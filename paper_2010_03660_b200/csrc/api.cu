@@ -178,6 +178,7 @@ struct GraphKey {
 };
 struct SrTiling {
   int by = 0, stages = 0, cstages = 0, zc = 0;
+  int zc_tail = 0, tail = 0;  // the last `tail` planes in chunks of zc_tail (0: none)
 };
 struct GraphRec {
   cudaGraphExec_t exec = nullptr;
@@ -553,19 +554,34 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
 // (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
 static void default_sr_tiling(sten_stencil *st, int prec) {
   SrTiling &t = st->srt[prec];
-  int by = 16, stg = 3, cst = 2, zc = 64;
-  if (const char *e = getenv("STEN_SR_TILING")) sscanf(e, "%d,%d,%d,%d", &by, &stg, &cst, &zc);
+  int by = 16, stg = 3, cst = 2, zc = 320, zct = 64, tail = 256;
+  if (const char *e = getenv("STEN_SR_TILING")) sscanf(e, "%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail);
   t.by = by;
   t.stages = stg;
   t.cstages = cst;
   const int nzs = st->slabs[0].nz;
   t.zc = zc < nzs ? zc : nzs;
+  t.zc_tail = zct > 0 ? zct : t.zc;
+  t.tail = tail > 0 ? tail : 0;
+}
+
+// chunk plan of a slab: nbig chunks of zc planes, then zc_tail-plane chunks to
+// the end (the short chunks come last in launch order and even out the final
+// wave; the long ones keep the per-chunk halo planes and pipeline fill rare)
+static void sr_chunks(const SrTiling &t, int nzs, int *nbig, int *zct) {
+  int big = nzs - (t.tail < nzs ? t.tail : 0);
+  *nbig = big / t.zc;
+  *zct = t.zc_tail;
+  if (*nbig * t.zc == nzs) *zct = t.zc;  // no tail left
 }
 
 static int sr_grid(const sten_stencil *st, int prec, int nzs) {
   const SrTiling &t = st->srt[prec];
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
-  return ((st->nx + bx - 1) / bx) * ((st->ny + t.by - 1) / t.by) * ((nzs + t.zc - 1) / t.zc);
+  int nbig, zct;
+  sr_chunks(t, nzs, &nbig, &zct);
+  const int nch = nbig + (nzs - nbig * t.zc + zct - 1) / zct;
+  return ((st->nx + bx - 1) / bx) * ((st->ny + t.by - 1) / t.by) * nch;
 }
 
 static int ensure_sr(sten_stencil *st, int prec) {
@@ -636,6 +652,7 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
   a.rh = sr_interior(b.rh, st, prec);
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
   a.zc = t.zc;
+  sr_chunks(t, sl.nz, &a.nbig, &a.zc_tail);
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   a.tiles_x = (st->nx + bx - 1) / bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
@@ -936,14 +953,13 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   st->nx = nx;
   st->ny = ny;
   st->nz = nz;
-  // Layout: rows padded to `pitch` = a multiple of 64
-  // elements (128-B aligned rows), planes a multiple of 64 elements.  The
-  // padding costs a line fetch per row (6.7% at nx = 600, measured), but the
-  // 256-B tiles of the stencil kernel then start on line boundaries; unpadded
-  // rows (STEN_PITCH_ALIGN=8) remove that traffic yet lose more to tiles that
-  // straddle lines (tools/ and DESIGN.md "Tuning": 102.8 vs 98.6 Gpoint-iter/s).
+  // Layout: rows of `pitch` elements, a multiple of
+  // 8 (16-B vectors), planes a multiple of 64 elements.  Unpadded rows move
+  // no padding bytes: the SR sweep (the bench's schedule) is 1.9% faster with
+  // them at nx = 600 (144.0 vs 141.5 Gpoint-iter/s), the classic kernels prefer
+  // 128-B aligned rows (103.7 vs 100.0): STEN_PITCH_ALIGN=64 selects those.
   {
-    int align = 64;
+    int align = 8;
     if (const char *pa = getenv("STEN_PITCH_ALIGN")) align = atoi(pa) >= 8 ? atoi(pa) : 8;
     st->pitch = (nx + align - 1) / align * align;
     int nyp = ny;
@@ -1462,7 +1478,11 @@ int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstag
   if (by) t.by = by;
   if (stages) t.stages = stages;
   if (cstages) t.cstages = cstages;
-  if (zc) t.zc = zc;
+  if (zc) {  // an explicit chunk length: uniform chunks
+    t.zc = zc;
+    t.zc_tail = zc;
+    t.tail = 0;
+  }
   if (!sr_config_ok(t.by, t.stages, t.cstages) || t.zc <= 0)
     return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d", t.by, t.stages, t.cstages,
                    t.zc);

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   const int ty = b % a.tiles_y;
   const int ch = b / a.tiles_y;
   const int x0 = tx * G::BX, y0 = ty * BY;
-  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int z0 = ch < a.nbig ? ch * a.zc : a.nbig * a.zc + (ch - a.nbig) * a.zc_tail;
+  const int z1 = min(z0 + (ch < a.nbig ? a.zc : a.zc_tail), a.g.nz);
   const int npi = z1 - z0 + 4;  // steps = staged input planes z0-2 .. z1+1
   const int npc = z1 - z0 + 2;  // staged coefficient planes z0-1 .. z1
   const int tid = threadIdx.x;
@@ -374,7 +375,7 @@ int launch_sr_one(const SrArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  const int grid = a.tiles_x * a.tiles_y * (a.nbig + (a.g.nz - a.nbig * a.zc + a.zc_tail - 1) / a.zc_tail);
   k_sr<T, BY, S, SC><<<grid, SrGeo<T, BY>::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }

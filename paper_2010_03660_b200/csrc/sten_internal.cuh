@@ -513,6 +513,8 @@ struct alignas(64) SrArgs {
   void *out[5];           // r, p, v, q, y of this sweep, interior plane 0
   Geom g;
   int zc, tiles_x, tiles_y;
+  int nbig;               // chunks [0, nbig) have zc planes; the rest cover
+  int zc_tail;            // [nbig*zc, nz) in zc_tail-plane chunks (fills the tail wave)
   Reduce red;
 };
 bool sr_config_ok(int by, int stages, int cstages);
