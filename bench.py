@@ -46,12 +46,18 @@ def parse():
     p.add_argument("--precision", default="mixed", choices=["mixed", "fp32"])
     p.add_argument("--maxit", type=int, default=100)
     p.add_argument("--tol", type=float, default=0.0, help="0: exactly maxit iterations (config 3a)")
-    p.add_argument("--workload", default="auto", choices=["auto", "cfg3", "cfg5"])
+    p.add_argument("--workload", default="auto", choices=["auto", "cfg3", "cfg4", "cfg5"],
+                   help="cfg3: 600x595x1536 on one GPU; cfg4: the same mesh split over the N GPUs (strong "
+                        "scaling); cfg5: 600x595x(1536 N), one slab per GPU (weak scaling, default for N>1)")
     p.add_argument("--nz", type=int, default=NZ, help="planes per GPU (debug / profiling)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--schedule", default="sr", choices=["sr", "classic"],
                    help="sr: single-reduction sweep (19 passes, DESIGN.md R19); classic: Alg. 1 as printed (29)")
+    p.add_argument("--operator", default="fields", choices=["fields", "poisson-const"],
+                   help="fields: the workload's per-point coefficient fields; poisson-const: the constant "
+                        "7-point Poisson operator (config 1's) at the same mesh via stencil_create_const "
+                        "(no coefficient streams in the SR sweep, NEXT-4)")
     p.add_argument("--tiling", default="", help="bx,by,zc,stages override (classic)")
     p.add_argument("--sr-tiling", default="", help="by,stages,cstages,zc override (sr)")
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
@@ -213,8 +219,10 @@ def run_sten(args):
     prec = sten.MIXED if args.precision == "mixed" else sten.FP32
     tdt = torch.float16 if prec == sten.MIXED else torch.float32
     from paper_2010_03660_b200 import dist as sdist
-    # weak scaling (config 5): every rank owns one args.nz-plane slab of the global mesh
-    z0, nzl = sdist.slab_of(rank, world, args.nz * world)
+    # weak scaling (config 5): every rank owns one args.nz-plane slab of the global mesh;
+    # strong scaling (config 4): the args.nz planes are split over the ranks
+    strong = workload == "cfg4"
+    z0, nzl = sdist.slab_of(rank, world, args.nz if strong else args.nz * world)
 
     comm = None
     if world > 1:
@@ -223,9 +231,12 @@ def run_sten(args):
     # problem: fields of this rank's slab generated on the device (inputs/gen_cuda.cu)
     kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
     kz = inputs.weak_kz_table(nzl * n) if kind == inputs.KIND_CD_WEAK else None
-    diag, offs = icuda.fields_device(kind, NX, NY, nzl, z0=z0, seed=1, delta=0.1, kz_table=kz)
-    st = sten.stencil_create(NX, NY, nzl, [diag] + offs, nslabs=1, comm=comm)
-    del diag, offs
+    if args.operator == "poisson-const":
+        st = sten.stencil_create_const(NX, NY, nzl, (6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0), nslabs=1, comm=comm)
+    else:
+        diag, offs = icuda.fields_device(kind, NX, NY, nzl, z0=z0, seed=1, delta=0.1, kz_table=kz)
+        st = sten.stencil_create(NX, NY, nzl, [diag] + offs, nslabs=1, comm=comm)
+        del diag, offs
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     if args.tiling:
@@ -311,22 +322,26 @@ def run_sten(args):
     pname = "mixed" if prec == sten.MIXED else "fp32"
     h1_avg_ms = h1_ms / max(h1_n, 1)
     # dominant kernel: the SR sweep (one per iteration) or the classic H1 stencil
-    h1_bytes = roofline.sweep_bytes(pname, npts_local) if sr else roofline.phase_bytes("H1", pname, npts_local)
+    const_op = args.operator == "poisson-const"
+    h1_bytes = (roofline.sweep_bytes(pname, npts_local, const_op) if sr
+                else roofline.phase_bytes("H1", pname, npts_local))
     achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
-    bpi = roofline.bytes_per_point_iter(pname, args.schedule)
+    bpi = roofline.bytes_per_point_iter(pname, args.schedule, const_op and sr)
     whole_gbs = npts_local * iters_done * bpi / (t_ms / 1e3) / 1e9
     tname = "half" if prec == sten.MIXED else "float"
     kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
     traffic, traffic_src = (None, None)
-    if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling:
+    if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
         traffic, traffic_src = measured_traffic("k_sr<__half" if sr else "k_stencil<__half, 1")
     line = {
         "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": value / PAPER_GPT_ITER_S,
         "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
         "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
-                   "precision": pname, "schedule": args.schedule, "maxit": maxit, "tol": tol,
+                   "precision": pname, "schedule": args.schedule, "operator": args.operator,
+                   "maxit": maxit, "tol": tol,
                    "iters_per_solve": iters_done / args.steps,
                    "parallelism": f"zslab{n}",
                    "l2": "no flush: 16.5 GB working set per GPU >> 126 MB L2",

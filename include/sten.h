@@ -124,6 +124,19 @@ void sten_comm_destroy(sten_comm *comm);
  * STEN_ENOMEM, STEN_ECUDA. */
 int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype,
                    int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out);
+/* The same for a CONSTANT-coefficient operator (e.g. the
+ * Poisson stencil of BASELINE config 1): coeffs[0..6] = a_P, A_xm, A_xp,
+ * A_ym, A_yp, A_zm, A_zp, the same at every point, with Dirichlet zero outside
+ * the global mesh (couplings leaving it dropped, a_P unchanged: R5).  The
+ * coefficient arrays are still built (for the classic schedule and
+ * stencil_apply), but the SR sweep then reads none of them: it takes the six
+ * scaled couplings (A_d / a_P in fp64, rounded once to fp32 / fp16) as
+ * scalars and moves 13 instead of 19 arrays per iteration.  Results equal those
+ * of stencil_create on the same constant fields (bitwise up to the sign of
+ * zero).  Errors: STEN_EINVAL (non-finite coefficient, a_P == 0, sizes),
+ * STEN_ENOMEM, STEN_ECUDA. */
+int stencil_create_const(int nx, int ny, int nz, const double coeffs[7], int nslabs, sten_comm *comm,
+                         void *cuda_stream, sten_stencil **out);
 void stencil_destroy(sten_stencil *st);
 
 /* y = A_hat x, A_hat the Jacobi-scaled operator (unit diagonal), one halo
@@ -215,8 +228,10 @@ int sten_sr_sweep(sten_stencil *st, int precision, double alpha, double omega, d
                   void *x, void *r, void *p, void *v, void *q, void *y, float *dots, void *cuda_stream);
 
 /* SR kernel geometry for tuning (0 = default): by rows per tile (8 or 16),
- * stages input TMA stages, cstages coefficient stages, zc planes per CTA. */
-int sten_set_sr_tiling(sten_stencil *st, int precision, int by, int stages, int cstages, int zc);
+ * stages input TMA stages, cstages coefficient stages, zc planes per CTA
+ * (uniform chunks), pack bytes per thread vector (16, or 8 = twice the
+ * threads per tile).  Errors: STEN_EINVAL for an unsupported combination. */
+int sten_set_sr_tiling(sten_stencil *st, int precision, int by, int stages, int cstages, int zc, int pack);
 
 /* Tile geometry override for tuning (0 = library default).  bx: points per
  * tile in x (multiple of 8), by: rows per tile, zc: planes per CTA,

@@ -64,6 +64,7 @@ def lib():
         L.sten_comm_destroy.argtypes = [P]
         L.stencil_create.argtypes = [I, I, I, P, I, I, P, P, ctypes.POINTER(P)]
         L.stencil_destroy.argtypes = [P]
+        L.stencil_create_const.argtypes = [I, I, I, P, I, P, P, ctypes.POINTER(P)]
         L.stencil_apply.argtypes = [P, I, P, P, P]
         L.bicgstab_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
         L.sten_scalar_history.argtypes = [P, I, P, P]
@@ -71,7 +72,7 @@ def lib():
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
         L.sten_set_schedule.argtypes = [P, I]
-        L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I]
+        L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I, I]
         L.sten_sr_sweep.argtypes = [P, I, D, D, D, P, P, P, P, P, P, P, P, P]
         L.bicgstab_refine.argtypes = [P, P, P, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(I), P,
                                       ctypes.POINTER(I), P]
@@ -210,6 +211,18 @@ def stencil_create(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Com
     return Stencil(h, nx, ny, nz, comm)
 
 
+def stencil_create_const(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
+                         stream=None) -> Stencil:
+    """Constant operator: coeffs = (a_P, A_xm, A_xp, A_ym, A_yp, A_zm, A_zp) as 7 floats."""
+    if len(coeffs) != 7:
+        raise StenError("coeffs must have 7 entries (diag, xm, xp, ym, yp, zm, zp)")
+    arr = np.ascontiguousarray(coeffs, dtype=np.float64)
+    h = ctypes.c_void_p()
+    _check(lib().stencil_create_const(nx, ny, nz, arr.ctypes.data_as(ctypes.c_void_p), nslabs,
+                                      comm.handle if comm else None, _stream(stream), ctypes.byref(h)))
+    return Stencil(h, nx, ny, nz, comm)
+
+
 def stencil_destroy(st: Stencil):
     st.close()
 
@@ -264,8 +277,9 @@ def set_schedule(st: Stencil, schedule: int):
     _check(lib().sten_set_schedule(st.handle, int(schedule)))
 
 
-def set_sr_tiling(st: Stencil, precision: int, by: int = 0, stages: int = 0, cstages: int = 0, zc: int = 0):
-    _check(lib().sten_set_sr_tiling(st.handle, precision, by, stages, cstages, zc))
+def set_sr_tiling(st: Stencil, precision: int, by: int = 0, stages: int = 0, cstages: int = 0, zc: int = 0,
+                  pack: int = 0):
+    _check(lib().sten_set_sr_tiling(st.handle, precision, by, stages, cstages, zc, pack))
 
 
 def sr_sweep(st: Stencil, precision: int, scalars, rh, x, r, p, v, q, y, stream=None):

@@ -166,6 +166,7 @@ struct Slab {
   float *c32b[6] = {};            // allocations: nz + 2 planes, halo planes 0 and nz+1
   __half *c16b[6] = {};
   double *aP = nullptr;
+  int has_below = 0, has_above = 0;  // a z-neighbour slab (this rank or the next) exists
   PrecBufs pb[2];
   SrBufs sr[2];
 };
@@ -179,6 +180,7 @@ struct GraphKey {
 struct SrTiling {
   int by = 0, stages = 0, cstages = 0, zc = 0;
   int zc_tail = 0, tail = 0;  // the last `tail` planes in chunks of zc_tail (0: none)
+  int pack = 16;              // bytes per thread vector (16, or 8: twice the threads per tile)
 };
 struct GraphRec {
   cudaGraphExec_t exec = nullptr;
@@ -218,6 +220,8 @@ struct sten_stencil {
   size_t stage_bytes = 0;
   unsigned *ir_amax = nullptr;  // refinement: max|r| (float bits), sigma
   float *ir_sigma = nullptr;
+  bool cc = false;              // constant-coefficient operator (stencil_create_const)
+  double cscaled[6] = {};       // its couplings A_d / a_P (fp64)
 };
 
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
@@ -554,8 +558,10 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
 // (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
 static void default_sr_tiling(sten_stencil *st, int prec) {
   SrTiling &t = st->srt[prec];
-  int by = 16, stg = 3, cst = 2, zc = 320, zct = 64, tail = 256;
-  if (const char *e = getenv("STEN_SR_TILING")) sscanf(e, "%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail);
+  int by = 16, stg = 3, cst = 2, zc = 320, zct = 64, tail = 256, pack = 16;
+  if (const char *e = getenv("STEN_SR_TILING"))
+    sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail, &pack);
+  t.pack = pack;
   t.by = by;
   t.stages = stg;
   t.cstages = cst;
@@ -587,11 +593,12 @@ static int sr_grid(const sten_stencil *st, int prec, int nzs) {
 static int ensure_sr(sten_stencil *st, int prec) {
   if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
   const SrTiling &t = st->srt[prec];
-  if (!sr_config_ok(t.by, t.stages, t.cstages) || t.zc <= 0)
-    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d", t.by, t.stages, t.cstages, t.zc);
+  if (!sr_config_ok(t.by, t.stages, t.cstages, t.pack) || t.zc <= 0)
+    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d pack=%d", t.by, t.stages,
+                   t.cstages, t.zc, t.pack);
   const int e = esize(prec);
   const size_t vb = (size_t)st->plane * e;
-  const int H = prec == STEN_FP32 ? 4 : 8, bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  const int H = 16 / e, bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();  // 16-B x halo pad
   g_plane_stride = st->plane;
   for (Slab &sl : st->slabs) {
     SrBufs &b = sl.sr[prec];
@@ -660,8 +667,17 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     return set_err(STEN_ECUDA, "internal: SR grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;
-  if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, s));
-  else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, s));
+  if (st->cc) {  // the same roundings as k_create_coeffs: fp64 quotient, RN to fp32 / fp16
+    for (int d = 0; d < 6; ++d) {
+      a.cf32[d] = (float)st->cscaled[d];
+      __half_raw hr = __half(__double2half(st->cscaled[d]));
+      a.cf16[d] = hr.x;
+    }
+    a.has_below = sl.has_below;
+    a.has_above = sl.has_above;
+  }
+  if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
+  else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
   st->launches++;
   return STEN_OK;
 }
@@ -937,16 +953,28 @@ static int is_device_ptr(const void *p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype, int nslabs,
-                   sten_comm *comm, void *cuda_stream, sten_stencil **out) {
+}  // extern "C"
+
+// cconst (host, 7 doubles: a_P, A_xm .. A_zp) selects a constant operator;
+// else coeffs[] are the per-point fields
+static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype, const double *cconst,
+                       int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out) {
   if (!out) return set_err(STEN_EINVAL, "out is NULL");
   if (nx <= 0 || ny <= 0 || nz <= 0) return set_err(STEN_EINVAL, "mesh %d x %d x %d must be positive", nx, ny, nz);
   if (nslabs < 1 || nz % nslabs != 0) return set_err(STEN_EINVAL, "nz=%d not divisible into nslabs=%d", nz, nslabs);
-  if (!coeffs) return set_err(STEN_EINVAL, "coeffs is NULL");
-  for (int d = 1; d < 7; ++d)
-    if (!coeffs[d]) return set_err(STEN_EINVAL, "coeffs[%d] is NULL", d);
-  if (coeff_dtype != STEN_DT_F64 && coeff_dtype != STEN_DT_F32)
-    return set_err(STEN_EINVAL, "coeff_dtype %d unsupported", coeff_dtype);
+  if (cconst) {
+    for (int d = 0; d < 7; ++d)
+      if (!std::isfinite(cconst[d])) return set_err(STEN_EINVAL, "constant coefficient %d is not finite", d);
+    if (cconst[0] == 0.0) return set_err(STEN_EINVAL, "constant diagonal is zero");
+    coeffs = nullptr;
+    coeff_dtype = STEN_DT_F64;
+  } else {
+    if (!coeffs) return set_err(STEN_EINVAL, "coeffs is NULL");
+    for (int d = 1; d < 7; ++d)
+      if (!coeffs[d]) return set_err(STEN_EINVAL, "coeffs[%d] is NULL", d);
+    if (coeff_dtype != STEN_DT_F64 && coeff_dtype != STEN_DT_F32)
+      return set_err(STEN_EINVAL, "coeff_dtype %d unsupported", coeff_dtype);
+  }
   if (nx > (1 << 20) || ny > (1 << 20)) return set_err(STEN_EINVAL, "nx, ny too large");
   cudaStream_t s = (cudaStream_t)cuda_stream;
   sten_stencil *st = new sten_stencil;
@@ -968,7 +996,11 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   }
   st->nslabs = nslabs;
   st->comm = comm;
-  st->has_diag = coeffs[0] != nullptr;
+  st->has_diag = cconst ? true : coeffs[0] != nullptr;
+  if (cconst) {
+    st->cc = true;
+    for (int d = 0; d < 6; ++d) st->cscaled[d] = cconst[1 + d] / cconst[0];  // fp64, as k_create_coeffs
+  }
   st->sm = device_sm_count();
   if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
   if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
@@ -980,9 +1012,16 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
   const int ein = coeff_dtype == STEN_DT_F64 ? 8 : 4;
   const size_t nin = (size_t)nx * ny * nz;
   // stage host inputs on the device
-  std::vector<void *> staged(7, nullptr);
-  const void *dev_in[7];
-  for (int d = 0; d < 7; ++d) {
+  std::vector<void *> staged(8, nullptr);
+  const void *dev_in[7] = {};
+  double *dconst = nullptr;
+  if (cconst) {
+    if (cudaMalloc(&staged[7], 7 * sizeof(double)) != cudaSuccess)
+      return fail(set_err(STEN_ENOMEM, "constant staging failed"));
+    dconst = (double *)staged[7];
+    cudaMemcpyAsync(dconst, cconst, 7 * sizeof(double), cudaMemcpyHostToDevice, s);
+  }
+  for (int d = 0; d < 7 && coeffs; ++d) {
     dev_in[d] = coeffs[d];
     if (coeffs[d] && !is_device_ptr(coeffs[d])) {
       if (cudaMalloc(&staged[d], nin * ein) != cudaSuccess) {
@@ -1017,12 +1056,14 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
       rc = set_err(STEN_ENOMEM, "diagonal allocation failed");
     if (rc != STEN_OK) break;
     const size_t soff = (size_t)sl.z_first * nx * ny * ein;
-    const void *off[6];
-    for (int d = 0; d < 6; ++d) off[d] = (const char *)dev_in[d + 1] + soff;
+    const void *off[6] = {};
+    for (int d = 0; d < 6 && !cconst; ++d) off[d] = (const char *)dev_in[d + 1] + soff;
     const void *dg = dev_in[0] ? (const char *)dev_in[0] + soff : nullptr;
     Geom g{nx, ny, nzs, st->pitch, st->plane};
     const int below = k > 0 || me > 0, above = k + 1 < nslabs || me + 1 < R;
-    int e = create_coeffs_launch(coeff_dtype, dg, off, g, below, above, sl.c32, sl.c16, sl.aP, s);
+    sl.has_below = below;
+    sl.has_above = above;
+    int e = create_coeffs_launch(coeff_dtype, dg, off, g, below, above, sl.c32, sl.c16, sl.aP, dconst, s);
     if (e) rc = set_err(STEN_ECUDA, "coefficient kernel: %s", cudaGetErrorString((cudaError_t)e));
   }
   if (rc == STEN_OK) rc = fill_coef_halos(st, s);
@@ -1048,6 +1089,19 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
     return fail(set_err(STEN_ECUDA, "stream/event creation failed"));
   *out = st;
   return STEN_OK;
+}
+
+extern "C" {
+
+int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype, int nslabs,
+                   sten_comm *comm, void *cuda_stream, sten_stencil **out) {
+  return create_impl(nx, ny, nz, coeffs, coeff_dtype, nullptr, nslabs, comm, cuda_stream, out);
+}
+
+int stencil_create_const(int nx, int ny, int nz, const double coeffs[7], int nslabs, sten_comm *comm,
+                         void *cuda_stream, sten_stencil **out) {
+  if (!coeffs) return set_err(STEN_EINVAL, "coeffs is NULL");
+  return create_impl(nx, ny, nz, nullptr, STEN_DT_F64, coeffs, nslabs, comm, cuda_stream, out);
 }
 
 void stencil_destroy(sten_stencil *st) {
@@ -1471,21 +1525,22 @@ int sten_set_schedule(sten_stencil *st, int schedule) {
   return STEN_OK;
 }
 
-int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstages, int zc) {
+int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstages, int zc, int pack) {
   if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
   if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
   SrTiling t = st->srt[prec];
   if (by) t.by = by;
   if (stages) t.stages = stages;
   if (cstages) t.cstages = cstages;
+  if (pack) t.pack = pack;
   if (zc) {  // an explicit chunk length: uniform chunks
     t.zc = zc;
     t.zc_tail = zc;
     t.tail = 0;
   }
-  if (!sr_config_ok(t.by, t.stages, t.cstages) || t.zc <= 0)
-    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d", t.by, t.stages, t.cstages,
-                   t.zc);
+  if (!sr_config_ok(t.by, t.stages, t.cstages, t.pack) || t.zc <= 0)
+    return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d pack=%d", t.by, t.stages,
+                   t.cstages, t.zc, t.pack);
   st->srt[prec] = t;
   for (Slab &sl : st->slabs) sl.sr[prec].maps_ok = false;
   drop_graphs(st);

@@ -214,7 +214,7 @@ __global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, con
                                 const TIN *o3, const TIN *o4, const TIN *o5, Geom g, int has_below,
                                 int has_above, float *c32_0, float *c32_1, float *c32_2, float *c32_3,
                                 float *c32_4, float *c32_5, __half *c16_0, __half *c16_1, __half *c16_2,
-                                __half *c16_3, __half *c16_4, __half *c16_5, double *aP) {
+                                __half *c16_3, __half *c16_4, __half *c16_5, double *aP, const double *cconst) {
   const TIN *off[6] = {o0, o1, o2, o3, o4, o5};
   float *c32[6] = {c32_0, c32_1, c32_2, c32_3, c32_4, c32_5};
   __half *c16[6] = {c16_0, c16_1, c16_2, c16_3, c16_4, c16_5};
@@ -235,10 +235,13 @@ __global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, con
     const long long P = x + (long long)g.nx * (y + (long long)g.ny * z);
     const bool inside[6] = {x > 0, x + 1 < g.nx, y > 0, y + 1 < g.ny, z > 0 || has_below != 0,
                             z + 1 < g.nz || has_above != 0};
-    const double dP = diag ? (double)diag[P] : 1.0;
+    // cconst: a constant operator (diag, xm..zp), the same scaling per point
+    const bool hasd = cconst ? cconst[0] != 0.0 : diag != nullptr;
+    const double dP = cconst ? (hasd ? cconst[0] : 1.0) : (diag ? (double)diag[P] : 1.0);
     for (int d = 0; d < 6; ++d) {
       double c = 0.0;  // R5: couplings leaving the mesh are dropped
-      if (inside[d]) c = diag ? __ddiv_rn((double)off[d][P], dP) : (double)off[d][P];
+      const double od = cconst ? cconst[1 + d] : (double)off[d][P];
+      if (inside[d]) c = hasd ? __ddiv_rn(od, dP) : od;
       c32[d][q] = __double2float_rn(c);
       c16[d][q] = __double2half(c);
     }
@@ -248,7 +251,7 @@ __global__ void k_create_coeffs(const TIN *__restrict__ diag, const TIN *o0, con
 
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g, int has_below,
                          int has_above, float *const c32[6], __half *const c16[6], double *aP,
-                         cudaStream_t s) {
+                         const double *cconst, cudaStream_t s) {
   const long long total = g.plane * g.nz;
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 32) grid = 148 * 32;
@@ -257,12 +260,14 @@ int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6
     const double *const *o = reinterpret_cast<const double *const *>(off);
     k_create_coeffs<double><<<grid, 256, 0, s>>>((const double *)diag, o[0], o[1], o[2], o[3], o[4], o[5], g,
                                                  has_below, has_above, c32[0], c32[1], c32[2], c32[3], c32[4],
-                                                 c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP);
+                                                 c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP,
+                                                 cconst);
   } else {
     const float *const *o = reinterpret_cast<const float *const *>(off);
     k_create_coeffs<float><<<grid, 256, 0, s>>>((const float *)diag, o[0], o[1], o[2], o[3], o[4], o[5], g,
                                                 has_below, has_above, c32[0], c32[1], c32[2], c32[3], c32[4],
-                                                c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP);
+                                                c32[5], c16[0], c16[1], c16[2], c16[3], c16[4], c16[5], aP,
+                                                cconst);
   }
   return (int)cudaGetLastError();
 }

@@ -45,6 +45,131 @@ constexpr int a128(int b) { return (b + 127) & ~127; }
 
 template <int V> struct IC { static constexpr int value = V; };
 
+// Per-thread vectors of the SR sweep: NB = 16 (8 fp16 / 4 fp32 lanes) or 8
+// bytes (4 / 2 lanes).  The 8-B form gives a tile twice the threads (16 warps
+// per SM for a 16-row tile) for the same shared-memory pipeline.
+template <typename T, int NB> struct SPack;
+template <int NB> struct SPack<__half, NB> {
+  static constexpr int NW = NB / 4;  // 32-bit words (half2)
+  static constexpr int VEC = 2 * NW;
+  using S = __half2;
+  uint32_t w[NW];
+  static __device__ __forceinline__ __half2 h2(uint32_t u) { return *reinterpret_cast<const __half2 *>(&u); }
+  static __device__ __forceinline__ uint32_t u32(__half2 h) { return *reinterpret_cast<const uint32_t *>(&h); }
+  static __device__ __forceinline__ SPack ld(const __half *p) {
+    SPack o;
+    if (NB == 16) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(p);
+      o.w[0] = q.x; o.w[1] = q.y; o.w[NW > 2 ? 2 : 0] = q.z; o.w[NW > 3 ? 3 : 1] = q.w;
+    } else {
+      const uint2 q = *reinterpret_cast<const uint2 *>(p);
+      o.w[0] = q.x; o.w[1] = q.y;
+    }
+    return o;
+  }
+  static __device__ __forceinline__ SPack ldg(const __half *p) {
+    SPack o;
+    if (NB == 16) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(p));
+      o.w[0] = q.x; o.w[1] = q.y; o.w[NW > 2 ? 2 : 0] = q.z; o.w[NW > 3 ? 3 : 1] = q.w;
+    } else {
+      const uint2 q = __ldcs(reinterpret_cast<const uint2 *>(p));
+      o.w[0] = q.x; o.w[1] = q.y;
+    }
+    return o;
+  }
+  __device__ __forceinline__ void st(__half *p) const {
+    if (NB == 16) *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[NW > 2 ? 2 : 0], w[NW > 3 ? 3 : 1]);
+    else *reinterpret_cast<uint2 *>(p) = make_uint2(w[0], w[1]);
+  }
+  static __device__ __forceinline__ SPack zero() {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) o.w[i] = 0u;
+    return o;
+  }
+  static __device__ __forceinline__ SPack fma(const SPack &a, const SPack &b, const SPack &c) {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) o.w[i] = u32(__hfma2(h2(a.w[i]), h2(b.w[i]), h2(c.w[i])));
+    return o;
+  }
+  static __device__ __forceinline__ S scalar(float a) { return __float2half2_rn(a); }
+  static __device__ __forceinline__ S neg(S a) { return __hneg2(a); }
+  static __device__ __forceinline__ SPack fmas(S a, const SPack &b, const SPack &c) {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) o.w[i] = u32(__hfma2(a, h2(b.w[i]), h2(c.w[i])));
+    return o;
+  }
+  // acc += a_i b_i in lane order: fma.rn.f32.f16 (exact fp16 product, fp32 add)
+  __device__ __forceinline__ float mdot(const SPack &b, float acc) const {
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+      asm("{\n .reg .b16 al, ah, bl, bh;\n mov.b32 {al, ah}, %1;\n mov.b32 {bl, bh}, %2;\n"
+          " fma.rn.f32.f16 %0, al, bl, %0;\n fma.rn.f32.f16 %0, ah, bh, %0;\n}"
+          : "+f"(acc)
+          : "r"(w[i]), "r"(b.w[i]));
+    return acc;
+  }
+};
+template <int NB> struct SPack<float, NB> {
+  static constexpr int VEC = NB / 4;
+  using S = float;
+  float v[VEC];
+  static __device__ __forceinline__ SPack ld(const float *p) {
+    SPack o;
+    if (NB == 16) {
+      const float4 q = *reinterpret_cast<const float4 *>(p);
+      o.v[0] = q.x; o.v[1] = q.y; o.v[VEC > 2 ? 2 : 0] = q.z; o.v[VEC > 3 ? 3 : 1] = q.w;
+    } else {
+      const float2 q = *reinterpret_cast<const float2 *>(p);
+      o.v[0] = q.x; o.v[1] = q.y;
+    }
+    return o;
+  }
+  static __device__ __forceinline__ SPack ldg(const float *p) {
+    SPack o;
+    if (NB == 16) {
+      const float4 q = __ldcs(reinterpret_cast<const float4 *>(p));
+      o.v[0] = q.x; o.v[1] = q.y; o.v[VEC > 2 ? 2 : 0] = q.z; o.v[VEC > 3 ? 3 : 1] = q.w;
+    } else {
+      const float2 q = __ldcs(reinterpret_cast<const float2 *>(p));
+      o.v[0] = q.x; o.v[1] = q.y;
+    }
+    return o;
+  }
+  __device__ __forceinline__ void st(float *p) const {
+    if (NB == 16) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[VEC > 2 ? 2 : 0], v[VEC > 3 ? 3 : 1]);
+    else *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+  }
+  static __device__ __forceinline__ SPack zero() {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) o.v[i] = 0.0f;
+    return o;
+  }
+  static __device__ __forceinline__ SPack fma(const SPack &a, const SPack &b, const SPack &c) {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) o.v[i] = __fmaf_rn(a.v[i], b.v[i], c.v[i]);
+    return o;
+  }
+  static __device__ __forceinline__ S scalar(float a) { return a; }
+  static __device__ __forceinline__ S neg(S a) { return -a; }
+  static __device__ __forceinline__ SPack fmas(S a, const SPack &b, const SPack &c) {
+    SPack o;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) o.v[i] = __fmaf_rn(a, b.v[i], c.v[i]);
+    return o;
+  }
+  __device__ __forceinline__ float mdot(const SPack &b, float acc) const {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc = __fmaf_rn(v[i], b.v[i], acc);
+    return acc;
+  }
+};
+
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int x, int y, int z) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -52,11 +177,12 @@ __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int x, i
                : "memory");
 }
 
-template <typename T, int BY>
+template <typename T, int BY, int NB>
 struct SrGeo {
-  static constexpr int VEC = Pack<T>::VEC;
+  static constexpr int VEC = SPack<T, NB>::VEC;
   static constexpr int BX = tile_bx<T>();
-  static constexpr int H = VEC;                  // x halo pad: one vector (keeps 16-B alignment)
+  static constexpr int H = 16 / (int)sizeof(T);  // x halo pad of the boxes: 16 B (TMA rows stay 16-B multiples)
+  static constexpr int VOFF = H - VEC;           // element offset of halo vector column 0 (x0 - VEC)
   static constexpr int VPR = BX / VEC;           // own vectors per tile row
   static constexpr int VW = VPR + 2;             // vectors per box row (incl. the x halo)
   static constexpr int HW = BX + 2 * H;          // box row (elements)
@@ -71,33 +197,86 @@ struct SrGeo {
   static_assert(NHF <= NT && NHV <= NT, "halo work must fit one extra item per thread");
 };
 
-template <typename T, int BY, int S, int SC>
+template <typename T, int BY, int S, int SC, bool CC, int NB>
 constexpr size_t sr_smem_c() {
-  using G = SrGeo<T, BY>;
-  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (size_t)SC * 6 * G::CE + (3 + G::NR) * (size_t)G::IE +
-                                    2 * (size_t)G::CE);
+  using G = SrGeo<T, BY, NB>;
+  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (CC ? 0 : (size_t)SC * 6 * G::CE) +
+                                    (3 + G::NR) * (size_t)G::IE + 2 * (size_t)G::CE);
 }
 
-template <typename T> struct SrShift;
-template <> struct SrShift<float> {
-  using E = float;
-  static __device__ __forceinline__ Pack<float> left(const Pack<float> &c, float l) {
-    return Pack<float>{{l, c.v[0], c.v[1], c.v[2]}};
+// constant coefficients as packs, and lane masks (keep lanes [lo, hi))
+template <typename T, int NB> struct SrConst;
+template <int NB> struct SrConst<float, NB> {
+  using P = SPack<float, NB>;
+  static __device__ __forceinline__ P splat(const SrArgs &a, int d) {
+    P o;
+#pragma unroll
+    for (int i = 0; i < P::VEC; ++i) o.v[i] = a.cf32[d];
+    return o;
   }
-  static __device__ __forceinline__ Pack<float> right(const Pack<float> &c, float r) {
-    return Pack<float>{{c.v[1], c.v[2], c.v[3], r}};
+  static __device__ __forceinline__ P keep(const P &v, int lo, int hi) {
+    P o;
+#pragma unroll
+    for (int i = 0; i < P::VEC; ++i) o.v[i] = (i >= lo && i < hi) ? v.v[i] : 0.0f;
+    return o;
+  }
+};
+template <int NB> struct SrConst<__half, NB> {
+  using P = SPack<__half, NB>;
+  static __device__ __forceinline__ P splat(const SrArgs &a, int d) {
+    const uint32_t h = a.cf16[d];
+    P o;
+#pragma unroll
+    for (int i = 0; i < P::NW; ++i) o.w[i] = h | (h << 16);
+    return o;
+  }
+  static __device__ __forceinline__ P keep(const P &v, int lo, int hi) {
+    P o;
+#pragma unroll
+    for (int i = 0; i < P::NW; ++i) {
+      const uint32_t m = ((2 * i >= lo && 2 * i < hi) ? 0x0000FFFFu : 0u) | ((2 * i + 1 >= lo && 2 * i + 1 < hi) ? 0xFFFF0000u : 0u);
+      o.w[i] = v.w[i] & m;
+    }
+    return o;
+  }
+};
+
+template <typename T, int NB> struct SrShift;
+template <int NB> struct SrShift<float, NB> {
+  using E = float;
+  using P = SPack<float, NB>;
+  static __device__ __forceinline__ P left(const P &c, float l) {
+    P o;
+    o.v[0] = l;
+#pragma unroll
+    for (int i = 1; i < P::VEC; ++i) o.v[i] = c.v[i - 1];
+    return o;
+  }
+  static __device__ __forceinline__ P right(const P &c, float r) {
+    P o;
+#pragma unroll
+    for (int i = 0; i + 1 < P::VEC; ++i) o.v[i] = c.v[i + 1];
+    o.v[P::VEC - 1] = r;
+    return o;
   }
   static __device__ __forceinline__ float ld1(const float *p) { return *p; }
 };
-template <> struct SrShift<__half> {
+template <int NB> struct SrShift<__half, NB> {
   using E = uint32_t;
-  static __device__ __forceinline__ Pack<__half> left(const Pack<__half> &c, uint32_t l) {
-    return Pack<__half>{{__byte_perm(l, c.w[0], 0x5410), __byte_perm(c.w[0], c.w[1], 0x5432),
-                         __byte_perm(c.w[1], c.w[2], 0x5432), __byte_perm(c.w[2], c.w[3], 0x5432)}};
+  using P = SPack<__half, NB>;
+  static __device__ __forceinline__ P left(const P &c, uint32_t l) {
+    P o;
+    o.w[0] = __byte_perm(l, c.w[0], 0x5410);
+#pragma unroll
+    for (int i = 1; i < P::NW; ++i) o.w[i] = __byte_perm(c.w[i - 1], c.w[i], 0x5432);
+    return o;
   }
-  static __device__ __forceinline__ Pack<__half> right(const Pack<__half> &c, uint32_t r) {
-    return Pack<__half>{{__byte_perm(c.w[0], c.w[1], 0x5432), __byte_perm(c.w[1], c.w[2], 0x5432),
-                         __byte_perm(c.w[2], c.w[3], 0x5432), __byte_perm(c.w[3], r, 0x5432)}};
+  static __device__ __forceinline__ P right(const P &c, uint32_t r) {
+    P o;
+#pragma unroll
+    for (int i = 0; i + 1 < P::NW; ++i) o.w[i] = __byte_perm(c.w[i], c.w[i + 1], 0x5432);
+    o.w[P::NW - 1] = __byte_perm(c.w[P::NW - 1], r, 0x5432);
+    return o;
   }
   static __device__ __forceinline__ uint32_t ld1(const __half *p) {
     return (uint32_t)*reinterpret_cast<const unsigned short *>(p);
@@ -105,11 +284,9 @@ template <> struct SrShift<__half> {
 };
 
 // u = m; u = fma(c_xm, x-1, u); ... xp, ym, yp, zm, zp (R10, oracle o16/o32 mirrors)
-template <typename T>
-__device__ __forceinline__ Pack<T> spmv(const Pack<T> (&c)[6], const Pack<T> &m, const Pack<T> &xl,
-                                        const Pack<T> &xr, const Pack<T> &ym, const Pack<T> &yp,
-                                        const Pack<T> &zm, const Pack<T> &zp) {
-  using P = Pack<T>;
+template <typename P>
+__device__ __forceinline__ P spmv(const P (&c)[6], const P &m, const P &xl, const P &xr, const P &ym, const P &yp,
+                                  const P &zm, const P &zp) {
   P acc = m;
   acc = P::fma(c[0], xl, acc);
   acc = P::fma(c[1], xr, acc);
@@ -122,21 +299,25 @@ __device__ __forceinline__ Pack<T> spmv(const Pack<T> (&c)[6], const Pack<T> &m,
 
 }  // namespace
 
-template <typename T, int BY, int S, int SC>
-__global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constant__ SrArgs a) {
-  using P = Pack<T>;
-  using G = SrGeo<T, BY>;
-  using SH = SrShift<T>;
+template <typename T, int BY, int S, int SC, bool CC, int NB>
+__global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_constant__ SrArgs a) {
+  using P = SPack<T, NB>;
+  using G = SrGeo<T, BY, NB>;
+  using SH = SrShift<T, NB>;
+  using SCn = SrConst<T, NB>;
   constexpr int VEC = G::VEC, H = G::H, HW = G::HW, VW = G::VW, VPR = G::VPR, IE = G::IE, CE = G::CE;
   static_assert(6 % S == 0 && 6 % SC == 0, "stage counts must divide the unroll period");
 
   if (sr_idle(a.red.st)) return;
+#ifdef STEN_DBG_STOP
+  if (STEN_DBG_STOP == 0) return;
+#endif
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);           // [S] inputs, [SC] coefficients
   T *const IN = reinterpret_cast<T *>(smem + 128);               // [S][5][IE]
   T *const CF = IN + S * 5 * IE;                                 // [SC][6][CE]
-  T *const PR = CF + SC * 6 * CE;                                // p' ring [3][IE]
+  T *const PR = CF + (CC ? 0 : SC * 6 * CE);                     // p' ring [3][IE]
   T *const RR = PR + 3 * IE;                                     // r' ring [6][IE]
   T *const VR = RR + G::NR * IE;                                 // v' ring [2][CE]
   __shared__ float scratch[32 * kMaxDots];
@@ -164,7 +345,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     if (tid < 2 * VW) { r = tid / VW; c = tid % VW; }
     else if (tid < 4 * VW) { r = BY + 2 + (tid - 2 * VW) / VW; c = (tid - 2 * VW) % VW; }
     else { const int m = tid - 4 * VW; r = 2 + m / 2; c = (m & 1) ? VW - 1 : 0; }
-    hf = r * HW + c * VEC;
+    hf = r * HW + G::VOFF + c * VEC;
   }
   // one halo item of the v' region (coef-box rows 0..RC-1, cols 0..VW-1 minus the own tile)
   int hv = -1, hvc = 0;
@@ -173,7 +354,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     if (tid < VW) { r = 0; c = tid; }
     else if (tid < 2 * VW) { r = G::RC - 1; c = tid - VW; }
     else { const int m = tid - 2 * VW; r = 1 + m / 2; c = (m & 1) ? VW - 1 : 0; }
-    hv = r * HW + c * VEC;
+    hv = r * HW + G::VOFF + c * VEC;
     hvc = c;
   }
   const int gx = x0 + cx * VEC, gy = y0 + ry;
@@ -188,6 +369,9 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   }
   __syncthreads();
 
+#ifdef STEN_DBG_STOP
+  if (STEN_DBG_STOP == 5) return;
+#endif
   auto issue_in = [&](int qi) {  // plane z0-2+qi of r, p, v, q, y (vectors: 2 halo planes)
     const int slot = qi % S, m = z0 - 2 + qi;
     mbar_expect_tx(&mbar[slot], 5u * HW * G::RI * (uint32_t)sizeof(T));
@@ -202,7 +386,26 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
   };
   if (tid == 0) {
     for (int q = 0; q < min(S, npi); ++q) issue_in(q);
-    for (int q = 0; q < min(SC, npc); ++q) issue_c(q);
+    if (!CC)
+      for (int q = 0; q < min(SC, npc); ++q) issue_c(q);
+  }
+  // CC: the couplings as packs; v' is zero outside the global mesh (lanes
+  // [vlo, vhi) of an item's vector are in x, vrow says the row is in y)
+  P cst[6];
+  int olo = 0, ohi = VEC, hlo = 0, hhi = VEC;
+  bool orow = true, hrow = true;
+  if (CC) {
+#pragma unroll
+    for (int d = 0; d < 6; ++d) cst[d] = SCn::splat(a, d);
+    const int gxo = x0 + cx * VEC;
+    ohi = min(VEC, a.g.nx - gxo);
+    orow = (y0 + ry) < a.g.ny;
+    if (hv >= 0) {
+      const int gxh = x0 + (hvc - 1) * VEC, gyh = y0 - 1 + hv / HW;
+      hlo = max(0, -gxh);
+      hhi = min(VEC, a.g.nx - gxh);
+      hrow = gyh >= 0 && gyh < a.g.ny;
+    }
   }
 
   const typename P::S al_s = P::scalar(a.red.st->alpha), mal_s = P::neg(al_s);
@@ -288,18 +491,23 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     // ---------------- (B) ----------------
     if (j >= 2) {
       constexpr int CS = (J + 6 - 2) % SC;  // coefficient slot of plane k+1 (ordinal j-2)
-      mbar_wait(&mbar[S + CS], (uint32_t)(((j - 2) / SC) & 1));
+      if (!CC) mbar_wait(&mbar[S + CS], (uint32_t)(((j - 2) / SC) & 1));
       const T *cf = CF + CS * 6 * CE;
+      // CC: plane k+1 exists (a neighbour slab's plane at an interface)?
+      const bool zin = (k + 1 >= 0 || a.has_below) && (k + 1 < a.g.nz || a.has_above);
       const T *p0 = PR + ((J + 1) % 3) * IE;  // plane k
       const T *p1 = PR + ((J + 2) % 3) * IE;  // plane k+1
       const T *p2 = PR + (J % 3) * IE;        // plane k+2
       T *vr = VR + ((J + 1) & 1) * CE;
       P (&cn)[6] = cw[J & 1];
+      if (!CC) {
 #pragma unroll
-      for (int d = 0; d < 6; ++d) cn[d] = P::ld(cf + d * CE + ec);
+        for (int d = 0; d < 6; ++d) cn[d] = P::ld(cf + d * CE + ec);
+      }
       const P &c1 = pw[(J + 2) % 3];
       const P xl = SH::left(c1, SH::ld1(p1 + ei - 1)), xr = SH::right(c1, SH::ld1(p1 + ei + VEC));
-      const P vn = spmv<T>(cn, c1, xl, xr, P::ld(p1 + ei - HW), P::ld(p1 + ei + HW), pw[(J + 1) % 3], pw[J % 3]);
+      P vn = spmv<P>(CC ? cst : cn, c1, xl, xr, P::ld(p1 + ei - HW), P::ld(p1 + ei + HW), pw[(J + 1) % 3], pw[J % 3]);
+      if (CC) vn = (orow && zin) ? SCn::keep(vn, olo, ohi) : P::zero();
       vn.st(vr + ec);
       vw[J % 3] = vn;
       if (inside && k + 1 >= z0 && k + 1 < z1) vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
@@ -307,28 +515,29 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
         const int hp = hv + HW;  // same point in the input-box layout
         P c[6];
 #pragma unroll
-        for (int d = 0; d < 6; ++d) c[d] = P::ld(cf + d * CE + hv);
+        for (int d = 0; d < 6; ++d) c[d] = CC ? cst[d] : P::ld(cf + d * CE + hv);
         const P m1 = P::ld(p1 + hp);
         const typename SH::E zl = hvc == 0 ? (typename SH::E)0 : SH::ld1(p1 + hp - 1);
         const typename SH::E zr = hvc == VW - 1 ? (typename SH::E)0 : SH::ld1(p1 + hp + VEC);
-        spmv<T>(c, m1, SH::left(m1, zl), SH::right(m1, zr), P::ld(p1 + hp - HW), P::ld(p1 + hp + HW),
-                P::ld(p0 + hp), P::ld(p2 + hp))
-            .st(vr + hv);
+        P hvn = spmv<P>(c, m1, SH::left(m1, zl), SH::right(m1, zr), P::ld(p1 + hp - HW), P::ld(p1 + hp + HW),
+                        P::ld(p0 + hp), P::ld(p2 + hp));
+        if (CC) hvn = (hrow && zin) ? SCn::keep(hvn, hlo, hhi) : P::zero();
+        hvn.st(vr + hv);
       }
       __syncthreads();
-      if (tid == 0 && j - 2 + SC < npc) issue_c(j - 2 + SC);
+      if (!CC && tid == 0 && j - 2 + SC < npc) issue_c(j - 2 + SC);
     }
 
     // ---------------- (C) ----------------
     if (j >= 4) {
       const T *r1 = RR + ((J + 4) % 6) * IE;  // r' plane k
       const T *v1 = VR + (J & 1) * CE;        // v' plane k
-      const P (&cc)[6] = cw[(J + 1) & 1];     // coefficients of plane k (loaded at step j-1)
+      const P (&cc)[6] = CC ? cst : cw[(J + 1) & 1];  // coefficients of plane k (loaded at step j-1)
       const P &rm = rw[(J + 3) % 6], &rc = rw[(J + 4) % 6], &rp = rw[(J + 5) % 6];
       const P &vm = vw[(J + 1) % 3], &vc = vw[(J + 2) % 3], &vp = vw[J % 3];
-      const P qn = spmv<T>(cc, rc, SH::left(rc, SH::ld1(r1 + ei - 1)), SH::right(rc, SH::ld1(r1 + ei + VEC)),
+      const P qn = spmv<P>(cc, rc, SH::left(rc, SH::ld1(r1 + ei - 1)), SH::right(rc, SH::ld1(r1 + ei + VEC)),
                            P::ld(r1 + ei - HW), P::ld(r1 + ei + HW), rm, rp);
-      const P yn = spmv<T>(cc, vc, SH::left(vc, SH::ld1(v1 + ec - 1)), SH::right(vc, SH::ld1(v1 + ec + VEC)),
+      const P yn = spmv<P>(cc, vc, SH::left(vc, SH::ld1(v1 + ec - 1)), SH::right(vc, SH::ld1(v1 + ec + VEC)),
                            P::ld(v1 + ec - HW), P::ld(v1 + ec + HW), vm, vp);
       const P rh = rq[(J + 2) % 3];  // r_hat of plane k (loaded three steps ago)
       rq[(J + 2) % 3] = ld_rh(k + 3);
@@ -352,6 +561,24 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
     }
   };
 
+#ifdef STEN_DBG_STOP
+  if (STEN_DBG_STOP == 1) {
+    __syncthreads();
+    if (tid == 0) {  // drain the issued TMA loads before leaving
+      for (int q = 0; q < min(S, npi); ++q) mbar_wait(&mbar[q % S], 0);
+      if (!CC) for (int q = 0; q < min(SC, npc); ++q) mbar_wait(&mbar[S + q % SC], 0);
+    }
+    __syncthreads();
+    return;
+  }
+  if (STEN_DBG_STOP >= 2) {
+    step(IC<0>{}, 0);
+    if (STEN_DBG_STOP >= 3) step(IC<1>{}, 1);
+    if (STEN_DBG_STOP >= 4) { step(IC<2>{}, 2); step(IC<3>{}, 3); step(IC<4>{}, 4); step(IC<5>{}, 5); }
+    __syncthreads();
+    return;
+  }
+#endif
   for (int j = 0; j < npi; j += 6) {
     step(IC<0>{}, j);
     if (j + 1 < npi) step(IC<1>{}, j + 1);
@@ -365,57 +592,64 @@ __global__ void __launch_bounds__(SrGeo<T, BY>::NT, 1) k_sr(const __grid_constan
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int BY, int S, int SC>
+template <typename T, int BY, int S, int SC, bool CC, int NB>
 int launch_sr_one(const SrArgs &a, cudaStream_t s) {
-  constexpr size_t smem = sr_smem_c<T, BY, S, SC>();
+  constexpr size_t smem = sr_smem_c<T, BY, S, SC, CC, NB>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC, CC, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * (a.nbig + (a.g.nz - a.nbig * a.zc + a.zc_tail - 1) / a.zc_tail);
-  k_sr<T, BY, S, SC><<<grid, SrGeo<T, BY>::NT, smem, s>>>(a);
+  k_sr<T, BY, S, SC, CC, NB><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 }  // namespace
 
-#define STEN_SR_CONFIGS(X) X(16, 3, 2) X(16, 2, 2) X(16, 2, 3) X(8, 2, 2) X(8, 3, 2) X(8, 3, 3)
+// (rows per tile, input stages, coefficient stages, bytes per thread vector)
+#define STEN_SR_CONFIGS(X)                                                                                  \
+  X(16, 3, 2, 16) X(16, 2, 2, 16) X(16, 2, 3, 16) X(8, 2, 2, 16) X(8, 3, 2, 16) X(8, 3, 3, 16) X(16, 3, 2, 8) \
+  X(16, 2, 2, 8) X(8, 2, 2, 8) X(8, 3, 2, 8)
 
-bool sr_config_ok(int by, int stages, int cstages) {
-#define X(B, S_, C_) if (by == B && stages == S_ && cstages == C_) return true;
+bool sr_config_ok(int by, int stages, int cstages, int pack) {
+#define X(B, S_, C_, N_) if (by == B && stages == S_ && cstages == C_ && pack == N_) return true;
   STEN_SR_CONFIGS(X)
 #undef X
   return false;
 }
 
 template <typename T>
-int sr_launch(const SrArgs &a, int by, int stages, int cstages, cudaStream_t s) {
-#define X(B, S_, C_) if (by == B && stages == S_ && cstages == C_) return launch_sr_one<T, B, S_, C_>(a, s);
+int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, cudaStream_t s) {
+#define X(B, S_, C_, N_)                                                  \
+  if (by == B && stages == S_ && cstages == C_ && pack == N_)             \
+    return cc ? launch_sr_one<T, B, S_, C_, true, N_>(a, s) : launch_sr_one<T, B, S_, C_, false, N_>(a, s);
   STEN_SR_CONFIGS(X)
 #undef X
   return (int)cudaErrorInvalidValue;
 }
 
 template <typename T>
-size_t sr_smem_bytes(int by, int stages, int cstages) {
-#define X(B, S_, C_) if (by == B && stages == S_ && cstages == C_) return sr_smem_c<T, B, S_, C_>();
+size_t sr_smem_bytes(int by, int stages, int cstages, int pack) {
+#define X(B, S_, C_, N_) \
+  if (by == B && stages == S_ && cstages == C_ && pack == N_) return sr_smem_c<T, B, S_, C_, false, N_>();
   STEN_SR_CONFIGS(X)
 #undef X
   return 0;
 }
 
 template <typename T>
-int sr_threads(int by) {
-  return (tile_bx<T>() / Pack<T>::VEC) * by;
+int sr_threads(int by, int pack) {
+  return (tile_bx<T>() / (pack / (int)sizeof(T))) * by;
 }
 
-template int sr_launch<float>(const SrArgs &, int, int, int, cudaStream_t);
-template int sr_launch<__half>(const SrArgs &, int, int, int, cudaStream_t);
-template size_t sr_smem_bytes<float>(int, int, int);
-template size_t sr_smem_bytes<__half>(int, int, int);
-template int sr_threads<float>(int);
-template int sr_threads<__half>(int);
+template int sr_launch<float>(const SrArgs &, int, int, int, int, bool, cudaStream_t);
+template int sr_launch<__half>(const SrArgs &, int, int, int, int, bool, cudaStream_t);
+template size_t sr_smem_bytes<float>(int, int, int, int);
+template size_t sr_smem_bytes<__half>(int, int, int, int);
+template int sr_threads<float>(int, int);
+template int sr_threads<__half>(int, int);
 
 }  // namespace sten

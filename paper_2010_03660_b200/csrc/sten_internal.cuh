@@ -515,16 +515,22 @@ struct alignas(64) SrArgs {
   int zc, tiles_x, tiles_y;
   int nbig;               // chunks [0, nbig) have zc planes; the rest cover
   int zc_tail;            // [nbig*zc, nz) in zc_tail-plane chunks (fills the tail wave)
+  // constant-coefficient operator (stencil_create_const): the six scaled
+  // couplings as scalars, no coefficient streams; v' is masked to zero outside
+  // the global mesh (planes below/above exist only at slab interfaces)
+  float cf32[6];
+  unsigned short cf16[6];
+  int has_below, has_above;
   Reduce red;
 };
-bool sr_config_ok(int by, int stages, int cstages);
-template <typename T> int sr_launch(const SrArgs &a, int by, int stages, int cstages, cudaStream_t s);
-template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages);
-template <typename T> int sr_threads(int by);
+bool sr_config_ok(int by, int stages, int cstages, int pack);
+template <typename T> int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, cudaStream_t s);
+template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages, int pack);
+template <typename T> int sr_threads(int by, int pack);
 
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g,
                          int has_below, int has_above, float *const c32[6], __half *const c16[6],
-                         double *aP, cudaStream_t s);
+                         double *aP, const double *cconst, cudaStream_t s);
 int device_sm_count();
 
 }  // namespace sten

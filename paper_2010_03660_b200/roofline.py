@@ -28,16 +28,22 @@ ELEM_BYTES = {"fp32": 4, "mixed": 2}
 PASSES_SR = 19
 
 
-def passes_per_iter(schedule: str = "classic") -> int:
-    return PASSES_SR if schedule == "sr" else PASSES_PER_ITER
+# constant-coefficient operator (stencil_create_const): the SR sweep reads no coefficient arrays
+PASSES_SR_CONST = PASSES_SR - 6
 
 
-def bytes_per_point_iter(precision: str, schedule: str = "classic") -> int:
-    return passes_per_iter(schedule) * ELEM_BYTES[precision]
+def passes_per_iter(schedule: str = "classic", const_op: bool = False) -> int:
+    if schedule == "sr":
+        return PASSES_SR_CONST if const_op else PASSES_SR
+    return PASSES_PER_ITER
 
 
-def sweep_bytes(precision: str, npoints: int) -> int:
-    return PASSES_SR * ELEM_BYTES[precision] * npoints
+def bytes_per_point_iter(precision: str, schedule: str = "classic", const_op: bool = False) -> int:
+    return passes_per_iter(schedule, const_op) * ELEM_BYTES[precision]
+
+
+def sweep_bytes(precision: str, npoints: int, const_op: bool = False) -> int:
+    return (PASSES_SR_CONST if const_op else PASSES_SR) * ELEM_BYTES[precision] * npoints
 
 
 def phase_bytes(phase: str, precision: str, npoints: int) -> int:

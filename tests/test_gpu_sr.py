@@ -75,6 +75,7 @@ def test_sr_sweep_bitwise(sten, prec, mesh):
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
 @pytest.mark.parametrize("tiling", [(16, 3, 2, 64), (16, 2, 2, 5), (8, 2, 2, 3), (8, 3, 2, 1), (8, 3, 3, 7), (16, 2, 3, 9),
+                                    (16, 3, 2, 5, 8), (16, 2, 2, 1, 8), (8, 2, 2, 7, 8), (8, 3, 2, 64, 8),
                                     (16, 3, 2, 1)])
 def test_sr_sweep_geometries(sten, prec, tiling):
     got, dots, ref, _ = _sweep_case(sten, prec, (141, 37, 23), tiling=tiling, seed=4)
@@ -86,9 +87,10 @@ def test_sr_sweep_geometries(sten, prec, tiling):
 @pytest.mark.parametrize("nslabs", [2, 3])
 def test_sr_sweep_slab_decomposition(sten, prec, nslabs):
     # two-plane vector halos and one-plane coefficient halos across the slab seams
-    got, dots, ref, _ = _sweep_case(sten, prec, (45, 19, 12), nslabs=nslabs, tiling=(8, 2, 2, 3), seed=6)
-    for g, w in zip(got, ref[:6]):
-        assert np.array_equal(widen(g, prec), widen(w, prec))
+    for tiling in ((8, 2, 2, 3), (16, 3, 2, 5, 8)):
+        got, dots, ref, _ = _sweep_case(sten, prec, (45, 19, 12), nslabs=nslabs, tiling=tiling, seed=6)
+        for g, w in zip(got, ref[:6]):
+            assert np.array_equal(widen(g, prec), widen(w, prec))
 
 
 def _solve(sten, st, prec, b, tol, maxit, x0=None):
