@@ -591,6 +591,9 @@ static int sr_grid(const sten_stencil *st, int prec, int nzs) {
 }
 
 static int ensure_sr(sten_stencil *st, int prec) {
+  for (const Slab &sl : st->slabs)  // the two-plane halos come from the z-neighbour's own planes
+    if (decomposed(st) && sl.nz < kSrHalo)
+      return set_err(STEN_EINVAL, "the SR schedule needs >= %d planes per slab (slab of %d)", kSrHalo, sl.nz);
   if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
   const SrTiling &t = st->srt[prec];
   if (!sr_config_ok(t.by, t.stages, t.cstages, t.pack) || t.zc <= 0)

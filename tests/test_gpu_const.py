@@ -28,7 +28,7 @@ def fields_const(c, nx, ny, nz):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-@pytest.mark.parametrize("mesh", [(37, 29, 19), (130, 17, 9), (1, 1, 1), (8, 40, 5)])
+@pytest.mark.parametrize("mesh", [(37, 29, 18), (130, 17, 9), (1, 1, 6), (13, 40, 6)])
 @pytest.mark.parametrize("coef", [POISSON, SKEW])
 @pytest.mark.parametrize("nslabs", [1, 3])
 def test_const_sweep_equals_oracle(sten, prec, mesh, coef, nslabs):
@@ -47,10 +47,17 @@ def test_const_sweep_equals_oracle(sten, prec, mesh, coef, nslabs):
     v, q = ap(cq, p), ap(cq, r)
     y = ap(cq, v)
     ts = [to_gpu_vec(a, prec) for a in (rh, x, r, p, v, q, y)]
-    sten.sr_sweep(st, PREC[prec], (0.61, 0.93, -0.27), *ts)
+    dots = sten.sr_sweep(st, PREC[prec], (0.61, 0.93, -0.27), *ts)
     ref = (orc.sr_sweep32 if prec == "fp32" else orc.sr_sweep16)(cq, (0.61, 0.93, -0.27), rh, x, r, p, v, q, y)
     for g, w in zip(ts[1:], ref[:6]):
         assert np.array_equal(widen(from_gpu_vec(g, prec), prec), widen(w, prec))
+    # the twelve sums see only mesh points (ragged x and y tails included)
+    got = [widen(from_gpu_vec(t, prec), prec) for t in ts]
+    rhw, rw, vw, qw, yw = got[0], got[2], got[4], got[5], got[6]
+    pairs = [(rhw, vw), (rhw, rw), (rhw, qw), (rhw, yw), (qw, rw), (qw, vw), (yw, rw), (yw, vw), (qw, qw),
+             (qw, yw), (yw, yw), (rw, rw)]
+    for d, (a_, b_) in enumerate(pairs):
+        assert abs(float(dots[d]) - float(np.vdot(a_, b_))) <= 1e-5 * float(np.vdot(np.abs(a_), np.abs(b_))) + 1e-30
     st.close()
     del torch
 
@@ -77,6 +84,16 @@ def test_const_solve_equals_general_kernel(sten, prec):
     assert np.array_equal(out["const"][0], out["general"][0])
     assert np.array_equal(out["const"][1], out["general"][1])
     assert np.array_equal(out["const_classic"], out["general_classic"])
+
+
+def test_sr_needs_two_planes_per_slab(sten):
+    st = sten.stencil_create_const(5, 4, 3, POISSON, nslabs=3)
+    sten.set_schedule(st, sten.SCHED_SR)
+    torch = torch_cuda()
+    b = torch.zeros((3, 4, 5), dtype=torch.float32, device="cuda")
+    with pytest.raises(sten.StenError):
+        sten.bicgstab_solve(st, 0, b, None, 0.0, 2, torch.empty_like(b))
+    st.close()
 
 
 def test_const_invalid(sten):
