@@ -220,6 +220,7 @@ struct sten_stencil {
   size_t stage_bytes = 0;
   unsigned *ir_amax = nullptr;  // refinement: max|r| (float bits), sigma
   float *ir_sigma = nullptr;
+  int sr_l2pf = 0;              // SR: L2 prefetch distance (tuning knob STEN_SR_L2PF)
   bool cc = false;              // constant-coefficient operator (stencil_create_const)
   double cscaled[6] = {};       // its couplings A_d / a_P (fp64)
 };
@@ -670,6 +671,7 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     return set_err(STEN_ECUDA, "internal: SR grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;
+  a.l2pf = st->sr_l2pf;
   if (st->cc) {  // the same roundings as k_create_coeffs: fp64 quotient, RN to fp32 / fp16
     for (int d = 0; d < 6; ++d) {
       a.cf32[d] = (float)st->cscaled[d];
@@ -1006,6 +1008,7 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   }
   st->sm = device_sm_count();
   if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
+  if (const char *pf = getenv("STEN_SR_L2PF")) st->sr_l2pf = atoi(pf);
   if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
   st->slabs.resize(nslabs);
   auto fail = [&](int rc) {

@@ -309,9 +309,6 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   static_assert(6 % S == 0 && 6 % SC == 0, "stage counts must divide the unroll period");
 
   if (sr_idle(a.red.st)) return;
-#ifdef STEN_DBG_STOP
-  if (STEN_DBG_STOP == 0) return;
-#endif
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);           // [S] inputs, [SC] coefficients
@@ -371,9 +368,6 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   }
   __syncthreads();
 
-#ifdef STEN_DBG_STOP
-  if (STEN_DBG_STOP == 5) return;
-#endif
   auto issue_in = [&](int qi) {  // plane z0-2+qi of r, p, v, q, y (vectors: 2 halo planes)
     const int slot = qi % S, m = z0 - 2 + qi;
     mbar_expect_tx(&mbar[slot], 5u * HW * G::RI * (uint32_t)sizeof(T));
@@ -386,10 +380,20 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 #pragma unroll
     for (int d = 0; d < 6; ++d) tma_load_3d(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot]);
   };
+  // optional L2 prefetch (cp.async.bulk.prefetch.tensor) of input planes beyond
+  // the shared-memory stages: bytes in flight to HBM without shared memory
+  const int l2pf = a.l2pf;
+  auto prefetch_in = [&](int qi) {
+    if (qi < npi) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) tma_prefetch_l2(&a.tm_in[i], x0 - H, y0 - 2, z0 - 2 + qi + 2);
+    }
+  };
   if (tid == 0) {
     for (int q = 0; q < min(S, npi); ++q) issue_in(q);
     if (!CC)
       for (int q = 0; q < min(SC, npc); ++q) issue_c(q);
+    for (int q = S; q < S + l2pf; ++q) prefetch_in(q);
   }
   // CC: the couplings as packs; v' is zero outside the global mesh (lanes
   // [vlo, vhi) of an item's vector are in x, vrow says the row is in y)
@@ -490,7 +494,10 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       }
     }
     __syncthreads();
-    if (tid == 0 && j + S < npi) issue_in(j + S);
+    if (tid == 0) {
+      if (j + S < npi) issue_in(j + S);
+      if (l2pf) prefetch_in(j + S + l2pf);
+    }
 
     // ---------------- (B) ----------------
     if (j >= 2) {
@@ -569,24 +576,6 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
     }
   };
 
-#ifdef STEN_DBG_STOP
-  if (STEN_DBG_STOP == 1) {
-    __syncthreads();
-    if (tid == 0) {  // drain the issued TMA loads before leaving
-      for (int q = 0; q < min(S, npi); ++q) mbar_wait(&mbar[q % S], 0);
-      if (!CC) for (int q = 0; q < min(SC, npc); ++q) mbar_wait(&mbar[S + q % SC], 0);
-    }
-    __syncthreads();
-    return;
-  }
-  if (STEN_DBG_STOP >= 2) {
-    step(IC<0>{}, 0);
-    if (STEN_DBG_STOP >= 3) step(IC<1>{}, 1);
-    if (STEN_DBG_STOP >= 4) { step(IC<2>{}, 2); step(IC<3>{}, 3); step(IC<4>{}, 4); step(IC<5>{}, 5); }
-    __syncthreads();
-    return;
-  }
-#endif
   for (int j = 0; j < npi; j += 6) {
     step(IC<0>{}, j);
     if (j + 1 < npi) step(IC<1>{}, j + 1);

@@ -521,6 +521,7 @@ struct alignas(64) SrArgs {
   float cf32[6];
   unsigned short cf16[6];
   int has_below, has_above;
+  int l2pf;               // input planes prefetched into L2 beyond the TMA stages (0: off)
   Reduce red;
 };
 bool sr_config_ok(int by, int stages, int cstages, int pack);
