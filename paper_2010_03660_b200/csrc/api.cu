@@ -221,6 +221,12 @@ struct sten_stencil {
   unsigned *ir_amax = nullptr;  // refinement: max|r| (float bits), sigma
   float *ir_sigma = nullptr;
   int sr_l2pf = 0;              // SR: L2 prefetch distance (tuning knob STEN_SR_L2PF)
+  bool sr_overlap = true;       // SR, decomposed: halo exchange overlapped with the interior chunks
+  cudaStream_t side = nullptr;  // capture side stream (exchange + boundary chunks)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  float *partials2 = nullptr;   // reduction scratch of the concurrent interior launch
+  int partials2_cap = 0;
+  unsigned *counter2 = nullptr;
   bool cc = false;              // constant-coefficient operator (stencil_create_const)
   double cscaled[6] = {};       // its couplings A_d / a_P (fp64)
 };
@@ -475,9 +481,9 @@ static int exchange(sten_stencil *st, int prec, Pick pick, cudaStream_t s) {
 }
 
 // Decomposed solve: slab sums -> (NCCL fp32 all-reduce) -> scalar step.
-static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s) {
+static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s, int nslots = 0) {
   if (!decomposed(st)) return STEN_OK;
-  const int ns = (int)st->slabs.size();
+  const int ns = nslots > 0 ? nslots : (int)st->slabs.size();
   if (st->comm && st->comm->nranks > 1) {
     KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
     NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
@@ -638,6 +644,16 @@ static int ensure_sr(sten_stencil *st, int prec) {
       st->partials_cap = g;
       drop_graphs(st);
     }
+    if (decomposed(st) && !st->partials2) {
+      CUDA_TRY(cudaMalloc(&st->partials2, (size_t)st->partials_cap * kMaxDots * sizeof(float)));
+      st->partials2_cap = st->partials_cap;
+    }
+    if (decomposed(st) && st->partials2_cap < st->partials_cap) {
+      cudaFree(st->partials2);
+      CUDA_TRY(cudaMalloc(&st->partials2, (size_t)st->partials_cap * kMaxDots * sizeof(float)));
+      st->partials2_cap = st->partials_cap;
+      drop_graphs(st);
+    }
   }
   return STEN_OK;
 }
@@ -647,8 +663,14 @@ static char *sr_interior(void *base, const sten_stencil *st, int prec) {
 }
 
 // one sweep of slab `slab`: reads set `set`, writes set `set ^ 1`.
-// capture: deposit the raw sums in slab_sums instead of finalising.
-static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture, cudaStream_t s) {
+// part: SR_ALL chunks, SR_INTERIOR (input planes all inside the slab: no halo
+// needed) or SR_BOUNDARY (the rest).  capture: deposit the raw sums in
+// slab_sums (slot 2*slab + (part == SR_INTERIOR)) instead of finalising.
+enum { SR_ALL = 0, SR_INTERIOR = 1, SR_BOUNDARY = 2 };
+static void sr_chunk_z(const SrTiling &t, int nbig, int zct, int c, int *z0) {
+  *z0 = c < nbig ? c * t.zc : nbig * t.zc + (c - nbig) * zct;
+}
+static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture, cudaStream_t s, int part = SR_ALL) {
   Slab &sl = st->slabs[slab];
   SrBufs &b = sl.sr[prec];
   const SrTiling &t = st->srt[prec];
@@ -664,6 +686,20 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
   a.zc = t.zc;
   sr_chunks(t, sl.nz, &a.nbig, &a.zc_tail);
+  const int ntot = a.nbig + (sl.nz - a.nbig * t.zc + a.zc_tail - 1) / a.zc_tail;
+  // interior chunks: [clo, chi), those whose staged planes z0-2 .. z1+1 lie in the slab
+  int clo = 0, chi = 0;
+  for (int c = 0; c < ntot; ++c) {
+    int z0c, z0n;
+    sr_chunk_z(t, a.nbig, a.zc_tail, c, &z0c);
+    sr_chunk_z(t, a.nbig, a.zc_tail, c + 1, &z0n);
+    const bool in = z0c >= 2 && (z0n < sl.nz ? z0n : sl.nz) <= sl.nz - 2;
+    if (in && chi == clo) clo = chi = c;
+    if (in) chi = c + 1;
+  }
+  if (part == SR_ALL) { a.nch = ntot; a.ch_lo_n = 0; a.ch_hi0 = 0; }
+  else if (part == SR_INTERIOR) { a.nch = chi - clo; a.ch_lo_n = 0; a.ch_hi0 = clo; }
+  else { a.nch = ntot - (chi - clo); a.ch_lo_n = clo; a.ch_hi0 = chi; }
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   a.tiles_x = (st->nx + bx - 1) / bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
@@ -671,6 +707,13 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     return set_err(STEN_ECUDA, "internal: SR grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;
+  if (part != SR_ALL) {
+    a.red.slab_out = st->slab_sums + (2 * slab + (part == SR_INTERIOR)) * kMaxDots;
+    if (part == SR_INTERIOR) {
+      a.red.partials = st->partials2;
+      a.red.counter = st->counter2;
+    }
+  }
   a.l2pf = st->sr_l2pf;
   if (st->cc) {  // the same roundings as k_create_coeffs: fp64 quotient, RN to fp32 / fp16
     for (int d = 0; d < 6; ++d) {
@@ -681,6 +724,7 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     a.has_below = sl.has_below;
     a.has_above = sl.has_above;
   }
+  if (a.nch == 0) return STEN_OK;
   if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
   else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
   st->launches++;
@@ -725,9 +769,25 @@ static int sr_exchange(sten_stencil *st, int prec, int set, cudaStream_t s) {
 // cross-slab / cross-rank scalar step.  evs: optional [2] events.
 static int enqueue_sr_sweep(sten_stencil *st, int prec, int set, cudaStream_t s, cudaEvent_t *evs) {
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
-  if (decomposed(st)) RC_TRY(sr_exchange(st, prec, set, s));
-  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_sr(st, prec, k, set, false, s));
-  RC_TRY(reduce_scalars(st, PH_SR, s));
+  const int ns = (int)st->slabs.size();
+  if (decomposed(st) && st->sr_overlap) {
+    // the halo exchange and the chunks that read halo planes on a side
+    // stream, concurrent with the interior chunks (north_star: halos
+    // "overlapped with interior compute"); both deposit slab sums
+    CUDA_TRY(cudaMemsetAsync(st->slab_sums, 0, sizeof(float) * kMaxDots * 2 * ns, s));
+    CUDA_TRY(cudaEventRecord(st->ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(st->side, st->ev_fork, 0));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, set, false, s, SR_INTERIOR));
+    RC_TRY(sr_exchange(st, prec, set, st->side));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, set, false, st->side, SR_BOUNDARY));
+    CUDA_TRY(cudaEventRecord(st->ev_join, st->side));
+    CUDA_TRY(cudaStreamWaitEvent(s, st->ev_join, 0));
+    RC_TRY(reduce_scalars(st, PH_SR, s, 2 * ns));
+  } else {
+    if (decomposed(st)) RC_TRY(sr_exchange(st, prec, set, s));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, set, false, s));
+    RC_TRY(reduce_scalars(st, PH_SR, s));
+  }
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
   return STEN_OK;
 }
@@ -1009,6 +1069,7 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   st->sm = device_sm_count();
   if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
   if (const char *pf = getenv("STEN_SR_L2PF")) st->sr_l2pf = atoi(pf);
+  if (const char *ov = getenv("STEN_SR_OVERLAP")) st->sr_overlap = atoi(ov) != 0;
   if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
   st->slabs.resize(nslabs);
   auto fail = [&](int rc) {
@@ -1083,14 +1144,19 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   if (cudaMalloc(&st->st, sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(&st->st_host, sizeof(DevState)) != cudaSuccess ||
       cudaMalloc(&st->counter, sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc(&st->slab_sums, sizeof(float) * kMaxDots * nslabs) != cudaSuccess ||
+      cudaMalloc(&st->slab_sums, sizeof(float) * kMaxDots * 2 * nslabs) != cudaSuccess ||
+      cudaMalloc(&st->counter2, sizeof(unsigned)) != cudaSuccess ||
       cudaMalloc(&st->red_total, sizeof(float) * kMaxDots) != cudaSuccess)
     return fail(set_err(STEN_ENOMEM, "state allocation failed"));
   cudaMemset(st->counter, 0, sizeof(unsigned));
+  cudaMemset(st->counter2, 0, sizeof(unsigned));
   cudaMemset(st->st, 0, sizeof(DevState));
-  cudaMemset(st->slab_sums, 0, sizeof(float) * kMaxDots * nslabs);
+  cudaMemset(st->slab_sums, 0, sizeof(float) * kMaxDots * 2 * nslabs);
   cudaMemset(st->red_total, 0, sizeof(float) * kMaxDots);
   if (cudaStreamCreateWithFlags(&st->cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&st->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreate(&st->ev_a) != cudaSuccess || cudaEventCreate(&st->ev_b) != cudaSuccess)
     return fail(set_err(STEN_ECUDA, "stream/event creation failed"));
   *out = st;
@@ -1133,7 +1199,12 @@ void stencil_destroy(sten_stencil *st) {
   cudaFree(st->st);
   if (st->st_host) cudaFreeHost(st->st_host);
   cudaFree(st->partials);
+  cudaFree(st->partials2);
   cudaFree(st->counter);
+  cudaFree(st->counter2);
+  if (st->side) cudaStreamDestroy(st->side);
+  if (st->ev_fork) cudaEventDestroy(st->ev_fork);
+  if (st->ev_join) cudaEventDestroy(st->ev_join);
   cudaFree(st->slab_sums);
   cudaFree(st->red_total);
   cudaFree(st->hist);

@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   const int tx = b % a.tiles_x;
   b /= a.tiles_x;
   const int ty = b % a.tiles_y;
-  const int ch = b / a.tiles_y;
+  const int ci = b / a.tiles_y;
+  const int ch = ci < a.ch_lo_n ? ci : a.ch_hi0 + (ci - a.ch_lo_n);
   const int x0 = tx * G::BX, y0 = ty * BY;
   const int z0 = ch < a.nbig ? ch * a.zc : a.nbig * a.zc + (ch - a.nbig) * a.zc_tail;
   const int z1 = min(z0 + (ch < a.nbig ? a.zc : a.zc_tail), a.g.nz);
@@ -600,7 +601,8 @@ int launch_sr_one(const SrArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int grid = a.tiles_x * a.tiles_y * (a.nbig + (a.g.nz - a.nbig * a.zc + a.zc_tail - 1) / a.zc_tail);
+  const int grid = a.tiles_x * a.tiles_y * a.nch;
+  if (grid == 0) return (int)cudaSuccess;
   k_sr<T, BY, S, SC, CC, NB><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }

@@ -515,6 +515,8 @@ struct alignas(64) SrArgs {
   int zc, tiles_x, tiles_y;
   int nbig;               // chunks [0, nbig) have zc planes; the rest cover
   int zc_tail;            // [nbig*zc, nz) in zc_tail-plane chunks (fills the tail wave)
+  int nch;                // chunks in this launch: its i-th chunk is i (i < ch_lo_n), else
+  int ch_lo_n, ch_hi0;    // ch_hi0 + i - ch_lo_n (all / interior / boundary subsets)
   // constant-coefficient operator (stencil_create_const): the six scaled
   // couplings as scalars, no coefficient streams; v' is masked to zero outside
   // the global mesh (planes below/above exist only at slab interfaces)
