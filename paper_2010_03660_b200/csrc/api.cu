@@ -146,7 +146,7 @@ struct SrBufs {
   bool ready = false, maps_ok = false;
   void *x = nullptr, *rh = nullptr;
   void *vec[2][5] = {};           // ping-pong sets of r, p, v, q, y
-  CUtensorMap m_vec[2][5], m_c[6];
+  CUtensorMap m_vec[2][5], m_c[6], m_x, m_rh;
 };
 
 struct PrecBufs {
@@ -565,7 +565,7 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
 // (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
 static void default_sr_tiling(sten_stencil *st, int prec) {
   SrTiling &t = st->srt[prec];
-  int by = 16, stg = 3, cst = 2, zc = 320, zct = 64, tail = 256, pack = 16;
+  int by = 16, stg = 2, cst = 2, zc = 160, zct = 64, tail = 320, pack = 16;
   if (const char *e = getenv("STEN_SR_TILING"))
     sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail, &pack);
   t.pack = pack;
@@ -635,6 +635,8 @@ static int ensure_sr(sten_stencil *st, int prec) {
         void *c = prec == STEN_FP32 ? (void *)sl.c32b[d] : (void *)sl.c16b[d];
         RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + 2 * H, t.by + 2));
       }
+      RC_TRY(make_map(&b.m_x, b.x, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
+      RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
       b.maps_ok = true;
     }
     const int g = sr_grid(st, prec, sl.nz);
@@ -681,6 +683,8 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     a.out[i] = sr_interior(b.vec[set ^ 1][i], st, prec);
   }
   for (int d = 0; d < 6; ++d) a.tm_c[d] = b.m_c[d];
+  a.tm_x = b.m_x;
+  a.tm_rh = b.m_rh;
   a.x = sr_interior(b.x, st, prec);
   a.rh = sr_interior(b.rh, st, prec);
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};

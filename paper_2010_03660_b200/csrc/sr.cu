@@ -45,6 +45,13 @@ constexpr int a128(int b) { return (b + 127) & ~127; }
 
 template <int V> struct IC { static constexpr int value = V; };
 
+#ifndef STEN_SR_XTMA
+#define STEN_SR_XTMA 1  // x arrives with the input stage by TMA (else a direct load three planes ahead)
+#endif
+#ifndef STEN_SR_RHTMA
+#define STEN_SR_RHTMA 1  // r_hat too, into a 6-plane ring (it is used two steps after its stage lands)
+#endif
+
 // Per-thread vectors of the SR sweep: NB = 16 (8 fp16 / 4 fp32 lanes) or 8
 // bytes (4 / 2 lanes).  The 8-B form gives a tile twice the threads (16 warps
 // per SM for a 16-row tile) for the same shared-memory pipeline.
@@ -194,13 +201,16 @@ struct SrGeo {
   static constexpr int NHF = RI * VW - NT;       // formed vectors outside the own tile
   static constexpr int NHV = RC * VW - NT;       // v' vectors outside the own tile
   static constexpr int NR = 6;                   // r' ring slots (= unroll period)
+  static constexpr int XE = a128(BX * BY * (int)sizeof(T)) / (int)sizeof(T);  // x tile per input stage
+  static constexpr int SE = 5 * IE + (STEN_SR_XTMA ? XE : 0);                  // elements per input stage
   static_assert(NHF <= NT && NHV <= NT, "halo work must fit one extra item per thread");
 };
 
 template <typename T, int BY, int S, int SC, bool CC, int NB>
 constexpr size_t sr_smem_c() {
   using G = SrGeo<T, BY, NB>;
-  return 128 + (size_t)sizeof(T) * ((size_t)S * 5 * G::IE + (CC ? 0 : (size_t)SC * 6 * G::CE) +
+  return 128 + (size_t)sizeof(T) * ((size_t)S * G::SE + (CC ? 0 : (size_t)SC * 6 * G::CE) +
+                                    (STEN_SR_RHTMA ? 6 * (size_t)G::XE : 0) +
                                     (3 + G::NR) * (size_t)G::IE + 2 * (size_t)G::CE);
 }
 
@@ -312,11 +322,12 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);           // [S] inputs, [SC] coefficients
-  T *const IN = reinterpret_cast<T *>(smem + 128);               // [S][5][IE]
-  T *const CF = IN + S * 5 * IE;                                 // [SC][6][CE]
+  T *const IN = reinterpret_cast<T *>(smem + 128);               // [S][SE]: 5 boxes of IE (+ the x tile)
+  T *const CF = IN + S * G::SE;                                  // [SC][6][CE]
   T *const PR = CF + (CC ? 0 : SC * 6 * CE);                     // p' ring [3][IE]
   T *const RR = PR + 3 * IE;                                     // r' ring [6][IE]
   T *const VR = RR + G::NR * IE;                                 // v' ring [2][CE]
+  T *const RHR = VR + 2 * CE;                                    // r_hat ring [6][XE] (RHTMA)
   __shared__ float scratch[32 * kMaxDots];
 
   int b = blockIdx.x;
@@ -371,9 +382,13 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 
   auto issue_in = [&](int qi) {  // plane z0-2+qi of r, p, v, q, y (vectors: 2 halo planes)
     const int slot = qi % S, m = z0 - 2 + qi;
-    mbar_expect_tx(&mbar[slot], 5u * HW * G::RI * (uint32_t)sizeof(T));
+    mbar_expect_tx(&mbar[slot],
+                   (5u * HW * G::RI + (STEN_SR_XTMA ? G::BX * BY : 0) + (STEN_SR_RHTMA ? G::BX * BY : 0)) *
+                       (uint32_t)sizeof(T));
 #pragma unroll
-    for (int i = 0; i < 5; ++i) tma_load_3d(IN + (slot * 5 + i) * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
+    for (int i = 0; i < 5; ++i) tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
+    if (STEN_SR_XTMA) tma_load_3d(IN + slot * G::SE + 5 * IE, &a.tm_x, x0, y0, m + 2, &mbar[slot]);
+    if (STEN_SR_RHTMA) tma_load_3d(RHR + (qi % 6) * G::XE, &a.tm_rh, x0, y0, m + 2, &mbar[slot]);
   };
   auto issue_c = [&](int qc) {  // plane z0-1+qc of the six coefficient arrays (1 halo plane)
     const int slot = qc % SC, m = z0 - 1 + qc;
@@ -443,8 +458,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     pw[i] = vw[i] = P::zero();
-    xq[i] = ld_x(z0 - 2 + i);  // x of the plane formed at step i
-    rq[i] = ld_rh(z0 + i);     // r_hat of the plane of the dots at step 4 + i
+    xq[i] = STEN_SR_XTMA ? P::zero() : ld_x(z0 - 2 + i);  // x of the plane formed at step i
+    rq[i] = STEN_SR_RHTMA ? P::zero() : ld_rh(z0 + i);  // r_hat of the plane of the dots at step 4 + i
   }
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -464,7 +479,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
     // ---------------- (A) ----------------
     mbar_wait(&mbar[J % S], (uint32_t)((j / S) & 1));
     {
-      const T *st = IN + (J % S) * 5 * IE;
+      const T *st = IN + (J % S) * G::SE;
       T *pr = PR + (J % 3) * IE;
       T *rr = RR + J * IE;
       const P r = P::ld(st + ei), p = P::ld(st + IE + ei), v = P::ld(st + 2 * IE + ei);
@@ -479,11 +494,12 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       rw[J] = rn;
       if (inside && m >= z0 && m < z1) {
         const long long o = (long long)m * plane + gofs;
-        P::fmas(om_s, s, P::fmas(al_s, p, xq[J % 3])).st(Xg + o);
+        const P xv = STEN_SR_XTMA ? P::ld(st + 5 * IE + ry * G::BX + cx * VEC) : xq[J % 3];
+        P::fmas(om_s, s, P::fmas(al_s, p, xv)).st(Xg + o);
         rn.st(Og[0] + o);
         pn.st(Og[1] + o);
       }
-      xq[J % 3] = ld_x(m + 3);
+      if (!STEN_SR_XTMA) xq[J % 3] = ld_x(m + 3);
       if (hf >= 0) {
         const P hr = P::ld(st + hf), hp = P::ld(st + IE + hf), hv_ = P::ld(st + 2 * IE + hf);
         const P hq = P::ld(st + 3 * IE + hf), hy = P::ld(st + 4 * IE + hf);
@@ -555,8 +571,9 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
         qn = orow ? SCn::keep(qn, olo, ohi) : P::zero();
         yn = orow ? SCn::keep(yn, olo, ohi) : P::zero();
       }
-      const P rh = rq[(J + 2) % 3];  // r_hat of plane k (loaded three steps ago)
-      rq[(J + 2) % 3] = ld_rh(k + 3);
+      // r_hat of plane k: from the ring (it arrived with stage j-2), or loaded three steps ago
+      const P rh = STEN_SR_RHTMA ? P::ld(RHR + ((J + 4) % 6) * G::XE + ry * G::BX + cx * VEC) : rq[(J + 2) % 3];
+      if (!STEN_SR_RHTMA) rq[(J + 2) % 3] = ld_rh(k + 3);
       if (inside) {
         const long long o = (long long)k * plane + gofs;
         qn.st(Og[3] + o);
@@ -609,9 +626,8 @@ int launch_sr_one(const SrArgs &a, cudaStream_t s) {
 }  // namespace
 
 // (rows per tile, input stages, coefficient stages, bytes per thread vector)
-#define STEN_SR_CONFIGS(X)                                                                                  \
-  X(16, 3, 2, 16) X(16, 2, 2, 16) X(16, 2, 3, 16) X(8, 2, 2, 16) X(8, 3, 2, 16) X(8, 3, 3, 16) X(16, 3, 2, 8) \
-  X(16, 2, 2, 8) X(8, 2, 2, 8) X(8, 3, 2, 8)
+#define STEN_SR_CONFIGS(X) \
+  X(16, 2, 2, 16) X(16, 2, 2, 8) X(8, 2, 2, 16) X(8, 3, 2, 16) X(8, 3, 3, 16) X(8, 2, 2, 8) X(8, 3, 2, 8)
 
 bool sr_config_ok(int by, int stages, int cstages, int pack) {
 #define X(B, S_, C_, N_) if (by == B && stages == S_ && cstages == C_ && pack == N_) return true;

@@ -508,6 +508,8 @@ enum { IR_BHAT = 0, IR_RESID = 1, IR_SCALE = 2, IR_UPDATE = 3 };
 struct alignas(64) SrArgs {
   CUtensorMap tm_in[5];   // r, p, v, q, y of the previous sweep: box (BX+2H) x (BY+4), 2 halo planes
   CUtensorMap tm_c[6];    // coefficients with one halo plane: box (BX+2H) x (BY+2)
+  CUtensorMap tm_x;       // x (2 halo planes): box BX x BY, arrives with the input stage
+  CUtensorMap tm_rh;      // r_hat, the same box
   void *x;                // in place (own points only), interior plane 0
   const void *rh;         // shadow residual, interior plane 0
   void *out[5];           // r, p, v, q, y of this sweep, interior plane 0
