@@ -4,11 +4,6 @@ mkdir -p gpurun_out
 run() {
   tag=$1; shift
   env "$@" python bench.py --steps 1 --warmup 1 --maxit 3 --no-e2e --no-cpu > /dev/null 2>&1 || { echo "$tag bench failed"; return; }
-  env "$@" ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum --clock-control none -k regex:k_sr -s 6 -c 1 --csv python bench.py --steps 1 --warmup 1 --maxit 3 --no-e2e --no-cpu 2>/dev/null | grep -E "dram__bytes|gpu__time|lts__" | awk -F'","' -v t="$tag" '{print t, $(NF-2), $(NF-1), $NF}'
+  env "$@" ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_sr -s 6 -c 1 --csv python bench.py --steps 1 --warmup 1 --maxit 3 --no-e2e --no-cpu 2>/dev/null | grep -E "dram__bytes|gpu__time" | awk -F'","' -v t="$tag" '{print t, $(NF-2), $(NF-1), $NF}'
 }
-run base
-run zc128 STEN_SR_TILING=16,2,2,128
-run zc32 STEN_SR_TILING=16,2,2,32
-run pitch8 STEN_PITCH_ALIGN=8
-run pitch32 STEN_PITCH_ALIGN=32
-run promo0 STEN_TMA_PROMO=0
+for v in "$@"; do run $v; done
