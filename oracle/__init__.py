@@ -15,7 +15,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["o64.c", "o16.c", "osr.c"]
+_SOURCES = ["o64.c", "o16.c", "osr.c", "o2d.c"]
 
 ORC_CONVERGED, ORC_MAXIT, ORC_BREAKDOWN, ORC_NONFINITE = 0, 1, 2, 3
 
@@ -85,6 +85,10 @@ def _declare(L):
     L.o16_bicgstab.restype = _I
     L.o32_apply_fma.argtypes = [_I, _I, _I, _P, _P, _P]
     L.oracle_num_threads.restype = _I
+    L.o64_jacobi_scale9.argtypes = [_I, _I, _P, _P, _P]
+    L.o64_apply9.argtypes = [_I, _I, _P, _P, _P]
+    L.o16_apply9.argtypes = [_I, _I, _P, _P, _P]
+    L.o32_apply9.argtypes = [_I, _I, _P, _P, _P]
     L.o64_sr_sweep.argtypes = [_I, _I, _I, _P, _D, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P]
     L.o16_sr_sweep.argtypes = [_I, _I, _I, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                _P, _P, _P, _P, _P, _P, _P, _P]
@@ -349,6 +353,49 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         inner += d["iters"]
         x = (x.astype(np.float64) + sigma * f16_to_double(d["x"])).astype(np.float32)
     return dict(x=x, hist=np.array(hist), outer=len(hist) - 1, inner=inner, status=status)
+
+
+# ---------------- 2D 9-point SpMV (o2d.c) ----------------
+
+def _arr8(arrs):
+    return (ctypes.c_void_p * 8)(*[a.ctypes.data for a in arrs])
+
+
+def jacobi_scale9(diag, offs):
+    """Scaled couplings of the 2D 9-point operator; arrays (ny, nx), offs in the o2d.c order."""
+    offs = [_c(o, np.float64) for o in offs]
+    ny, nx = offs[0].shape
+    d = None if diag is None else _c(diag, np.float64)
+    out = [np.empty((ny, nx), np.float64) for _ in range(8)]
+    lib().o64_jacobi_scale9(nx, ny, None if d is None else _ptr(d), _arr8(offs), _arr8(out))
+    return out
+
+
+def apply9_64(c, v):
+    c = [_c(a, np.float64) for a in c]
+    v = _c(v, np.float64)
+    ny, nx = v.shape
+    u = np.empty_like(v)
+    lib().o64_apply9(nx, ny, _arr8(c), _ptr(v), _ptr(u))
+    return u
+
+
+def apply9_16(c16, v16):
+    c16 = [_c(a, np.uint16) for a in c16]
+    v16 = _c(v16, np.uint16)
+    ny, nx = v16.shape
+    u = np.empty_like(v16)
+    lib().o16_apply9(nx, ny, _arr8(c16), _ptr(v16), _ptr(u))
+    return u
+
+
+def apply9_32(c32, v32):
+    c32 = [_c(a, np.float32) for a in c32]
+    v32 = _c(v32, np.float32)
+    ny, nx = v32.shape
+    u = np.empty_like(v32)
+    lib().o32_apply9(nx, ny, _arr8(c32), _ptr(v32), _ptr(u))
+    return u
 
 
 # ---------------- fp32 mirror ----------------

@@ -144,6 +144,14 @@ int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
                     uint16_t *x, double *hist, float *alpha, float *omega,
                     int *status, int *event_it);
 
+/* ---------------- 2D 9-point SpMV (o2d.c; NEXT-3) ------- */
+/* Mesh nx*ny, P = i + nx*j; c[0..7] couple P to its (dx,dy) neighbour in the
+ * order (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1). */
+void o64_jacobi_scale9(int nx, int ny, const double *diag, const double *const off[8], double *const c[8]);
+void o64_apply9(int nx, int ny, const double *const c[8], const double *v, double *u);
+void o16_apply9(int nx, int ny, const uint16_t *const c[8], const uint16_t *v, uint16_t *u);  /* mirror */
+void o32_apply9(int nx, int ny, const float *const c[8], const float *v, float *u);           /* mirror */
+
 /* informational */
 int oracle_num_threads(void);
 
