@@ -238,6 +238,28 @@ int sten_set_sr_tiling(sten_stencil *st, int precision, int by, int stages, int 
  * stages: TMA pipeline depth (2..8). */
 int sten_set_tiling(sten_stencil *st, int precision, int bx, int by, int zc, int stages);
 
+/* ------------------------------------------------- 2D 9-point SpMV ----- */
+/* The paper's second kernel (Sec. "SpMV (2D)"; SURVEY
+ * §8(f) NEXT-3): u = A v for a 9-point stencil on an nx x ny mesh, P = i + nx*j.
+ *   coeffs[0]   : main diagonal A_P (or NULL: already unit); coeffs[1..8]: the
+ *                 couplings to the (dx, dy) neighbours in the order (-1,-1)
+ *                 (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1); dense
+ *                 (ny, nx) arrays of coeff_dtype, host or device, copied.
+ * The operator is Jacobi-scaled as in 3D (c_d = A_d / A_P in fp64, couplings
+ * leaving the mesh dropped, rounded RN to fp32 and fp16: "most
+ * problems will precondition the main diagonal to unity").  Errors:
+ * STEN_EINVAL, STEN_ENOMEM, STEN_ECUDA. */
+typedef struct sten_stencil2d sten_stencil2d;
+int stencil2d_create(int nx, int ny, const void *const coeffs[9], int coeff_dtype, void *cuda_stream,
+                     sten_stencil2d **out);
+/* y = A_hat x: u = x + sum_d c_d x_nb(d), one FMA per term in the order above
+ * (fp32, or fp16 for STEN_MIXED; oracle/o2d.c mirrors it).  x, y: dense
+ * (ny, nx), host or device, must not overlap.  Synchronises cuda_stream. */
+int stencil2d_apply(sten_stencil2d *st, int precision, const void *x, void *y, void *cuda_stream);
+/* device time (ms) of the last apply's kernel (CUDA events around it) */
+int stencil2d_last_ms(sten_stencil2d *st, double *ms);
+void stencil2d_destroy(sten_stencil2d *st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,10 @@ def lib():
         L.stencil_create.argtypes = [I, I, I, P, I, I, P, P, ctypes.POINTER(P)]
         L.stencil_destroy.argtypes = [P]
         L.stencil_create_const.argtypes = [I, I, I, P, I, P, P, ctypes.POINTER(P)]
+        L.stencil2d_create.argtypes = [I, I, P, I, P, ctypes.POINTER(P)]
+        L.stencil2d_apply.argtypes = [P, I, P, P, P]
+        L.stencil2d_last_ms.argtypes = [P, ctypes.POINTER(D)]
+        L.stencil2d_destroy.argtypes = [P]
         L.stencil_apply.argtypes = [P, I, P, P, P]
         L.bicgstab_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
         L.sten_scalar_history.argtypes = [P, I, P, P]
@@ -307,3 +311,49 @@ def bicgstab_refine(st: Stencil, b, x0, tol: float, outer_maxit: int, inner_tol:
                                  int(inner_maxit), _ptr(x_out), ctypes.byref(ko), ctypes.byref(ki),
                                  hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(status), _stream(stream)))
     return ko.value, ki.value, hist[: ko.value + 1].copy(), status.value
+
+
+# ------------------------------------------------------- 2D 9-point SpMV --
+class Stencil2D:
+    def __init__(self, handle, nx, ny):
+        self.handle, self.nx, self.ny = handle, nx, ny
+
+    def close(self):
+        if self.handle:
+            lib().stencil2d_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stencil2d_create(nx: int, ny: int, coeffs, stream=None) -> Stencil2D:
+    """coeffs = [diag or None, 8 couplings in the order (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0)
+    (-1,+1) (0,+1) (+1,+1)], dense (ny, nx) each, float64 or float32."""
+    if len(coeffs) != 9:
+        raise StenError("coeffs must have 9 entries (diag + 8 couplings)")
+    ref = next(c for c in coeffs[1:] if c is not None)
+    dt = DT_F64 if _itemsize(ref) == 8 else DT_F32
+    arr = (ctypes.c_void_p * 9)()
+    for i, c in enumerate(coeffs):
+        if c is None:
+            arr[i] = None
+            continue
+        if _itemsize(c) != _itemsize(ref) or _numel(c) != nx * ny:
+            raise StenError(f"coeffs[{i}] has the wrong dtype or size")
+        arr[i] = _ptr(c).value
+    h = ctypes.c_void_p()
+    _check(lib().stencil2d_create(nx, ny, arr, dt, _stream(stream), ctypes.byref(h)))
+    return Stencil2D(h, nx, ny)
+
+
+def stencil2d_apply(st: Stencil2D, precision: int, x, y, stream=None):
+    _check_vec(x, precision, st.nx * st.ny, "x")
+    _check_vec(y, precision, st.nx * st.ny, "y")
+    _check(lib().stencil2d_apply(st.handle, precision, _ptr(x), _ptr(y), _stream(stream)))
+    ms = ctypes.c_double(0.0)
+    _check(lib().stencil2d_last_ms(st.handle, ctypes.byref(ms)))
+    return ms.value

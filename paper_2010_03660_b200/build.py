@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsten.so")
-SOURCES = ["kernels.cu", "stencil.cu", "sr.cu", "api.cu"]
+SOURCES = ["kernels.cu", "stencil.cu", "sr.cu", "sten2d.cu", "api.cu"]
 HEADERS = ["sten_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

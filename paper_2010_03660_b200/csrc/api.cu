@@ -1673,3 +1673,141 @@ int sten_sr_sweep(sten_stencil *st, int prec, double alpha, double omega, double
 }
 
 }  // extern "C"
+
+// ====================================================== 2D 9-point SpMV ==
+// NEXT-3 of SURVEY §8(f): the paper's second kernel.
+struct sten_stencil2d {
+  int nx = 0, ny = 0, pitch = 0;
+  float *c32[8] = {};
+  __half *c16[8] = {};
+  void *v[2] = {}, *u[2] = {};     // per precision: pitched input / output
+  bool maps_ok[2] = {false, false};
+  CUtensorMap m_v[2];
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double last_ms = 0.0;
+};
+
+static int create2d_impl(int nx, int ny, const void *const coeffs[9], int dtype, cudaStream_t s,
+                         sten_stencil2d **out) {
+  if (!out || !coeffs) return set_err(STEN_EINVAL, "NULL argument");
+  if (nx <= 0 || ny <= 0 || nx > (1 << 24) || ny > (1 << 24)) return set_err(STEN_EINVAL, "bad 2D mesh %d x %d", nx, ny);
+  for (int d = 1; d < 9; ++d)
+    if (!coeffs[d]) return set_err(STEN_EINVAL, "coeffs[%d] is NULL", d);
+  if (dtype != STEN_DT_F64 && dtype != STEN_DT_F32) return set_err(STEN_EINVAL, "coeff_dtype %d unsupported", dtype);
+  sten_stencil2d *st = new sten_stencil2d;
+  st->nx = nx;
+  st->ny = ny;
+  st->pitch = (nx + 7) / 8 * 8;  // 16-B rows (TMA row strides are 16-B multiples)
+  auto fail = [&](int rc) {
+    stencil2d_destroy(st);
+    return rc;
+  };
+  const size_t n = (size_t)nx * ny, ein = dtype == STEN_DT_F64 ? 8 : 4;
+  const size_t cells = (size_t)st->pitch * ny;
+  std::vector<void *> staged(9, nullptr);
+  const void *dev[9];
+  for (int d = 0; d < 9; ++d) {
+    dev[d] = coeffs[d];
+    if (coeffs[d] && !ptr_on_device(coeffs[d])) {
+      if (cudaMalloc(&staged[d], n * ein) != cudaSuccess) {
+        for (void *p : staged) cudaFree(p);
+        return fail(set_err(STEN_ENOMEM, "staging 2D coefficients failed"));
+      }
+      cudaMemcpyAsync(staged[d], coeffs[d], n * ein, cudaMemcpyHostToDevice, s);
+      dev[d] = staged[d];
+    }
+  }
+  Coef9In in;
+  Coef9Out co;
+  int rc = STEN_OK;
+  for (int d = 0; d < 8 && rc == STEN_OK; ++d) {
+    in.off[d] = dev[d + 1];
+    if (cudaMalloc(&st->c32[d], cells * 4) != cudaSuccess || cudaMalloc(&st->c16[d], cells * 2) != cudaSuccess)
+      rc = set_err(STEN_ENOMEM, "2D coefficient allocation failed");
+    co.c32[d] = st->c32[d];
+    co.c16[d] = st->c16[d];
+  }
+  if (rc == STEN_OK) {
+    int e = create9_launch(dtype, dev[0], in, nx, ny, st->pitch, co, s);
+    if (e) rc = set_err(STEN_ECUDA, "2D coefficient kernel: %s", cudaGetErrorString((cudaError_t)e));
+  }
+  if (rc == STEN_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = set_err(STEN_ECUDA, "stencil2d_create sync failed");
+  for (void *p : staged) cudaFree(p);
+  if (rc != STEN_OK) return fail(rc);
+  if (cudaEventCreate(&st->e0) != cudaSuccess || cudaEventCreate(&st->e1) != cudaSuccess)
+    return fail(set_err(STEN_ECUDA, "event creation failed"));
+  *out = st;
+  return STEN_OK;
+}
+
+extern "C" {
+
+int stencil2d_create(int nx, int ny, const void *const coeffs[9], int coeff_dtype, void *cuda_stream,
+                     sten_stencil2d **out) {
+  return create2d_impl(nx, ny, coeffs, coeff_dtype, (cudaStream_t)cuda_stream, out);
+}
+
+void stencil2d_destroy(sten_stencil2d *st) {
+  if (!st) return;
+  for (int d = 0; d < 8; ++d) {
+    cudaFree(st->c32[d]);
+    cudaFree(st->c16[d]);
+  }
+  for (int p = 0; p < 2; ++p) {
+    cudaFree(st->v[p]);
+    cudaFree(st->u[p]);
+  }
+  if (st->e0) cudaEventDestroy(st->e0);
+  if (st->e1) cudaEventDestroy(st->e1);
+  delete st;
+}
+
+int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *cuda_stream) {
+  if (!st || !x || !y) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int e = esize(prec);
+  const size_t bytes = (size_t)st->pitch * st->ny * e;
+  if (!st->v[prec]) {
+    CUDA_TRY(cudaMalloc(&st->v[prec], bytes));
+    CUDA_TRY(cudaMalloc(&st->u[prec], bytes));
+    CUDA_TRY(cudaMemset(st->v[prec], 0, bytes));  // padding columns stay zero
+  }
+  if (!st->maps_ok[prec]) {
+    g_plane_stride = (long long)st->pitch * st->ny;
+    const int bx = prec == STEN_FP32 ? 64 : 128, H = 16 / e;
+    RC_TRY(make_map(&st->m_v[prec], st->v[prec], e, st->nx, st->ny, 1, st->pitch, bx + 2 * H, 32 + 2));
+    st->maps_ok[prec] = true;
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(st->v[prec], (size_t)st->pitch * e, x, (size_t)st->nx * e, (size_t)st->nx * e, st->ny,
+                             cudaMemcpyDefault, s));
+  Apply9Args a;
+  memset(&a, 0, sizeof a);
+  a.tm_v = st->m_v[prec];
+  for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
+  a.u = st->u[prec];
+  a.nx = st->nx;
+  a.ny = st->ny;
+  a.pitch = st->pitch;
+  const int bx = prec == STEN_FP32 ? 64 : 128;
+  a.tiles_x = (st->nx + bx - 1) / bx;
+  CUDA_TRY(cudaEventRecord(st->e0, s));
+  if (prec == STEN_FP32) KLAUNCH(apply9_launch<float>(a, s));
+  else KLAUNCH(apply9_launch<__half>(a, s));
+  CUDA_TRY(cudaEventRecord(st->e1, s));
+  CUDA_TRY(cudaMemcpy2DAsync(y, (size_t)st->nx * e, st->u[prec], (size_t)st->pitch * e, (size_t)st->nx * e, st->ny,
+                             cudaMemcpyDefault, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, st->e0, st->e1));
+  st->last_ms = ms;
+  return STEN_OK;
+}
+
+int stencil2d_last_ms(sten_stencil2d *st, double *ms) {
+  if (!st || !ms) return set_err(STEN_EINVAL, "NULL argument");
+  *ms = st->last_ms;
+  return STEN_OK;
+}
+
+}  // extern "C"

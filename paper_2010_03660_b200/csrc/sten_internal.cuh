@@ -533,6 +533,19 @@ template <typename T> int sr_launch(const SrArgs &a, int by, int stages, int cst
 template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages, int pack);
 template <typename T> int sr_threads(int by, int pack);
 
+// sten2d.cu: the 2D 9-point SpMV (NEXT-3)
+struct alignas(64) Apply9Args {
+  CUtensorMap tm_v;       // v: box (BX + 2H) x (BY + 2), one plane
+  const void *c[8];       // scaled couplings, rows of `pitch`
+  void *u;
+  int nx, ny, pitch, tiles_x;
+};
+struct Coef9In { const void *off[8]; };
+struct Coef9Out { float *c32[8]; __half *c16[8]; };
+template <typename T> int apply9_launch(const Apply9Args &a, cudaStream_t s);
+int create9_launch(int in_dtype, const void *diag, const Coef9In &in, int nx, int ny, int pitch, const Coef9Out &out,
+                   cudaStream_t s);
+
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g,
                          int has_below, int has_above, float *const c32[6], __half *const c16[6],
                          double *aP, const double *cconst, cudaStream_t s);
