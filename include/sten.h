@@ -9,12 +9,19 @@
  *     only store six other diagonals" (Sec. IV);
  *   - stencil_apply: u = A v as the local value plus six coefficient-times-
  *     neighbour products (Sec. "SpMV (3D)");
- *   - bicgstab_solve: Algorithm 1 "Standard BiCGStab";
+ *   - bicgstab_solve: Algorithm 1 "Standard BiCGStab", as
+ *     printed (STEN_SCHED_CLASSIC) or rearranged to one sweep and one
+ *     reduction per iteration (STEN_SCHED_SR, R19);
+ *   - bicgstab_refine: mixed-precision iterative refinement, the remedy the
+ *     paper names for the fp16 plateau (R21);
+ *   - stencil_create_const: a constant-coefficient operator (no coefficient
+ *     streams in the SR sweep);
+ *   - stencil2d_*: the paper's 2D 9-point SpMV;
  *   - precisions: fp32 throughout, or the paper's mixed mode - fp16 storage
  *     and arithmetic, inner products with fp16 multiply / fp32 accumulate, the
  *     cross-device reduction in fp32.
  * Readings of the paper where it is silent (stopping rule, breakdown, x0, the
- * order of floating-point operations ...) are R1..R13 in DESIGN.md.
+ * order of floating-point operations ...) are R1..R21 in DESIGN.md.
  *
  * Layout.  A mesh (or a rank's slab of it) of nx*ny*nz points is a dense
  * array with linear index P = i + nx*(j + ny*k): x fastest, z slowest, so a
@@ -27,8 +34,10 @@
  *
  * Multi-GPU.  With a communicator, rank r of R owns the z-planes directly
  * above rank r-1's (rank order = z order) and passes only its own planes;
- * the library exchanges one halo plane per neighbour over NCCL and all-reduces
- * the 1-2 fp32 dot-product partial sums of each half-iteration.
+ * the library exchanges halo planes with the z-neighbours over NCCL (one plane
+ * per SpMV input for the classic schedule; two planes of five vectors once per
+ * iteration for SR, overlapped with the interior z chunks) and all-reduces the
+ * fp32 dot-product partial sums (1-3 per phase classic, 12 once per SR sweep).
  *
  * Errors.  Every int-returning entry point returns STEN_OK (0) or a negative
  * STEN_E* code; sten_last_error() then gives a thread-local message.
