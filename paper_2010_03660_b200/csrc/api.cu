@@ -565,7 +565,17 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
 // (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
 static void default_sr_tiling(sten_stencil *st, int prec) {
   SrTiling &t = st->srt[prec];
+  // measured at 600x595x1536: mixed 16-row tiles, 160-plane
+  // chunks + 64-plane tail chunks; fp32 uniform 64-plane chunks (73.7 vs 70.2);
+  // the constant-coefficient mixed sweep 8-row tiles with 3 input stages (192.7 vs 186.5)
   int by = 16, stg = 2, cst = 2, zc = 160, zct = 64, tail = 320, pack = 16;
+  if (prec == STEN_FP32) {
+    zc = 64;
+    tail = 0;
+  } else if (st->cc) {
+    by = 8;
+    stg = 3;
+  }
   if (const char *e = getenv("STEN_SR_TILING"))
     sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail, &pack);
   t.pack = pack;

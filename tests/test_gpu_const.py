@@ -72,6 +72,7 @@ def test_const_solve_equals_general_kernel(sten, prec):
     for name in ("const", "general"):
         st = (sten.stencil_create_const(nx, ny, nz, POISSON) if name == "const" else gpu_stencil(diag, offs))
         sten.set_schedule(st, sten.SCHED_SR)
+        sten.set_sr_tiling(st, PREC[prec], 16, 2, 2)  # the same geometry (and dot order) on both handles
         bt = to_gpu_vec(b, prec)
         xt = torch.empty_like(bt)
         it, hist, status = sten.bicgstab_solve(st, PREC[prec], bt, None, 0.0, 30, xt)
