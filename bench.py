@@ -244,6 +244,8 @@ def run_sten(args):
         sten.set_tiling(st, prec, bx, by, zc, stg)
     sr = args.schedule == "sr"
     sten.set_schedule(st, sten.SCHED_SR if sr else sten.SCHED_CLASSIC)
+    if sr and world > 1 and os.environ.get("STEN_P2P", "0") == "1":
+        sten.p2p_setup(st, prec)  # fused peer-memory halos + all-reduce across ranks (opt-in)
     if args.sr_tiling:
         sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
     b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)

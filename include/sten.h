@@ -236,6 +236,36 @@ int sten_set_schedule(sten_stencil *st, int schedule);
 int sten_sr_sweep(sten_stencil *st, int precision, double alpha, double omega, double beta, const void *rh,
                   void *x, void *r, void *p, void *v, void *q, void *y, float *dots, void *cuda_stream);
 
+/* How a decomposed SR sweep exchanges its halos and sums:
+ *   STEN_XCHG_SERIAL : exchange (device copies / NCCL send-recv), then the sweep,
+ *                      then the all-reduce of the slab sums;
+ *   STEN_XCHG_OVERLAP: the exchange and the chunks that read halo planes on a side
+ *                      stream, concurrent with the interior chunks;
+ *   STEN_XCHG_FUSED  : ONE kernel per slab does the sweep, stores its boundary
+ *                      planes straight into the z-neighbours' halo buffers (peer
+ *                      memory) and deposits its sums in every participant's inbox
+ *                      (one-shot all-reduce, flags with system-scope release /
+ *                      acquire); a 1-thread kernel waits (bounded: ~20 s, then
+ *                      STEN_NONFINITE) and runs the scalar step.  Loopback slabs and
+ *                      1-rank communicators use it directly; across ranks it needs
+ *                      sten_p2p_import (else the handle falls back to OVERLAP).
+ * Default: FUSED (STEN_SR_P2P=0 in the environment selects OVERLAP).  SERIAL and
+ * FUSED add the slab sums in the same order: their results are bitwise equal. */
+/* Peer memory across ranks (one node, NVLink/NVSwitch): export writes CUDA IPC
+ * handles of this rank's boundary-slab SR buffers and its inbox for `precision`
+ * (out == NULL: *bytes = the record size); every rank passes all ranks'
+ * records, in rank order, to import, which opens the z-neighbours' buffers and
+ * the other inboxes and selects STEN_XCHG_FUSED across ranks.  All ranks must
+ * import before the next solve.  Errors: STEN_EINVAL, STEN_EUNSUPPORTED (> 8
+ * ranks), STEN_ECUDA (IPC). */
+int sten_p2p_export(sten_stencil *st, int precision, void *out, size_t *bytes);
+int sten_p2p_import(sten_stencil *st, int precision, const void *all, size_t bytes_per_rank);
+
+#define STEN_XCHG_SERIAL 0
+#define STEN_XCHG_OVERLAP 1
+#define STEN_XCHG_FUSED 2
+int sten_set_sr_exchange(sten_stencil *st, int mode);
+
 /* SR kernel geometry for tuning (0 = default): by rows per tile (8 or 16),
  * stages input TMA stages, cstages coefficient stages, zc planes per CTA
  * (uniform chunks), pack bytes per thread vector (16, or 8 = twice the

@@ -22,6 +22,7 @@ FP32 = 0
 MIXED = 1
 SCHED_CLASSIC = 0
 SCHED_SR = 1
+XCHG_SERIAL, XCHG_OVERLAP, XCHG_FUSED = 0, 1, 2
 DT_F64 = 0
 DT_F32 = 1
 
@@ -77,6 +78,9 @@ def lib():
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
         L.sten_set_schedule.argtypes = [P, I]
         L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I, I]
+        L.sten_set_sr_exchange.argtypes = [P, I]
+        L.sten_p2p_export.argtypes = [P, I, P, ctypes.POINTER(ctypes.c_size_t)]
+        L.sten_p2p_import.argtypes = [P, I, P, ctypes.c_size_t]
         L.sten_sr_sweep.argtypes = [P, I, D, D, D, P, P, P, P, P, P, P, P, P]
         L.bicgstab_refine.argtypes = [P, P, P, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(I), P,
                                       ctypes.POINTER(I), P]
@@ -281,6 +285,11 @@ def set_schedule(st: Stencil, schedule: int):
     _check(lib().sten_set_schedule(st.handle, int(schedule)))
 
 
+def set_sr_exchange(st: Stencil, mode: int):
+    """XCHG_SERIAL / XCHG_OVERLAP / XCHG_FUSED (peer-memory halo stores + one-shot all-reduce)."""
+    _check(lib().sten_set_sr_exchange(st.handle, int(mode)))
+
+
 def set_sr_tiling(st: Stencil, precision: int, by: int = 0, stages: int = 0, cstages: int = 0, zc: int = 0,
                   pack: int = 0):
     _check(lib().sten_set_sr_tiling(st.handle, precision, by, stages, cstages, zc, pack))
@@ -357,3 +366,31 @@ def stencil2d_apply(st: Stencil2D, precision: int, x, y, stream=None):
     ms = ctypes.c_double(0.0)
     _check(lib().stencil2d_last_ms(st.handle, ctypes.byref(ms)))
     return ms.value
+
+
+def p2p_export(st: Stencil, precision: int) -> bytes:
+    n = ctypes.c_size_t(0)
+    _check(lib().sten_p2p_export(st.handle, precision, None, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib().sten_p2p_export(st.handle, precision, buf, ctypes.byref(n)))
+    return buf.raw[: n.value]
+
+
+def p2p_import(st: Stencil, precision: int, records):
+    """records: every rank's p2p_export() bytes, in rank order."""
+    size = len(records[0])
+    if any(len(r) != size for r in records):
+        raise StenError("p2p records differ in size")
+    blob = b"".join(records)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(lib().sten_p2p_import(st.handle, precision, buf, size))
+
+
+def p2p_setup(st: Stencil, precision: int):
+    """Exchange the IPC records over the default torch.distributed group and import them
+    (selects the fused peer-memory halo + all-reduce path across ranks)."""
+    import torch.distributed as dist
+    mine = p2p_export(st, precision)
+    allrec = [None] * dist.get_world_size()
+    dist.all_gather_object(allrec, mine)
+    p2p_import(st, precision, allrec)

@@ -222,6 +222,15 @@ struct sten_stencil {
   float *ir_sigma = nullptr;
   int sr_l2pf = 0;              // SR: L2 prefetch distance (tuning knob STEN_SR_L2PF)
   bool sr_overlap = true;       // SR, decomposed: halo exchange overlapped with the interior chunks
+  bool sr_p2p = true;           // SR, decomposed: fused halo stores + peer-memory all-reduce (STEN_SR_P2P)
+  bool p2p_ranks = false;       // ... across ranks too (after sten_p2p_import: CUDA IPC peers)
+  float *p2p_sums = nullptr;    // own inbox: [slots][kMaxDots]
+  unsigned *p2p_flags = nullptr;  // [slots]
+  unsigned *p2p_seq = nullptr;  // sweeps finalised so far (persistent sequence number)
+  int p2p_slots = 0;
+  std::vector<P2PBox> p2p_remote;           // other ranks' inboxes (IPC)
+  void *p2p_lo[2][2][5] = {}, *p2p_hi[2][2][5] = {};  // [prec][set][vec]: the z-neighbour ranks' buffers (IPC)
+  std::vector<void *> ipc_opened;
   cudaStream_t side = nullptr;  // capture side stream (exchange + boundary chunks)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   float *partials2 = nullptr;   // reduction scratch of the concurrent interior launch
@@ -679,10 +688,16 @@ static char *sr_interior(void *base, const sten_stencil *st, int prec) {
 // needed) or SR_BOUNDARY (the rest).  capture: deposit the raw sums in
 // slab_sums (slot 2*slab + (part == SR_INTERIOR)) instead of finalising.
 enum { SR_ALL = 0, SR_INTERIOR = 1, SR_BOUNDARY = 2 };
+// fused (peer-memory) halo + all-reduce path for decomposed SR sweeps
+static bool sr_fused(const sten_stencil *st) {
+  if (!decomposed(st) || !st->sr_p2p) return false;
+  return !st->comm || st->comm->nranks == 1 || st->p2p_ranks;
+}
 static void sr_chunk_z(const SrTiling &t, int nbig, int zct, int c, int *z0) {
   *z0 = c < nbig ? c * t.zc : nbig * t.zc + (c - nbig) * zct;
 }
-static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture, cudaStream_t s, int part = SR_ALL) {
+static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture, cudaStream_t s, int part = SR_ALL,
+                     bool fused = false) {
   Slab &sl = st->slabs[slab];
   SrBufs &b = sl.sr[prec];
   const SrTiling &t = st->srt[prec];
@@ -729,6 +744,31 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     }
   }
   a.l2pf = st->sr_l2pf;
+  if (fused) {
+    // halo planes straight into the z-neighbours' next-set buffers ...
+    const size_t pb = (size_t)st->plane * esize(prec);
+    const int ns = (int)st->slabs.size();
+    for (int i = 0; i < 5; ++i) {
+      void *lo = nullptr, *hi = nullptr;
+      if (slab > 0) {
+        Slab &n = st->slabs[slab - 1];
+        lo = (char *)n.sr[prec].vec[set ^ 1][i] + (size_t)(n.nz + kSrHalo) * pb;
+      } else if (st->p2p_lo[prec][set ^ 1][i]) {
+        lo = (char *)st->p2p_lo[prec][set ^ 1][i] + (size_t)(sl.nz + kSrHalo) * pb;  // equal slabs on every rank
+      }
+      if (slab + 1 < ns) hi = st->slabs[slab + 1].sr[prec].vec[set ^ 1][i];
+      else if (st->p2p_hi[prec][set ^ 1][i]) hi = st->p2p_hi[prec][set ^ 1][i];
+      a.peer_lo[i] = lo;
+      a.peer_hi[i] = hi;
+    }
+    // ... and the sums into every participant's inbox, slot = global slab index
+    a.red.slab_out = nullptr;
+    a.red.p2p_slot = (st->comm ? st->comm->rank : 0) * ns + slab;
+    a.red.p2p_seq = st->p2p_seq;
+    a.red.p2p[0] = P2PBox{st->p2p_sums, st->p2p_flags};
+    a.red.p2p_n = 1;
+    for (const P2PBox &b2 : st->p2p_remote) a.red.p2p[a.red.p2p_n++] = b2;
+  }
   if (st->cc) {  // the same roundings as k_create_coeffs: fp64 quotient, RN to fp32 / fp16
     for (int d = 0; d < 6; ++d) {
       a.cf32[d] = (float)st->cscaled[d];
@@ -784,7 +824,14 @@ static int sr_exchange(sten_stencil *st, int prec, int set, cudaStream_t s) {
 static int enqueue_sr_sweep(sten_stencil *st, int prec, int set, cudaStream_t s, cudaEvent_t *evs) {
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
   const int ns = (int)st->slabs.size();
-  if (decomposed(st) && st->sr_overlap) {
+  if (sr_fused(st)) {
+    // one kernel per slab does the sweep, its halo exchange (stores into the
+    // neighbours' buffers) and its share of the all-reduce (inbox deposits);
+    // a 1-thread kernel waits for every slot and runs the scalar step
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, set, false, s, SR_ALL, true));
+    KLAUNCH(p2p_fin_launch(P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
+    st->launches++;
+  } else if (decomposed(st) && st->sr_overlap) {
     // the halo exchange and the chunks that read halo planes on a side
     // stream, concurrent with the interior chunks (north_star: halos
     // "overlapped with interior compute"); both deposit slab sums
@@ -1084,6 +1131,7 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
   if (const char *pf = getenv("STEN_SR_L2PF")) st->sr_l2pf = atoi(pf);
   if (const char *ov = getenv("STEN_SR_OVERLAP")) st->sr_overlap = atoi(ov) != 0;
+  if (const char *pp = getenv("STEN_SR_P2P")) st->sr_p2p = atoi(pp) != 0;
   if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
   st->slabs.resize(nslabs);
   auto fail = [&](int rc) {
@@ -1162,6 +1210,14 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
       cudaMalloc(&st->counter2, sizeof(unsigned)) != cudaSuccess ||
       cudaMalloc(&st->red_total, sizeof(float) * kMaxDots) != cudaSuccess)
     return fail(set_err(STEN_ENOMEM, "state allocation failed"));
+  st->p2p_slots = nslabs * (comm ? comm->nranks : 1);
+  if (cudaMalloc(&st->p2p_sums, sizeof(float) * kMaxDots * st->p2p_slots) != cudaSuccess ||
+      cudaMalloc(&st->p2p_flags, sizeof(unsigned) * st->p2p_slots) != cudaSuccess ||
+      cudaMalloc(&st->p2p_seq, sizeof(unsigned)) != cudaSuccess)
+    return fail(set_err(STEN_ENOMEM, "inbox allocation failed"));
+  cudaMemset(st->p2p_sums, 0, sizeof(float) * kMaxDots * st->p2p_slots);
+  cudaMemset(st->p2p_flags, 0, sizeof(unsigned) * st->p2p_slots);
+  cudaMemset(st->p2p_seq, 0, sizeof(unsigned));
   cudaMemset(st->counter, 0, sizeof(unsigned));
   cudaMemset(st->counter2, 0, sizeof(unsigned));
   cudaMemset(st->st, 0, sizeof(DevState));
@@ -1214,6 +1270,10 @@ void stencil_destroy(sten_stencil *st) {
   if (st->st_host) cudaFreeHost(st->st_host);
   cudaFree(st->partials);
   cudaFree(st->partials2);
+  for (void *p : st->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(st->p2p_sums);
+  cudaFree(st->p2p_flags);
+  cudaFree(st->p2p_seq);
   cudaFree(st->counter);
   cudaFree(st->counter2);
   if (st->side) cudaStreamDestroy(st->side);
@@ -1359,6 +1419,9 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   for (int k = 0; k < (int)st->slabs.size(); ++k)
     RC_TRY(sr ? launch_init_sr(st, prec, k, with_x0, s, scale_rhs) : launch_init(st, prec, k, with_x0, s, scale_rhs));
   RC_TRY(reduce_scalars(st, PH_INIT, s));
+  // fused SR: every sweep writes the halos of the set the next one reads; the
+  // first sweep's (set 0, from the init) are exchanged here once
+  if (sr && sr_fused(st)) RC_TRY(sr_exchange(st, prec, 0, s));
   // iterations: CUDA graphs of `chunk` iterations (even, so the ping-pong
   // parity of p/v is the same at every replay)
   const int nsteps = sr ? maxit + 1 : maxit;  // SR: sweep i computes x_i, r_i (i = 0..maxit)
@@ -1613,6 +1676,75 @@ int sten_set_schedule(sten_stencil *st, int schedule) {
   if (schedule != STEN_SCHED_CLASSIC && schedule != STEN_SCHED_SR)
     return set_err(STEN_EINVAL, "unknown schedule %d", schedule);
   st->schedule = schedule;
+  return STEN_OK;
+}
+
+// ------------------------------------------- peer memory across ranks --
+// export: IPC handles of this rank's bottom-slab and top-slab SR buffers
+// (2 sets x 5 vectors each) and of its inbox (sums, flags)
+constexpr int kIpcN = 22;
+int sten_p2p_export(sten_stencil *st, int prec, void *out, size_t *bytes) {
+  if (!st || !bytes) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  const size_t need = sizeof(cudaIpcMemHandle_t) * kIpcN;
+  if (!out) {
+    *bytes = need;
+    return STEN_OK;
+  }
+  if (*bytes < need) return set_err(STEN_EINVAL, "export buffer of %zu bytes, need %zu", *bytes, need);
+  RC_TRY(ensure_bufs(st, prec));
+  RC_TRY(ensure_sr(st, prec));
+  cudaIpcMemHandle_t *h = (cudaIpcMemHandle_t *)out;
+  int n = 0;
+  for (Slab *sl : {&st->slabs.front(), &st->slabs.back()})
+    for (int set = 0; set < 2; ++set)
+      for (int i = 0; i < 5; ++i) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->sr[prec].vec[set][i]));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[n++], st->p2p_sums));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[n++], st->p2p_flags));
+  *bytes = need;
+  return STEN_OK;
+}
+
+// import: every rank's export in rank order (nranks x bytes_per_rank); opens the
+// z-neighbours' buffers and the other ranks' inboxes, then selects the fused
+// exchange across ranks
+int sten_p2p_import(sten_stencil *st, int prec, const void *all, size_t bytes_per_rank) {
+  if (!st || !all) return set_err(STEN_EINVAL, "NULL argument");
+  if (!st->comm || st->comm->nranks < 2) return set_err(STEN_EINVAL, "p2p import needs a multi-rank communicator");
+  if (bytes_per_rank < sizeof(cudaIpcMemHandle_t) * kIpcN) return set_err(STEN_EINVAL, "short export record");
+  const int R = st->comm->nranks, me = st->comm->rank;
+  if (R > kMaxPeers) return set_err(STEN_EUNSUPPORTED, "at most %d ranks in the peer-memory all-reduce", kMaxPeers);
+  auto rec = [&](int r) { return (const cudaIpcMemHandle_t *)((const char *)all + (size_t)r * bytes_per_rank); };
+  auto open = [&](const cudaIpcMemHandle_t &h, void **p) -> int {
+    cudaError_t e = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_err(STEN_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    st->ipc_opened.push_back(*p);
+    return STEN_OK;
+  };
+  for (int set = 0; set < 2; ++set)
+    for (int i = 0; i < 5; ++i) {
+      if (me > 0) RC_TRY(open(rec(me - 1)[10 + set * 5 + i], &st->p2p_lo[prec][set][i]));   // its top slab
+      if (me + 1 < R) RC_TRY(open(rec(me + 1)[set * 5 + i], &st->p2p_hi[prec][set][i]));  // its bottom slab
+    }
+  st->p2p_remote.clear();
+  for (int r = 0; r < R; ++r) {
+    if (r == me) continue;
+    P2PBox b;
+    RC_TRY(open(rec(r)[20], (void **)&b.sums));
+    RC_TRY(open(rec(r)[21], (void **)&b.flags));
+    st->p2p_remote.push_back(b);
+  }
+  st->p2p_ranks = true;
+  st->sr_p2p = true;
+  drop_graphs(st);
+  return STEN_OK;
+}
+
+int sten_set_sr_exchange(sten_stencil *st, int mode) {
+  if (!st || mode < STEN_XCHG_SERIAL || mode > STEN_XCHG_FUSED) return set_err(STEN_EINVAL, "bad exchange mode");
+  st->sr_p2p = mode == STEN_XCHG_FUSED;
+  st->sr_overlap = mode == STEN_XCHG_OVERLAP;
+  drop_graphs(st);
   return STEN_OK;
 }
 

@@ -199,6 +199,42 @@ __global__ void k_slabsum(const float *__restrict__ slab_sums, int nslabs, float
   for (int d = 0; d < kMaxDots; ++d) out[d] = s[d];
 }
 
+// SR scalar step after a peer-memory all-reduce: wait (bounded) until every
+// slot of this participant's inbox holds the current sweep's sums, add them in
+// slot order (deterministic, identical on every rank), finalise.
+__global__ void k_p2p_fin(P2PBox inbox, int nslots, unsigned *seqp, DevState *st) {
+  if (sr_idle(st)) return;
+  const unsigned seq = *seqp + 1u;
+  const long long t0 = clock64();
+  bool timeout = false;
+  for (int k = 0; k < nslots && !timeout; ++k) {
+    unsigned f;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(inbox.flags + k) : "memory");
+      if (f == seq) break;
+      __nanosleep(200);
+      if (clock64() - t0 > 40000000000ll) timeout = true;  // ~20 s: a peer never arrived
+    } while (!timeout);
+  }
+  float s[kMaxDots];
+  for (int d = 0; d < kMaxDots; ++d) s[d] = 0.0f;
+  for (int k = 0; k < nslots; ++k)
+    for (int d = 0; d < kMaxDots; ++d) s[d] += __ldcv(&inbox.sums[k * kMaxDots + d]);
+  if (timeout) {  // never hang the device: report and stop the solve
+    st_event(st, STEN_NONFINITE, st->sweep, false);
+    st->stop = 1;
+    st->status = STEN_NONFINITE;
+    return;
+  }
+  *seqp = seq;
+  fin_sr(st, s);
+}
+
+int p2p_fin_launch(P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s) {
+  k_p2p_fin<<<1, 1, 0, s>>>(inbox, nslots, seq, st);
+  return (int)cudaGetLastError();
+}
+
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s) {
   k_scalars<<<1, 1, 0, s>>>(phase, slab_sums, nslabs, st);
   return (int)cudaGetLastError();

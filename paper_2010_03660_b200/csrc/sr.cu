@@ -440,6 +440,18 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
                     reinterpret_cast<T *>(a.out[3]), reinterpret_cast<T *>(a.out[4])};
   // own x / r_hat arrive by plain 16-B loads three planes ahead of their use
   // (x at the step that forms its plane, r_hat at the dots of its plane)
+  // fused halo exchange: planes 0, 1 / nz-2, nz-1 of the outputs also to the
+  // z-neighbours' halo planes (peer memory)
+  T *const PL[5] = {reinterpret_cast<T *>(a.peer_lo[0]), reinterpret_cast<T *>(a.peer_lo[1]),
+                    reinterpret_cast<T *>(a.peer_lo[2]), reinterpret_cast<T *>(a.peer_lo[3]),
+                    reinterpret_cast<T *>(a.peer_lo[4])};
+  T *const PH[5] = {reinterpret_cast<T *>(a.peer_hi[0]), reinterpret_cast<T *>(a.peer_hi[1]),
+                    reinterpret_cast<T *>(a.peer_hi[2]), reinterpret_cast<T *>(a.peer_hi[3]),
+                    reinterpret_cast<T *>(a.peer_hi[4])};
+  auto halo_st = [&](int i, int m, const P &val) {
+    if (m < 2 && PL[i]) val.st(PL[i] + (long long)m * plane + gofs);
+    if (m >= nzl - 2 && PH[i]) val.st(PH[i] + (long long)(m - (nzl - 2)) * plane + gofs);
+  };
   // (measured: unconditional loads from clamped addresses with branch-free
   // dots ran 14% slower than these predicated loads)
   auto ld_x = [&](int m) {
@@ -498,6 +510,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
         P::fmas(om_s, s, P::fmas(al_s, p, xv)).st(Xg + o);
         rn.st(Og[0] + o);
         pn.st(Og[1] + o);
+        halo_st(0, m, rn);
+        halo_st(1, m, pn);
       }
       if (!STEN_SR_XTMA) xq[J % 3] = ld_x(m + 3);
       if (hf >= 0) {
@@ -538,7 +552,10 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       if (CC) vn = (orow && zin) ? SCn::keep(vn, olo, ohi) : P::zero();
       vn.st(vr + ec);
       vw[J % 3] = vn;
-      if (inside && k + 1 >= z0 && k + 1 < z1) vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
+      if (inside && k + 1 >= z0 && k + 1 < z1) {
+        vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
+        halo_st(2, k + 1, vn);
+      }
       if (hv >= 0) {
         const int hp = hv + HW;  // same point in the input-box layout
         P c[6];
@@ -578,6 +595,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
         const long long o = (long long)k * plane + gofs;
         qn.st(Og[3] + o);
         yn.st(Og[4] + o);
+        halo_st(3, k, qn);
+        halo_st(4, k, yn);
         dacc[0] = rh.mdot(vc, dacc[0]);    // (rh, v)
         dacc[1] = rh.mdot(rc, dacc[1]);    // (rh, r)
         dacc[2] = rh.mdot(qn, dacc[2]);    // (rh, q)

@@ -39,12 +39,27 @@ enum Phase { PH_INIT = 0, PH_H1 = 1, PH_H2 = 2, PH_H3 = 3, PH_SR = 4 };
 enum Mode { MODE_APPLY = 0, MODE_H1 = 1, MODE_H2 = 2 };
 constexpr int kMaxDots = 12;  // SR sweep: 12 inner products (classic phases use 1-3)
 
+// One participant's inbox of the peer-memory all-reduce (SR):
+// sums[slot][kMaxDots] and flags[slot] (= the sequence number of the sweep
+// whose sums landed in that slot).
+constexpr int kMaxPeers = 8;
+struct P2PBox {
+  float *sums;
+  unsigned *flags;
+};
+
 // Grid reduction plumbing of one kernel launch.
 struct Reduce {
   float *partials;      // [gridDim.x * kMaxDots]
   unsigned *counter;    // zero between launches (reset by the last CTA)
   float *slab_out;      // decomposed solve: write the slab's sums here ...
   DevState *st;         // ... else finalize the scalars directly
+  // peer-memory all-reduce (p2p_n > 0): the last CTA writes its sums into
+  // slot p2p_slot of every inbox, then the flag (*p2p_seq + 1), after a
+  // system-scope fence that also publishes the kernel's remote halo stores
+  int p2p_n, p2p_slot;
+  const unsigned *p2p_seq;
+  P2PBox p2p[kMaxPeers];
 };
 
 // Geometry of one z-slab in the internal layout: planes 0 and nz+1 are the
@@ -435,6 +450,10 @@ template <int ND, int PH>
 __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduce &red, float *scratch) {
   block_sum<ND>(v, scratch);
   __shared__ int am_last;
+  if (red.p2p_n > 0) {
+    __syncthreads();
+    __threadfence_system();  // this CTA's stores to peer memory (halo planes) are visible before its ticket
+  }
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int d = 0; d < ND; ++d) red.partials[blockIdx.x * kMaxDots + d] = v[d];
@@ -454,7 +473,15 @@ __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduc
   block_sum<ND>(s, scratch);
   if (threadIdx.x == 0) {
     *red.counter = 0u;
-    if (red.slab_out) {
+    if (red.p2p_n > 0) {  // one-shot all-reduce through peer memory: deposit, fence, flag
+      const unsigned seq = *red.p2p_seq + 1u;
+      for (int r = 0; r < red.p2p_n; ++r)
+#pragma unroll
+        for (int d = 0; d < ND; ++d) red.p2p[r].sums[red.p2p_slot * kMaxDots + d] = s[d];
+      __threadfence_system();
+      for (int r = 0; r < red.p2p_n; ++r)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(red.p2p[r].flags + red.p2p_slot), "r"(seq) : "memory");
+    } else if (red.slab_out) {
 #pragma unroll
       for (int d = 0; d < ND; ++d) red.slab_out[d] = s[d];
     } else {
@@ -485,6 +512,7 @@ template <typename T> int rows_threads(int nx, int by);
 template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);
+int p2p_fin_launch(P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s);
 int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s);
 // Iterative refinement (bicgstab_refine, R21): fp32 outer steps
 // around the mixed inner solve.  All pointers at interior plane 0.
@@ -526,6 +554,11 @@ struct alignas(64) SrArgs {
   unsigned short cf16[6];
   int has_below, has_above;
   int l2pf;               // input planes prefetched into L2 beyond the TMA stages (0: off)
+  // fused halo exchange (peer memory): this sweep's planes 0, 1 also go to the
+  // lower z-neighbour's top halo planes, planes nz-2, nz-1 to the upper one's
+  // bottom halo planes (null: no neighbour or not fused).  Base = the
+  // neighbour buffer's element of OUR plane 0 (resp. nz-2), same pitch/plane.
+  void *peer_lo[5], *peer_hi[5];
   Reduce red;
 };
 bool sr_config_ok(int by, int stages, int cstages, int pack);

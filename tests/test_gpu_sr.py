@@ -276,6 +276,7 @@ def test_sr_overlapped_halo_exchange(sten, prec):
     _, it1, h1, _ = _solve(sten, st1, prec, b, 0.0, 12)
     for ns in (2, 3):
         stn = gpu_stencil(diag, offs, nslabs=ns)
+        sten.set_sr_exchange(stn, sten.XCHG_OVERLAP)
         sten.set_sr_tiling(stn, PREC[prec], 16, 2, 2, 4)  # 4-plane chunks: interior chunks exist
         _, itn, hn, _ = _solve(sten, stn, prec, b, 0.0, 12)
         assert itn == it1 == 12
@@ -285,3 +286,36 @@ def test_sr_overlapped_halo_exchange(sten, prec):
         assert np.all(np.abs(hn - h1) <= tol_all * h1)
         stn.close()
     st1.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("ns", [2, 4])
+def test_sr_fused_peer_exchange_equals_serial(sten, prec, ns):
+    """The fused path (one kernel per slab: sweep + halo stores into the neighbour
+    slabs' buffers + inbox deposits, then the flag-waiting scalar step) adds the
+    slab sums in the serial path's order: the whole solve is bitwise identical."""
+    nx, ny, nz = 45, 23, 32
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=12)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=12), prec)
+    out = {}
+    for mode in (sten.XCHG_SERIAL, sten.XCHG_FUSED):
+        st = gpu_stencil(diag, offs, nslabs=ns)
+        sten.set_sr_exchange(st, mode)
+        sten.set_sr_tiling(st, PREC[prec], 16, 2, 2, 4)
+        x, it, h, status = _solve(sten, st, prec, b, 0.0, 15)
+        out[mode] = (x, h)
+        x2, it2, h2, _ = _solve(sten, st, prec, b, 0.0, 15)  # a second solve: persistent flag sequence
+        assert np.array_equal(x2, x) and np.array_equal(h2, h)
+        st.close()
+    assert np.array_equal(out[0][0], out[2][0]) and np.array_equal(out[0][1], out[2][1])
+
+
+def test_p2p_export_and_import_guards(sten):
+    nx, ny, nz = 20, 10, 8
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=3)
+    st = gpu_stencil(diag, offs, nslabs=2)
+    rec = sten.p2p_export(st, PREC["mixed"])
+    assert len(rec) == 22 * 64  # 2 boundary slabs x 2 sets x 5 vectors + inbox sums, flags
+    with pytest.raises(sten.StenError):  # needs a multi-rank communicator
+        sten.p2p_import(st, PREC["mixed"], [rec, rec])
+    st.close()
