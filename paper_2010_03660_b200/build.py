@@ -32,16 +32,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "sten.h")]
     if not force and not _stale(LIB, deps):
         return LIB
-    objs = []
+    # all translation units at once, ptxas split over the cores (many kernel instances)
+    procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        cmd = [NVCC] + ARCH + FLAGS + ["--split-compile=0", "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs = []
+    for src, obj, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
-            sys.stderr.write(r.stderr)
+            sys.stderr.write(err)
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"]

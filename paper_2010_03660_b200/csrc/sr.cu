@@ -309,7 +309,7 @@ __device__ __forceinline__ P spmv(const P (&c)[6], const P &m, const P &xl, cons
 
 }  // namespace
 
-template <typename T, int BY, int S, int SC, bool CC, int NB>
+template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU>
 __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_constant__ SrArgs a) {
   using P = SPack<T, NB>;
   using G = SrGeo<T, BY, NB>;
@@ -449,8 +449,10 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
                     reinterpret_cast<T *>(a.peer_hi[2]), reinterpret_cast<T *>(a.peer_hi[3]),
                     reinterpret_cast<T *>(a.peer_hi[4])};
   auto halo_st = [&](int i, int m, const P &val) {
-    if (m < 2 && PL[i]) val.st(PL[i] + (long long)m * plane + gofs);
-    if (m >= nzl - 2 && PH[i]) val.st(PH[i] + (long long)(m - (nzl - 2)) * plane + gofs);
+    if (FU) {  // a compile-time switch: the checks cost 4.7% in the single-GPU sweep
+      if (m < 2 && PL[i]) val.st(PL[i] + (long long)m * plane + gofs);
+      if (m >= nzl - 2 && PH[i]) val.st(PH[i] + (long long)(m - (nzl - 2)) * plane + gofs);
+    }
   };
   // (measured: unconditional loads from clamped addresses with branch-free
   // dots ran 14% slower than these predicated loads)
@@ -626,20 +628,20 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int BY, int S, int SC, bool CC, int NB>
+template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU>
 int launch_sr_one(const SrArgs &a, cudaStream_t s) {
   constexpr size_t smem = sr_smem_c<T, BY, S, SC, CC, NB>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC, CC, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC, CC, NB, FU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * a.nch;
   if (grid == 0) return (int)cudaSuccess;
-  k_sr<T, BY, S, SC, CC, NB><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
+  k_sr<T, BY, S, SC, CC, NB, FU><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 }  // namespace
@@ -657,9 +659,13 @@ bool sr_config_ok(int by, int stages, int cstages, int pack) {
 
 template <typename T>
 int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, cudaStream_t s) {
-#define X(B, S_, C_, N_)                                                  \
-  if (by == B && stages == S_ && cstages == C_ && pack == N_)             \
-    return cc ? launch_sr_one<T, B, S_, C_, true, N_>(a, s) : launch_sr_one<T, B, S_, C_, false, N_>(a, s);
+  const bool fu = a.peer_lo[0] || a.peer_hi[0];
+#define X(B, S_, C_, N_)                                                                              \
+  if (by == B && stages == S_ && cstages == C_ && pack == N_) {                                       \
+    if (fu) return cc ? launch_sr_one<T, B, S_, C_, true, N_, true>(a, s)                             \
+                      : launch_sr_one<T, B, S_, C_, false, N_, true>(a, s);                           \
+    return cc ? launch_sr_one<T, B, S_, C_, true, N_, false>(a, s) : launch_sr_one<T, B, S_, C_, false, N_, false>(a, s); \
+  }
   STEN_SR_CONFIGS(X)
 #undef X
   return (int)cudaErrorInvalidValue;
