@@ -182,9 +182,10 @@ int bicgstab_solve(sten_stencil *st, int precision, const void *b, const void *x
  *   for k = 0, 1, ...:
  *     r = b_hat - A_hat x in fp32 (fp32 coefficients, the FMA-chain SpMV of R10);
  *     res_hist[k] = ||r||_2 / ||b_hat||_2 (fp32 sums);
- *     stop: res <= tol -> STEN_CONVERGED; res not below the previous step's ->
- *           STEN_BREAKDOWN (stagnation); k == outer_maxit -> STEN_MAXIT;
- *           non-finite -> STEN_NONFINITE;
+ *     stop: res <= tol -> STEN_CONVERGED; three consecutive steps without
+ *           a 1% gain on the best residual so far -> STEN_BREAKDOWN
+ *           (stagnation); k == outer_maxit -> STEN_MAXIT; non-finite ->
+ *           STEN_NONFINITE;
  *     sigma = 2^e, the power of two with max|r| <= sigma; r16 = rn16(r / sigma);
  *     d = the mixed-precision solve of A_hat d = r16 (the handle's schedule,
  *         relative tolerance inner_tol, at most inner_maxit iterations, x0 = 0);

@@ -330,7 +330,7 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
     x = np.zeros_like(b) if x0 is None else np.asarray(x0, np.float32).copy()
     if nb == 0.0:
         return dict(x=np.zeros_like(b), hist=np.array([0.0]), outer=0, inner=0, status=ORC_CONVERGED)
-    hist, inner, status, prev = [], 0, ORC_MAXIT, None
+    hist, inner, status, best, stale = [], 0, ORC_MAXIT, None, 0
     for k in range(outer_maxit + 1):
         r = b - apply32_fma(c32, x)                      # fp32: one rounding per element
         res = float(np.sqrt(np.sum(r.astype(np.float64) ** 2))) / nb
@@ -341,12 +341,16 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         if res <= tol:
             status = ORC_CONVERGED
             break
-        if prev is not None and res >= prev:
-            status = ORC_BREAKDOWN                       # stagnation
-            break
+        if best is None or res < 0.99 * best:          # stagnation: 3 steps without a 1% gain
+            best = res if best is None else min(best, res)
+            stale = 0
+        else:
+            stale += 1
+            if stale >= 3:
+                status = ORC_BREAKDOWN
+                break
         if k == outer_maxit:
             break
-        prev = res
         sigma = 2.0 ** np.frexp(float(np.max(np.abs(r))))[1]  # power of two >= max|r|
         r16 = f16_from_double(r.astype(np.float64) / sigma)
         d = bicgstab16(c16, r16, tol=inner_tol, maxit=inner_maxit, schedule=schedule)

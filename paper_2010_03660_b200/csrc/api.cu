@@ -1600,8 +1600,8 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
   const double nb = sqrt(bb);
   const bool zero_b = nb == 0.0;  // b = 0: x = 0 is exact, whatever x0 is
   if (x0 && !zero_b) RC_TRY(copy_in(st, F, sel_s, x0, s));
-  int k = 0, inner = 0, stat = STEN_MAXIT;
-  double prev = 0.0;
+  int k = 0, inner = 0, stat = STEN_MAXIT, stale = 0;
+  double best = 0.0;
   for (;; ++k) {
     if (zero_b) {
       res_hist[0] = 0.0;
@@ -1614,9 +1614,15 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
     res_hist[k] = res;
     if (!std::isfinite(res)) { stat = STEN_NONFINITE; break; }
     if (res <= tol) { stat = STEN_CONVERGED; break; }
-    if (k > 0 && res >= prev) { stat = STEN_BREAKDOWN; break; }  // stagnation (R21)
+    // stagnation (R21): three consecutive steps without a 1% gain on the best residual
+    if (k == 0 || res < 0.99 * best) {
+      best = (k == 0 || res < best) ? res : best;
+      stale = 0;
+    } else if (++stale >= 3) {
+      stat = STEN_BREAKDOWN;
+      break;
+    }
     if (k == outer_maxit) { stat = STEN_MAXIT; break; }
-    prev = res;
     // inner right-hand side: r / sigma in fp16 (sigma = 2^e >= max|r|)
     for (Slab &sl : st->slabs) {
       IrArgs a;
