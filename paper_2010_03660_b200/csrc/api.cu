@@ -252,6 +252,19 @@ static int rows_thr(int prec, int nx, int by) {
 // 99.9 for the best full-row strip (by 2, 3 stages) - the strips need more
 // CTAs in flight than their shared-memory footprint allows.  Strips remain
 // selectable with sten_set_tiling(bx >= nx).
+// z-chunk length for a small mesh: enough chunks that the grid fills ~2 waves of
+// the SMs (a 32^3 mesh has 2 xy tiles; one chunk each would leave the GPU idle
+// and the z-march latency-bound), never below 4 planes
+static int small_mesh_zc(const sten_stencil *st, int bx, int by, int nzs, int zc, int ctas_per_sm) {
+  const long long tiles = (long long)((st->nx + bx - 1) / bx) * ((st->ny + by - 1) / by);
+  const long long want = 2LL * st->sm * ctas_per_sm;
+  const long long chunks = (want + tiles - 1) / tiles;
+  if (chunks <= 1) return zc;
+  int z = (int)((nzs + chunks - 1) / chunks);
+  if (z < 4) z = 4;
+  return z < zc ? z : zc;
+}
+
 static void default_tiling(sten_stencil *st, int prec) {
   Tiling &t = st->tiling[prec];
   int nzs = st->slabs[0].nz;
@@ -259,6 +272,7 @@ static void default_tiling(sten_stencil *st, int prec) {
   t.rows = 0;
   t.bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   t.by = 16;
+  t.zc = small_mesh_zc(st, t.bx, t.by, nzs, t.zc, 2);
   t.stages = 4;
   t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);
 }
@@ -595,6 +609,12 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
   t.zc = zc < nzs ? zc : nzs;
   t.zc_tail = zct > 0 ? zct : t.zc;
   t.tail = tail > 0 ? tail : 0;
+  const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
+  const int zs = small_mesh_zc(st, bx, t.by, nzs, t.zc, 1);
+  if (zs < t.zc && !getenv("STEN_SR_TILING")) {  // a small mesh: uniform short chunks
+    t.zc = t.zc_tail = zs;
+    t.tail = 0;
+  }
 }
 
 // chunk plan of a slab: nbig chunks of zc planes, then zc_tail-plane chunks to
