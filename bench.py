@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--schedule", default="sr", choices=["sr", "classic"],
                    help="sr: single-reduction sweep (19 passes, DESIGN.md R19); classic: Alg. 1 as printed (29)")
+    p.add_argument("--dots", default="mixed", choices=["mixed", "half"],
+                   help="mixed precision only: inner products as fp16 products summed in fp32 (the paper's "
+                        "instruction), or half: fp16 column pencils (DESIGN.md R22, NEXT-4; SR schedule)")
     p.add_argument("--operator", default="fields", choices=["fields", "poisson-const"],
                    help="fields: the workload's per-point coefficient fields; poisson-const: the constant "
                         "7-point Poisson operator (config 1's) at the same mesh via stencil_create_const "
@@ -248,6 +251,8 @@ def run_sten(args):
         sten.p2p_setup(st, prec)  # fused peer-memory halos + all-reduce across ranks (opt-in)
     if args.sr_tiling:
         sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
+    if args.dots == "half":
+        sten.set_dot_precision(st, sten.DOTS_HALF)
     b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)
     x = torch.empty_like(b)
     maxit = args.maxit
@@ -343,6 +348,7 @@ def run_sten(args):
         "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
         "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
                    "precision": pname, "schedule": args.schedule, "operator": args.operator,
+                   **({"dots": "half"} if args.dots == "half" and prec == sten.MIXED else {}),
                    "maxit": maxit, "tol": tol,
                    "iters_per_solve": iters_done / args.steps,
                    "parallelism": f"zslab{n}",

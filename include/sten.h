@@ -19,9 +19,11 @@
  *   - stencil2d_*: the paper's 2D 9-point SpMV;
  *   - precisions: fp32 throughout, or the paper's mixed mode - fp16 storage
  *     and arithmetic, inner products with fp16 multiply / fp32 accumulate, the
- *     cross-device reduction in fp32.
+ *     cross-device reduction in fp32; optionally
+ *     (sten_set_dot_precision) the unpublished 16-bit mode's fp16 dot
+ *     accumulation (R22).
  * Readings of the paper where it is silent (stopping rule, breakdown, x0, the
- * order of floating-point operations ...) are R1..R21 in DESIGN.md.
+ * order of floating-point operations ...) are R1..R22 in DESIGN.md.
  *
  * Layout.  A mesh (or a rank's slab of it) of nx*ny*nz points is a dense
  * array with linear index P = i + nx*(j + ny*k): x fastest, z slowest, so a
@@ -56,7 +58,7 @@
 extern "C" {
 #endif
 
-#define STEN_VERSION 2
+#define STEN_VERSION 3
 
 /* precision of a solve / apply */
 #define STEN_FP32 0   /* fp32 storage, fp32 arithmetic, fp32 dots */
@@ -222,6 +224,33 @@ int sten_get_stats(sten_stencil *st, sten_stats *out);
  *     halo planes per z-neighbour (exchanged once per iteration).
  * Errors: STEN_EINVAL. */
 int sten_set_schedule(sten_stencil *st, int schedule);
+
+/* Inner-product precision of STEN_MIXED SR sweeps (R22; SURVEY
+ * §8(f) NEXT-4, the "half" mode the paper sized but did not publish,
+ * PAPER.md:427-441 (commented-out performance model: "16-bit mode")):
+ *   STEN_DOTS_MIXED (default): fp16 products summed in fp32 (the paper's
+ *     "mixed 16-bit multiply/32-bit add" instruction);
+ *   STEN_DOTS_HALF: each point's product is added with ONE fp16 FMA into the
+ *     running fp16 sum of its (x, y) column over one z segment (the CS-1 PE's
+ *     core-local dot over its z pencil, in 16-bit); the column-segment sums
+ *     are then added in fp32 (the AllReduce stays 32-bit).
+ *     The segments are the SR chunk plan, listed by sten_sr_segments.
+ * Vector arithmetic and HBM traffic are identical in both modes.  FP32
+ * solves ignore the setting.  Supported with the SR schedule, the
+ * field-coefficient operator, 16-B packs and the SERIAL/OVERLAP exchanges;
+ * otherwise the solve / sweep returns STEN_EUNSUPPORTED.
+ * Errors: STEN_EINVAL. */
+#define STEN_DOTS_MIXED 0
+#define STEN_DOTS_HALF 1
+int sten_set_dot_precision(sten_stencil *st, int dots);
+
+/* The z segments of the SR chunk plan of `precision` on this rank: *n =
+ * their number; z0 (host, room for cap ints, may be NULL to query *n)
+ * receives each segment's first plane, relative to the rank's first plane,
+ * ascending; a segment ends where the next one (or its slab) starts.  The
+ * segments partition every (x, y) column into the pencils of
+ * STEN_DOTS_HALF.  Errors: STEN_EINVAL (cap too small, NULL n). */
+int sten_sr_segments(sten_stencil *st, int precision, int *z0, int cap, int *n);
 
 /* One SR sweep on caller vectors, for parity tests (oracle/osr.c
  * o16_sr_sweep / o32_sr_sweep).  With the scalars (alpha, omega, beta) of

@@ -98,6 +98,11 @@ def _declare(L):
     L.o64_sr_bicgstab.restype = _I
     L.o16_sr_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
     L.o16_sr_bicgstab.restype = _I
+    L.o16h_dot.argtypes = [_I, _I, _I, _P, _P, _I, _P, _P, _P]
+    L.o16h_sr_sweep.argtypes = [_I, _I, _I, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P]
+    L.o16h_sr_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P, _P]
+    L.o16h_sr_bicgstab.restype = _I
 
 
 def _ptr(a: np.ndarray):
@@ -248,7 +253,26 @@ def dot16(a16, b16):
     return float(lib().o16_dot(nx, ny, nz, _ptr(a16), _ptr(b16)))
 
 
-def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False, schedule="classic"):
+def _segments(segments, nz):
+    seg = np.ascontiguousarray(np.asarray(segments, dtype=np.int32))
+    if seg.ndim != 1 or len(seg) == 0 or seg[0] != 0 or np.any(np.diff(seg) <= 0) or seg[-1] >= max(nz, 1):
+        raise ValueError(f"segments must start at 0 and ascend strictly below nz={nz}: {segments}")
+    return seg
+
+
+def dot16h(a16, b16, segments):
+    """Half dot (R22): fp16 pencil per (x, y) column and z segment, exact sum of the
+    segment sums.  Returns (sum, sum of |segment sums|)."""
+    a16 = _c(a16, np.uint16)
+    b16 = _c(b16, np.uint16)
+    nz, ny, nx = a16.shape
+    seg = _segments(segments, nz)
+    sm, ab = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    lib().o16h_dot(nx, ny, nz, _ptr(a16), _ptr(b16), len(seg), _ptr(seg), ctypes.byref(sm), ctypes.byref(ab))
+    return sm.value, ab.value
+
+
+def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False, schedule="classic", segments=None):
     c16 = [_c(a, np.uint16) for a in c16]
     b16 = _c(b16, np.uint16)
     nz, ny, nx = b16.shape
@@ -262,11 +286,15 @@ def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False, schedule="cl
     if schedule == "sr":
         if unfused:
             raise ValueError("the SR schedule has only the fused (GPU-mirroring) variant")
-        it = lib().o16_sr_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
-                                   None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
-                                   _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
-                                   ctypes.byref(st), ctypes.byref(ev))
+        seg = np.zeros(1, np.int32) if segments is None else _segments(segments, nz)
+        it = lib().o16h_sr_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
+                                    None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
+                                    0 if segments is None else len(seg), _ptr(seg),
+                                    _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
+                                    ctypes.byref(st), ctypes.byref(ev))
     else:
+        if segments is not None:
+            raise ValueError("half dots (segments=) are defined for the SR schedule")
         it = lib().o16_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
                                 None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
                                 int(bool(unfused)), _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
@@ -289,16 +317,24 @@ def sr_sweep64(c, scalars, rh, x, r, p, v, q, y):
     return (*vecs, dots)
 
 
-def sr_sweep16(c16, scalars, rh, x, r, p, v, q, y):
-    """One SR sweep, fp16 mirror (uint16 bit patterns; fp32 scalars and dots)."""
+def sr_sweep16(c16, scalars, rh, x, r, p, v, q, y, segments=None):
+    """One SR sweep, fp16 mirror (uint16 bit patterns; fp32 scalars and dots).
+    segments (list of first planes): half dots over those z segments (R22); then
+    the result has a 9th element, the 12 scales (sums of |segment sums|)."""
     c16 = [_c(a, np.uint16) for a in c16]
     vecs = [_c(a, np.uint16).copy() for a in (x, r, p, v, q, y)]
     rh = _c(rh, np.uint16)
     nz, ny, nx = rh.shape
     dots = np.zeros(12, np.float32)
     a, w, b = (float(np.float32(s)) for s in scalars)
-    lib().o16_sr_sweep(nx, ny, nz, _arr6(c16), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], _ptr(dots))
-    return (*vecs, dots)
+    if segments is None:
+        lib().o16_sr_sweep(nx, ny, nz, _arr6(c16), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], _ptr(dots))
+        return (*vecs, dots)
+    seg = _segments(segments, nz)
+    dabs = np.zeros(12, np.float64)
+    lib().o16h_sr_sweep(nx, ny, nz, _arr6(c16), a, w, b, _ptr(rh), *[_ptr(t) for t in vecs], len(seg), _ptr(seg),
+                        _ptr(dots), _ptr(dabs))
+    return (*vecs, dots, dabs)
 
 
 def sr_sweep32(c32, scalars, rh, x, r, p, v, q, y):

@@ -144,6 +144,24 @@ int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
                     uint16_t *x, double *hist, float *alpha, float *omega,
                     int *status, int *event_it);
 
+/* Half dots (R22, NEXT-4): per (x, y) column and z segment
+ * [seg[s], seg[s+1]) an fp16 running sum acc = fma16(a, b, acc) from +0, z
+ * ascending; *sum = the exact (fp64) sum of the segment sums, *abs = the sum
+ * of their magnitudes (may be NULL).  o16h_sr_sweep / o16h_sr_bicgstab: the
+ * O16-SR sweep and solve with those dots rounded once to fp32 (nseg = 0: the
+ * mixed dots of o16_sr_sweep / o16_sr_bicgstab); dabs may be NULL. */
+void o16h_dot(int nx, int ny, int nz, const uint16_t *a, const uint16_t *b, int nseg,
+              const int *seg, double *sum, double *abs);
+void o16h_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alpha,
+                   float omega, float beta, const uint16_t *rh, uint16_t *x,
+                   uint16_t *r, uint16_t *p, uint16_t *v, uint16_t *q, uint16_t *y,
+                   int nseg, const int *seg, float dots[12], double dabs[12]);
+int o16h_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                     const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                     int nseg, const int *seg,
+                     uint16_t *x, double *hist, float *alpha, float *omega,
+                     int *status, int *event_it);
+
 /* ---------------- 2D 9-point SpMV (o2d.c; NEXT-3) ------- */
 /* Mesh nx*ny, P = i + nx*j; c[0..7] couple P to its (dx,dy) neighbour in the
  * order (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1). */

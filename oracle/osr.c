@@ -160,10 +160,57 @@ static int sr_usable16(float s) {
   return isfinite(s) && ((h >> 10) & 31) != 31;
 }
 
-void o16_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alpha,
-                  float omega, float beta, const uint16_t *rh, uint16_t *x,
-                  uint16_t *r, uint16_t *p, uint16_t *v, uint16_t *q, uint16_t *y,
-                  float dots[12]) {
+/* ---- half dots (R22, the "16-bit mode" of
+ * the paper's unpublished performance model) ----
+ * The CS-1 PE forms its core-local part of a dot over its z pencil
+ * (PAPER.md:394); in 16-bit mode that running sum is fp16: one fp16 FMAC per
+ * point, acc = fma16(a, b, acc), z ascending from +0.  The pencil of column
+ * (i, j) is cut into the z segments [seg[s], seg[s+1]) (the last one ends at
+ * nz); the AllReduce stays 32-bit: here the segment sums are
+ * added exactly in fp64 (*sum) -- the GPU adds them in fp32 in its own order,
+ * a difference bounded by the fp32 rounding of that sum, for which *abs (the
+ * sum of |segment sums|) is the scale. */
+void o16h_dot(int nx, int ny, int nz, const uint16_t *a, const uint16_t *b, int nseg,
+              const int *seg, double *sum, double *abs) {
+  double t = 0.0, ta = 0.0;
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i)
+      for (int sgi = 0; sgi < nseg; ++sgi) {
+        const int z0 = seg[sgi], z1 = sgi + 1 < nseg ? seg[sgi + 1] : nz;
+        uint16_t acc = 0; /* +0 */
+        for (int k = z0; k < z1; ++k) {
+          const int64_t P = (int64_t)i + (int64_t)nx * ((int64_t)j + (int64_t)ny * k);
+          acc = o16_fma(a[P], b[P], acc);
+        }
+        const double d = o16_to_double(acc);
+        t += d;
+        ta += fabs(d);
+      }
+  *sum = t;
+  if (abs) *abs = ta;
+}
+
+/* the twelve sums of a sweep: mixed (o16_dot) or, nseg > 0, half pencils
+ * over the segments, rounded once to fp32 (dabs: their scales, may be NULL) */
+static void sr16_dots(int nx, int ny, int nz, const uint16_t *const a[12], const uint16_t *const b[12],
+                      int nseg, const int *seg, float dots[12], double *dabs) {
+  for (int d = 0; d < 12; ++d) {
+    if (nseg > 0) {
+      double sm, ab;
+      o16h_dot(nx, ny, nz, a[d], b[d], nseg, seg, &sm, &ab);
+      dots[d] = (float)sm;
+      if (dabs) dabs[d] = ab;
+    } else {
+      dots[d] = o16_dot(nx, ny, nz, a[d], b[d]);
+      if (dabs) dabs[d] = 0.0;
+    }
+  }
+}
+
+void o16h_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alpha,
+                   float omega, float beta, const uint16_t *rh, uint16_t *x,
+                   uint16_t *r, uint16_t *p, uint16_t *v, uint16_t *q, uint16_t *y,
+                   int nseg, const int *seg, float dots[12], double dabs[12]) {
   int64_t n = (int64_t)nx * ny * nz;
   const uint16_t ah = sr_rn16f(alpha), wh = sr_rn16f(omega), bh = sr_rn16f(beta);
   for (int64_t P = 0; P < n; ++P) {
@@ -176,9 +223,16 @@ void o16_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alph
   o16_apply_fused(nx, ny, nz, c, p, v);
   o16_apply_fused(nx, ny, nz, c, r, q);
   o16_apply_fused(nx, ny, nz, c, v, y);
-  const uint16_t *a[12] = {rh, rh, rh, rh, q, q, y, y, q, q, y, r};
-  const uint16_t *b[12] = {v, r, q, y, r, v, r, v, q, y, y, r};
-  for (int d = 0; d < 12; ++d) dots[d] = o16_dot(nx, ny, nz, a[d], b[d]);
+  const uint16_t *const a[12] = {rh, rh, rh, rh, q, q, y, y, q, q, y, r};
+  const uint16_t *const b[12] = {v, r, q, y, r, v, r, v, q, y, y, r};
+  sr16_dots(nx, ny, nz, a, b, nseg, seg, dots, dabs);
+}
+
+void o16_sr_sweep(int nx, int ny, int nz, const uint16_t *const c[6], float alpha,
+                  float omega, float beta, const uint16_t *rh, uint16_t *x,
+                  uint16_t *r, uint16_t *p, uint16_t *v, uint16_t *q, uint16_t *y,
+                  float dots[12]) {
+  o16h_sr_sweep(nx, ny, nz, c, alpha, omega, beta, rh, x, r, p, v, q, y, 0, NULL, dots, NULL);
 }
 
 /* The fp32 scalar step shared by the two fp32-scalar mirrors below.  Written
@@ -197,10 +251,13 @@ static float sr_omega32(const float *dots, float alpha, int *nonfinite) {
   return ts / tt;
 }
 
-int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
-                    const uint16_t *b, const uint16_t *x0, double tol, int maxit,
-                    uint16_t *x, double *hist, float *alpha_out, float *omega_out,
-                    int *status, int *event_it) {
+/* O16-SR with half dots over the segments seg[0..nseg) (nseg = 0: mixed dots,
+ * = o16_sr_bicgstab).  ||b|| stays a mixed dot (setup, not an iteration op). */
+int o16h_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                     const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                     int nseg, const int *seg,
+                     uint16_t *x, double *hist, float *alpha_out, float *omega_out,
+                     int *status, int *event_it) {
   int64_t n = (int64_t)nx * ny * nz;
   size_t bytes = sizeof(uint16_t) * (size_t)(n > 0 ? n : 1);
   uint16_t *r = (uint16_t *)malloc(bytes), *rh = (uint16_t *)malloc(bytes);
@@ -232,7 +289,7 @@ int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
   }
   float alpha = 0.0f, omega = 0.0f, beta = 0.0f, dots[12];
   for (int i = 0; i <= maxit; ++i) {
-    o16_sr_sweep(nx, ny, nz, c, alpha, omega, beta, rh, x, r, p, v, q, y, dots);
+    o16h_sr_sweep(nx, ny, nz, c, alpha, omega, beta, rh, x, r, p, v, q, y, nseg, seg, dots, NULL);
     const float sigma = dots[0], rho = dots[1], phi = dots[2], psi = dots[3], rr = dots[11];
     hist[i] = sqrt((double)rr) / nb;
     it = i;
@@ -264,6 +321,14 @@ int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
 done:
   free(r); free(rh); free(p); free(v); free(q); free(y);
   return it;
+}
+
+int o16_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                    const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                    uint16_t *x, double *hist, float *alpha_out, float *omega_out,
+                    int *status, int *event_it) {
+  return o16h_sr_bicgstab(nx, ny, nz, c, b, x0, tol, maxit, 0, NULL, x, hist, alpha_out, omega_out, status,
+                          event_it);
 }
 
 /* ====================== fp32 mirror (vector ops only) ====================== */

@@ -22,6 +22,7 @@ FP32 = 0
 MIXED = 1
 SCHED_CLASSIC = 0
 SCHED_SR = 1
+DOTS_MIXED, DOTS_HALF = 0, 1
 XCHG_SERIAL, XCHG_OVERLAP, XCHG_FUSED = 0, 1, 2
 DT_F64 = 0
 DT_F32 = 1
@@ -77,6 +78,8 @@ def lib():
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
         L.sten_set_schedule.argtypes = [P, I]
+        L.sten_set_dot_precision.argtypes = [P, I]
+        L.sten_sr_segments.argtypes = [P, I, P, I, ctypes.POINTER(I)]
         L.sten_set_sr_tiling.argtypes = [P, I, I, I, I, I, I]
         L.sten_set_sr_exchange.argtypes = [P, I]
         L.sten_p2p_export.argtypes = [P, I, P, ctypes.POINTER(ctypes.c_size_t)]
@@ -283,6 +286,21 @@ def set_tiling(st: Stencil, precision: int, bx: int = 0, by: int = 0, zc: int = 
 def set_schedule(st: Stencil, schedule: int):
     """SCHED_CLASSIC (Alg. 1 as printed) or SCHED_SR (single reduction, R19)."""
     _check(lib().sten_set_schedule(st.handle, int(schedule)))
+
+
+def set_dot_precision(st: Stencil, dots: int):
+    """DOTS_MIXED (fp16 products summed in fp32) or DOTS_HALF (fp16 column pencils, R22)
+    for the MIXED SR sweeps of this handle."""
+    _check(lib().sten_set_dot_precision(st.handle, int(dots)))
+
+
+def sr_segments(st: Stencil, precision: int):
+    """First planes of the SR chunk plan's z segments on this rank (the pencils of DOTS_HALF)."""
+    n = ctypes.c_int(0)
+    _check(lib().sten_sr_segments(st.handle, precision, None, 0, ctypes.byref(n)))
+    buf = (ctypes.c_int * max(n.value, 1))()
+    _check(lib().sten_sr_segments(st.handle, precision, buf, n.value, ctypes.byref(n)))
+    return [int(buf[i]) for i in range(n.value)]
 
 
 def set_sr_exchange(st: Stencil, mode: int):

@@ -237,6 +237,7 @@ struct sten_stencil {
   int partials2_cap = 0;
   unsigned *counter2 = nullptr;
   bool cc = false;              // constant-coefficient operator (stencil_create_const)
+  bool half_dots = false;       // mixed SR sweeps accumulate the sums in fp16 pencils (R22)
   double cscaled[6] = {};       // its couplings A_d / a_P (fp64)
 };
 
@@ -645,6 +646,14 @@ static int ensure_sr(sten_stencil *st, int prec) {
   if (!sr_config_ok(t.by, t.stages, t.cstages, t.pack) || t.zc <= 0)
     return set_err(STEN_EINVAL, "unsupported SR tiling by=%d stages=%d cstages=%d zc=%d pack=%d", t.by, t.stages,
                    t.cstages, t.zc, t.pack);
+  if (prec == STEN_MIXED && st->half_dots) {  // R22: general operator, 16-B packs, no fused exchange
+    if (st->cc) return set_err(STEN_EUNSUPPORTED, "half dots: not with the constant-coefficient operator");
+    if (st->sr_p2p && decomposed(st))
+      return set_err(STEN_EUNSUPPORTED, "half dots: not with the fused peer-memory exchange (STEN_XCHG_FUSED)");
+    if (!sr_hd_config_ok(t.by, t.stages, t.cstages, t.pack))
+      return set_err(STEN_EUNSUPPORTED, "half dots: SR tiling by=%d stages=%d cstages=%d pack=%d not built", t.by,
+                     t.stages, t.cstages, t.pack);
+  }
   const int e = esize(prec);
   const size_t vb = (size_t)st->plane * e;
   const int H = 16 / e, bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();  // 16-B x halo pad
@@ -799,8 +808,8 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     a.has_above = sl.has_above;
   }
   if (a.nch == 0) return STEN_OK;
-  if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
-  else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, t.pack, st->cc, s));
+  if (prec == STEN_FP32) KLAUNCH(sr_launch<float>(a, t.by, t.stages, t.cstages, t.pack, st->cc, false, s));
+  else KLAUNCH(sr_launch<__half>(a, t.by, t.stages, t.cstages, t.pack, st->cc, st->half_dots, s));
   st->launches++;
   return STEN_OK;
 }
@@ -1389,6 +1398,8 @@ struct SolveOut {
 static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, double tol, int maxit, cudaStream_t s,
                       SolveOut *out) {
   const bool sr = st->schedule == STEN_SCHED_SR;
+  if (!sr && prec == STEN_MIXED && st->half_dots)
+    return set_err(STEN_EUNSUPPORTED, "half dots (STEN_DOTS_HALF) are built for the SR schedule only");
   RC_TRY(ensure_bufs(st, prec));
   if (sr) RC_TRY(ensure_sr(st, prec));
   if (maxit + 2 > st->hist_cap) {
@@ -1694,6 +1705,35 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega) {
     alpha[i - 1] = a[i];
     omega[i - 1] = w[i];
   }
+  return STEN_OK;
+}
+
+int sten_set_dot_precision(sten_stencil *st, int dots) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  if (dots != STEN_DOTS_MIXED && dots != STEN_DOTS_HALF) return set_err(STEN_EINVAL, "unknown dot precision %d", dots);
+  if (st->half_dots != (dots == STEN_DOTS_HALF)) drop_graphs(st);
+  st->half_dots = dots == STEN_DOTS_HALF;
+  return STEN_OK;
+}
+
+int sten_sr_segments(sten_stencil *st, int prec, int *z0, int cap, int *n) {
+  if (!st || !n) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
+  const SrTiling &t = st->srt[prec];
+  int cnt = 0;
+  for (const Slab &sl : st->slabs) {
+    int nbig, zct;
+    sr_chunks(t, sl.nz, &nbig, &zct);
+    const int nch = nbig + (sl.nz - nbig * t.zc + zct - 1) / zct;
+    for (int c = 0; c < nch; ++c, ++cnt) {
+      int zc0;
+      sr_chunk_z(t, nbig, zct, c, &zc0);
+      if (z0 && cnt < cap) z0[cnt] = (int)sl.z_first + zc0;
+    }
+  }
+  *n = cnt;
+  if (z0 && cnt > cap) return set_err(STEN_EINVAL, "%d segments, room for %d", cnt, cap);
   return STEN_OK;
 }
 

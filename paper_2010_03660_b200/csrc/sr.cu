@@ -36,6 +36,8 @@
 //    modulo arithmetic and no register rotation per plane.
 #include "sten_internal.cuh"
 
+#include <type_traits>
+
 namespace sten {
 
 namespace {
@@ -251,6 +253,51 @@ template <int NB> struct SrConst<__half, NB> {
   }
 };
 
+// experiment switch: L2 eviction hints (bit 0: the sweep's stores evict-first,
+// bit 1: the x / r_hat TMA loads evict-first, bit 2: the coefficient TMA loads
+// evict-first, bit 3: the halo'd input loads evict-last); 0 in the product
+#ifndef STEN_SR_EVF
+#define STEN_SR_EVF 0
+#endif
+template <typename PK, typename T>
+__device__ __forceinline__ void sr_st(const PK &v, T *p, uint64_t pol) {
+  if (STEN_SR_EVF & 1) {
+    if (sizeof(PK) == 16) {
+      uint4 u;
+      memcpy(&u, &v, 16);
+      asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(u.x), "r"(u.y),
+                   "r"(u.z), "r"(u.w), "l"(pol)
+                   : "memory");
+    } else {
+      uint2 u;
+      memcpy(&u, &v, 8);
+      asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(u.x), "r"(u.y), "l"(pol)
+                   : "memory");
+    }
+  } else {
+    v.st(p);
+  }
+}
+
+// half-dot mode (HD, DESIGN R22): the lane pencils of a pack, each an fp16
+// running sum over the thread's z range, widened and added in lane order
+template <int NB> __device__ __forceinline__ float sr_lanesum(const SPack<__half, NB> &a) {
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < SPack<__half, NB>::NW; ++i) {
+    const float2 f = __half22float2(SPack<__half, NB>::h2(a.w[i]));
+    s += f.x;
+    s += f.y;
+  }
+  return s;
+}
+template <int NB> __device__ __forceinline__ float sr_lanesum(const SPack<float, NB> &a) {
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < SPack<float, NB>::VEC; ++i) s += a.v[i];
+  return s;
+}
+
 template <typename T, int NB> struct SrShift;
 template <int NB> struct SrShift<float, NB> {
   using E = float;
@@ -309,7 +356,7 @@ __device__ __forceinline__ P spmv(const P (&c)[6], const P &m, const P &xl, cons
 
 }  // namespace
 
-template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU>
+template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU, bool HD>
 __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_constant__ SrArgs a) {
   using P = SPack<T, NB>;
   using G = SrGeo<T, BY, NB>;
@@ -342,6 +389,11 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   const int npi = z1 - z0 + 4;  // steps = staged input planes z0-2 .. z1+1
   const int npc = z1 - z0 + 2;  // staged coefficient planes z0-1 .. z1
   const int tid = threadIdx.x;
+  uint64_t pol = 0;
+  if (STEN_SR_EVF) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint64_t pol_in = 0;  // bit 3: the halo'd inputs evict-last (bit 4: at fraction 0.5)
+  if (STEN_SR_EVF & 16) asm("createpolicy.fractional.L2::evict_last.b64 %0, 0.5;" : "=l"(pol_in));
+  else if (STEN_SR_EVF & 8) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_in));
 
   // own vector: tile row ry, vector column cx
   const int ry = tid / VPR, cx = tid - (tid / VPR) * VPR;
@@ -386,15 +438,26 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
                    (5u * HW * G::RI + (STEN_SR_XTMA ? G::BX * BY : 0) + (STEN_SR_RHTMA ? G::BX * BY : 0)) *
                        (uint32_t)sizeof(T));
 #pragma unroll
-    for (int i = 0; i < 5; ++i) tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
-    if (STEN_SR_XTMA) tma_load_3d(IN + slot * G::SE + 5 * IE, &a.tm_x, x0, y0, m + 2, &mbar[slot]);
-    if (STEN_SR_RHTMA) tma_load_3d(RHR + (qi % 6) * G::XE, &a.tm_rh, x0, y0, m + 2, &mbar[slot]);
+    for (int i = 0; i < 5; ++i) {
+      if (STEN_SR_EVF & 8) tma_load_3d_hint(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot], pol_in);
+      else tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
+    }
+    if (STEN_SR_EVF & 2) {
+      tma_load_3d_hint(IN + slot * G::SE + 5 * IE, &a.tm_x, x0, y0, m + 2, &mbar[slot], pol);
+      tma_load_3d_hint(RHR + (qi % 6) * G::XE, &a.tm_rh, x0, y0, m + 2, &mbar[slot], pol);
+    } else {
+      if (STEN_SR_XTMA) tma_load_3d(IN + slot * G::SE + 5 * IE, &a.tm_x, x0, y0, m + 2, &mbar[slot]);
+      if (STEN_SR_RHTMA) tma_load_3d(RHR + (qi % 6) * G::XE, &a.tm_rh, x0, y0, m + 2, &mbar[slot]);
+    }
   };
   auto issue_c = [&](int qc) {  // plane z0-1+qc of the six coefficient arrays (1 halo plane)
     const int slot = qc % SC, m = z0 - 1 + qc;
     mbar_expect_tx(&mbar[S + slot], 6u * HW * G::RC * (uint32_t)sizeof(T));
 #pragma unroll
-    for (int d = 0; d < 6; ++d) tma_load_3d(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot]);
+    for (int d = 0; d < 6; ++d) {
+      if (STEN_SR_EVF & 4) tma_load_3d_hint(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot], pol);
+      else tma_load_3d(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot]);
+    }
   };
   // optional L2 prefetch (cp.async.bulk.prefetch.tensor) of input planes beyond
   // the shared-memory stages: bytes in flight to HBM without shared memory
@@ -483,6 +546,9 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   float dacc[12];
 #pragma unroll
   for (int d = 0; d < 12; ++d) dacc[d] = 0.0f;
+  P hacc[HD ? 12 : 1];  // HD: per-lane fp16 pencils of the twelve sums
+#pragma unroll
+  for (int d = 0; d < (HD ? 12 : 1); ++d) hacc[d] = P::zero();
 
   // one step j (= J mod 6): (A) form p', r' of plane m = k+2 and update the own
   // x, r, p; (B) v' = A p' on plane k+1; (C) q' = A r', y' = A v' and the
@@ -509,9 +575,9 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       if (inside && m >= z0 && m < z1) {
         const long long o = (long long)m * plane + gofs;
         const P xv = STEN_SR_XTMA ? P::ld(st + 5 * IE + ry * G::BX + cx * VEC) : xq[J % 3];
-        P::fmas(om_s, s, P::fmas(al_s, p, xv)).st(Xg + o);
-        rn.st(Og[0] + o);
-        pn.st(Og[1] + o);
+        sr_st(P::fmas(om_s, s, P::fmas(al_s, p, xv)), Xg + o, pol);
+        sr_st(rn, Og[0] + o, pol);
+        sr_st(pn, Og[1] + o, pol);
         halo_st(0, m, rn);
         halo_st(1, m, pn);
       }
@@ -555,7 +621,7 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       vn.st(vr + ec);
       vw[J % 3] = vn;
       if (inside && k + 1 >= z0 && k + 1 < z1) {
-        vn.st(Og[2] + (long long)(k + 1) * plane + gofs);
+        sr_st(vn, Og[2] + (long long)(k + 1) * plane + gofs, pol);
         halo_st(2, k + 1, vn);
       }
       if (hv >= 0) {
@@ -595,22 +661,37 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
       if (!STEN_SR_RHTMA) rq[(J + 2) % 3] = ld_rh(k + 3);
       if (inside) {
         const long long o = (long long)k * plane + gofs;
-        qn.st(Og[3] + o);
-        yn.st(Og[4] + o);
+        sr_st(qn, Og[3] + o, pol);
+        sr_st(yn, Og[4] + o, pol);
         halo_st(3, k, qn);
         halo_st(4, k, yn);
-        dacc[0] = rh.mdot(vc, dacc[0]);    // (rh, v)
-        dacc[1] = rh.mdot(rc, dacc[1]);    // (rh, r)
-        dacc[2] = rh.mdot(qn, dacc[2]);    // (rh, q)
-        dacc[3] = rh.mdot(yn, dacc[3]);    // (rh, y)
-        dacc[4] = qn.mdot(rc, dacc[4]);    // (q, r)
-        dacc[5] = qn.mdot(vc, dacc[5]);    // (q, v)
-        dacc[6] = yn.mdot(rc, dacc[6]);    // (y, r)
-        dacc[7] = yn.mdot(vc, dacc[7]);    // (y, v)
-        dacc[8] = qn.mdot(qn, dacc[8]);    // (q, q)
-        dacc[9] = qn.mdot(yn, dacc[9]);    // (q, y)
-        dacc[10] = yn.mdot(yn, dacc[10]);  // (y, y)
-        dacc[11] = rc.mdot(rc, dacc[11]);  // (r, r)
+        if constexpr (HD) {  // one fp16 FMA per point into the lane's pencil (R22)
+          hacc[0] = P::fma(rh, vc, hacc[0]);
+          hacc[1] = P::fma(rh, rc, hacc[1]);
+          hacc[2] = P::fma(rh, qn, hacc[2]);
+          hacc[3] = P::fma(rh, yn, hacc[3]);
+          hacc[4] = P::fma(qn, rc, hacc[4]);
+          hacc[5] = P::fma(qn, vc, hacc[5]);
+          hacc[6] = P::fma(yn, rc, hacc[6]);
+          hacc[7] = P::fma(yn, vc, hacc[7]);
+          hacc[8] = P::fma(qn, qn, hacc[8]);
+          hacc[9] = P::fma(qn, yn, hacc[9]);
+          hacc[10] = P::fma(yn, yn, hacc[10]);
+          hacc[11] = P::fma(rc, rc, hacc[11]);
+        } else {
+          dacc[0] = rh.mdot(vc, dacc[0]);    // (rh, v)
+          dacc[1] = rh.mdot(rc, dacc[1]);    // (rh, r)
+          dacc[2] = rh.mdot(qn, dacc[2]);    // (rh, q)
+          dacc[3] = rh.mdot(yn, dacc[3]);    // (rh, y)
+          dacc[4] = qn.mdot(rc, dacc[4]);    // (q, r)
+          dacc[5] = qn.mdot(vc, dacc[5]);    // (q, v)
+          dacc[6] = yn.mdot(rc, dacc[6]);    // (y, r)
+          dacc[7] = yn.mdot(vc, dacc[7]);    // (y, v)
+          dacc[8] = qn.mdot(qn, dacc[8]);    // (q, q)
+          dacc[9] = qn.mdot(yn, dacc[9]);    // (q, y)
+          dacc[10] = yn.mdot(yn, dacc[10]);  // (y, y)
+          dacc[11] = rc.mdot(rc, dacc[11]);  // (r, r)
+        }
       }
     }
   };
@@ -623,25 +704,29 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
     if (j + 4 < npi) step(IC<4>{}, j + 4);
     if (j + 5 < npi) step(IC<5>{}, j + 5);
   }
+  if constexpr (HD) {
+#pragma unroll
+    for (int d = 0; d < 12; ++d) dacc[d] = sr_lanesum(hacc[d]);
+  }
   grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
 }
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU>
+template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU, bool HD = false>
 int launch_sr_one(const SrArgs &a, cudaStream_t s) {
   constexpr size_t smem = sr_smem_c<T, BY, S, SC, CC, NB>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC, CC, NB, FU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_sr<T, BY, S, SC, CC, NB, FU, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * a.nch;
   if (grid == 0) return (int)cudaSuccess;
-  k_sr<T, BY, S, SC, CC, NB, FU><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
+  k_sr<T, BY, S, SC, CC, NB, FU, HD><<<grid, SrGeo<T, BY, NB>::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 }  // namespace
@@ -657,9 +742,29 @@ bool sr_config_ok(int by, int stages, int cstages, int pack) {
   return false;
 }
 
+// the half-dot variant (R22): fp16 sweeps with the general operator, 16-B packs
+#define STEN_SR_HD_CONFIGS(X) X(16, 2, 2, 16) X(8, 2, 2, 16) X(8, 3, 2, 16) X(8, 3, 3, 16)
+
+bool sr_hd_config_ok(int by, int stages, int cstages, int pack) {
+#define X(B, S_, C_, N_) if (by == B && stages == S_ && cstages == C_ && pack == N_) return true;
+  STEN_SR_HD_CONFIGS(X)
+#undef X
+  return false;
+}
+
 template <typename T>
-int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, cudaStream_t s) {
+int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, bool hd, cudaStream_t s) {
   const bool fu = a.peer_lo[0] || a.peer_hi[0];
+  if (hd) {
+    if constexpr (std::is_same<T, __half>::value) {
+      if (cc || fu) return (int)cudaErrorNotSupported;
+#define X(B, S_, C_, N_) \
+  if (by == B && stages == S_ && cstages == C_ && pack == N_) return launch_sr_one<T, B, S_, C_, false, N_, false, true>(a, s);
+      STEN_SR_HD_CONFIGS(X)
+#undef X
+    }
+    return (int)cudaErrorNotSupported;
+  }
 #define X(B, S_, C_, N_)                                                                              \
   if (by == B && stages == S_ && cstages == C_ && pack == N_) {                                       \
     if (fu) return cc ? launch_sr_one<T, B, S_, C_, true, N_, true>(a, s)                             \
@@ -685,8 +790,8 @@ int sr_threads(int by, int pack) {
   return (tile_bx<T>() / (pack / (int)sizeof(T))) * by;
 }
 
-template int sr_launch<float>(const SrArgs &, int, int, int, int, bool, cudaStream_t);
-template int sr_launch<__half>(const SrArgs &, int, int, int, int, bool, cudaStream_t);
+template int sr_launch<float>(const SrArgs &, int, int, int, int, bool, bool, cudaStream_t);
+template int sr_launch<__half>(const SrArgs &, int, int, int, int, bool, bool, cudaStream_t);
 template size_t sr_smem_bytes<float>(int, int, int, int);
 template size_t sr_smem_bytes<__half>(int, int, int, int);
 template int sr_threads<float>(int, int);

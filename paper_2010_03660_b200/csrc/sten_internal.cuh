@@ -271,6 +271,15 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_3d_hint(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -562,7 +571,9 @@ struct alignas(64) SrArgs {
   Reduce red;
 };
 bool sr_config_ok(int by, int stages, int cstages, int pack);
-template <typename T> int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, cudaStream_t s);
+bool sr_hd_config_ok(int by, int stages, int cstages, int pack);
+template <typename T>
+int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, bool hd, cudaStream_t s);
 template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages, int pack);
 template <typename T> int sr_threads(int by, int pack);
 

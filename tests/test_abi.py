@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(sten.LIB_PATH)
     missing = [n for n in declared_functions() if not hasattr(L, n)]
     assert not missing, missing
-    assert sten.version() == 2
+    assert sten.version() == 3
 
 
 def test_product_never_imports_oracle():

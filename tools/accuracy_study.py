@@ -23,10 +23,12 @@ import inputs.cuda as icuda  # noqa: E402
 import paper_2010_03660_b200 as sten  # noqa: E402
 
 
-def hist_run(st, prec, b, maxit, sched):
+def hist_run(st, prec, b, maxit, sched, half=False):
     sten.set_schedule(st, sched)
+    sten.set_dot_precision(st, sten.DOTS_HALF if half else sten.DOTS_MIXED)
     x = torch.empty_like(b)
     it, hist, status = sten.bicgstab_solve(st, prec, b, None, 0.0, maxit, x)
+    sten.set_dot_precision(st, sten.DOTS_MIXED)
     return hist, x
 
 
@@ -45,8 +47,9 @@ def main(tag="r1"):
         b16 = b32.half()
         rows = {}
         for name, prec, b, sched in (("fp32 classic", sten.FP32, b32, 0), ("fp32 SR", sten.FP32, b32, 1),
-                                     ("mixed classic", sten.MIXED, b16, 0), ("mixed SR", sten.MIXED, b16, 1)):
-            h, x = hist_run(st, prec, b, 60, sched)
+                                     ("mixed classic", sten.MIXED, b16, 0), ("mixed SR", sten.MIXED, b16, 1),
+                                     ("half-dot SR", sten.MIXED, b16, 2)):
+            h, x = hist_run(st, prec, b, 60, min(sched, 1), half=sched == 2)
             rows[name] = h
             if prec == sten.MIXED:
                 # true residual of the mixed solution: one refinement step with outer_maxit = 0 from x0 = x
@@ -69,6 +72,13 @@ def main(tag="r1"):
         ko, ki, rh, status = sten.bicgstab_refine(st, b32, None, 1e-6, 30, 1e-2, 200, xo)
         out.append(f"\nIterative refinement (SR inner, inner tol 1e-2): {ko} outer steps, {ki} mixed iterations, "
                    f"status {sten.STATUS_NAMES[status]}; outer residuals " + ", ".join(f"{v:.1e}" for v in rh) + "\n")
+        if delta == 0.0:  # the weakly dominant system: short, loose inner solves
+            for sched, sname in ((1, "SR"), (0, "classic")):
+                sten.set_schedule(st, sched)
+                ko, ki, rh, status = sten.bicgstab_refine(st, b32, None, 1e-6, 60, 0.1, 25, xo)
+                out.append(f"Iterative refinement ({sname} inner, inner tol 0.1, <= 25 inner iterations): {ko} outer "
+                           f"steps, {ki} mixed iterations, status {sten.STATUS_NAMES[status]}, final outer residual "
+                           f"{rh[-1]:.1e}\n")
         st.close()
         del diag, offs
         torch.cuda.empty_cache()
