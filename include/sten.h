@@ -177,6 +177,23 @@ int bicgstab_solve(sten_stencil *st, int precision, const void *b, const void *x
                    int maxit, void *x_out, int *iters, double *res_hist, int *status,
                    void *cuda_stream);
 
+/* n independent solves with the same operator (a serving batch): system i
+ * is bicgstab_solve(b[i], x0 = NULL, tol, maxit) -> x_out[i], in order, with
+ * identical results.  The host<->device traffic is pipelined: host vectors
+ * (pinned memory, for the copies to be asynchronous) go through two device
+ * staging buffers per direction, the upload of b[i+1] and the download of
+ * x[i-1] running on a library copy stream while system i is solved.  Device
+ * pointers are used in place.
+ *   b, x_out : n pointers each (this rank's points, storage type of precision);
+ *   iters, status : host, n ints each;
+ *   res_hist : host, n * (maxit+1) doubles, row i = system i's history (NaN
+ *              after iters[i]).
+ * Extra device memory: 4 staging vectors.  Synchronises cuda_stream and the
+ * copy stream before return.  Errors: as bicgstab_solve (a NULL vector:
+ * STEN_EINVAL); n == 0 is a no-op. */
+int bicgstab_solve_batch(sten_stencil *st, int precision, int n, const void *const *b, void *const *x_out,
+                         double tol, int maxit, int *iters, double *res_hist, int *status, void *cuda_stream);
+
 /* Mixed-precision iterative refinement (the remedy the paper names for the
  * fp16 plateau; R21).  Solves A x = b to an fp32
  * accuracy while the iterations run in the mixed mode:

@@ -73,6 +73,7 @@ def lib():
         L.stencil2d_destroy.argtypes = [P]
         L.stencil_apply.argtypes = [P, I, P, P, P]
         L.bicgstab_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
+        L.bicgstab_solve_batch.argtypes = [P, I, I, P, P, D, I, P, P, P, P]
         L.sten_scalar_history.argtypes = [P, I, P, P]
         L.sten_set_timing.argtypes = [P, I]
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
@@ -258,6 +259,26 @@ def bicgstab_solve(st: Stencil, precision: int, b, x0, tol: float, maxit: int, x
                                 ctypes.byref(it), hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(status),
                                 _stream(stream)))
     return it.value, hist[: it.value + 1].copy(), status.value
+
+
+def bicgstab_solve_batch(st: Stencil, precision: int, bs, xs, tol: float, maxit: int, stream=None):
+    """n independent solves (x0 = 0) with pipelined host<->device copies (pinned host
+    vectors overlap with the solves).  Returns [(iters, res_hist, status)] per system."""
+    if len(bs) != len(xs):
+        raise StenError("bs and xs must have the same length")
+    n = len(bs)
+    for i, (b, x) in enumerate(zip(bs, xs)):
+        _check_vec(b, precision, st.npoints, f"b[{i}]")
+        _check_vec(x, precision, st.npoints, f"x[{i}]")
+    bp = (ctypes.c_void_p * max(n, 1))(*[_ptr(b) for b in bs])
+    xp = (ctypes.c_void_p * max(n, 1))(*[_ptr(x) for x in xs])
+    its = np.zeros(max(n, 1), np.int32)
+    sts = np.zeros(max(n, 1), np.int32)
+    hist = np.zeros((max(n, 1), max(maxit, 0) + 1), np.float64)
+    _check(lib().bicgstab_solve_batch(st.handle, precision, n, bp, xp, float(tol), int(maxit),
+                                      its.ctypes.data_as(ctypes.c_void_p), hist.ctypes.data_as(ctypes.c_void_p),
+                                      sts.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+    return [(int(its[i]), hist[i, : its[i] + 1].copy(), int(sts[i])) for i in range(n)]
 
 
 def scalar_history(st: Stencil, n: int):

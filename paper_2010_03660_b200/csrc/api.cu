@@ -239,6 +239,11 @@ struct sten_stencil {
   bool cc = false;              // constant-coefficient operator (stencil_create_const)
   bool half_dots = false;       // mixed SR sweeps accumulate the sums in fp16 pencils (R22)
   double cscaled[6] = {};       // its couplings A_d / a_P (fp64)
+  // bicgstab_solve_batch: copy stream, double-buffered dense staging of b / x
+  cudaStream_t io = nullptr;
+  void *bstage[2] = {}, *xstage[2] = {};
+  size_t io_bytes = 0;
+  cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_dn[2] = {};
 };
 
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
@@ -1306,6 +1311,13 @@ void stencil_destroy(sten_stencil *st) {
   cudaFree(st->counter);
   cudaFree(st->counter2);
   if (st->side) cudaStreamDestroy(st->side);
+  if (st->io) cudaStreamDestroy(st->io);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(st->bstage[k]);
+    cudaFree(st->xstage[k]);
+    for (cudaEvent_t e : {st->ev_in[k], st->ev_used[k], st->ev_out[k], st->ev_dn[k]})
+      if (e) cudaEventDestroy(e);
+  }
   if (st->ev_fork) cudaEventDestroy(st->ev_fork);
   if (st->ev_join) cudaEventDestroy(st->ev_join);
   cudaFree(st->slab_sums);
@@ -1544,6 +1556,101 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   st->stats.kernel_launches = st->launches + so.kernels;
   st->stats.event_iter = fin.ev >= 0 ? fin.ev_it : 0;
   st->stats.graph_chunk = so.chunk;
+  return STEN_OK;
+}
+
+// Many right-hand sides: the host<->device copies of solve i+1 / i-1 run on a
+// copy stream during solve i (double-buffered dense staging).
+static int ensure_io(sten_stencil *st, size_t bytes) {
+  if (!st->io) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&st->io, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t *e : {&st->ev_in[k], &st->ev_used[k], &st->ev_out[k], &st->ev_dn[k]}) {
+        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(*e, st->io));  // "done" before first use
+      }
+  }
+  if (bytes > st->io_bytes) {
+    CUDA_TRY(cudaStreamSynchronize(st->io));
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(st->bstage[k]);
+      cudaFree(st->xstage[k]);
+      st->bstage[k] = st->xstage[k] = nullptr;
+      st->io_bytes = 0;
+      if (cudaMalloc(&st->bstage[k], bytes) != cudaSuccess || cudaMalloc(&st->xstage[k], bytes) != cudaSuccess)
+        return set_err(STEN_ENOMEM, "bicgstab_solve_batch: staging of 4 x %zu bytes", bytes);
+    }
+    st->io_bytes = bytes;
+  }
+  return STEN_OK;
+}
+
+int bicgstab_solve_batch(sten_stencil *st, int prec, int n, const void *const *b, void *const *x_out, double tol,
+                         int maxit, int *iters, double *res_hist, int *status, void *cuda_stream) {
+  if (!st || n < 0 || (n > 0 && (!b || !x_out || !iters || !res_hist || !status)))
+    return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (!(tol >= 0.0) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
+  for (int i = 0; i < n; ++i)
+    if (!b[i] || !x_out[i]) return set_err(STEN_EINVAL, "NULL vector %d", i);
+  if (n == 0) return STEN_OK;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const bool sr = st->schedule == STEN_SCHED_SR;
+  RC_TRY(ensure_bufs(st, prec));
+  if (sr) RC_TRY(ensure_sr(st, prec));
+  long long pts = 0;
+  for (const Slab &sl : st->slabs) pts += (long long)sl.nz;
+  const size_t bytes = (size_t)pts * st->nx * st->ny * esize(prec);
+  RC_TRY(ensure_io(st, bytes));
+  st->launches = 0;
+  memset(&st->stats, 0, sizeof st->stats);
+  CUDA_TRY(cudaEventRecord(st->ev_a, s));
+  // H2D of b[i] into slot i&1 once the solve of i-2 has consumed that slot
+  auto upload = [&](int i) -> int {
+    const int k = i & 1;
+    if (ptr_on_device(b[i])) return STEN_OK;
+    CUDA_TRY(cudaStreamWaitEvent(st->io, st->ev_used[k], 0));
+    CUDA_TRY(cudaMemcpyAsync(st->bstage[k], b[i], bytes, cudaMemcpyHostToDevice, st->io));
+    CUDA_TRY(cudaEventRecord(st->ev_in[k], st->io));
+    return STEN_OK;
+  };
+  RC_TRY(upload(0));
+  long long kernels = 0;
+  for (int i = 0; i < n; ++i) {
+    const int k = i & 1;
+    if (i + 1 < n) RC_TRY(upload(i + 1));
+    const bool bdev = ptr_on_device(b[i]), xdev = ptr_on_device(x_out[i]);
+    if (!bdev) CUDA_TRY(cudaStreamWaitEvent(s, st->ev_in[k], 0));
+    RC_TRY(copy_in(st, prec, sel_bw, bdev ? b[i] : st->bstage[k], s));
+    if (!bdev) CUDA_TRY(cudaEventRecord(st->ev_used[k], s));
+    SolveOut so;
+    RC_TRY(solve_core(st, prec, false, true, tol, maxit, s, &so));
+    kernels += so.kernels;
+    const DevState &fin = so.fin;
+    if (!xdev) CUDA_TRY(cudaStreamWaitEvent(s, st->ev_dn[k], 0));  // the D2H of solve i-2 left the slot
+    void *xd = xdev ? x_out[i] : st->xstage[k];
+    if (sr) RC_TRY(sr_copy_out(st, prec, [prec](Slab &sl) { return sl.sr[prec].x; }, xd, s));
+    else RC_TRY(copy_out(st, prec, sel_x, xd, s));
+    CUDA_TRY(cudaMemcpyAsync(res_hist + (size_t)i * (maxit + 1), st->hist, sizeof(double) * (fin.it + 1),
+                             cudaMemcpyDeviceToHost, s));
+    for (int j = fin.it + 1; j <= maxit; ++j) res_hist[(size_t)i * (maxit + 1) + j] = NAN;
+    if (!xdev) {
+      CUDA_TRY(cudaEventRecord(st->ev_out[k], s));
+      CUDA_TRY(cudaStreamWaitEvent(st->io, st->ev_out[k], 0));
+      CUDA_TRY(cudaMemcpyAsync(x_out[i], st->xstage[k], bytes, cudaMemcpyDeviceToHost, st->io));
+      CUDA_TRY(cudaEventRecord(st->ev_dn[k], st->io));
+    }
+    iters[i] = fin.it;
+    status[i] = fin.stop ? fin.status : (fin.ev >= 0 ? fin.ev : STEN_MAXIT);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st->io));
+  CUDA_TRY(cudaEventRecord(st->ev_b, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, st->ev_a, st->ev_b);
+  st->stats.solve_ms = ms;
+  st->stats.kernel_launches = st->launches + kernels;
   return STEN_OK;
 }
 

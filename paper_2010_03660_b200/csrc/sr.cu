@@ -253,11 +253,14 @@ template <int NB> struct SrConst<__half, NB> {
   }
 };
 
-// experiment switch: L2 eviction hints (bit 0: the sweep's stores evict-first,
-// bit 1: the x / r_hat TMA loads evict-first, bit 2: the coefficient TMA loads
-// evict-first, bit 3: the halo'd input loads evict-last); 0 in the product
+// L2 eviction hints (bit 0: the sweep's stores evict-first -- the product
+// default, +0.5%: the outputs are next read a whole sweep later, so they
+// should not displace the input planes that neighbouring tiles still read as
+// halos; experiments: bit 1 x / r_hat TMA loads evict-first (-4%), bit 2 the
+// coefficient loads evict-first (-20%), bit 3 the halo'd inputs evict-last
+// (+-0), bit 4 at fraction 0.5)
 #ifndef STEN_SR_EVF
-#define STEN_SR_EVF 0
+#define STEN_SR_EVF 1
 #endif
 template <typename PK, typename T>
 __device__ __forceinline__ void sr_st(const PK &v, T *p, uint64_t pol) {
