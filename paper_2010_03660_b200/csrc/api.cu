@@ -590,8 +590,8 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
   return STEN_OK;
 }
 
-// Default SR geometry: 16-row tiles, 3 input stages, 2 coefficient stages
-// (199 KB of shared memory, one 256-thread CTA per SM), 64 planes per CTA.
+// Default SR geometry: 16-row tiles, 2 input stages, 2 coefficient stages (one
+// 256-thread CTA per SM), 160-plane chunks with a 320-plane tail of 64-plane chunks.
 static void default_sr_tiling(sten_stencil *st, int prec) {
   SrTiling &t = st->srt[prec];
   // measured at 600x595x1536: mixed 16-row tiles, 160-plane
