@@ -258,7 +258,8 @@ template <int NB> struct SrConst<__half, NB> {
 // should not displace the input planes that neighbouring tiles still read as
 // halos; experiments: bit 1 x / r_hat TMA loads evict-first (-4%), bit 2 the
 // coefficient loads evict-first (-20%), bit 3 the halo'd inputs evict-last
-// (+-0), bit 4 at fraction 0.5)
+// (+-0), bit 4 at fraction 0.5; keeping the four planes the next chunk of a tile
+// stages again evict-last cost 2-4%)
 #ifndef STEN_SR_EVF
 #define STEN_SR_EVF 1
 #endif
@@ -437,15 +438,18 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 
   auto issue_in = [&](int qi) {  // plane z0-2+qi of r, p, v, q, y (vectors: 2 halo planes)
     const int slot = qi % S, m = z0 - 2 + qi;
-    mbar_expect_tx(&mbar[slot],
-                   (5u * HW * G::RI + (STEN_SR_XTMA ? G::BX * BY : 0) + (STEN_SR_RHTMA ? G::BX * BY : 0)) *
-                       (uint32_t)sizeof(T));
+    // x and r_hat only on the chunk's own planes (the four halo planes need neither)
+    const bool own = m >= z0 && m < z1;
+    mbar_expect_tx(&mbar[slot], (5u * HW * G::RI + (own && STEN_SR_XTMA ? G::BX * BY : 0) +
+                                 (own && STEN_SR_RHTMA ? G::BX * BY : 0)) *
+                                    (uint32_t)sizeof(T));
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       if (STEN_SR_EVF & 8) tma_load_3d_hint(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot], pol_in);
       else tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
     }
-    if (STEN_SR_EVF & 2) {
+    if (!own) {
+    } else if (STEN_SR_EVF & 2) {
       tma_load_3d_hint(IN + slot * G::SE + 5 * IE, &a.tm_x, x0, y0, m + 2, &mbar[slot], pol);
       tma_load_3d_hint(RHR + (qi % 6) * G::XE, &a.tm_rh, x0, y0, m + 2, &mbar[slot], pol);
     } else {
