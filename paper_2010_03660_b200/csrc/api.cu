@@ -1562,13 +1562,16 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
 // Many right-hand sides: the host<->device copies of solve i+1 / i-1 run on a
 // copy stream during solve i (double-buffered dense staging).
 static int ensure_io(sten_stencil *st, size_t bytes) {
-  if (!st->io) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&st->io, cudaStreamNonBlocking));
+  if (!st->io) {  // events first, the stream last: a half-made set is retried on the next call
     for (int k = 0; k < 2; ++k)
-      for (cudaEvent_t *e : {&st->ev_in[k], &st->ev_used[k], &st->ev_out[k], &st->ev_dn[k]}) {
-        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(*e, st->io));  // "done" before first use
-      }
+      for (cudaEvent_t *e : {&st->ev_in[k], &st->ev_used[k], &st->ev_out[k], &st->ev_dn[k]})
+        if (!*e) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    cudaStream_t io = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&io, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {st->ev_in[k], st->ev_used[k], st->ev_out[k], st->ev_dn[k]})
+        CUDA_TRY(cudaEventRecord(e, io));  // "done" before first use
+    st->io = io;
   }
   if (bytes > st->io_bytes) {
     CUDA_TRY(cudaStreamSynchronize(st->io));
@@ -1602,6 +1605,12 @@ int bicgstab_solve_batch(sten_stencil *st, int prec, int n, const void *const *b
   for (const Slab &sl : st->slabs) pts += (long long)sl.nz;
   const size_t bytes = (size_t)pts * st->nx * st->ny * esize(prec);
   RC_TRY(ensure_io(st, bytes));
+  // every exit (errors included) waits for the copy stream: no copy into or out of the
+  // caller's buffers may still be in flight when the call returns
+  struct IoDrain {
+    cudaStream_t io;
+    ~IoDrain() { cudaStreamSynchronize(io); }
+  } drain{st->io};
   st->launches = 0;
   memset(&st->stats, 0, sizeof st->stats);
   CUDA_TRY(cudaEventRecord(st->ev_a, s));
