@@ -13,8 +13,11 @@
  *   - SpMV u = A v as the sum of the local iterate and six coefficient-times-
  *     neighbour products, PAPER.md:198-201, 338-346 (Sec. SpMV(3D));
  *   - mixed precision: fp16 storage and arithmetic, inner products with fp16
- *     multiply / fp32 add, AllReduce in fp32.
- * Readings where the paper is silent are numbered R1..R13 in DESIGN.md.
+ *     multiply / fp32 add, AllReduce in fp32, PAPER.md:82, 116-120, 397;
+ *   - the single-reduction rearrangement of Alg. 1 (osr.c, R19), the 16-bit
+ *     dot accumulation of the unpublished half mode (osr.c o16h_*, R22), the
+ *     2D 9-point SpMV (o2d.c).
+ * Readings where the paper is silent are numbered R1..R22 in DESIGN.md.
  *
  * Mesh: nx*ny*nz points, linear index P = i + nx*(j + ny*k), x fastest.
  * Coefficient arrays c[0..5] = (xm, xp, ym, yp, zm, zp): c_d[P] multiplies
