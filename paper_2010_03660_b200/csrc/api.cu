@@ -137,6 +137,7 @@ static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int pl
 struct Tiling {
   int rows = 0;  // 1: full-row strips (k_rows), 0: BX-wide tiles with an x halo (k_stencil)
   int bx = 0, by = 0, zc = 0, stages = 0, threads = 0;
+  int cstages = 0;  // > 0: coefficient (+ rhat) tiles by TMA into a ring of this depth (k_stencil)
 };
 
 // SR schedule buffers (R19): two halo planes per side, because the
@@ -279,7 +280,11 @@ static void default_tiling(sten_stencil *st, int prec) {
   t.bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   t.by = 16;
   t.zc = small_mesh_zc(st, t.bx, t.by, nzs, t.zc, 2);
-  t.stages = 4;
+  // coefficient (+ rhat) tiles by TMA, 2 input + 2 coefficient stages (2 CTAs/SM): H1 2.12 ms vs
+  // 2.31 ms with per-thread coefficient loads, which straddle sectors on unpadded rows
+  t.stages = 2;
+  t.cstages = 2;
+  if (const char *e = getenv("STEN_CLS_TILING")) sscanf(e, "%d,%d", &t.stages, &t.cstages);  // tuning knob
   t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);
 }
 
@@ -400,8 +405,8 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     if (prec == STEN_FP32) KLAUNCH(rows_launch<float>(mode, a, t.by, t.stages, s));
     else KLAUNCH(rows_launch<__half>(mode, a, t.by, t.stages, s));
   } else {
-    if (prec == STEN_FP32) KLAUNCH(stencil_launch<float>(mode, a, t.by, t.stages, s));
-    else KLAUNCH(stencil_launch<__half>(mode, a, t.by, t.stages, s));
+    if (prec == STEN_FP32) KLAUNCH(stencil_launch<float>(mode, a, t.by, t.stages, t.cstages, s));
+    else KLAUNCH(stencil_launch<__half>(mode, a, t.by, t.stages, t.cstages, s));
   }
   st->launches++;
   return STEN_OK;
@@ -1350,14 +1355,20 @@ int sten_set_tiling(sten_stencil *st, int prec, int bx, int by, int zc, int stag
   }
   if (by) t.by = by;
   if (zc) t.zc = zc;
-  if (stages) t.stages = stages;
+  if (stages) {  // an explicit pipeline depth selects the per-thread coefficient loads (3 or 4 stages)
+    t.stages = stages;
+    t.cstages = 0;
+  } else if (t.rows || (t.cstages && !stencil_config_ok(t.by, t.stages, t.cstages))) {
+    t.stages = 4;  // row strips, or a tile height without a coefficient-TMA instance
+    t.cstages = 0;
+  }
   if (t.rows) {
     if (t.zc <= 0 || !rows_config_ok(t.by, t.stages) || rows_thr(prec, st->nx, t.by) > 512 ||
         rows_smem_bytes(MODE_H1, esize(prec), st->pitch, t.by, t.stages) > 227 * 1024)
       return set_err(STEN_EINVAL, "unsupported row-strip tiling by=%d zc=%d stages=%d", t.by, t.zc, t.stages);
     t.threads = rows_thr(prec, st->nx, t.by);
   } else {
-    if (t.zc <= 0 || !stencil_config_ok(t.by, t.stages))
+    if (t.zc <= 0 || !stencil_config_ok(t.by, t.stages, t.cstages))
       return set_err(STEN_EINVAL, "unsupported tiling by=%d zc=%d stages=%d (by 4/8/16, stages 3/4)", t.by, t.zc,
                      t.stages);
     t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);

@@ -508,8 +508,9 @@ __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduc
 // 128 fp16 / 64 fp32 points); rows per tile (by) and TMA stages are template
 // instances chosen at run time.
 template <typename T> constexpr int tile_bx() { return sizeof(T) == 2 ? 128 : 64; }
-bool stencil_config_ok(int by, int stages);
-template <typename T> int stencil_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s);
+bool stencil_config_ok(int by, int stages, int cstages = 0);
+template <typename T>
+int stencil_launch(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
 template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
 template <typename T> int stencil_threads(int by);
 // row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits

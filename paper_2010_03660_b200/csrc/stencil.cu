@@ -44,10 +44,20 @@ struct Geo {
   static constexpr int PF = 4;                  // L2 prefetch distance of the coefficients (planes)
 };
 
-template <typename T, int MODE, int BY, int S>
+// SC > 0: the six coefficient tiles (and rhat for H1) of a plane arrive by TMA
+// into an SC-stage ring (no per-thread global loads on misaligned rows)
+template <typename T, int MODE, int BY>
+struct CGeo {
+  static constexpr int NC = MODE == MODE_H1 ? 7 : 6;                                   // tiles per plane
+  static constexpr int XE = align128c(tile_bx<T>() * BY * (int)sizeof(T)) / (int)sizeof(T);  // elements per tile
+};
+
+template <typename T, int MODE, int BY, int S, int SC = 0>
 constexpr size_t smem_bytes_c() {
   using G = Geo<T, MODE, BY>;
-  return 128 /* mbarriers */ + (size_t)S * G::NIN * G::HBYTES + 3 * (size_t)G::HBYTES;
+  using C = CGeo<T, MODE, BY>;
+  return 128 /* mbarriers */ + (size_t)S * G::NIN * G::HBYTES + 3 * (size_t)G::HBYTES +
+         (size_t)SC * C::NC * C::XE * sizeof(T);
 }
 
 __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int x, int y, int z) {
@@ -84,10 +94,11 @@ template <> struct Shift<__half> {
 
 }  // namespace
 
-template <typename T, int MODE, int BY, int S>
+template <typename T, int MODE, int BY, int S, int SC>
 __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __grid_constant__ StencilArgs a) {
   using P = Pack<T>;
   using G = Geo<T, MODE, BY>;
+  using CG = CGeo<T, MODE, BY>;
   constexpr int VEC = G::VEC, BX = G::BX, H = G::H, HW = G::HW, NIN = G::NIN;
   constexpr int HSTR = G::HBYTES / (int)sizeof(T);  // elements between halo boxes
   constexpr int ND = MODE == MODE_H2 ? 2 : 1;
@@ -98,6 +109,7 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   uint64_t *mbar = reinterpret_cast<uint64_t *>(smem);
   T *stage0 = reinterpret_cast<T *>(smem + 128);         // [S][NIN][HSTR]
   T *U = stage0 + S * NIN * HSTR;                       // [3][HSTR]
+  T *CF = U + 3 * HSTR;                                  // [SC][NC][XE] coefficient (+ rhat) tiles
   __shared__ float scratch[32 * kMaxDots];
 
   int b = blockIdx.x;
@@ -124,11 +136,18 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
 
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < S + SC; ++s) mbar_init(&mbar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
+  auto issue_c = [&](int k) {  // coefficient (+ rhat) tiles of plane k, one thread
+    const int s = (k - z0) % (SC > 0 ? SC : 1);
+    mbar_expect_tx(&mbar[S + s], CG::NC * BX * BY * (uint32_t)sizeof(T));
+#pragma unroll
+    for (int d = 0; d < 6; ++d) tma_load_3d(CF + (s * CG::NC + d) * CG::XE, &a.tm_c[d], x0, y0, k, &mbar[S + s]);
+    if (MODE == MODE_H1) tma_load_3d(CF + (s * CG::NC + 6) * CG::XE, &a.tm_aux, x0, y0, k + 1, &mbar[S + s]);
+  };
   auto issue = [&](int q) {  // planes z0-1+q of every halo'd operand, one thread
     const int s = q % S, p = z0 - 1 + q;
     mbar_expect_tx(&mbar[s], NIN * G::HBOX * (uint32_t)sizeof(T));
@@ -144,7 +163,10 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   };
   if (tid == 0) {
     for (int q = 0; q < min(S, np); ++q) issue(q);
-    for (int k = z0; k < z0 + a.pf; ++k) prefetch(k);
+    if (SC > 0)
+      for (int k = z0; k < min(z0 + SC, z1); ++k) issue_c(k);
+    else
+      for (int k = z0; k < z0 + a.pf; ++k) prefetch(k);
   }
   // coefficients (+ rhat) of a plane straight into registers, one plane ahead
   const T *const *cp = reinterpret_cast<const T *const *>(a.cptr);
@@ -161,7 +183,7 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
       rhn = P::zero();
     }
   };
-  load_coefs(z0);
+  if (SC == 0) load_coefs(z0);
 
   typename P::S beta_s{}, momega_s{}, malpha_s{};
   if (MODE == MODE_H1) {
@@ -202,11 +224,20 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   for (int k = z0; k < z1; ++k) {
     const int qc = k - z0 + 1, qn = qc + 1;
     P c[6], rh;
+    if (SC > 0) {  // this plane's tiles from the ring (slot refilled after the barrier below)
+      const int cs = (k - z0) % (SC > 0 ? SC : 1);
+      mbar_wait(&mbar[S + cs], (uint32_t)(((k - z0) / (SC > 0 ? SC : 1)) & 1));
+      const T *cf = CF + cs * CG::NC * CG::XE + ry * BX + cx * VEC;
 #pragma unroll
-    for (int d = 0; d < 6; ++d) c[d] = cn[d];
-    rh = rhn;
-    load_coefs(k + 1);  // in flight during this plane's work
-    if (tid == 0 && a.pf > 0) prefetch(k + a.pf);
+      for (int d = 0; d < 6; ++d) c[d] = P::ld(cf + d * CG::XE);
+      if (MODE == MODE_H1) rh = P::ld(cf + 6 * CG::XE);
+    } else {
+#pragma unroll
+      for (int d = 0; d < 6; ++d) c[d] = cn[d];
+      rh = rhn;
+      load_coefs(k + 1);  // in flight during this plane's work
+      if (tid == 0 && a.pf > 0) prefetch(k + a.pf);
+    }
     // SpMV input of plane k+1
     wait(qn);
     T *Un = U + (qn % 3) * HSTR;
@@ -215,6 +246,7 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
     if (hhalo >= 0) form(qn, hhalo).st(Un + hhalo);
     __syncthreads();
     if (tid == 0 && qn + S < np) issue(qn + S);  // stage of plane k+1 is consumed
+    if (SC > 0 && tid == 0 && k + SC < z1) issue_c(k + SC);  // and the coefficient slot of plane k
     // u_k = v_k + sum of the six products (order xm, xp, ym, yp, zm, zp)
     const T *Uc = U + (qc % 3) * HSTR;
     P acc = uc;
@@ -469,23 +501,30 @@ template int rows_threads<__half>(int, int);
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int MODE, int BY, int S>
+template <typename T, int MODE, int BY, int S, int SC = 0>
 int launch_one(const StencilArgs &a, cudaStream_t s) {
   using G = Geo<T, MODE, BY>;
-  constexpr size_t smem = smem_bytes_c<T, MODE, BY, S>();
+  constexpr size_t smem = smem_bytes_c<T, MODE, BY, S, SC>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
-  k_stencil<T, MODE, BY, S><<<grid, G::NT, smem, s>>>(a);
+  k_stencil<T, MODE, BY, S, SC><<<grid, G::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 template <typename T, int MODE>
-int launch_mode(const StencilArgs &a, int by, int stages, cudaStream_t s) {
+int launch_mode(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
+  if (cstages) {  // coefficient tiles by TMA
+    if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE, 16, 2, 2>(a, s);
+    if (by == 16 && stages == 3 && cstages == 1) return launch_one<T, MODE, 16, 3, 1>(a, s);
+    if (by == 16 && stages == 2 && cstages == 1) return launch_one<T, MODE, 16, 2, 1>(a, s);
+    if (by == 8 && stages == 3 && cstages == 2) return launch_one<T, MODE, 8, 3, 2>(a, s);
+    return (int)cudaErrorInvalidValue;
+  }
   if (by == 8 && stages == 3) return launch_one<T, MODE, 8, 3>(a, s);
   if (by == 8 && stages == 4) return launch_one<T, MODE, 8, 4>(a, s);
   if (by == 16 && stages == 3) return launch_one<T, MODE, 16, 3>(a, s);
@@ -504,16 +543,19 @@ size_t smem_mode(int by, int stages) {
 }
 }  // namespace
 
-bool stencil_config_ok(int by, int stages) {
+bool stencil_config_ok(int by, int stages, int cstages) {
+  if (cstages)
+    return (by == 16 && ((stages == 2 && (cstages == 1 || cstages == 2)) || (stages == 3 && cstages == 1))) ||
+           (by == 8 && stages == 3 && cstages == 2);
   return (by == 8 && (stages == 3 || stages == 4)) || (by == 16 && (stages == 3 || stages == 4)) ||
          (by == 4 && stages == 4);
 }
 
 template <typename T>
-int stencil_launch(int mode, const StencilArgs &a, int by, int stages, cudaStream_t s) {
-  if (mode == MODE_H1) return launch_mode<T, MODE_H1>(a, by, stages, s);
-  if (mode == MODE_H2) return launch_mode<T, MODE_H2>(a, by, stages, s);
-  return launch_mode<T, MODE_APPLY>(a, by, stages, s);
+int stencil_launch(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
+  if (mode == MODE_H1) return launch_mode<T, MODE_H1>(a, by, stages, cstages, s);
+  if (mode == MODE_H2) return launch_mode<T, MODE_H2>(a, by, stages, cstages, s);
+  return launch_mode<T, MODE_APPLY>(a, by, stages, cstages, s);
 }
 template <typename T>
 size_t stencil_smem_bytes(int mode, int by, int stages) {
@@ -526,8 +568,8 @@ int stencil_threads(int by) {
   return (tile_bx<T>() / Pack<T>::VEC) * by;
 }
 
-template int stencil_launch<float>(int, const StencilArgs &, int, int, cudaStream_t);
-template int stencil_launch<__half>(int, const StencilArgs &, int, int, cudaStream_t);
+template int stencil_launch<float>(int, const StencilArgs &, int, int, int, cudaStream_t);
+template int stencil_launch<__half>(int, const StencilArgs &, int, int, int, cudaStream_t);
 template size_t stencil_smem_bytes<float>(int, int, int);
 template size_t stencil_smem_bytes<__half>(int, int, int);
 template int stencil_threads<float>(int);
