@@ -34,9 +34,9 @@ def read_ncu_csv(path):
 CMDS = {
     "r1": {"traffic": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                       "--clock-control none -k regex:'k_stencil|k_h3|k_init' -s 30 -c 6 "
-                      "python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu",
+                      "python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --schedule classic",
            "full": "ncu --set full --clock-control none --import-source on -k regex:'k_stencil|k_h3' -s 0 -c 3 "
-                   "python bench.py --steps 1 --warmup 1 --maxit 2 --nz 384 --no-e2e --no-cpu"},
+                   "python bench.py --steps 1 --warmup 1 --maxit 2 --nz 384 --no-e2e --no-cpu --schedule classic"},
     "r1_sr": {"traffic": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                          "--clock-control none -k regex:'k_sr|k_init' -s 20 -c 4 "
                          "python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu",
