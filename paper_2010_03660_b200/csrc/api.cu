@@ -262,13 +262,13 @@ static int rows_thr(int prec, int nx, int by) {
 // z-chunk length for a small mesh: enough chunks that the grid fills ~2 waves of
 // the SMs (a 32^3 mesh has 2 xy tiles; one chunk each would leave the GPU idle
 // and the z-march latency-bound), never below 4 planes
-static int small_mesh_zc(const sten_stencil *st, int bx, int by, int nzs, int zc, int ctas_per_sm) {
+static int small_mesh_zc(const sten_stencil *st, int bx, int by, int nzs, int zc, int ctas_per_sm, int zmin = 4) {
   const long long tiles = (long long)((st->nx + bx - 1) / bx) * ((st->ny + by - 1) / by);
   const long long want = 2LL * st->sm * ctas_per_sm;
   const long long chunks = (want + tiles - 1) / tiles;
   if (chunks <= 1) return zc;
   int z = (int)((nzs + chunks - 1) / chunks);
-  if (z < 4) z = 4;
+  if (z < zmin) z = zmin;
   return z < zc ? z : zc;
 }
 
@@ -621,7 +621,8 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
   t.zc_tail = zct > 0 ? zct : t.zc;
   t.tail = tail > 0 ? tail : 0;
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
-  const int zs = small_mesh_zc(st, bx, t.by, nzs, t.zc, 1);
+  // SR: chunks down to 2 planes (config 1, 32^3: 11.8 vs 14.3 us per iteration at 4)
+  const int zs = small_mesh_zc(st, bx, t.by, nzs, t.zc, 1, 2);
   if (zs < t.zc && !getenv("STEN_SR_TILING")) {  // a small mesh: uniform short chunks
     t.zc = t.zc_tail = zs;
     t.tail = 0;
