@@ -621,9 +621,23 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
   t.zc_tail = zct > 0 ? zct : t.zc;
   t.tail = tail > 0 ? tail : 0;
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
-  // SR: chunks down to 2 planes (config 1, 32^3: 11.8 vs 14.3 us per iteration at 4)
-  const int zs = small_mesh_zc(st, bx, t.by, nzs, t.zc, 1, 2);
-  if (zs < t.zc && !getenv("STEN_SR_TILING")) {  // a small mesh: uniform short chunks
+  if (getenv("STEN_SR_TILING")) return;
+  // Small meshes: uniform short chunks.  HBM-bound ones: enough chunks to fill ~2 waves
+  // (chunks down to 2 planes).  L2-resident ones (the sweep's ~15 arrays within 2x L2): at
+  // most one wave, which balances the z-halo overhead of short chunks against parallelism
+  // (config 2, 128^3 fp32, 16 tiles: 36 us per iteration at 16-plane chunks / 128 CTAs, 42 at
+  // 8 / 256, 51 at 32 / 64; config 1, 32^3: 2-plane chunks / 32 CTAs, 12 us).
+  const long long tiles = (long long)((st->nx + bx - 1) / bx) * ((st->ny + t.by - 1) / t.by);
+  const double ws = 15.0 * (double)st->nx * st->ny * nzs * esize(prec);
+  int zs;
+  if (ws <= 2.0 * 126e6) {
+    const long long chunks = st->sm / tiles > 1 ? st->sm / tiles : 1;
+    zs = (int)((nzs + chunks - 1) / chunks);
+    if (zs < 2) zs = 2;
+  } else {
+    zs = small_mesh_zc(st, bx, t.by, nzs, t.zc, 1, 2);
+  }
+  if (zs < t.zc) {
     t.zc = t.zc_tail = zs;
     t.tail = 0;
   }
