@@ -197,7 +197,8 @@ def run_reference(args):
             "dtype": "f16" if args.precision == "mixed" else "f64", "data": "synthetic",
             "config": {"workload": workload, "mesh": [NX, NY, NZ], "precision": args.precision,
                        "sample_planes": planes, "iters_per_step": iters},
-            "cpu_baseline": res,
+            "cpu_baseline": dict(res, value=value,
+                                 sample=f"{args.steps} steps, each: " + res["sample"].rsplit(",", 1)[0]),
             "e2e": {"value": value, "unit": "Gpoint-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
