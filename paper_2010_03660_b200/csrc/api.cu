@@ -625,8 +625,8 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
   // Small meshes: uniform short chunks.  HBM-bound ones: enough chunks to fill ~2 waves
   // (chunks down to 2 planes).  L2-resident ones (the sweep's ~15 arrays within 2x L2): at
   // most one wave, which balances the z-halo overhead of short chunks against parallelism
-  // (config 2, 128^3 fp32, 16 tiles: 36 us per iteration at 16-plane chunks / 128 CTAs, 42 at
-  // 8 / 256, 51 at 32 / 64; config 1, 32^3: 2-plane chunks / 32 CTAs, 12 us).
+  // (config 2, 128^3 fp32, 16 tiles: 36 us per iteration at 15- or 16-plane chunks / 144 or 128
+  // CTAs, 42 at 8 / 256, 51 at 32 / 64; config 1, 32^3: 2-plane chunks / 32 CTAs, 12 us).
   const long long tiles = (long long)((st->nx + bx - 1) / bx) * ((st->ny + t.by - 1) / t.by);
   const double ws = 15.0 * (double)st->nx * st->ny * nzs * esize(prec);
   int zs;

@@ -324,3 +324,20 @@ def test_p2p_export_and_import_guards(sten):
     with pytest.raises(sten.StenError):  # needs a multi-rank communicator
         sten.p2p_import(st, PREC["mixed"], [rec, rec])
     st.close()
+
+
+def test_sr_chunk_plan_of_small_meshes(sten):
+    """L2-resident meshes: at most one wave of CTAs, chunks of >= 2 planes (DESIGN §7 small
+    configs); the plan is what sten_sr_segments reports and what the half-dot pencils follow."""
+    import torch
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    for n, prec, bx in ((128, 0, 64), (32, 0, 64), (32, 1, 128), (64, 1, 128)):
+        tiles = -(-n // bx) * -(-n // 16)
+        chunks = max(sm // tiles, 1)
+        zc = max(-(-n // chunks), 2)
+        diag, offs = fields(inputs.KIND_CD, n, n, n, seed=1)
+        st = gpu_stencil(diag, offs)
+        seg = sten.sr_segments(st, prec)
+        assert seg == list(range(0, n, zc)), (n, prec, seg)
+        assert tiles * len(seg) <= max(sm, tiles)  # one wave
+        st.close()
