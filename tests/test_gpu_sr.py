@@ -61,7 +61,8 @@ def _sweep_case(sten, prec, mesh, tiling=None, nslabs=1, scalars=(0.61, 0.93, -0
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-@pytest.mark.parametrize("mesh", [(37, 29, 19), (1, 1, 1), (5, 3, 2), (130, 17, 9), (264, 20, 11), (8, 40, 4)])
+@pytest.mark.parametrize("mesh", [(37, 29, 19), (1, 1, 1), (5, 3, 2), (130, 17, 9), (264, 20, 11), (8, 40, 4),
+                                  (1, 300, 5), (600, 1, 3), (8, 4, 2000), (129, 2, 7)])
 def test_sr_sweep_bitwise(sten, prec, mesh):
     got, dots, ref, rh = _sweep_case(sten, prec, mesh)
     names = ["x", "r", "p", "v", "q", "y"]
