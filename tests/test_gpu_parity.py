@@ -19,7 +19,8 @@ from gpu_util import (fields, from_gpu_vec, gpu_stencil, oracle_coeffs, quantize
 pytestmark = pytest.mark.gpu
 
 PREC = {"fp32": 0, "mixed": 1}
-MESHES = [(32, 32, 32), (37, 29, 19), (1, 1, 1), (5, 3, 2), (130, 17, 9), (8, 300, 4), (264, 20, 70)]
+MESHES = [(32, 32, 32), (37, 29, 19), (1, 1, 1), (5, 3, 2), (130, 17, 9), (8, 300, 4), (264, 20, 70),
+          (600, 1, 3), (1, 300, 5), (8, 4, 700)]
 
 
 @pytest.fixture(scope="module")
