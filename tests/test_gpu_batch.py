@@ -74,3 +74,16 @@ def test_batch_edge_cases(sten):
     (it, h, status), (it2, h2, _) = sten.bicgstab_solve_batch(st, 0, [b1, b1], [x, torch.empty_like(x)], 0.0, 7)
     assert it == it2 == 7 and np.all(np.isfinite(h)) and np.array_equal(h, h2)
     st.close()
+
+
+def test_quickstart_example_runs():
+    """examples/quickstart.py (the user-facing walk-through) runs and reaches its targets."""
+    import importlib.util
+    import os
+    torch_cuda()
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "quickstart.py")
+    spec = importlib.util.spec_from_file_location("quickstart", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    h_mixed, h_refine, true = mod.main(64, 48, 32)
+    assert h_mixed <= 1e-3 and h_refine <= 1e-6 and true <= 1e-5
