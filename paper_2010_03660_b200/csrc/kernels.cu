@@ -11,6 +11,9 @@
 namespace sten {
 
 // ------------------------------------------------------------------ H3 --
+#ifndef STEN_H3_QUAD
+#define STEN_H3_QUAD 1  // four vectors per trip: H3 1.284 -> 1.256 ms at config 3 (tools/h3_exp.sh)
+#endif
 // Element offset of the v-th vector of the interior range.  The element-wise
 // kernels stream the whole 128-B-aligned range linearly, row padding included:
 // the padding holds zeros in every vector (never written with anything else),
@@ -40,6 +43,26 @@ __global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
   float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
   const long long stride = (long long)gridDim.x * blockDim.x;
   long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+#if STEN_H3_QUAD
+  // four vectors per thread per trip: twenty loads in flight, then the pairs and the tail
+  for (; v + 3 * stride < a.nvec; v += 4 * stride) {
+    P xs[4], ps[4], ss[4], ts[4], rs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long o = vofs<VEC>(v + u * stride, a);
+      xs[u] = P::ldg(X + o); ps[u] = P::ldg(Pp + o); ss[u] = P::ldg(Sv + o); ts[u] = P::ldg(Tv + o); rs[u] = P::ldg(Rh + o);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long o = vofs<VEC>(v + u * stride, a);
+      P xn = P::fmas(ws, ss[u], P::fmas(as, ps[u], xs[u])), rn = P::fmas(mws, ts[u], ss[u]);
+      xn.st(XO + o);
+      rn.st(RO + o);
+      rs[u].dot4(rn, d0);
+      rn.dot4(rn, d1);
+    }
+  }
+#endif
   // two vectors per thread per trip: all ten loads issued before any math
   for (; v + stride < a.nvec; v += 2 * stride) {
     const long long o0 = vofs<VEC>(v, a), o1 = vofs<VEC>(v + stride, a);
