@@ -1460,6 +1460,9 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   h.hist = st->hist;
   h.ahist = st->ahist;
   h.whist = st->whist;
+  // SR on one slab: the last sweep without its SpMVs (k_sr_last)
+  const bool light = sr && !decomposed(st) && !(prec == STEN_MIXED && st->half_dots) && !getenv("STEN_SR_NOLIGHT");
+  h.light = light ? 1 : 0;
   *st->st_host = h;
   CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
   // S1: b_hat, r0, rhat, p0 (Alg. 1 l.174; R1, R3)
@@ -1527,6 +1530,27 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
         }
         if (st->st_host->stop || st->st_host->it >= maxit) break;
       }
+    }
+    if (light) {  // sweep maxit (a no-op unless the solve got there)
+      Slab &sl = st->slabs[0];
+      SrBufs &b = sl.sr[prec];
+      const int set = maxit & 1, vec = prec == STEN_FP32 ? 4 : 8;
+      SrLastArgs la;
+      memset(&la, 0, sizeof la);
+      la.x = sr_interior(b.x, st, prec);
+      la.rh = sr_interior(b.rh, st, prec);
+      la.r = sr_interior(b.vec[set][0], st, prec);
+      la.p = sr_interior(b.vec[set][1], st, prec);
+      la.v = sr_interior(b.vec[set][2], st, prec);
+      la.q = sr_interior(b.vec[set][3], st, prec);
+      la.y = sr_interior(b.vec[set][4], st, prec);
+      la.nvec = (long long)st->plane * sl.nz / vec;
+      la.red = make_red(st, 0);
+      const int g = ew_grid(st, la.nvec);
+      if (g > st->partials_cap) return set_err(STEN_ECUDA, "internal: last-sweep grid exceeds the partial-sum buffer");
+      if (prec == STEN_FP32) KLAUNCH(sr_last_launch<float>(la, g, s));
+      else KLAUNCH(sr_last_launch<__half>(la, g, s));
+      out->kernels += 1;
     }
   }
   CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));

@@ -718,6 +718,49 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
 }
 
+// The last sweep of a solve (i = maxit, DevState::light): phase A of k_sr -- the
+// same element-wise operations in the same order -- and the sums (rhat, r_maxit)
+// and (r_maxit, r_maxit), the only ones the scalar step reads at i = maxit (fin_sr
+// stops there); v', q', y' are never used.  A linear stream over the interior.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sr_last(const __grid_constant__ SrLastArgs a) {
+  using P = SPack<T, 16>;
+  __shared__ float scratch[32 * kMaxDots];
+  const DevState *st = a.red.st;
+  if (st->stop || !st->light || st->sweep != st->maxit) return;
+  const typename P::S al_s = P::scalar(st->alpha), mal_s = P::neg(al_s);
+  const typename P::S om_s = P::scalar(st->omega), mom_s = P::neg(om_s);
+  constexpr int VEC = P::VEC;
+  T *X = reinterpret_cast<T *>(a.x);
+  const T *RH = reinterpret_cast<const T *>(a.rh), *R = reinterpret_cast<const T *>(a.r);
+  const T *Pp = reinterpret_cast<const T *>(a.p), *V = reinterpret_cast<const T *>(a.v);
+  const T *Q = reinterpret_cast<const T *>(a.q), *Y = reinterpret_cast<const T *>(a.y);
+  float dacc[12];
+#pragma unroll
+  for (int d = 0; d < 12; ++d) dacc[d] = 0.0f;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.nvec; i += stride) {
+    const long long o = i * VEC;
+    const P r = P::ldg(R + o), p = P::ldg(Pp + o), v = P::ldg(V + o), q = P::ldg(Q + o), y = P::ldg(Y + o);
+    const P x = P::ldg(X + o), rh = P::ldg(RH + o);
+    const P s = P::fmas(mal_s, v, r);
+    const P t = P::fmas(mal_s, y, q);
+    const P rn = P::fmas(mom_s, t, s);
+    P::fmas(om_s, s, P::fmas(al_s, p, x)).st(X + o);
+    dacc[1] = rh.mdot(rn, dacc[1]);   // (rh, r)
+    dacc[11] = rn.mdot(rn, dacc[11]);  // (r, r)
+  }
+  grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
+}
+
+template <typename T>
+int sr_last_launch(const SrLastArgs &a, int grid, cudaStream_t s) {
+  k_sr_last<T><<<grid, 256, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+template int sr_last_launch<float>(const SrLastArgs &, int, cudaStream_t);
+template int sr_last_launch<__half>(const SrLastArgs &, int, cudaStream_t);
+
 // ------------------------------------------------------------ host side --
 namespace {
 template <typename T, int BY, int S, int SC, bool CC, int NB, bool FU, bool HD = false>

@@ -30,6 +30,7 @@ struct DevState {
   int ev_it;                       // iteration of the first event
   int zero_x;                      // b_hat == 0: x must be returned as 0
   int sweep;                       // SR schedule: index of the next sweep
+  int light;                       // SR: the last sweep (i = maxit) is k_sr_last, not k_sr
   int half;                        // mixed mode: scalars must be finite in fp16 (R7)
   double *hist;                    // [maxit+1] ||r_i|| / ||b_hat||
   float *ahist, *whist;            // [maxit+1] alpha_i, omega_i
@@ -450,7 +451,9 @@ __device__ __forceinline__ void finalize_phase(DevState *st, const float *s) {
 }
 
 __device__ __forceinline__ bool st_idle(const DevState *st) { return st->stop || st->it >= st->maxit; }
-__device__ __forceinline__ bool sr_idle(const DevState *st) { return st->stop || st->sweep > st->maxit; }
+__device__ __forceinline__ bool sr_idle(const DevState *st) {
+  return st->stop || st->sweep > st->maxit || (st->light && st->sweep == st->maxit);
+}
 
 // Grid-level end of a reduction: every CTA deposits its block sum; the last
 // CTA to arrive sums the deposits in CTA order (deterministic) and either
@@ -573,6 +576,15 @@ struct alignas(64) SrArgs {
 };
 bool sr_config_ok(int by, int stages, int cstages, int pack);
 bool sr_hd_config_ok(int by, int stages, int cstages, int pack);
+// the last SR sweep (i = maxit) without its three SpMVs: x_maxit, r_maxit and the two sums
+// the scalar step still reads, (rhat, r) and (r, r) -- 8 passes instead of 19
+struct SrLastArgs {
+  void *x;                              // in place
+  const void *rh, *r, *p, *v, *q, *y;   // the set sweep maxit reads
+  long long nvec;                       // 16-B vectors of the interior range (padding holds zeros)
+  Reduce red;
+};
+template <typename T> int sr_last_launch(const SrLastArgs &a, int grid, cudaStream_t s);
 template <typename T>
 int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool cc, bool hd, cudaStream_t s);
 template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages, int pack);

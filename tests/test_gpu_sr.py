@@ -342,3 +342,24 @@ def test_sr_chunk_plan_of_small_meshes(sten):
         assert seg == list(range(0, n, zc)), (n, prec, seg)
         assert tiles * len(seg) <= max(sm, tiles)  # one wave
         st.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_sr_light_last_sweep(sten, prec, monkeypatch):
+    """The last sweep of a solve runs without its three SpMVs (k_sr_last): x and every earlier
+    history entry are bitwise those of the full sweep; hist[maxit] differs only by the order of
+    its fp32 sum.  STEN_SR_NOLIGHT=1 selects the full sweep."""
+    nx, ny, nz = 45, 33, 20
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=4)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=4), prec)
+    st = gpu_stencil(diag, offs)
+    for maxit in (0, 1, 12):
+        x1, it1, h1, s1 = _solve(sten, st, prec, b, 0.0, maxit)
+        monkeypatch.setenv("STEN_SR_NOLIGHT", "1")
+        x2, it2, h2, s2 = _solve(sten, st, prec, b, 0.0, maxit)
+        monkeypatch.delenv("STEN_SR_NOLIGHT")
+        assert it1 == it2 == maxit and s1 == s2
+        assert np.array_equal(widen(x1, prec), widen(x2, prec))
+        assert np.array_equal(h1[:-1], h2[:-1])
+        assert abs(h1[-1] - h2[-1]) <= 1e-5 * h2[-1]
+    st.close()
