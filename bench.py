@@ -52,8 +52,11 @@ def parse():
     p.add_argument("--nz", type=int, default=NZ, help="planes per GPU (debug / profiling)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--schedule", default="sr", choices=["sr", "classic"],
-                   help="sr: single-reduction sweep (19 passes, DESIGN.md R19); classic: Alg. 1 as printed (29)")
+    p.add_argument("--schedule", default="classic", choices=["sr", "classic"],
+                   help="headline schedule. classic: Alg. 1 as printed (29 passes); sr: single-reduction sweep "
+                        "(19 passes, DESIGN.md R19, NEXT-1). The other one is measured in the same run and "
+                        "reported as a labelled field unless --no-other")
+    p.add_argument("--no-other", action="store_true", help="do not measure the non-headline schedule")
     p.add_argument("--dots", default="mixed", choices=["mixed", "half"],
                    help="mixed precision only: inner products as fp16 products summed in fp32 (the paper's "
                         "instruction), or half: fp16 column pencils (DESIGN.md R22, NEXT-4; SR schedule)")
@@ -141,8 +144,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- oracle --
-def oracle_sample(precision: str, workload: str, planes: int, iters: int, z0: int = 0):
-    """Time the oracle as it stands on a z-slab sample [z0, z0+planes) of the workload."""
+def _slab_system(workload: str, planes: int, z0: int = 0):
     import inputs
     import oracle as orc
     kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
@@ -150,29 +152,89 @@ def oracle_sample(precision: str, workload: str, planes: int, iters: int, z0: in
     diag, offs = inputs.problem_fields(kind, NX, NY, planes, z0=z0, seed=1, delta=0.1, kz_table=kz)
     b64 = inputs.rhs_uniform(NX, NY, planes, z0=z0, seed=1)
     c64 = orc.jacobi_scale(diag, offs)
-    t0 = time.perf_counter()
+    return diag, c64, b64
+
+
+def oracle_sample(precision: str, workload: str, planes: int, iters: int, z0: int = 0, threads: int = 0,
+                  system=None):
+    """Time the oracle as it stands on a z-slab sample [z0, z0+planes) of the workload:
+    O16 (the fp16-emulating oracle of the mixed path) or O64 (fp64; for fp32 runs on the
+    fp32-quantised couplings)."""
+    import oracle as orc
+    diag, c64, b64 = system or _slab_system(workload, planes, z0)
+    if threads:
+        orc.set_threads(threads)
     if precision == "mixed":
         c16 = orc.quantize_coeffs(c64, "mixed")
         bh = orc.scale_rhs(orc.f16_from_double(b64), diag, "mixed")
         t0 = time.perf_counter()
         orc.bicgstab16(c16, bh, tol=0.0, maxit=iters)
+        name = "O16"
     else:
-        c32 = [c.astype(np.float32).astype(np.float64) for c in c64]
-        bh = orc.scale_rhs(b64.astype(np.float32), diag, "fp32").astype(np.float64)
+        if precision == "fp32":
+            c64 = [c.astype(np.float32).astype(np.float64) for c in c64]
+            bh = orc.scale_rhs(b64.astype(np.float32), diag, "fp32").astype(np.float64)
+        else:  # "fp64": the method in the host's native precision
+            bh = b64 / diag
         t0 = time.perf_counter()
-        orc.bicgstab64(c32, bh, tol=0.0, maxit=iters)
+        orc.bicgstab64(c64, bh, tol=0.0, maxit=iters)
+        name = "O64"
     dt = time.perf_counter() - t0
     pts = NX * NY * planes
     return dict(value=pts * iters / dt / 1e9, unit="Gpoint-iter/s", cores=orc.num_threads(), kind="oracle",
-                sample=f"{'O16' if precision == 'mixed' else 'O64'} BiCGStab, {iters} iterations on a "
-                       f"{NX}x{NY}x{planes} z-slab of {workload} ({pts} points), {dt:.1f} s"), dt
+                sample=f"{name} BiCGStab, {iters} iterations on a {NX}x{NY}x{planes} z-slab of {workload} "
+                       f"({pts} points), {dt:.1f} s"), dt
+
+
+def host_copy_gbs():
+    """STREAM-like host copy (numpy, one thread, 1 GiB, read + write bytes)."""
+    n = 1 << 27
+    a = np.ones(n)
+    b_ = np.empty_like(a)
+    np.copyto(b_, a)
+    best = 0.0
+    for _ in range(3):
+        t0 = time.perf_counter()
+        np.copyto(b_, a)
+        best = max(best, 2 * a.nbytes / (time.perf_counter() - t0) / 1e9)
+    return best
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_auto(precision, workload, planes_override=0):
-    # size the sample to ~10-30 s of oracle work
-    planes = planes_override or (16 if precision == "mixed" else 64)
-    iters = 3
-    res, dt = oracle_sample(precision, workload, planes, iters)
+    """SURVEY.md 8(d) CPU oracle timing on this host: O64 on all cores and on one thread
+    (10 iterations, 600x595x192 slab of the workload), next to O16 (the fp16-emulating
+    oracle, software binary16: 3 iterations on a 600x595x16 slab), with nproc and the host
+    copy bandwidth.  `value` = O64 on all cores: the fastest the oracle runs here."""
+    import oracle as orc
+    nproc = os.cpu_count()
+    planes = planes_override or 192
+    system = _slab_system(workload, planes)
+    o64p = "fp32" if precision == "fp32" else "fp64"
+    allc, _ = oracle_sample(o64p, workload, planes, 10, threads=nproc, system=system)
+    one, _ = oracle_sample(o64p, workload, planes, 10, threads=1, system=system)
+    del system
+    orc.set_threads(nproc)
+    o16 = None
+    if precision == "mixed":
+        o16, _ = oracle_sample("mixed", workload, 16, 3, threads=nproc)
+    res = dict(allc)
+    res.update({"nproc": nproc, "cpu_model": cpu_model(), "host_copy_gbs": host_copy_gbs(),
+                "o64_all_cores": allc, "o64_1_thread": one,
+                "note": "O64 = fp64 oracle (the method in the host's native precision)" +
+                        ("" if precision == "fp32" else "; O16 = fp16-emulating oracle of the mixed path")})
+    if o16:
+        res["o16_all_cores"] = o16
     return res
 
 
@@ -205,6 +267,99 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU --
+def event_split(iter_ms, event_iter, schedule):
+    """Per-iteration device ms before / after the first breakdown event of a solve.
+    Classic: entry j is iteration j + 1; SR: entry j is sweep j (it produces r_j).
+    Iterations up to and including the event iteration count as pre-event."""
+    if not iter_ms:
+        return None
+    first = 0 if schedule == "sr" else 1
+    its = list(range(first, first + len(iter_ms)))
+    if event_iter <= 0:
+        pre, post = iter_ms, []
+    else:
+        pre = [m for it, m in zip(its, iter_ms) if it <= event_iter]
+        post = [m for it, m in zip(its, iter_ms) if it > event_iter]
+    mean = lambda v: float(np.mean(v)) if v else None  # noqa: E731
+    return {"event_iter": int(event_iter), "n_pre": len(pre), "n_post": len(post),
+            "ms_per_iter_pre": mean(pre), "ms_per_iter_post": mean(post), "ms_per_iter_all": mean(iter_ms)}
+
+
+def run_schedule(sten, st, prec, schedule, b, x, args, world, sdist, npts, clocks_gpu=None):
+    """W warm-up solves, then K timed solves of `schedule` on handle `st` (CUDA events on the
+    solve's stream, max over ranks).  Returns the timing record."""
+    import torch
+    import torch.distributed as dist
+
+    sten.set_schedule(st, sten.SCHED_SR if schedule == "sr" else sten.SCHED_CLASSIC)
+    sten.set_timing(st, True)
+    for _ in range(args.warmup):
+        sten.bicgstab_solve(st, prec, b, None, args.tol, args.maxit, x)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(clocks_gpu) if clocks_gpu is not None else None
+    launches, iters_done = 0, 0
+    ph_ms, ph_n = [0.0, 0.0, 0.0], [0, 0, 0]
+    per_iter, events = [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    last = None
+    for _ in range(args.steps):
+        last = sten.bicgstab_solve(st, prec, b, None, args.tol, args.maxit, x)
+        iters_done += last[0]
+        s = sten.get_stats(st)
+        launches += s["kernel_launches"]
+        for p in range(3):
+            ph_ms[p] += s["phase_ms"][p]
+            ph_n[p] += s["phase_launches"][p]
+        per_iter.append([sten.iter_ms(st, p) for p in range(3)])
+        events.append(s["event_iter"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    t_ms = sdist.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
+    it, hist, status = last
+    # first-event split, per step, from the per-launch events inside the solve graphs
+    splits = [event_split([a + b_ + c for a, b_, c in zip(*pi)], ev, schedule) for pi, ev in zip(per_iter, events)]
+    splits = [sp for sp in splits if sp]
+    value_window = npts * iters_done / (t_ms / 1e3) / 1e9
+    value, basis = value_window, "all timed iterations"
+    ev_rec = None
+    if splits:
+        pre = float(np.mean([sp["ms_per_iter_pre"] for sp in splits]))
+        allm = float(np.mean([sp["ms_per_iter_all"] for sp in splits]))
+        posts = [sp["ms_per_iter_post"] for sp in splits if sp["ms_per_iter_post"] is not None]
+        post = float(np.mean(posts)) if posts else None
+        ev_rec = {"event_iter": int(events[-1]), "event_iters_all_steps": sorted(set(int(e) for e in events)),
+                  "iters_pre_event": splits[-1]["n_pre"], "iters_post_event": splits[-1]["n_post"],
+                  "ms_per_iter_pre_event": pre, "ms_per_iter_post_event": post, "ms_per_iter_all": allm}
+        if post is not None and post < 0.99 * pre:
+            # post-event iterations ran > 1% faster: rate the whole window as if every iteration
+            # took the pre-event time (init and graph gaps stay in)
+            value = value_window * allm / pre
+            basis = "pre-event iterations (post-event ran %.1f%% faster)" % (100 * (1 - post / pre))
+        ev_rec["value_basis"] = basis
+        ev_rec["value_all_iterations"] = value_window
+    # dominant kernel's per-launch time: pre-event launches when the rule above applied
+    dom = 0
+    if ev_rec and basis.startswith("pre-event"):
+        dom_ms = float(np.mean([np.mean([m for k, m in enumerate(pi[dom]) if (k + (0 if schedule == "sr" else 1)) <= ev])
+                                for pi, ev in zip(per_iter, events)]))
+    else:
+        dom_ms = ph_ms[dom] / max(ph_n[dom], 1)
+    return {"t_ms": t_ms, "iters_done": iters_done, "value": value, "value_window": value_window,
+            "launches": launches, "ph_ms": ph_ms, "ph_n": ph_n, "dom_ms": dom_ms, "events": ev_rec,
+            "status": sten.STATUS_NAMES.get(status, status), "final_rel_residual": float(hist[-1]),
+            "hist_10": float(hist[min(10, len(hist) - 1)]), "clocks": clk}
+
+
 def run_sten(args):
     import torch
     import torch.distributed as dist
@@ -226,7 +381,8 @@ def run_sten(args):
     # weak scaling (config 5): every rank owns one args.nz-plane slab of the global mesh;
     # strong scaling (config 4): the args.nz planes are split over the ranks
     strong = workload == "cfg4"
-    z0, nzl = sdist.slab_of(rank, world, args.nz if strong else args.nz * world)
+    nz_global = args.nz if strong else args.nz * world
+    z0, nzl = sdist.slab_of(rank, world, nz_global)
 
     comm = None
     if world > 1:
@@ -234,8 +390,9 @@ def run_sten(args):
 
     # problem: fields of this rank's slab generated on the device (inputs/gen_cuda.cu)
     kind = inputs.KIND_CD_WEAK if workload == "cfg5" else inputs.KIND_CD
-    kz = inputs.weak_kz_table(nzl * n) if kind == inputs.KIND_CD_WEAK else None
-    if args.operator == "poisson-const":
+    kz = inputs.weak_kz_table(nz_global) if kind == inputs.KIND_CD_WEAK else None
+    const_op = args.operator == "poisson-const"
+    if const_op:
         st = sten.stencil_create_const(NX, NY, nzl, (6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0), nslabs=1, comm=comm)
     else:
         diag, offs = icuda.fields_device(kind, NX, NY, nzl, z0=z0, seed=1, delta=0.1, kz_table=kz)
@@ -246,82 +403,81 @@ def run_sten(args):
     if args.tiling:
         bx, by, zc, stg = (int(v) for v in args.tiling.split(","))
         sten.set_tiling(st, prec, bx, by, zc, stg)
-    sr = args.schedule == "sr"
-    sten.set_schedule(st, sten.SCHED_SR if sr else sten.SCHED_CLASSIC)
-    if sr and world > 1 and os.environ.get("STEN_P2P", "0") == "1":
-        sten.p2p_setup(st, prec)  # fused peer-memory halos + all-reduce across ranks (opt-in)
     if args.sr_tiling:
         sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
     if args.dots == "half":
         sten.set_dot_precision(st, sten.DOTS_HALF)
+    if world > 1 and os.environ.get("STEN_P2P", "0") == "1":
+        sten.set_schedule(st, sten.SCHED_SR)
+        sten.p2p_setup(st, prec)  # fused peer-memory halos + all-reduce across ranks (opt-in, SR)
     b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)
     x = torch.empty_like(b)
-    maxit = args.maxit
     npts_local = NX * NY * nzl
     npts = npts_local * n
+    pname = "mixed" if prec == sten.MIXED else "fp32"
+    peak, peak_kind = measured_peak()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    # the headline schedule first, then (unless --no-sr / it is the headline) the SR schedule
+    head = args.schedule
+    scheds = [head] + ([] if args.no_other else [s_ for s_ in ("classic", "sr") if s_ != head])
+    if const_op or args.dots == "half":
+        scheds = [s_ for s_ in scheds if s_ == "sr"] or ["sr"]
+        head = "sr"
+    recs = {}
+    for sch in scheds:
+        recs[sch] = run_schedule(sten, st, prec, sch, b, x, args, world, sdist, npts,
+                                 clocks_gpu=local if sch == head else None)
 
-    tol = args.tol
-    sten.set_timing(st, True)
-    for _ in range(args.warmup):
-        sten.bicgstab_solve(st, prec, b, None, tol, maxit, x)
-    torch.cuda.synchronize()
-    barrier()
-
-    stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
-    launches = 0
-    h1_ms, h1_n = 0.0, 0
-    ph_ms = [0.0, 0.0, 0.0]
-    iters_done = 0
-    barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    last = None
-    for _ in range(args.steps):
-        last = sten.bicgstab_solve(st, prec, b, None, tol, maxit, x)
-        iters_done += last[0]
-        s = sten.get_stats(st)
-        launches += s["kernel_launches"]
-        for p in range(3):
-            ph_ms[p] += s["phase_ms"][p]
-        h1_ms += s["phase_ms"][0]
-        h1_n += s["phase_launches"][0]
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    t_ms = sdist.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
-    it, hist, status = last
-    value = npts * iters_done / (t_ms / 1e3) / 1e9
+    def roofline_of(sch, r):
+        sr = sch == "sr"
+        kb = (roofline.sweep_bytes(pname, npts_local, const_op) if sr
+              else roofline.phase_bytes("H1", pname, npts_local))
+        achieved = kb / (r["dom_ms"] / 1e3) / 1e9
+        tname = "half" if prec == sten.MIXED else "float"
+        kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
+        traffic, traffic_src = (None, None)
+        if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
+            traffic, traffic_src = measured_traffic("k_sr<__half" if sr else "k_stencil<__half, 1")
+        passes = roofline.passes_per_iter(sch, const_op and sr)
+        bpi = roofline.bytes_per_point_iter(pname, sch, const_op and sr)
+        # whole step against the schedule's algorithmic bytes (classic: SURVEY 8(d)'s 29 passes)
+        whole_gbs = npts_local * r["iters_done"] * bpi / (r["t_ms"] / 1e3) / 1e9
+        whole_gbs_v = r["value"] / n * bpi  # Gpt-iter/s per GPU x B/pt-iter = GB/s
+        phase_n = max(r["ph_n"][0], 1)
+        return {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": kb, "avg_launch_ms": r["dom_ms"],
+                "passes_per_iter": passes, "bytes_per_point_iter": bpi,
+                "whole_step_frac": whole_gbs / peak, "whole_step_frac_value_basis": whole_gbs_v / peak,
+                "phase_ms_per_iter": [p / phase_n for p in r["ph_ms"]][:1 if sr else 3]}
 
     # end to end through the C ABI with pinned HOST buffers: one bicgstab_solve_batch call
     # solves the K steps' systems, every step's b uploaded and x downloaded (pipelined
     # with the neighbouring steps' solves on the library's copy stream)
-    e2e = None
-    if not args.no_e2e:
+    def e2e_of(sch):
+        sten.set_schedule(st, sten.SCHED_SR if sch == "sr" else sten.SCHED_CLASSIC)
         bh = [b.cpu().pin_memory() for _ in range(2)]
         xh = [torch.empty_like(bh[0]).pin_memory() for _ in range(2)]
         sten.set_timing(st, False)
-        sten.bicgstab_solve_batch(st, prec, bh, xh, tol, maxit)
-        barrier()
+        sten.bicgstab_solve_batch(st, prec, bh, xh, args.tol, args.maxit)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = sten.bicgstab_solve_batch(st, prec, [bh[i % 2] for i in range(args.steps)],
-                                        [xh[i % 2] for i in range(args.steps)], tol, maxit)
+                                        [xh[i % 2] for i in range(args.steps)], args.tol, args.maxit)
         torch.cuda.synchronize()
         te = sdist.max_over_ranks(time.perf_counter() - t0, device="cuda")
-        e_iters = sum(r[0] for r in res)
+        e_iters = sum(r_[0] for r_ in res)
         esz = b.element_size()
-        e2e = {"value": npts * e_iters / te / 1e9, "unit": "Gpoint-iter/s",
-               "h2d_bytes_per_step": npts_local * esz,
-               "d2h_bytes_per_step": npts_local * esz + 8 * (e_iters // max(args.steps, 1) + 1),
-               "api": "bicgstab_solve_batch (pinned host b in, x out every step; copies overlap the "
-                      "neighbouring steps' solves)", "clock": "host wall clock around the call"}
+        return {"value": npts * e_iters / te / 1e9, "unit": "Gpoint-iter/s",
+                "h2d_bytes_per_step": npts_local * esz,
+                "d2h_bytes_per_step": npts_local * esz + 8 * (e_iters // max(args.steps, 1) + 1),
+                "schedule": sch,
+                "api": "bicgstab_solve_batch (pinned host b in, x out every step; copies overlap the "
+                       "neighbouring steps' solves)", "clock": "host wall clock around the call"}
+
+    e2e = {} if args.no_e2e else {sch: e2e_of(sch) for sch in scheds}
 
     if rank != 0:
         if world > 1:
@@ -329,47 +485,45 @@ def run_sten(args):
             dist.destroy_process_group()
         return 0
 
-    peak, peak_kind = measured_peak()
-    pname = "mixed" if prec == sten.MIXED else "fp32"
-    h1_avg_ms = h1_ms / max(h1_n, 1)
-    # dominant kernel: the SR sweep (one per iteration) or the classic H1 stencil
-    const_op = args.operator == "poisson-const"
-    h1_bytes = (roofline.sweep_bytes(pname, npts_local, const_op) if sr
-                else roofline.phase_bytes("H1", pname, npts_local))
-    achieved = h1_bytes / (h1_avg_ms / 1e3) / 1e9
-    bpi = roofline.bytes_per_point_iter(pname, args.schedule, const_op and sr)
-    whole_gbs = npts_local * iters_done * bpi / (t_ms / 1e3) / 1e9
-    tname = "half" if prec == sten.MIXED else "float"
-    kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
-    traffic, traffic_src = (None, None)
-    if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
-        traffic, traffic_src = measured_traffic("k_sr<__half" if sr else "k_stencil<__half, 1")
+    h = recs[head]
+    sched_names = {"classic": "Alg. 1 as printed (PAPER.md:172-186): H1, H2, H3, 3 reductions, 29 passes",
+                   "sr": "single-reduction sweep (DESIGN.md R19, SURVEY 8(f) NEXT-1): 19 passes, 1 reduction"}
     line = {
-        "metric": METRIC, "value": value, "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": h["value"], "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": h["t_ms"] / args.steps, "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
-        "vs_baseline": value / PAPER_GPT_ITER_S,
+        "vs_baseline": h["value"] / PAPER_GPT_ITER_S,
         "dtype": "f16" if prec == sten.MIXED else "f32", "data": "synthetic",
-        "config": {"workload": workload, "mesh": [NX, NY, nzl * n], "mesh_per_gpu": [NX, NY, nzl],
-                   "precision": pname, "schedule": args.schedule, "operator": args.operator,
+        "config": {"workload": workload, "mesh": [NX, NY, nz_global], "mesh_per_gpu": [NX, NY, nzl],
+                   "precision": pname, "schedule": head, "schedule_is": sched_names[head],
+                   "operator": args.operator,
                    **({"dots": "half"} if args.dots == "half" and prec == sten.MIXED else {}),
-                   "maxit": maxit, "tol": tol,
-                   "iters_per_solve": iters_done / args.steps,
+                   "maxit": args.maxit, "tol": args.tol,
+                   "iters_per_solve": h["iters_done"] / args.steps,
                    "parallelism": f"zslab{n}",
                    "l2": "no flush: 16.5 GB working set per GPU >> 126 MB L2",
-                   "gflops": value * roofline.FLOPS_PER_POINT_ITER,
-                   "hbm_frac_whole_step": whole_gbs / peak, "bytes_per_point_iter": bpi,
-                   "status": sten.STATUS_NAMES.get(status, status), "final_rel_residual": float(hist[-1])},
-        "roofline": {"bound": "hbm", "kernel": kname,
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": h1_bytes, "avg_launch_ms": h1_avg_ms,
-                     "phase_ms_per_iter": [p / max(h1_n, 1) for p in ph_ms][:1 if sr else 3]},
-        "gpu_launches": int(launches),
-        "clocks": clk,
+                   "gflops": h["value"] * roofline.FLOPS_PER_POINT_ITER,
+                   "status": h["status"], "final_rel_residual": h["final_rel_residual"],
+                   "rel_residual_iter10": h["hist_10"],
+                   "events": h["events"],
+                   "paper_cs1_gpt_iter_s_context": PAPER_GPT_ITER_S},
+        "roofline": roofline_of(head, h),
+        "gpu_launches": int(h["launches"]),
+        "clocks": h["clocks"],
     }
-    if e2e:
-        line["e2e"] = e2e
+    if head in e2e:
+        line["e2e"] = e2e[head]
+    for sch in scheds:
+        if sch == head:
+            continue
+        r = recs[sch]
+        line[sch] = {"label": sched_names[sch], "value": r["value"], "unit": "Gpoint-iter/s",
+                     "ms_per_step": r["t_ms"] / args.steps, "iters_per_solve": r["iters_done"] / args.steps,
+                     "gflops": r["value"] * roofline.FLOPS_PER_POINT_ITER,
+                     "status": r["status"], "final_rel_residual": r["final_rel_residual"],
+                     "rel_residual_iter10": r["hist_10"], "events": r["events"],
+                     "roofline": roofline_of(sch, r), "gpu_launches": int(r["launches"]),
+                     **({"e2e": e2e[sch]} if sch in e2e else {})}
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_auto(pname, workload, args.cpu_planes)
     print(json.dumps(line), flush=True)

@@ -226,6 +226,15 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
 /* Record per-phase CUDA events inside the solve's graphs (enable != 0). */
 int sten_set_timing(sten_stencil *st, int enable);
 int sten_get_stats(sten_stencil *st, sten_stats *out);
+/* Device time of each iteration of the last bicgstab_solve run with timing on,
+ * in iteration order: phase 0/1/2 = the H1/H2/H3 kernel's events, -1 = their
+ * sum (SR: phase 0 = the sweep, index 0 = sweep 0; phases 1, 2 read 0).
+ * Writes min(cap, n) floats to out (host) and the number of iterations timed to
+ * *n.  Iterations that the device state turned into no-ops (after a stop) are
+ * not included; the SR solve's light last sweep (k_sr_last) is not timed.
+ * Errors: STEN_EINVAL (NULL handle / n, out == NULL with cap > 0, phase not
+ * in -1..2). */
+int sten_iter_ms(sten_stencil *st, int phase, float *out, int cap, int *n);
 
 /* Select the iteration schedule of later bicgstab_solve calls on this handle.
  *   STEN_SCHED_CLASSIC: Algorithm 1 exactly as printed:

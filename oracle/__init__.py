@@ -57,6 +57,7 @@ def _declare(L):
     L.o64_apply.argtypes = [_I, _I, _I, _P, _P, _P]
     L.o64_apply_raw.argtypes = [_I, _I, _I, _P, _P, _P, _P]
     L.o64_dot.argtypes = [_I64, _P, _P]
+    L.oracle_set_threads.argtypes = [_I]
     L.o64_dot.restype = _D
     L.o64_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
     L.o64_bicgstab.restype = _I
@@ -451,6 +452,11 @@ def apply32_fma(c32, v32):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's loops (timing only)."""
+    lib().oracle_set_threads(int(n))
 
 
 # ---------------- quantisation helpers (R3: RN from the fp64 scaled value) ----

@@ -27,6 +27,15 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops (timing of the oracle on 1 thread vs all cores). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 static int64_t idx3(int nx, int ny, int i, int j, int k) {
   return (int64_t)i + (int64_t)nx * ((int64_t)j + (int64_t)ny * (int64_t)k);
 }

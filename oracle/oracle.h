@@ -175,6 +175,7 @@ void o32_apply9(int nx, int ny, const float *const c[8], const float *v, float *
 
 /* informational */
 int oracle_num_threads(void);
+void oracle_set_threads(int n);
 
 #ifdef __cplusplus
 }

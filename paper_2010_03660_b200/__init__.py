@@ -77,6 +77,7 @@ def lib():
         L.sten_scalar_history.argtypes = [P, I, P, P]
         L.sten_set_timing.argtypes = [P, I]
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
+        L.sten_iter_ms.argtypes = [P, I, ctypes.POINTER(ctypes.c_float), I, ctypes.POINTER(ctypes.c_int)]
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
         L.sten_set_schedule.argtypes = [P, I]
         L.sten_set_dot_precision.argtypes = [P, I]
@@ -298,6 +299,16 @@ def get_stats(st: Stencil) -> dict:
     _check(lib().sten_get_stats(st.handle, ctypes.byref(s)))
     return dict(phase_ms=list(s.phase_ms), phase_launches=list(s.phase_launches), solve_ms=s.solve_ms,
                 kernel_launches=s.kernel_launches, event_iter=s.event_iter, graph_chunk=s.graph_chunk)
+
+
+def iter_ms(st: Stencil, phase: int = -1) -> list:
+    """Per-iteration device ms of the last timed solve (sten_iter_ms): phase 0-2 = H1/H2/H3
+    (SR: 0 = the sweep), -1 = the sum."""
+    n = ctypes.c_int(0)
+    _check(lib().sten_iter_ms(st.handle, phase, None, 0, ctypes.byref(n)))
+    buf = (ctypes.c_float * max(n.value, 1))()
+    _check(lib().sten_iter_ms(st.handle, phase, buf, n.value, ctypes.byref(n)))
+    return [float(buf[i]) for i in range(n.value)]
 
 
 def set_tiling(st: Stencil, precision: int, bx: int = 0, by: int = 0, zc: int = 0, stages: int = 0):

@@ -216,6 +216,7 @@ struct sten_stencil {
   int coef_pf = 0;              // L2 prefetch distance of coefficient tiles (tuning knob STEN_COEF_PF)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   sten_stats stats{};
+  std::vector<float> iter_ms;   // [it][3] per-iteration phase ms of the last timed bicgstab_solve
   long long launches = 0;       // kernel launches (direct + graph nodes) of the current call
   void *stage = nullptr;        // contiguous device staging for pitched host copies
   size_t stage_bytes = 0;
@@ -1432,6 +1433,7 @@ struct SolveOut {
   long long kernels = 0;
   double ph_ms[3] = {0, 0, 0};
   long long ph_n[3] = {0, 0, 0};
+  std::vector<float> iter_ms;  // device ms of each timed iteration: [it][H1, H2, H3] (SR: [it][sweep, 0, 0])
 };
 static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, double tol, int maxit, cudaStream_t s,
                       SolveOut *out) {
@@ -1516,6 +1518,7 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
           const int first = rep * chunk;
           for (int j = 0; j < chunk; ++j) {
             if (sr ? first + j > done_it : first + j >= done_it) break;  // later kernels were no-ops
+            float it_ms[3] = {0.f, 0.f, 0.f};
             for (int p = 0; p < (sr ? 1 : 3); ++p) {
               float ms = 0.f;
               cudaError_t te =
@@ -1525,7 +1528,9 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
                                cudaGetErrorString(te));
               out->ph_ms[p] += ms;
               out->ph_n[p] += 1;
+              it_ms[p] = ms;
             }
+            out->iter_ms.insert(out->iter_ms.end(), it_ms, it_ms + 3);
           }
         }
         if (st->st_host->stop || st->st_host->it >= maxit) break;
@@ -1606,6 +1611,18 @@ int bicgstab_solve(sten_stencil *st, int prec, const void *b, const void *x0, do
   st->stats.kernel_launches = st->launches + so.kernels;
   st->stats.event_iter = fin.ev >= 0 ? fin.ev_it : 0;
   st->stats.graph_chunk = so.chunk;
+  st->iter_ms = so.iter_ms;
+  return STEN_OK;
+}
+
+int sten_iter_ms(sten_stencil *st, int phase, float *out, int cap, int *n) {
+  if (!st || !n || (cap > 0 && !out)) return set_err(STEN_EINVAL, "NULL argument");
+  if (phase < -1 || phase > 2) return set_err(STEN_EINVAL, "phase %d not in -1..2", phase);
+  *n = (int)(st->iter_ms.size() / 3);
+  for (int i = 0; i < cap && i < *n; ++i) {
+    const float *m = &st->iter_ms[(size_t)i * 3];
+    out[i] = phase < 0 ? m[0] + m[1] + m[2] : m[phase];
+  }
   return STEN_OK;
 }
 
