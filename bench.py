@@ -393,10 +393,10 @@ def run_sten(args):
     kz = inputs.weak_kz_table(nz_global) if kind == inputs.KIND_CD_WEAK else None
     const_op = args.operator == "poisson-const"
     if const_op:
-        st = sten.stencil_create_const(NX, NY, nzl, (6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0), nslabs=1, comm=comm)
+        st = sten.stencil_create_const(NX, NY, nz_global, (6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0), nslabs=1, comm=comm)
     else:
         diag, offs = icuda.fields_device(kind, NX, NY, nzl, z0=z0, seed=1, delta=0.1, kz_table=kz)
-        st = sten.stencil_create(NX, NY, nzl, [diag] + offs, nslabs=1, comm=comm)
+        st = sten.stencil_create(NX, NY, nz_global, [diag] + offs, nslabs=1, comm=comm)
         del diag, offs
     torch.cuda.synchronize()
     torch.cuda.empty_cache()

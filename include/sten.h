@@ -85,6 +85,8 @@ extern "C" {
 #define STEN_MAXIT 1     /* maxit iterations done without an event             */
 #define STEN_BREAKDOWN 2 /* (rhat, v) == 0, omega == 0 or (rhat, r_new) == 0   */
 #define STEN_NONFINITE 3 /* a dot product or scalar became Inf/NaN             */
+#define STEN_TIMEOUT 4   /* peer-memory all-reduce: a rank's sums never arrived
+                            (bounded ~20 s wait; a dead or stalled peer) */
 
 typedef struct sten_comm sten_comm;       /* opaque: NCCL communicator wrapper */
 typedef struct sten_stencil sten_stencil; /* opaque: operator + solver workspace */
@@ -108,32 +110,43 @@ const char *sten_last_error(void);
 /* Write a fresh ncclUniqueId (128 bytes) into id_out; call on rank 0 and
  * broadcast the bytes to the other ranks by any means. */
 int sten_comm_unique_id(void *id_out);
-/* Create the communicator of rank `rank` of `nranks` on the CURRENT CUDA
- * device.  NCCL is loaded at run time (libnccl.so.2).  Errors: STEN_EINVAL
- * (bad rank/nranks), STEN_ENCCL (NCCL missing or ncclCommInitRank failed). */
-int sten_comm_create(const void *unique_id, int nranks, int rank, sten_comm **out);
+/* Create the communicator of rank `rank` of `nranks` on CUDA device
+ * `cuda_device`, which becomes the calling thread's current device; handles
+ * built on the communicator must be created and used with that device current.
+ *   unique_id != NULL: NCCL (loaded at run time, libnccl.so.2) carries the
+ *     halo planes and the fp32 all-reduces of every schedule;
+ *   unique_id == NULL: a peer-memory-only communicator (no NCCL): the only
+ *     supported solve is the SR schedule with the fused exchange after
+ *     sten_p2p_import (CUDA IPC peer stores and the one-shot peer all-reduce;
+ *     x0 == NULL); everything else returns STEN_EUNSUPPORTED.
+ * Errors: STEN_EINVAL (bad rank/nranks/cuda_device), STEN_ECUDA, STEN_ENCCL
+ * (NCCL missing or ncclCommInitRank failed). */
+int sten_comm_create(const void *unique_id, int nranks, int rank, int cuda_device, sten_comm **out);
 void sten_comm_destroy(sten_comm *comm);
 
 /* ------------------------------------------------------------- stencil -- */
-/* Build the Jacobi-scaled operator of this rank's nx*ny*nz points.
+/* Build the Jacobi-scaled operator of an nx*ny*nz_global mesh; this rank owns
+ * planes [r*nz_global/R, (r+1)*nz_global/R) of it (R ranks of `comm`, 1
+ * without one; rank order = z order) and passes only those planes.
  *   coeffs[0]   : main diagonal a_P of A, or NULL if A already has a unit
  *                 diagonal;
  *   coeffs[1..6]: off-diagonal entries of A coupling P to its -x, +x, -y, +y,
  *                 -z, +z neighbour (A[P, P-1], A[P, P+1], A[P, P-nx], ...);
- *   all dense (nz, ny, nx) arrays of coeff_dtype (STEN_DT_F64 or _F32), host
- *   or device; they are copied, the caller keeps ownership.
+ *   all dense (nz_global/R, ny, nx) arrays of coeff_dtype (STEN_DT_F64 or
+ *   _F32), host or device; they are copied, the caller keeps ownership.
  * The library forms c_d = A_d / a_P in fp64 (c_d = A_d without a diagonal),
  * drops couplings to points outside the global mesh (Dirichlet zero), and
  * stores c_d rounded to nearest in fp32 AND in fp16 (R3, R5), plus a_P in fp64
  * to scale right-hand sides.
  *   nslabs >= 1: split this rank's planes into nslabs z-slabs with one-plane
  *                halos exchanged by device copies - the same halo/reduction
- *                path as multi-GPU, for testing it on one GPU (nz % nslabs
- *                must be 0; 1 for normal use);
- *   comm: NULL for a single rank, else this rank's communicator.
- * Errors: STEN_EINVAL (sizes <= 0, nz % nslabs, NULL coefficient),
- * STEN_ENOMEM, STEN_ECUDA. */
-int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype,
+ *                path as multi-GPU, for testing it on one GPU ((nz_global/R)
+ *                % nslabs must be 0; 1 for normal use);
+ *   comm: NULL for a single rank, else this rank's communicator (its device
+ *         must be current).
+ * Errors: STEN_EINVAL (sizes <= 0, nz_global % R, (nz_global/R) % nslabs,
+ * NULL coefficient, wrong current device), STEN_ENOMEM, STEN_ECUDA. */
+int stencil_create(int nx, int ny, int nz_global, const void *const coeffs[7], int coeff_dtype,
                    int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out);
 /* The same for a CONSTANT-coefficient operator (e.g. the
  * Poisson stencil of BASELINE config 1): coeffs[0..6] = a_P, A_xm, A_xp,
@@ -146,7 +159,7 @@ int stencil_create(int nx, int ny, int nz, const void *const coeffs[7], int coef
  * of stencil_create on the same constant fields (bitwise up to the sign of
  * zero).  Errors: STEN_EINVAL (non-finite coefficient, a_P == 0, sizes),
  * STEN_ENOMEM, STEN_ECUDA. */
-int stencil_create_const(int nx, int ny, int nz, const double coeffs[7], int nslabs, sten_comm *comm,
+int stencil_create_const(int nx, int ny, int nz_global, const double coeffs[7], int nslabs, sten_comm *comm,
                          void *cuda_stream, sten_stencil **out);
 void stencil_destroy(sten_stencil *st);
 
@@ -222,6 +235,35 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
 /* Per-iteration scalars alpha_i, omega_i (i = 1..n) of the last solve, as
  * computed on the device (fp32), for parity checks.  n <= iters. */
 int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
+
+/* Tuning options of a handle (the library reads no environment variables:
+ * every knob is an explicit call).  Changing one drops the handle's cached
+ * graphs.  Errors: STEN_EINVAL (NULL handle, unknown option, value out of
+ * range).
+ *   STEN_OPT_TMA_L2_PROMOTION  L2 promotion of every TMA tensor map: 0 none,
+ *                              1 64 B, 2 128 B, 3 256 B (default 3)
+ *   STEN_OPT_EW_CTAS_PER_SM    CTAs per SM of the element-wise kernels (H3,
+ *                              init, refinement), 1..64 (default 64)
+ *   STEN_OPT_COEF_PREFETCH     classic kernels with per-thread coefficient
+ *                              loads (sten_set_tiling with explicit stages):
+ *                              L2 prefetch distance in planes, 0..16 (default 0)
+ *   STEN_OPT_SR_L2_PREFETCH    SR sweep: L2 prefetch distance, 0..16 (default 0)
+ *   STEN_OPT_SR_LIGHT_LAST     SR on one slab: the last sweep of a solve
+ *                              without its SpMVs (k_sr_last), 0 or 1 (default 1)
+ *   STEN_OPT_CLASSIC_OVERLAP   classic schedule, decomposed (slabs >= 3
+ *                              planes): the halo exchange before H1 / H2 runs
+ *                              on a side stream with the two boundary planes,
+ *                              concurrent with the interior planes, 0 or 1
+ *                              (default 1).  Changes only the order in which
+ *                              the phase sums are added. */
+#define STEN_OPT_TMA_L2_PROMOTION 1
+#define STEN_OPT_EW_CTAS_PER_SM 2
+#define STEN_OPT_COEF_PREFETCH 3
+#define STEN_OPT_SR_L2_PREFETCH 4
+#define STEN_OPT_SR_LIGHT_LAST 5
+#define STEN_OPT_CLASSIC_OVERLAP 6
+int sten_set_option(sten_stencil *st, int option, int value);
+int sten_get_option(sten_stencil *st, int option, int *value);
 
 /* Record per-phase CUDA events inside the solve's graphs (enable != 0). */
 int sten_set_timing(sten_stencil *st, int enable);
@@ -301,19 +343,26 @@ int sten_sr_sweep(sten_stencil *st, int precision, double alpha, double omega, d
  *                      planes straight into the z-neighbours' halo buffers (peer
  *                      memory) and deposits its sums in every participant's inbox
  *                      (one-shot all-reduce, flags with system-scope release /
- *                      acquire); a 1-thread kernel waits (bounded: ~20 s, then
- *                      STEN_NONFINITE) and runs the scalar step.  Loopback slabs and
- *                      1-rank communicators use it directly; across ranks it needs
- *                      sten_p2p_import (else the handle falls back to OVERLAP).
- * Default: FUSED (STEN_SR_P2P=0 in the environment selects OVERLAP).  SERIAL and
- * FUSED add the slab sums in the same order: their results are bitwise equal. */
+ *                      acquire, inboxes double-buffered by the parity of the
+ *                      sweep); a 1-thread kernel waits (bounded: ~20 s, then the
+ *                      solve stops with status STEN_TIMEOUT) and runs the scalar
+ *                      step.  Loopback slabs and 1-rank communicators use it
+ *                      directly; across ranks it needs sten_p2p_import (else the
+ *                      handle falls back to OVERLAP).
+ * Default: FUSED.  SERIAL and FUSED add the slab sums in the same order: their
+ * results are bitwise equal. */
 /* Peer memory across ranks (one node, NVLink/NVSwitch): export writes CUDA IPC
- * handles of this rank's boundary-slab SR buffers and its inbox for `precision`
- * (out == NULL: *bytes = the record size); every rank passes all ranks'
- * records, in rank order, to import, which opens the z-neighbours' buffers and
- * the other inboxes and selects STEN_XCHG_FUSED across ranks.  All ranks must
- * import before the next solve.  Errors: STEN_EINVAL, STEN_EUNSUPPORTED (> 8
- * ranks), STEN_ECUDA (IPC). */
+ * handles of this rank's boundary-slab SR buffers, its inbox and its boundary
+ * slabs' coefficient arrays for `precision` (out == NULL: *bytes = the record
+ * size); every rank passes all ranks' records, in rank order, to import, which
+ * opens the z-neighbours' buffers and the other inboxes and selects
+ * STEN_XCHG_FUSED across ranks.  With a peer-memory-only communicator
+ * (sten_comm_create with unique_id == NULL) import also copies the
+ * z-neighbours' boundary coefficient planes into this rank's coefficient halo
+ * planes (NCCL does it at create otherwise), so every rank must have finished
+ * stencil_create before any rank imports.  All ranks must import before the
+ * next solve.  Errors: STEN_EINVAL, STEN_EUNSUPPORTED (> 8 ranks), STEN_ECUDA
+ * (IPC). */
 int sten_p2p_export(sten_stencil *st, int precision, void *out, size_t *bytes);
 int sten_p2p_import(sten_stencil *st, int precision, const void *all, size_t bytes_per_rank);
 
@@ -321,6 +370,18 @@ int sten_p2p_import(sten_stencil *st, int precision, const void *all, size_t byt
 #define STEN_XCHG_OVERLAP 1
 #define STEN_XCHG_FUSED 2
 int sten_set_sr_exchange(sten_stencil *st, int mode);
+
+/* Host lockstep for several ranks sharing ONE GPU (tests of the cross-rank
+ * peer-memory path; fn == NULL turns it off).  Kernels that wait on a flag
+ * written by another process's kernel are not guaranteed to make progress when
+ * both processes share a GPU (a context-switch timeout, Xid 109, on B200), so
+ * with a barrier set and a peer-memory-only communicator the solve runs sweep by
+ * sweep without graphs and, before every peer-memory all-reduce's waiting
+ * kernel, synchronises its stream and calls fn(ctx) - which must return only
+ * after every rank has called it for the same reduction (e.g. a gloo barrier).
+ * The waiting kernel then finds every peer's sums already deposited.  Results
+ * are bitwise those of the unsynchronised path.  Errors: STEN_EINVAL. */
+int sten_set_host_barrier(sten_stencil *st, void (*fn)(void *ctx), void *ctx);
 
 /* SR kernel geometry for tuning (0 = default): by rows per tile (8 or 16),
  * stages input TMA stages, cstages coefficient stages, zc planes per CTA

@@ -24,11 +24,13 @@ SCHED_CLASSIC = 0
 SCHED_SR = 1
 DOTS_MIXED, DOTS_HALF = 0, 1
 XCHG_SERIAL, XCHG_OVERLAP, XCHG_FUSED = 0, 1, 2
+(OPT_TMA_L2_PROMOTION, OPT_EW_CTAS_PER_SM, OPT_COEF_PREFETCH, OPT_SR_L2_PREFETCH, OPT_SR_LIGHT_LAST,
+ OPT_CLASSIC_OVERLAP) = 1, 2, 3, 4, 5, 6
 DT_F64 = 0
 DT_F32 = 1
 
-CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3
-STATUS_NAMES = {0: "converged", 1: "maxit", 2: "breakdown", 3: "nonfinite"}
+CONVERGED, MAXIT, BREAKDOWN, NONFINITE, TIMEOUT = 0, 1, 2, 3, 4
+STATUS_NAMES = {0: "converged", 1: "maxit", 2: "breakdown", 3: "nonfinite", 4: "timeout"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsten.so")
@@ -36,6 +38,9 @@ LIB_PATH = os.path.join(_HERE, "libsten.so")
 
 class StenError(RuntimeError):
     pass
+
+
+_BARRIER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
 
 
 class _Stats(ctypes.Structure):
@@ -62,7 +67,7 @@ def lib():
         L.sten_version.restype = I
         L.sten_last_error.restype = ctypes.c_char_p
         L.sten_comm_unique_id.argtypes = [P]
-        L.sten_comm_create.argtypes = [P, I, I, ctypes.POINTER(P)]
+        L.sten_comm_create.argtypes = [P, I, I, I, ctypes.POINTER(P)]
         L.sten_comm_destroy.argtypes = [P]
         L.stencil_create.argtypes = [I, I, I, P, I, I, P, P, ctypes.POINTER(P)]
         L.stencil_destroy.argtypes = [P]
@@ -76,6 +81,9 @@ def lib():
         L.bicgstab_solve_batch.argtypes = [P, I, I, P, P, D, I, P, P, P, P]
         L.sten_scalar_history.argtypes = [P, I, P, P]
         L.sten_set_timing.argtypes = [P, I]
+        L.sten_set_option.argtypes = [P, I, I]
+        L.sten_set_host_barrier.argtypes = [P, _BARRIER_FN, P]
+        L.sten_get_option.argtypes = [P, I, ctypes.POINTER(ctypes.c_int)]
         L.sten_get_stats.argtypes = [P, ctypes.POINTER(_Stats)]
         L.sten_iter_ms.argtypes = [P, I, ctypes.POINTER(ctypes.c_float), I, ctypes.POINTER(ctypes.c_int)]
         L.sten_set_tiling.argtypes = [P, I, I, I, I, I]
@@ -170,10 +178,15 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
-def comm_create(unique_id: bytes, nranks: int, rank: int) -> Comm:
+def comm_create(unique_id: bytes | None, nranks: int, rank: int, cuda_device: int | None = None) -> Comm:
+    """sten_comm_create on `cuda_device` (default: the current device).  unique_id None gives a
+    peer-memory-only communicator (no NCCL; SR schedule with the fused exchange only)."""
+    if cuda_device is None:
+        import torch
+        cuda_device = torch.cuda.current_device()
     h = ctypes.c_void_p()
-    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
-    _check(lib().sten_comm_create(buf, nranks, rank, ctypes.byref(h)))
+    buf = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(lib().sten_comm_create(buf, nranks, rank, int(cuda_device), ctypes.byref(h)))
     return Comm(h, nranks, rank)
 
 
@@ -200,9 +213,14 @@ class Stencil:
             pass
 
 
-def stencil_create(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
+def stencil_create(nx: int, ny: int, nz_global: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
                    stream=None) -> Stencil:
-    """coeffs = [diag or None, A_xm, A_xp, A_ym, A_yp, A_zm, A_zp], dense (nz,ny,nx) each."""
+    """coeffs = [diag or None, A_xm, A_xp, A_ym, A_yp, A_zm, A_zp], dense (nz, ny, nx) each with
+    nz = nz_global / comm.nranks: this rank's z-slab (sten.h slab convention)."""
+    R = comm.nranks if comm else 1
+    if nz_global % R:
+        raise StenError(f"nz_global={nz_global} not divisible by {R} ranks")
+    nz = nz_global // R
     if len(coeffs) != 7:
         raise StenError("coeffs must have 7 entries (diag, xm, xp, ym, yp, zm, zp)")
     ref = next(c for c in coeffs[1:] if c is not None)
@@ -219,21 +237,24 @@ def stencil_create(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Com
         keep.append(c)
         arr[i] = _ptr(c).value
     h = ctypes.c_void_p()
-    _check(lib().stencil_create(nx, ny, nz, arr, dt, nslabs, comm.handle if comm else None,
+    _check(lib().stencil_create(nx, ny, nz_global, arr, dt, nslabs, comm.handle if comm else None,
                                 _stream(stream), ctypes.byref(h)))
     return Stencil(h, nx, ny, nz, comm)
 
 
-def stencil_create_const(nx: int, ny: int, nz: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
+def stencil_create_const(nx: int, ny: int, nz_global: int, coeffs, nslabs: int = 1, comm: Comm | None = None,
                          stream=None) -> Stencil:
     """Constant operator: coeffs = (a_P, A_xm, A_xp, A_ym, A_yp, A_zm, A_zp) as 7 floats."""
+    R = comm.nranks if comm else 1
+    if nz_global % R:
+        raise StenError(f"nz_global={nz_global} not divisible by {R} ranks")
     if len(coeffs) != 7:
         raise StenError("coeffs must have 7 entries (diag, xm, xp, ym, yp, zm, zp)")
     arr = np.ascontiguousarray(coeffs, dtype=np.float64)
     h = ctypes.c_void_p()
-    _check(lib().stencil_create_const(nx, ny, nz, arr.ctypes.data_as(ctypes.c_void_p), nslabs,
+    _check(lib().stencil_create_const(nx, ny, nz_global, arr.ctypes.data_as(ctypes.c_void_p), nslabs,
                                       comm.handle if comm else None, _stream(stream), ctypes.byref(h)))
-    return Stencil(h, nx, ny, nz, comm)
+    return Stencil(h, nx, ny, nz_global // R, comm)
 
 
 def stencil_destroy(st: Stencil):
@@ -288,6 +309,26 @@ def scalar_history(st: Stencil, n: int):
     _check(lib().sten_scalar_history(st.handle, n, a.ctypes.data_as(ctypes.c_void_p),
                                      w.ctypes.data_as(ctypes.c_void_p)))
     return a, w
+
+
+def set_option(st: Stencil, option: int, value: int):
+    """sten_set_option: an explicit tuning knob of the handle (OPT_*)."""
+    _check(lib().sten_set_option(st.handle, int(option), int(value)))
+
+
+def get_option(st: Stencil, option: int) -> int:
+    v = ctypes.c_int(0)
+    _check(lib().sten_get_option(st.handle, int(option), ctypes.byref(v)))
+    return v.value
+
+
+def set_host_barrier(st: Stencil, fn):
+    """sten_set_host_barrier: fn() (a Python callable, e.g. torch.distributed.barrier over gloo) is
+    called before every peer-memory all-reduce's waiting kernel; None turns it off.  For several
+    ranks sharing one GPU only."""
+    cb = _BARRIER_FN(lambda _ctx: fn()) if fn is not None else _BARRIER_FN()
+    st._barrier_cb = cb  # keep the trampoline alive as long as the handle may call it
+    _check(lib().sten_set_host_barrier(st.handle, cb, None))
 
 
 def set_timing(st: Stencil, enable: bool):

@@ -91,8 +91,8 @@ static int nccl_load() {
   } while (0)
 
 struct sten_comm {
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;  // NULL: peer-memory-only communicator (no NCCL)
+  int nranks = 1, rank = 0, device = 0;
 };
 
 // -------------------------------------------------- tensor-map encoding --
@@ -109,19 +109,15 @@ static int load_encode() {
   g_encode = reinterpret_cast<EncodeTiledFn>(fn);
   return STEN_OK;
 }
-// 3D map over an array of `planes` planes of (ny rows x pitch elements), logical width nx.
-static long long g_plane_stride = 0;  // set by the caller (elements between z-planes)
-static int make_map(CUtensorMap *m, void *base, int elem, int nx, int ny, int planes, int pitch, int boxx, int boxy) {
+// 3D map over an array of `planes` planes of (ny rows x pitch elements, `pstride`
+// elements apart), logical width nx; `promo` = L2 promotion (0 none, 1 64 B, 2 128 B, 3 256 B).
+static int make_map_p(CUtensorMap *m, void *base, int elem, int nx, int ny, int planes, int pitch, long long pstride,
+                      int promo, int boxx, int boxy) {
   RC_TRY(load_encode());
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
-  cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)g_plane_stride * elem};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * elem, (cuuint64_t)pstride * elem};
   cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  static int promo = -1;
-  if (promo < 0) {
-    const char *e = getenv("STEN_TMA_PROMO");  // tuning knob: 0 none, 1 64B, 2 128B, 3 256B
-    promo = e ? atoi(e) : 3;
-  }
   const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUresult r = g_encode(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base,
@@ -213,7 +209,13 @@ struct sten_stencil {
   cudaStream_t cap = nullptr;   // capture stream
   std::map<GraphKey, GraphRec> graphs;
   bool timing = false;
-  int coef_pf = 0;              // L2 prefetch distance of coefficient tiles (tuning knob STEN_COEF_PF)
+  int coef_pf = 0;              // L2 prefetch distance of coefficient tiles (STEN_OPT_COEF_PREFETCH)
+  int tma_promo = 3;            // TMA L2 promotion of every tensor map (STEN_OPT_TMA_L2_PROMOTION)
+  int ew_bps = 64;              // element-wise kernels: CTAs per SM (STEN_OPT_EW_CTAS_PER_SM)
+  bool sr_light = true;         // SR, one slab: last sweep without its SpMVs (STEN_OPT_SR_LIGHT_LAST)
+  bool cls_overlap = true;      // classic, decomposed: halo exchange overlapped with the interior (STEN_OPT_CLASSIC_OVERLAP)
+  void (*barrier_fn)(void *) = nullptr;  // host lockstep of several ranks on ONE GPU (sten_set_host_barrier)
+  void *barrier_ctx = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   sten_stats stats{};
   std::vector<float> iter_ms;   // [it][3] per-iteration phase ms of the last timed bicgstab_solve
@@ -222,9 +224,9 @@ struct sten_stencil {
   size_t stage_bytes = 0;
   unsigned *ir_amax = nullptr;  // refinement: max|r| (float bits), sigma
   float *ir_sigma = nullptr;
-  int sr_l2pf = 0;              // SR: L2 prefetch distance (tuning knob STEN_SR_L2PF)
+  int sr_l2pf = 0;              // SR: L2 prefetch distance (STEN_OPT_SR_L2_PREFETCH)
   bool sr_overlap = true;       // SR, decomposed: halo exchange overlapped with the interior chunks
-  bool sr_p2p = true;           // SR, decomposed: fused halo stores + peer-memory all-reduce (STEN_SR_P2P)
+  bool sr_p2p = true;           // SR, decomposed: fused halo stores + peer-memory all-reduce (sten_set_sr_exchange)
   bool p2p_ranks = false;       // ... across ranks too (after sten_p2p_import: CUDA IPC peers)
   float *p2p_sums = nullptr;    // own inbox: [slots][kMaxDots]
   unsigned *p2p_flags = nullptr;  // [slots]
@@ -233,6 +235,7 @@ struct sten_stencil {
   std::vector<P2PBox> p2p_remote;           // other ranks' inboxes (IPC)
   void *p2p_lo[2][2][5] = {}, *p2p_hi[2][2][5] = {};  // [prec][set][vec]: the z-neighbour ranks' buffers (IPC)
   std::vector<void *> ipc_opened;
+  std::map<std::string, void *> ipc_map;  // IPC handle bytes -> mapped pointer
   cudaStream_t side = nullptr;  // capture side stream (exchange + boundary chunks)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   float *partials2 = nullptr;   // reduction scratch of the concurrent interior launch
@@ -249,6 +252,14 @@ struct sten_stencil {
 };
 
 static bool decomposed(const sten_stencil *st) { return st->nslabs > 1 || st->comm != nullptr; }
+// several ranks, no NCCL: only the fused SR path (CUDA IPC peer memory) moves data between them
+static bool p2p_only(const sten_stencil *st) { return st->comm && st->comm->nranks > 1 && !st->comm->comm; }
+static bool nccl_ranks(const sten_stencil *st) { return st->comm && st->comm->nranks > 1 && st->comm->comm; }
+// tensor map over one of the handle's z-major arrays (planes st->plane elements apart)
+static int make_map(const sten_stencil *st, CUtensorMap *m, void *base, int elem, int nx, int ny, int planes,
+                    int pitch, int boxx, int boxy) {
+  return make_map_p(m, base, elem, nx, ny, planes, pitch, st->plane, st->tma_promo, boxx, boxy);
+}
 static int esize(int prec) { return prec == STEN_FP32 ? 4 : 2; }
 
 static int rows_thr(int prec, int nx, int by) {
@@ -285,7 +296,6 @@ static void default_tiling(sten_stencil *st, int prec) {
   // 2.31 ms with per-thread coefficient loads, which straddle sectors on unpadded rows
   t.stages = 2;
   t.cstages = 2;
-  if (const char *e = getenv("STEN_CLS_TILING")) sscanf(e, "%d,%d", &t.stages, &t.cstages);  // tuning knob
   t.threads = prec == STEN_FP32 ? stencil_threads<float>(t.by) : stencil_threads<__half>(t.by);
 }
 
@@ -293,24 +303,23 @@ static int ensure_maps(sten_stencil *st, int prec) {
   const Tiling &t = st->tiling[prec];
   const int e = esize(prec);
   const int H = prec == STEN_FP32 ? 4 : 8;
-  g_plane_stride = st->plane;
   for (Slab &sl : st->slabs) {
     PrecBufs &b = sl.pb[prec];
     if (b.maps_ok) continue;
     const int planes = sl.nz + 2;
     const int hx = t.rows ? kRowBoxElems : t.bx + 2 * H, hy = t.by + 2;
     const int ix = t.rows ? kRowBoxElems : t.bx;  // interior box (coefficient / rhat prefetch)
-    RC_TRY(make_map(&b.m_r, b.r, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    RC_TRY(make_map(st, &b.m_r, b.r, e, st->nx, st->ny, planes, st->pitch, hx, hy));
     for (int i = 0; i < 2; ++i) {
-      RC_TRY(make_map(&b.m_p[i], b.p[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
-      RC_TRY(make_map(&b.m_v[i], b.v[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
+      RC_TRY(make_map(st, &b.m_p[i], b.p[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
+      RC_TRY(make_map(st, &b.m_v[i], b.v[i], e, st->nx, st->ny, planes, st->pitch, hx, hy));
     }
-    RC_TRY(make_map(&b.m_s, b.s, e, st->nx, st->ny, planes, st->pitch, hx, hy));
-    RC_TRY(make_map(&b.m_x, b.x, e, st->nx, st->ny, planes, st->pitch, hx, hy));
-    RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, planes, st->pitch, ix, t.by));
+    RC_TRY(make_map(st, &b.m_s, b.s, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    RC_TRY(make_map(st, &b.m_x, b.x, e, st->nx, st->ny, planes, st->pitch, hx, hy));
+    RC_TRY(make_map(st, &b.m_rh, b.rh, e, st->nx, st->ny, planes, st->pitch, ix, t.by));
     for (int d = 0; d < 6; ++d) {
       void *c = prec == STEN_FP32 ? (void *)sl.c32[d] : (void *)sl.c16[d];
-      RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz, st->pitch, ix, t.by));
+      RC_TRY(make_map(st, &b.m_c[d], c, e, st->nx, st->ny, sl.nz, st->pitch, ix, t.by));
     }
     b.maps_ok = true;
   }
@@ -353,6 +362,12 @@ static int ensure_bufs(sten_stencil *st, int prec) {
     st->partials_cap = need;
     drop_graphs(st);
   }
+  if (decomposed(st) && st->partials2_cap < st->partials_cap) {  // concurrent interior launches
+    if (st->partials2) cudaFree(st->partials2);
+    CUDA_TRY(cudaMalloc(&st->partials2, (size_t)st->partials_cap * kMaxDots * sizeof(float)));
+    st->partials2_cap = st->partials_cap;
+    drop_graphs(st);
+  }
   return STEN_OK;
 }
 
@@ -366,7 +381,13 @@ static Reduce make_red(sten_stencil *st, int slab) {
   return r;
 }
 
-static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int parity, cudaStream_t s) {
+// part: CLS_ALL planes [0, nz) of the slab; CLS_INTERIOR [1, nz-1) (no halo plane
+// read), CLS_BOTTOM plane 0, CLS_TOP plane nz-1 (decomposed, overlapped exchange:
+// each part deposits its sums in slot 3*slab + part - 1, CLS_INTERIOR with the
+// second reduction scratch because it runs concurrently with the other two)
+enum { CLS_ALL = 0, CLS_INTERIOR = 1, CLS_BOTTOM = 2, CLS_TOP = 3 };
+static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int parity, cudaStream_t s,
+                          int part = CLS_ALL) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   const Tiling &t = st->tiling[prec];
@@ -396,12 +417,23 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
   }
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
   a.zc = t.zc;
+  a.zlo = part == CLS_INTERIOR ? 1 : (part == CLS_TOP ? sl.nz - 1 : 0);
+  a.zhi = part == CLS_INTERIOR ? sl.nz - 1 : (part == CLS_BOTTOM ? 1 : sl.nz);
+  if (part == CLS_BOTTOM || part == CLS_TOP) a.zc = 1;
   a.pf = st->coef_pf;
   a.tiles_x = t.rows ? 1 : (st->nx + t.bx - 1) / t.bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
   if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + t.zc - 1) / t.zc) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: stencil grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
+  if (part != CLS_ALL) {
+    a.red.slab_out = st->slab_sums + (3 * slab + part - 1) * kMaxDots;
+    if (part == CLS_INTERIOR) {
+      a.red.partials = st->partials2;
+      a.red.counter = st->counter2;
+    }
+  }
+  if (a.zhi <= a.zlo) return STEN_OK;
   if (t.rows) {
     if (prec == STEN_FP32) KLAUNCH(rows_launch<float>(mode, a, t.by, t.stages, s));
     else KLAUNCH(rows_launch<__half>(mode, a, t.by, t.stages, s));
@@ -415,14 +447,9 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
 
 // Element-wise grid: 64 CTAs of 256 threads per SM (measured best for the H3
 // stream, 1.33 -> 1.29 ms at 600x595x1536 vs 8/SM), capped by the work so a
-// small mesh does not launch idle CTAs.  STEN_EW_BPS is the tuning knob.
+// small mesh does not launch idle CTAs (STEN_OPT_EW_CTAS_PER_SM).
 static int ew_grid(sten_stencil *st, long long nvec) {
-  static int bps = -1;
-  if (bps < 0) {
-    const char *e = getenv("STEN_EW_BPS");
-    bps = e ? atoi(e) : 64;
-    if (bps < 1) bps = 1;
-  }
+  const int bps = st->ew_bps;
   long long need = (nvec + 511) / 512;  // two vectors per thread
   long long g = (long long)st->sm * bps;
   if (need < g) g = need;
@@ -496,7 +523,7 @@ static int exchange(sten_stencil *st, int prec, Pick pick, cudaStream_t s) {
     CUDA_TRY(cudaMemcpyAsync(hi, lo + (size_t)nzl * pb, pb, cudaMemcpyDeviceToDevice, s));        // top -> halo 0
     CUDA_TRY(cudaMemcpyAsync(lo + (size_t)(nzl + 1) * pb, hi + pb, pb, cudaMemcpyDeviceToDevice, s));  // bottom -> halo top
   }
-  if (st->comm && st->comm->nranks > 1) {
+  if (nccl_ranks(st)) {
     const int R = st->comm->nranks, me = st->comm->rank;
     char *bot = (char *)pick(st->slabs[0].pb[prec]);
     char *top = (char *)pick(st->slabs[ns - 1].pb[prec]);
@@ -516,10 +543,38 @@ static int exchange(sten_stencil *st, int prec, Pick pick, cudaStream_t s) {
 }
 
 // Decomposed solve: slab sums -> (NCCL fp32 all-reduce) -> scalar step.
+static int host_barrier(sten_stencil *st, cudaStream_t s);
+// Host lockstep (sten_set_host_barrier): before a peer-memory all-reduce's
+// waiting kernel, finish this rank's work and meet the other ranks, so that the
+// waiting kernel finds every flag already set and never spins on a kernel of
+// another process (several ranks on one GPU: such waits are not guaranteed to
+// make progress).  Not allowed inside a graph capture.
+static int host_barrier(sten_stencil *st, cudaStream_t s) {
+  if (!st->barrier_fn || !p2p_only(st)) return STEN_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return set_err(STEN_ECUDA, "internal: host barrier inside a graph capture");
+  CUDA_TRY(cudaStreamSynchronize(s));
+  st->barrier_fn(st->barrier_ctx);
+  return STEN_OK;
+}
+
 static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s, int nslots = 0) {
   if (!decomposed(st)) return STEN_OK;
   const int ns = nslots > 0 ? nslots : (int)st->slabs.size();
-  if (st->comm && st->comm->nranks > 1) {
+  if (p2p_only(st)) {  // peer-memory all-reduce: deposit this rank's slab sums, wait for every rank's
+    if (phase != PH_INIT || nslots > 0 || !st->p2p_ranks)
+      return set_err(STEN_EUNSUPPORTED, "internal: peer-memory reduction of phase %d", phase);
+    std::vector<P2PBox> boxes{P2PBox{st->p2p_sums, st->p2p_flags}};
+    for (const P2PBox &b : st->p2p_remote) boxes.push_back(b);
+    KLAUNCH(p2p_put_launch(st->slab_sums, ns, st->comm->rank * ns, st->p2p_slots, boxes.data(), (int)boxes.size(),
+                           st->p2p_seq, s));
+    RC_TRY(host_barrier(st, s));
+    KLAUNCH(p2p_fin_launch(PH_INIT, P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
+    st->launches += 2;
+    return STEN_OK;
+  }
+  if (nccl_ranks(st)) {
     KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
     NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
     KLAUNCH(scalars_launch(phase, st->red_total, 1, st->st, s));
@@ -533,9 +588,55 @@ static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s, int nslot
 
 // One BiCGStab iteration (Alg. 1 l.176-184); iteration parity selects the
 // ping-pong p/v buffers.  evs: optional [3][2] events around H1, H2, H3.
+// Decomposed and overlapped (north_star (4)): the interior planes [1, nz-1) of
+// every slab on the solve's stream while a side stream exchanges the halo
+// planes and then runs the two boundary planes; the three parts' sums meet in
+// the phase's reduction.
+template <typename Xchg>
+static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cudaStream_t s, Xchg xchg) {
+  const int ns = (int)st->slabs.size();
+  CUDA_TRY(cudaEventRecord(st->ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(st->side, st->ev_fork, 0));
+  for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, mode, k, parity, s, CLS_INTERIOR));
+  RC_TRY(xchg(st->side));
+  for (int k = 0; k < ns; ++k) {
+    RC_TRY(launch_stencil(st, prec, mode, k, parity, st->side, CLS_BOTTOM));
+    RC_TRY(launch_stencil(st, prec, mode, k, parity, st->side, CLS_TOP));
+  }
+  CUDA_TRY(cudaEventRecord(st->ev_join, st->side));
+  CUDA_TRY(cudaStreamWaitEvent(s, st->ev_join, 0));
+  return reduce_scalars(st, mode == MODE_H1 ? PH_H1 : PH_H2, s, 3 * ns);
+}
+
+static bool cls_overlapped(const sten_stencil *st) {
+  if (!decomposed(st) || !st->cls_overlap) return false;
+  for (const Slab &sl : st->slabs)
+    if (sl.nz < 3) return false;
+  return true;
+}
+
 static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
   const int ns = (int)st->slabs.size();
   const bool dec = decomposed(st);
+  if (cls_overlapped(st)) {
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
+    RC_TRY(overlapped_phase(st, prec, MODE_H1, parity, s, [&](cudaStream_t ss) {
+      RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, ss));
+      RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.p[parity]; }, ss));
+      return exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity]; }, ss);
+    }));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
+    RC_TRY(overlapped_phase(st, prec, MODE_H2, parity, s, [&](cudaStream_t ss) {
+      return exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity ^ 1]; }, ss);
+    }));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[4], s, cudaEventRecordExternal));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_h3(st, prec, k, parity, s));
+    RC_TRY(reduce_scalars(st, PH_H3, s));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[5], s, cudaEventRecordExternal));
+    return STEN_OK;
+  }
   // H1: halos of r (new from H3), p, v (new from the previous H1)
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
   if (dec) {
@@ -576,7 +677,7 @@ static int fill_coef_halos(sten_stencil *st, cudaStream_t s) {
         CUDA_TRY(cudaMemcpyAsync(base(lo, d) + (size_t)(lo.nz + 1) * pb, base(hi, d) + pb, pb, cudaMemcpyDeviceToDevice, s));
       }
     }
-    if (st->comm && st->comm->nranks > 1) {
+    if (nccl_ranks(st)) {
       const int R = st->comm->nranks, me = st->comm->rank;
       Slab &bot = st->slabs[0], &top = st->slabs[ns - 1];
       NCCL_TRY(g_nccl.GroupStart());
@@ -611,8 +712,6 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
     by = 8;
     stg = 3;
   }
-  if (const char *e = getenv("STEN_SR_TILING"))
-    sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &by, &stg, &cst, &zc, &zct, &tail, &pack);
   t.pack = pack;
   t.by = by;
   t.stages = stg;
@@ -622,7 +721,6 @@ static void default_sr_tiling(sten_stencil *st, int prec) {
   t.zc_tail = zct > 0 ? zct : t.zc;
   t.tail = tail > 0 ? tail : 0;
   const int bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
-  if (getenv("STEN_SR_TILING")) return;
   // Small meshes: uniform short chunks.  HBM-bound ones: enough chunks to fill ~2 waves
   // (chunks down to 2 planes).  L2-resident ones (the sweep's ~15 arrays within 2x L2): at
   // most one wave, which balances the z-halo overhead of short chunks against parallelism
@@ -683,7 +781,6 @@ static int ensure_sr(sten_stencil *st, int prec) {
   const int e = esize(prec);
   const size_t vb = (size_t)st->plane * e;
   const int H = 16 / e, bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();  // 16-B x halo pad
-  g_plane_stride = st->plane;
   for (Slab &sl : st->slabs) {
     SrBufs &b = sl.sr[prec];
     if (!b.ready) {
@@ -703,14 +800,14 @@ static int ensure_sr(sten_stencil *st, int prec) {
     if (!b.maps_ok) {
       for (int k = 0; k < 2; ++k)
         for (int i = 0; i < 5; ++i)
-          RC_TRY(make_map(&b.m_vec[k][i], b.vec[k][i], e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx + 2 * H,
+          RC_TRY(make_map(st, &b.m_vec[k][i], b.vec[k][i], e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx + 2 * H,
                           t.by + 4));
       for (int d = 0; d < 6; ++d) {
         void *c = prec == STEN_FP32 ? (void *)sl.c32b[d] : (void *)sl.c16b[d];
-        RC_TRY(make_map(&b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + 2 * H, t.by + 2));
+        RC_TRY(make_map(st, &b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + 2 * H, t.by + 2));
       }
-      RC_TRY(make_map(&b.m_x, b.x, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
-      RC_TRY(make_map(&b.m_rh, b.rh, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
+      RC_TRY(make_map(st, &b.m_x, b.x, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
+      RC_TRY(make_map(st, &b.m_rh, b.rh, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
       b.maps_ok = true;
     }
     const int g = sr_grid(st, prec, sl.nz);
@@ -819,6 +916,7 @@ static int launch_sr(sten_stencil *st, int prec, int slab, int set, bool capture
     // ... and the sums into every participant's inbox, slot = global slab index
     a.red.slab_out = nullptr;
     a.red.p2p_slot = (st->comm ? st->comm->rank : 0) * ns + slab;
+    a.red.p2p_nslots = st->p2p_slots;
     a.red.p2p_seq = st->p2p_seq;
     a.red.p2p[0] = P2PBox{st->p2p_sums, st->p2p_flags};
     a.red.p2p_n = 1;
@@ -853,7 +951,25 @@ static int sr_exchange(sten_stencil *st, int prec, int set, cudaStream_t s) {
       CUDA_TRY(cudaMemcpyAsync(lo + (size_t)(nzl + kSrHalo) * pb, hi + hb, hb, cudaMemcpyDeviceToDevice, s));
     }
   }
-  if (st->comm && st->comm->nranks > 1) {
+  if (p2p_only(st)) {
+    // no NCCL: PULL the z-neighbour ranks' boundary planes into our halo planes
+    // through peer memory (their init, which wrote them, finished before the
+    // init's peer-memory all-reduce completed; nothing writes them again before
+    // our first sweep's sums have been deposited)
+    if (!st->p2p_ranks) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: call sten_p2p_import first");
+    const int R = st->comm->nranks, me = st->comm->rank;
+    for (int i = 0; i < 5; ++i) {
+      char *bot = (char *)st->slabs[0].sr[prec].vec[set][i];
+      char *top = (char *)st->slabs[ns - 1].sr[prec].vec[set][i];
+      const int nzt = st->slabs[ns - 1].nz;  // equal slabs on every rank
+      if (me > 0)
+        CUDA_TRY(cudaMemcpyAsync(bot, (char *)st->p2p_lo[prec][set][i] + (size_t)nzt * pb, hb, cudaMemcpyDefault, s));
+      if (me + 1 < R)
+        CUDA_TRY(cudaMemcpyAsync(top + (size_t)(nzt + kSrHalo) * pb, (char *)st->p2p_hi[prec][set][i] + hb, hb,
+                                 cudaMemcpyDefault, s));
+    }
+  }
+  if (nccl_ranks(st)) {
     const int R = st->comm->nranks, me = st->comm->rank;
     NCCL_TRY(g_nccl.GroupStart());
     for (int i = 0; i < 5; ++i) {
@@ -884,7 +1000,8 @@ static int enqueue_sr_sweep(sten_stencil *st, int prec, int set, cudaStream_t s,
     // neighbours' buffers) and its share of the all-reduce (inbox deposits);
     // a 1-thread kernel waits for every slot and runs the scalar step
     for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, set, false, s, SR_ALL, true));
-    KLAUNCH(p2p_fin_launch(P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
+    RC_TRY(host_barrier(st, s));
+    KLAUNCH(p2p_fin_launch(PH_SR, P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
     st->launches++;
   } else if (decomposed(st) && st->sr_overlap) {
     // the halo exchange and the chunks that read halo planes on a side
@@ -1101,15 +1218,29 @@ int sten_comm_unique_id(void *id_out) {
   return STEN_OK;
 }
 
-int sten_comm_create(const void *unique_id, int nranks, int rank, sten_comm **out) {
-  if (!unique_id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+int sten_comm_create(const void *unique_id, int nranks, int rank, int cuda_device, sten_comm **out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks)
     return set_err(STEN_EINVAL, "bad comm arguments (nranks=%d rank=%d)", nranks, rank);
-  RC_TRY(nccl_load());
-  ncclUniqueId id;
-  memcpy(&id, unique_id, sizeof id);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev)
+    return set_err(STEN_EINVAL, "cuda_device %d not in 0..%d", cuda_device, ndev - 1);
+  CUDA_TRY(cudaSetDevice(cuda_device));
   sten_comm *c = new sten_comm;
   c->nranks = nranks;
   c->rank = rank;
+  c->device = cuda_device;
+  if (!unique_id) {  // peer-memory only: the data plane comes from sten_p2p_import
+    *out = c;
+    return STEN_OK;
+  }
+  int rc = nccl_load();
+  if (rc != STEN_OK) {
+    delete c;
+    return rc;
+  }
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof id);
   ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
   if (r != ncclSuccess) {
     delete c;
@@ -1138,10 +1269,22 @@ static int is_device_ptr(const void *p) {
 
 // cconst (host, 7 doubles: a_P, A_xm .. A_zp) selects a constant operator;
 // else coeffs[] are the per-point fields
-static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int coeff_dtype, const double *cconst,
-                       int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out) {
+static int create_impl(int nx, int ny, int nz_global, const void *const coeffs[7], int coeff_dtype,
+                       const double *cconst, int nslabs, sten_comm *comm, void *cuda_stream, sten_stencil **out) {
   if (!out) return set_err(STEN_EINVAL, "out is NULL");
-  if (nx <= 0 || ny <= 0 || nz <= 0) return set_err(STEN_EINVAL, "mesh %d x %d x %d must be positive", nx, ny, nz);
+  if (nx <= 0 || ny <= 0 || nz_global <= 0)
+    return set_err(STEN_EINVAL, "mesh %d x %d x %d must be positive", nx, ny, nz_global);
+  // slab convention: rank r of R owns planes [r nz/R, (r+1) nz/R)
+  const int R_ = comm ? comm->nranks : 1;
+  if (nz_global % R_ != 0)
+    return set_err(STEN_EINVAL, "nz_global=%d not divisible by %d ranks", nz_global, R_);
+  const int nz = nz_global / R_;
+  if (comm) {
+    int dev = -1;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev != comm->device)
+      return set_err(STEN_EINVAL, "current CUDA device %d is not the communicator's device %d", dev, comm->device);
+  }
   if (nslabs < 1 || nz % nslabs != 0) return set_err(STEN_EINVAL, "nz=%d not divisible into nslabs=%d", nz, nslabs);
   if (cconst) {
     for (int d = 0; d < 7; ++d)
@@ -1161,15 +1304,14 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   sten_stencil *st = new sten_stencil;
   st->nx = nx;
   st->ny = ny;
-  st->nz = nz;
+  st->nz = nz;  // this rank's planes
   // Layout: rows of `pitch` elements, a multiple of
   // 8 (16-B vectors), planes a multiple of 64 elements.  Unpadded rows move
   // no padding bytes: the SR sweep (the bench's schedule) is 1.9% faster with
-  // them at nx = 600 (144.0 vs 141.5 Gpoint-iter/s), the classic kernels prefer
-  // 128-B aligned rows (103.7 vs 100.0): STEN_PITCH_ALIGN=64 selects those.
+  // them at nx = 600 (144.0 vs 141.5 Gpoint-iter/s); with their coefficient tiles by
+  // TMA the classic kernels are fastest unpadded too (107.1 vs 103.4 on 128-B rows).
   {
-    int align = 8;
-    if (const char *pa = getenv("STEN_PITCH_ALIGN")) align = atoi(pa) >= 8 ? atoi(pa) : 8;
+    const int align = 8;
     st->pitch = (nx + align - 1) / align * align;
     int nyp = ny;
     while (((long long)st->pitch * nyp) % 64) ++nyp;
@@ -1183,11 +1325,6 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
     for (int d = 0; d < 6; ++d) st->cscaled[d] = cconst[1 + d] / cconst[0];  // fp64, as k_create_coeffs
   }
   st->sm = device_sm_count();
-  if (const char *pf = getenv("STEN_COEF_PF")) st->coef_pf = atoi(pf);
-  if (const char *pf = getenv("STEN_SR_L2PF")) st->sr_l2pf = atoi(pf);
-  if (const char *ov = getenv("STEN_SR_OVERLAP")) st->sr_overlap = atoi(ov) != 0;
-  if (const char *pp = getenv("STEN_SR_P2P")) st->sr_p2p = atoi(pp) != 0;
-  if (const char *fg = getenv("STEN_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
   st->slabs.resize(nslabs);
   auto fail = [&](int rc) {
     stencil_destroy(st);
@@ -1261,22 +1398,22 @@ static int create_impl(int nx, int ny, int nz, const void *const coeffs[7], int 
   if (cudaMalloc(&st->st, sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(&st->st_host, sizeof(DevState)) != cudaSuccess ||
       cudaMalloc(&st->counter, sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc(&st->slab_sums, sizeof(float) * kMaxDots * 2 * nslabs) != cudaSuccess ||
+      cudaMalloc(&st->slab_sums, sizeof(float) * kMaxDots * 3 * nslabs) != cudaSuccess ||
       cudaMalloc(&st->counter2, sizeof(unsigned)) != cudaSuccess ||
       cudaMalloc(&st->red_total, sizeof(float) * kMaxDots) != cudaSuccess)
     return fail(set_err(STEN_ENOMEM, "state allocation failed"));
-  st->p2p_slots = nslabs * (comm ? comm->nranks : 1);
-  if (cudaMalloc(&st->p2p_sums, sizeof(float) * kMaxDots * st->p2p_slots) != cudaSuccess ||
-      cudaMalloc(&st->p2p_flags, sizeof(unsigned) * st->p2p_slots) != cudaSuccess ||
+  st->p2p_slots = nslabs * (comm ? comm->nranks : 1);  // x 2: double-buffered by sequence parity
+  if (cudaMalloc(&st->p2p_sums, sizeof(float) * kMaxDots * 2 * st->p2p_slots) != cudaSuccess ||
+      cudaMalloc(&st->p2p_flags, sizeof(unsigned) * 2 * st->p2p_slots) != cudaSuccess ||
       cudaMalloc(&st->p2p_seq, sizeof(unsigned)) != cudaSuccess)
     return fail(set_err(STEN_ENOMEM, "inbox allocation failed"));
-  cudaMemset(st->p2p_sums, 0, sizeof(float) * kMaxDots * st->p2p_slots);
-  cudaMemset(st->p2p_flags, 0, sizeof(unsigned) * st->p2p_slots);
+  cudaMemset(st->p2p_sums, 0, sizeof(float) * kMaxDots * 2 * st->p2p_slots);
+  cudaMemset(st->p2p_flags, 0, sizeof(unsigned) * 2 * st->p2p_slots);
   cudaMemset(st->p2p_seq, 0, sizeof(unsigned));
   cudaMemset(st->counter, 0, sizeof(unsigned));
   cudaMemset(st->counter2, 0, sizeof(unsigned));
   cudaMemset(st->st, 0, sizeof(DevState));
-  cudaMemset(st->slab_sums, 0, sizeof(float) * kMaxDots * 2 * nslabs);
+  cudaMemset(st->slab_sums, 0, sizeof(float) * kMaxDots * 3 * nslabs);
   cudaMemset(st->red_total, 0, sizeof(float) * kMaxDots);
   if (cudaStreamCreateWithFlags(&st->cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1396,6 +1533,67 @@ int sten_set_tiling(sten_stencil *st, int prec, int bx, int by, int zc, int stag
   return STEN_OK;
 }
 
+int sten_set_host_barrier(sten_stencil *st, void (*fn)(void *ctx), void *ctx) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  st->barrier_fn = fn;
+  st->barrier_ctx = ctx;
+  drop_graphs(st);
+  return STEN_OK;
+}
+
+int sten_set_option(sten_stencil *st, int option, int value) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  switch (option) {
+    case STEN_OPT_TMA_L2_PROMOTION:
+      if (value < 0 || value > 3) return set_err(STEN_EINVAL, "TMA L2 promotion %d not in 0..3", value);
+      st->tma_promo = value;
+      for (Slab &sl : st->slabs)
+        for (int p = 0; p < 2; ++p) {
+          sl.pb[p].maps_ok = false;
+          sl.sr[p].maps_ok = false;
+        }
+      break;
+    case STEN_OPT_EW_CTAS_PER_SM:
+      if (value < 1 || value > 64) return set_err(STEN_EINVAL, "element-wise CTAs per SM %d not in 1..64", value);
+      st->ew_bps = value;
+      break;
+    case STEN_OPT_COEF_PREFETCH:
+      if (value < 0 || value > 16) return set_err(STEN_EINVAL, "coefficient prefetch distance %d not in 0..16", value);
+      st->coef_pf = value;
+      break;
+    case STEN_OPT_SR_L2_PREFETCH:
+      if (value < 0 || value > 16) return set_err(STEN_EINVAL, "SR L2 prefetch distance %d not in 0..16", value);
+      st->sr_l2pf = value;
+      break;
+    case STEN_OPT_SR_LIGHT_LAST:
+      if (value != 0 && value != 1) return set_err(STEN_EINVAL, "SR light last sweep must be 0 or 1 (got %d)", value);
+      st->sr_light = value != 0;
+      break;
+    case STEN_OPT_CLASSIC_OVERLAP:
+      if (value != 0 && value != 1) return set_err(STEN_EINVAL, "classic overlap must be 0 or 1 (got %d)", value);
+      st->cls_overlap = value != 0;
+      break;
+    default:
+      return set_err(STEN_EINVAL, "unknown option %d", option);
+  }
+  drop_graphs(st);
+  return STEN_OK;
+}
+
+int sten_get_option(sten_stencil *st, int option, int *value) {
+  if (!st || !value) return set_err(STEN_EINVAL, "NULL argument");
+  switch (option) {
+    case STEN_OPT_TMA_L2_PROMOTION: *value = st->tma_promo; break;
+    case STEN_OPT_EW_CTAS_PER_SM: *value = st->ew_bps; break;
+    case STEN_OPT_COEF_PREFETCH: *value = st->coef_pf; break;
+    case STEN_OPT_SR_L2_PREFETCH: *value = st->sr_l2pf; break;
+    case STEN_OPT_SR_LIGHT_LAST: *value = st->sr_light ? 1 : 0; break;
+    case STEN_OPT_CLASSIC_OVERLAP: *value = st->cls_overlap ? 1 : 0; break;
+    default: return set_err(STEN_EINVAL, "unknown option %d", option);
+  }
+  return STEN_OK;
+}
+
 int sten_set_timing(sten_stencil *st, int enable) {
   if (!st) return set_err(STEN_EINVAL, "NULL handle");
   st->timing = enable != 0;
@@ -1410,6 +1608,7 @@ int sten_get_stats(sten_stencil *st, sten_stats *out) {
 
 int stencil_apply(sten_stencil *st, int prec, const void *x, void *y, void *cuda_stream) {
   if (!st || !x || !y) return set_err(STEN_EINVAL, "NULL argument");
+  if (p2p_only(st)) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: stencil_apply needs NCCL");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
   cudaStream_t s = (cudaStream_t)cuda_stream;
   RC_TRY(ensure_bufs(st, prec));
@@ -1440,6 +1639,12 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   const bool sr = st->schedule == STEN_SCHED_SR;
   if (!sr && prec == STEN_MIXED && st->half_dots)
     return set_err(STEN_EUNSUPPORTED, "half dots (STEN_DOTS_HALF) are built for the SR schedule only");
+  if (p2p_only(st)) {  // no NCCL: only the fused SR sweep moves data between ranks
+    if (!sr || !st->p2p_ranks || !st->sr_p2p)
+      return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: SR schedule with the fused exchange after "
+                                        "sten_p2p_import only");
+    if (with_x0) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: x0 must be NULL");
+  }
   RC_TRY(ensure_bufs(st, prec));
   if (sr) RC_TRY(ensure_sr(st, prec));
   if (maxit + 2 > st->hist_cap) {
@@ -1463,7 +1668,7 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   h.ahist = st->ahist;
   h.whist = st->whist;
   // SR on one slab: the last sweep without its SpMVs (k_sr_last)
-  const bool light = sr && !decomposed(st) && !(prec == STEN_MIXED && st->half_dots) && !getenv("STEN_SR_NOLIGHT");
+  const bool light = sr && !decomposed(st) && !(prec == STEN_MIXED && st->half_dots) && st->sr_light;
   h.light = light ? 1 : 0;
   *st->st_host = h;
   CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
@@ -1500,12 +1705,22 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   // parity of p/v is the same at every replay)
   const int nsteps = sr ? maxit + 1 : maxit;  // SR: sweep i computes x_i, r_i (i = 0..maxit)
   if (nsteps > 0) {
+    const bool lockstep = st->barrier_fn && p2p_only(st);
     int chunk = tol > 0.0 ? 8 : ((nsteps + 1) / 2) * 2;
     if (chunk > 2048) chunk = 2048;
+    if (lockstep) chunk = 0;
     out->chunk = chunk;
+    // host lockstep (several ranks on one GPU): sweep by sweep, no graph; every
+    // rank runs the same sweeps because every rank takes the same scalar decisions
+    for (int i = 0; lockstep && i < nsteps; ++i) {
+      RC_TRY(enqueue_sr_sweep(st, prec, i & 1, s, nullptr));
+      CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (st->st_host->stop || st->st_host->it >= maxit) break;
+    }
     GraphRec *gr = nullptr;
-    RC_TRY(get_graph(st, prec, chunk, &gr));
-    const int nrep = (nsteps + chunk - 1) / chunk;
+    if (!lockstep) RC_TRY(get_graph(st, prec, chunk, &gr));
+    const int nrep = lockstep ? 0 : (nsteps + chunk - 1) / chunk;
     for (int rep = 0; rep < nrep; ++rep) {
       CUDA_TRY(cudaGraphLaunch(gr->exec, s));
       out->kernels += gr->kernels;
@@ -1763,7 +1978,7 @@ static int ir_residual(sten_stencil *st, cudaStream_t s, double *rr) {
     st->launches++;
   }
   KLAUNCH(slabsum_launch(st->slab_sums, (int)st->slabs.size(), st->red_total, s));
-  if (st->comm && st->comm->nranks > 1) {
+  if (nccl_ranks(st)) {
     NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, 1, ncclFloat32, ncclSum, st->comm->comm, s));
     NCCL_TRY(g_nccl.AllReduce(st->ir_amax, st->ir_amax, 1, ncclUint32, ncclMax, st->comm->comm, s));
   }
@@ -1779,6 +1994,7 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
                     void *cuda_stream) {
   if (!st || !b || !x_out || !outer_iters || !inner_iters || !res_hist || !status)
     return set_err(STEN_EINVAL, "NULL argument");
+  if (p2p_only(st)) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: bicgstab_refine needs NCCL");
   if (!(tol > 0.0) || !(inner_tol >= 0.0) || outer_maxit < 0 || inner_maxit < 1)
     return set_err(STEN_EINVAL, "tol=%g inner_tol=%g outer_maxit=%d inner_maxit=%d invalid", tol, inner_tol,
                    outer_maxit, inner_maxit);
@@ -1930,8 +2146,10 @@ int sten_set_schedule(sten_stencil *st, int schedule) {
 
 // ------------------------------------------- peer memory across ranks --
 // export: IPC handles of this rank's bottom-slab and top-slab SR buffers
-// (2 sets x 5 vectors each) and of its inbox (sums, flags)
-constexpr int kIpcN = 22;
+// (2 sets x 5 vectors each), of its inbox (sums, flags) and of the bottom- and
+// top-slab coefficient arrays (6 fp32 + 6 fp16 each: a p2p-only communicator
+// fills the coefficient halo planes from them at import)
+constexpr int kIpcN = 46;
 int sten_p2p_export(sten_stencil *st, int prec, void *out, size_t *bytes) {
   if (!st || !bytes) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
@@ -1950,6 +2168,10 @@ int sten_p2p_export(sten_stencil *st, int prec, void *out, size_t *bytes) {
       for (int i = 0; i < 5; ++i) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->sr[prec].vec[set][i]));
   CUDA_TRY(cudaIpcGetMemHandle(&h[n++], st->p2p_sums));
   CUDA_TRY(cudaIpcGetMemHandle(&h[n++], st->p2p_flags));
+  for (Slab *sl : {&st->slabs.front(), &st->slabs.back()}) {
+    for (int d = 0; d < 6; ++d) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->c32b[d]));
+    for (int d = 0; d < 6; ++d) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->c16b[d]));
+  }
   *bytes = need;
   return STEN_OK;
 }
@@ -1964,10 +2186,17 @@ int sten_p2p_import(sten_stencil *st, int prec, const void *all, size_t bytes_pe
   const int R = st->comm->nranks, me = st->comm->rank;
   if (R > kMaxPeers) return set_err(STEN_EUNSUPPORTED, "at most %d ranks in the peer-memory all-reduce", kMaxPeers);
   auto rec = [&](int r) { return (const cudaIpcMemHandle_t *)((const char *)all + (size_t)r * bytes_per_rank); };
-  auto open = [&](const cudaIpcMemHandle_t &h, void **p) -> int {
+  auto open = [&](const cudaIpcMemHandle_t &h, void **p) -> int {  // each handle opened once per handle
+    std::string key((const char *)&h, sizeof h);
+    auto it = st->ipc_map.find(key);
+    if (it != st->ipc_map.end()) {
+      *p = it->second;
+      return STEN_OK;
+    }
     cudaError_t e = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return set_err(STEN_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
     st->ipc_opened.push_back(*p);
+    st->ipc_map[key] = *p;
     return STEN_OK;
   };
   for (int set = 0; set < 2; ++set)
@@ -1982,6 +2211,27 @@ int sten_p2p_import(sten_stencil *st, int prec, const void *all, size_t bytes_pe
     RC_TRY(open(rec(r)[20], (void **)&b.sums));
     RC_TRY(open(rec(r)[21], (void **)&b.flags));
     st->p2p_remote.push_back(b);
+  }
+  if (p2p_only(st)) {  // coefficient halo planes (NCCL fills them at create otherwise)
+    const int ns = (int)st->slabs.size();
+    Slab &bot = st->slabs[0], &top = st->slabs[ns - 1];
+    for (int pr = 0; pr < 2; ++pr) {
+      const size_t pb = (size_t)st->plane * (pr == 0 ? 4 : 2);
+      for (int d = 0; d < 6; ++d) {
+        const int k = pr * 6 + d;
+        char *mine_b = pr == 0 ? (char *)bot.c32b[d] : (char *)bot.c16b[d];
+        char *mine_t = pr == 0 ? (char *)top.c32b[d] : (char *)top.c16b[d];
+        void *peer = nullptr;
+        if (me > 0) {  // the lower rank's top slab: its top interior plane -> our bottom halo plane
+          RC_TRY(open(rec(me - 1)[34 + k], &peer));
+          CUDA_TRY(cudaMemcpy(mine_b, (char *)peer + (size_t)top.nz * pb, pb, cudaMemcpyDefault));
+        }
+        if (me + 1 < R) {  // the upper rank's bottom slab: its bottom interior plane -> our top halo plane
+          RC_TRY(open(rec(me + 1)[22 + k], &peer));
+          CUDA_TRY(cudaMemcpy(mine_t + (size_t)(top.nz + 1) * pb, (char *)peer + pb, pb, cudaMemcpyDefault));
+        }
+      }
+    }
   }
   st->p2p_ranks = true;
   st->sr_p2p = true;
@@ -2023,6 +2273,7 @@ int sten_sr_sweep(sten_stencil *st, int prec, double alpha, double omega, double
                   void *r, void *p, void *v, void *q, void *y, float *dots, void *cuda_stream) {
   if (!st || !rh || !x || !r || !p || !v || !q || !y || !dots) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (p2p_only(st)) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: sten_sr_sweep needs NCCL");
   cudaStream_t s = (cudaStream_t)cuda_stream;
   RC_TRY(ensure_bufs(st, prec));
   RC_TRY(ensure_sr(st, prec));
@@ -2046,7 +2297,7 @@ int sten_sr_sweep(sten_stencil *st, int prec, double alpha, double omega, double
   const int ns = (int)st->slabs.size();
   for (int k = 0; k < ns; ++k) RC_TRY(launch_sr(st, prec, k, 0, true, s));
   float *sums = st->slab_sums;
-  if (st->comm && st->comm->nranks > 1) {
+  if (nccl_ranks(st)) {
     KLAUNCH(slabsum_launch(st->slab_sums, ns, st->red_total, s));
     NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
     sums = st->red_total;
@@ -2165,9 +2416,8 @@ int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *
     CUDA_TRY(cudaMemset(st->v[prec], 0, bytes));  // padding columns stay zero
   }
   if (!st->maps_ok[prec]) {
-    g_plane_stride = (long long)st->pitch * st->ny;
     const int bx = prec == STEN_FP32 ? 64 : 128, H = 16 / e;
-    RC_TRY(make_map(&st->m_v[prec], st->v[prec], e, st->nx, st->ny, 1, st->pitch, bx + 2 * H, 32 + 2));
+    RC_TRY(make_map_p(&st->m_v[prec], st->v[prec], e, st->nx, st->ny, 1, st->pitch, (long long)st->pitch * st->ny, 3, bx + 2 * H, 32 + 2));
     st->maps_ok[prec] = true;
   }
   CUDA_TRY(cudaMemcpy2DAsync(st->v[prec], (size_t)st->pitch * e, x, (size_t)st->nx * e, (size_t)st->nx * e, st->ny,

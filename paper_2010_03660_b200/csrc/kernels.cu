@@ -222,18 +222,22 @@ __global__ void k_slabsum(const float *__restrict__ slab_sums, int nslabs, float
   for (int d = 0; d < kMaxDots; ++d) out[d] = s[d];
 }
 
-// SR scalar step after a peer-memory all-reduce: wait (bounded) until every
-// slot of this participant's inbox holds the current sweep's sums, add them in
-// slot order (deterministic, identical on every rank), finalise.
+// Scalar step after a peer-memory all-reduce: wait (bounded) until every slot
+// of this participant's inbox (the half of the sequence number's parity) holds
+// the current reduction's sums, add them in slot order (deterministic,
+// identical on every rank), finalise.  A peer that never arrives stops the
+// solve with STEN_TIMEOUT after ~20 s instead of hanging the device.
+template <int PH>
 __global__ void k_p2p_fin(P2PBox inbox, int nslots, unsigned *seqp, DevState *st) {
-  if (sr_idle(st)) return;
+  if (PH == PH_SR && sr_idle(st)) return;
   const unsigned seq = *seqp + 1u;
+  const int base = (int)(seq & 1u) * nslots;
   const long long t0 = clock64();
   bool timeout = false;
   for (int k = 0; k < nslots && !timeout; ++k) {
     unsigned f;
     do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(inbox.flags + k) : "memory");
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(inbox.flags + base + k) : "memory");
       if (f == seq) break;
       __nanosleep(200);
       if (clock64() - t0 > 40000000000ll) timeout = true;  // ~20 s: a peer never arrived
@@ -242,19 +246,45 @@ __global__ void k_p2p_fin(P2PBox inbox, int nslots, unsigned *seqp, DevState *st
   float s[kMaxDots];
   for (int d = 0; d < kMaxDots; ++d) s[d] = 0.0f;
   for (int k = 0; k < nslots; ++k)
-    for (int d = 0; d < kMaxDots; ++d) s[d] += __ldcv(&inbox.sums[k * kMaxDots + d]);
+    for (int d = 0; d < kMaxDots; ++d) s[d] += __ldcv(&inbox.sums[(base + k) * kMaxDots + d]);
   if (timeout) {  // never hang the device: report and stop the solve
-    st_event(st, STEN_NONFINITE, st->sweep, false);
+    st_event(st, STEN_TIMEOUT, PH == PH_SR ? st->sweep : 0, false);
     st->stop = 1;
-    st->status = STEN_NONFINITE;
+    st->status = STEN_TIMEOUT;
     return;
   }
   *seqp = seq;
-  fin_sr(st, s);
+  finalize_phase<PH>(st, s);
 }
 
-int p2p_fin_launch(P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s) {
-  k_p2p_fin<<<1, 1, 0, s>>>(inbox, nslots, seq, st);
+int p2p_fin_launch(int phase, P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s) {
+  if (phase == PH_INIT) k_p2p_fin<PH_INIT><<<1, 1, 0, s>>>(inbox, nslots, seq, st);
+  else k_p2p_fin<PH_SR><<<1, 1, 0, s>>>(inbox, nslots, seq, st);
+  return (int)cudaGetLastError();
+}
+
+struct P2PBoxes {
+  P2PBox b[kMaxPeers];
+};
+__global__ void k_p2p_put(const float *__restrict__ slab_sums, int nslabs, int base, int nslots, P2PBoxes boxes,
+                          int nboxes, const unsigned *seqp) {
+  const unsigned seq = *seqp + 1u;
+  const int half = (int)(seq & 1u) * nslots;
+  for (int r = 0; r < nboxes; ++r)
+    for (int k = 0; k < nslabs; ++k)
+      for (int d = 0; d < kMaxDots; ++d) boxes.b[r].sums[(half + base + k) * kMaxDots + d] = slab_sums[k * kMaxDots + d];
+  __threadfence_system();
+  for (int r = 0; r < nboxes; ++r)
+    for (int k = 0; k < nslabs; ++k)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(boxes.b[r].flags + half + base + k), "r"(seq) : "memory");
+}
+
+int p2p_put_launch(const float *slab_sums, int nslabs, int base, int nslots, const P2PBox *boxes, int nboxes,
+                   const unsigned *seq, cudaStream_t s) {
+  if (nboxes > kMaxPeers) return (int)cudaErrorInvalidValue;
+  P2PBoxes bx;
+  for (int r = 0; r < nboxes; ++r) bx.b[r] = boxes[r];
+  k_p2p_put<<<1, 1, 0, s>>>(slab_sums, nslabs, base, nslots, bx, nboxes, seq);
   return (int)cudaGetLastError();
 }
 

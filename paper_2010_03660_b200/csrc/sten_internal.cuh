@@ -57,8 +57,11 @@ struct Reduce {
   DevState *st;         // ... else finalize the scalars directly
   // peer-memory all-reduce (p2p_n > 0): the last CTA writes its sums into
   // slot p2p_slot of every inbox, then the flag (*p2p_seq + 1), after a
-  // system-scope fence that also publishes the kernel's remote halo stores
-  int p2p_n, p2p_slot;
+  // system-scope fence that also publishes the kernel's remote halo stores.
+  // Inboxes are double-buffered by the parity of the sequence number
+  // (p2p_nslots slots each), so a rank that has passed reduction i can deposit
+  // its reduction-(i+1) sums while a slower rank still reads reduction i's.
+  int p2p_n, p2p_slot, p2p_nslots;
   const unsigned *p2p_seq;
   P2PBox p2p[kMaxPeers];
 };
@@ -82,6 +85,7 @@ struct alignas(64) StencilArgs {
   void *out1;             // H1: p_new  H2: s
   Geom g;
   int zc, tiles_x, tiles_y;
+  int zlo, zhi;           // planes [zlo, zhi) of the slab, in chunks of zc from zlo
   int pf;                 // L2 prefetch distance of the coefficient tiles (planes; 0 = off)
   Reduce red;
 };
@@ -487,12 +491,13 @@ __device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduc
     *red.counter = 0u;
     if (red.p2p_n > 0) {  // one-shot all-reduce through peer memory: deposit, fence, flag
       const unsigned seq = *red.p2p_seq + 1u;
+      const int slot = (int)(seq & 1u) * red.p2p_nslots + red.p2p_slot;
       for (int r = 0; r < red.p2p_n; ++r)
 #pragma unroll
-        for (int d = 0; d < ND; ++d) red.p2p[r].sums[red.p2p_slot * kMaxDots + d] = s[d];
+        for (int d = 0; d < ND; ++d) red.p2p[r].sums[slot * kMaxDots + d] = s[d];
       __threadfence_system();
       for (int r = 0; r < red.p2p_n; ++r)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(red.p2p[r].flags + red.p2p_slot), "r"(seq) : "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(red.p2p[r].flags + slot), "r"(seq) : "memory");
     } else if (red.slab_out) {
 #pragma unroll
       for (int d = 0; d < ND; ++d) red.slab_out[d] = s[d];
@@ -525,7 +530,11 @@ template <typename T> int rows_threads(int nx, int by);
 template <typename T> int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 template <typename T> int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s);
 int scalars_launch(int phase, const float *slab_sums, int nslabs, DevState *st, cudaStream_t s);
-int p2p_fin_launch(P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s);
+// phase PH_SR (the fused SR sweep's all-reduce) or PH_INIT (a p2p-only communicator's init)
+int p2p_fin_launch(int phase, P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s);
+// deposit the nslabs slab sums into slots base .. base+nslabs-1 of every inbox (peer-memory all-reduce)
+int p2p_put_launch(const float *slab_sums, int nslabs, int base, int nslots, const P2PBox *boxes, int nboxes,
+                   const unsigned *seq, cudaStream_t s);
 int slabsum_launch(const float *slab_sums, int nslabs, float *out, cudaStream_t s);
 // Iterative refinement (bicgstab_refine, R21): fp32 outer steps
 // around the mixed inner solve.  All pointers at interior plane 0.

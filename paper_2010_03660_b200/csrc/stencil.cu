@@ -16,9 +16,15 @@
 //    H2: s = r - alpha v, l.178) is formed once per point into a 3-deep shared
 //    ring for the xy neighbours; each thread keeps its own column k-1, k, k+1 in
 //    registers for the z terms.  One __syncthreads per plane.
-//  * The six coefficient arrays (and rhat for H1) are read once per point: TMA
-//    prefetches their tiles into L2 (cp.async.bulk.prefetch.tensor) PF planes
-//    ahead and each thread loads its 16-B vectors straight into registers.
+//  * The six coefficient arrays (and rhat for H1) are read once per point, as
+//    BX x BY TMA tiles into an SC-stage ring of their own (the default, SC = 2;
+//    per-thread 16-B loads straddle 32-B sectors on unpadded 1200-B rows).  The
+//    older variant (SC = 0, selected by sten_set_tiling with explicit stages)
+//    prefetches the tiles into L2 (cp.async.bulk.prefetch.tensor) and each
+//    thread loads its 16-B vectors straight into registers one plane ahead.
+//  * A launch covers planes [zlo, zhi) of its slab in chunks of zc (the
+//    decomposed classic schedule launches the interior and the two boundary
+//    planes separately, so the halo exchange overlaps the interior).
 //  * The dot products that follow each SpMV in Alg. 1 are accumulated in fp32
 //    registers and reduced by the deterministic last-CTA reduction.
 #include "sten_internal.cuh"
@@ -41,7 +47,6 @@ struct Geo {
   static constexpr int HBYTES = align128c(HBOX * (int)sizeof(T));
   static constexpr int NIN = MODE == MODE_H1 ? 3 : (MODE == MODE_H2 ? 2 : 1);
   static constexpr int NHALO = 2 * VPR + 2 * BY;  // halo vectors formed per plane
-  static constexpr int PF = 4;                  // L2 prefetch distance of the coefficients (planes)
 };
 
 // SC > 0: the six coefficient tiles (and rhat for H1) of a plane arrive by TMA
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   const int ty = b % a.tiles_y;
   const int ch = b / a.tiles_y;
   const int x0 = tx * BX, y0 = ty * BY;
-  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int z0 = a.zlo + ch * a.zc, z1 = min(z0 + a.zc, a.zhi);
   const int np = z1 - z0 + 2;  // staged planes z0-1 .. z1
   const int tid = threadIdx.x;
 
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(512, 1) k_rows(const __grid_constant__ Stencil
   const int ty = blockIdx.x % a.tiles_y;  // y-neighbours are consecutive CTAs
   const int ch = blockIdx.x / a.tiles_y;
   const int y0 = ty * BY;
-  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int z0 = a.zlo + ch * a.zc, z1 = min(z0 + a.zc, a.zhi);
   const int np = z1 - z0 + 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -469,7 +474,7 @@ int launch_rows(const StencilArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = smem;
   }
-  const int grid = a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  const int grid = a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc);
   k_rows<T, MODE, BY, S><<<grid, rows_threads<T>(a.g.nx, BY), smem, s>>>(a);
   return (int)cudaGetLastError();
 }
@@ -512,7 +517,7 @@ int launch_one(const StencilArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  const int grid = a.tiles_x * a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc);
   k_stencil<T, MODE, BY, S, SC><<<grid, G::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }

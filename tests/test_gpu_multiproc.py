@@ -1,0 +1,122 @@
+"""libsten across PROCESSES (PAPER.md:193-195 z decomposition; PAPER.md:376-397 AllReduce).
+
+Two processes share cuda:0 (the only GPU of the test box), each one rank of a
+peer-memory-only communicator: rank r owns half of the z planes, imports the other
+rank's CUDA IPC records (boundary-slab SR buffers, inbox, boundary coefficient
+planes), and runs the fused SR solve - its sweep kernel stores its boundary planes
+straight into the neighbour process's halo buffers and deposits its sums in both
+processes' inboxes; the one-shot all-reduce is read by k_p2p_fin.  The solve runs
+in host lockstep (sten_set_host_barrier + a gloo barrier), because kernels of two
+processes on one GPU that wait on each other are not guaranteed to run together
+(B200_PROFILING: Xid 109); with the barrier every flag is set before the waiting
+kernel starts.  The result must be BITWISE the single-process solve on two
+loopback slabs (same kernels, same slot order of the sums)."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import inputs
+from gpu_util import fields, from_gpu_vec, quantize_vec, to_gpu_vec, torch_cuda
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PREC = {"fp32": 0, "mixed": 1}
+
+
+@pytest.fixture(scope="module")
+def sten():
+    import paper_2010_03660_b200 as s
+    return s
+
+
+def _free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed):
+    port = _free_port()
+    procs = []
+    for r in range(world):
+        cmd = [sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), str(world), str(port),
+               str(tmp_path), prec, str(maxit), repr(tol), str(nx), str(ny), str(nz), str(seed)]
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=300)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        outs.append(out)
+    for p, out in zip(procs, outs):
+        assert p.returncode == 0, out[-3000:]
+    return [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
+
+
+def _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, world):
+    torch = torch_cuda()
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=seed)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=seed), prec)
+    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+    st = sten.stencil_create(nx, ny, nz, coeffs, nslabs=world)
+    sten.set_schedule(st, sten.SCHED_SR)
+    sten.set_sr_exchange(st, sten.XCHG_FUSED)
+    bt = to_gpu_vec(b, prec)
+    xt = torch.empty_like(bt)
+    it, hist, status = sten.bicgstab_solve(st, PREC[prec], bt, None, tol, maxit, xt)
+    x = from_gpu_vec(xt, prec)
+    st.close()
+    return x, it, hist, status
+
+
+@pytest.mark.parametrize("prec,maxit,tol,mesh", [
+    ("fp32", 12, 0.0, (40, 33, 24)),
+    ("mixed", 12, 0.0, (40, 33, 24)),
+    ("mixed", 40, 1e-3, (37, 29, 16)),  # stops on the tolerance: both ranks take the same decision
+    ("fp32", 30, 1e-6, (64, 9, 10)),
+])
+def test_two_processes_fused_sr_equals_loopback_slabs(sten, tmp_path, prec, maxit, tol, mesh):
+    nx, ny, nz = mesh
+    seed = 5
+    res = _run_ranks(tmp_path, 2, prec, maxit, tol, nx, ny, nz, seed)
+    x_ref, it_ref, h_ref, s_ref = _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, 2)
+    for r in res:
+        assert int(r["it"]) == it_ref and int(r["status"]) == s_ref
+        assert np.array_equal(r["hist"], h_ref)
+        assert int(r["launches"]) > 0
+    x = np.concatenate([r["x"] for r in res], axis=0)
+    assert x.shape == x_ref.shape
+    assert np.array_equal(x, x_ref)
+    if tol > 0:
+        assert s_ref == sten.CONVERGED and it_ref < maxit and h_ref[-1] <= tol
+
+
+def test_p2p_only_comm_refuses_what_needs_nccl(sten):
+    """A peer-memory-only communicator: create checks the slab convention; everything but the
+    imported fused SR solve is refused (no silent fallback)."""
+    torch = torch_cuda()
+    nx, ny, nz = 16, 8, 8
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz // 2, seed=3)
+    comm = sten.comm_create(None, 2, 0, 0)
+    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+    with pytest.raises(sten.StenError):
+        sten.stencil_create(nx, ny, 7, coeffs, comm=comm)  # 7 planes do not split over 2 ranks
+    st = sten.stencil_create(nx, ny, nz, coeffs, comm=comm)
+    assert st.nz == nz // 2
+    b = torch.zeros(nz // 2, ny, nx, dtype=torch.float32, device="cuda")
+    x = torch.empty_like(b)
+    with pytest.raises(sten.StenError, match="p2p-only"):
+        sten.bicgstab_solve(st, sten.FP32, b, None, 0.0, 3, x)  # SR not imported / classic
+    with pytest.raises(sten.StenError, match="p2p-only"):
+        sten.stencil_apply(st, sten.FP32, b, x)
+    st.close()
+    comm.close()
+    with pytest.raises(sten.StenError):
+        sten.comm_create(None, 2, 0, 9999)  # no such device

@@ -321,7 +321,7 @@ def test_p2p_export_and_import_guards(sten):
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=3)
     st = gpu_stencil(diag, offs, nslabs=2)
     rec = sten.p2p_export(st, PREC["mixed"])
-    assert len(rec) == 22 * 64  # 2 boundary slabs x 2 sets x 5 vectors + inbox sums, flags
+    assert len(rec) == 46 * 64  # 2 boundary slabs x (2 sets x 5 vectors + 12 coefficient arrays) + inbox sums, flags
     with pytest.raises(sten.StenError):  # needs a multi-rank communicator
         sten.p2p_import(st, PREC["mixed"], [rec, rec])
     st.close()
@@ -345,21 +345,34 @@ def test_sr_chunk_plan_of_small_meshes(sten):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-def test_sr_light_last_sweep(sten, prec, monkeypatch):
+def test_sr_light_last_sweep(sten, prec):
     """The last sweep of a solve runs without its three SpMVs (k_sr_last): x and every earlier
     history entry are bitwise those of the full sweep; hist[maxit] differs only by the order of
-    its fp32 sum.  STEN_SR_NOLIGHT=1 selects the full sweep."""
+    its fp32 sum.  sten_set_option(STEN_OPT_SR_LIGHT_LAST, 0) selects the full sweep.  With
+    tol > 0: a solve that stops before maxit never reaches the light sweep (bitwise equal); one
+    that reaches maxit decides its status on the light sweep's sum (equal away from the tol
+    boundary)."""
     nx, ny, nz = 45, 33, 20
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=4)
     b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=4), prec)
     st = gpu_stencil(diag, offs)
-    for maxit in (0, 1, 12):
-        x1, it1, h1, s1 = _solve(sten, st, prec, b, 0.0, maxit)
-        monkeypatch.setenv("STEN_SR_NOLIGHT", "1")
-        x2, it2, h2, s2 = _solve(sten, st, prec, b, 0.0, maxit)
-        monkeypatch.delenv("STEN_SR_NOLIGHT")
-        assert it1 == it2 == maxit and s1 == s2
+    assert sten.get_option(st, sten.OPT_SR_LIGHT_LAST) == 1
+    tol_stop = 1e-5 if prec == "fp32" else 2e-3
+    for tol, maxit in ((0.0, 0), (0.0, 1), (0.0, 12), (tol_stop, 60), (1e-12, 6)):
+        x1, it1, h1, s1 = _solve(sten, st, prec, b, tol, maxit)
+        sten.set_option(st, sten.OPT_SR_LIGHT_LAST, 0)
+        x2, it2, h2, s2 = _solve(sten, st, prec, b, tol, maxit)
+        sten.set_option(st, sten.OPT_SR_LIGHT_LAST, 1)
+        assert it1 == it2 and s1 == s2, (tol, maxit, it1, it2, s1, s2)
         assert np.array_equal(widen(x1, prec), widen(x2, prec))
+        if tol > 0 and it1 < maxit:  # stopped early: the light sweep never ran
+            assert s1 == sten.CONVERGED and np.array_equal(h1, h2)
+            continue
+        assert it1 == maxit
         assert np.array_equal(h1[:-1], h2[:-1])
         assert abs(h1[-1] - h2[-1]) <= 1e-5 * h2[-1]
+    with pytest.raises(sten.StenError):
+        sten.set_option(st, sten.OPT_SR_LIGHT_LAST, 2)
+    with pytest.raises(sten.StenError):
+        sten.set_option(st, 99, 0)
     st.close()
