@@ -77,6 +77,7 @@ def _declare(L):
     L.o16_to_double_array.argtypes = [_I64, _P, _P]
     L.o16_fma_array.argtypes = [_I64, _P, _P, _P, _P]
     L.o16_add_array.argtypes = [_I64, _P, _P, _P]
+    L.o32_fma_array.argtypes = [_I64, _P, _P, _P, _P]
     L.o16_mul_array.argtypes = [_I64, _P, _P, _P]
     L.o16_apply_fused.argtypes = [_I, _I, _I, _P, _P, _P]
     L.o16_apply_unfused.argtypes = [_I, _I, _I, _P, _P, _P]
@@ -220,6 +221,15 @@ def fma16_array(a, b, c):
     a, b, c = (_c(t, np.uint16) for t in (a, b, c))
     out = np.empty(a.shape, np.uint16)
     lib().o16_fma_array(a.size, _ptr(a), _ptr(b), _ptr(c), _ptr(out))
+    return out
+
+
+def fma32_array(a, b, c):
+    """a*b + c with ONE rounding to fp32 (C99 fmaf), element-wise; broadcasts scalars."""
+    a, b, c = np.broadcast_arrays(*(np.asarray(t, np.float32) for t in (a, b, c)))
+    a, b, c = (_c(t, np.float32) for t in (a, b, c))
+    out = np.empty(a.shape, np.float32)
+    lib().o32_fma_array(a.size, _ptr(a), _ptr(b), _ptr(c), _ptr(out))
     return out
 
 

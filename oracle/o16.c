@@ -314,6 +314,12 @@ void o16_fma_array(int64_t n, const uint16_t *a, const uint16_t *b, const uint16
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = o16_fma(a[i], b[i], c[i]);
 }
+/* fp32 fused multiply-add, one rounding (C99 fmaf): the fp32 AXPY primitive of the
+ * classic phases' mirrors (R11 in fp32: p' = fma(beta, fma(-omega, v, p), r), s = fma(-alpha, v, r)) */
+void o32_fma_array(int64_t n, const float *a, const float *b, const float *c, float *out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = fmaf(a[i], b[i], c[i]);
+}
 void o16_add_array(int64_t n, const uint16_t *a, const uint16_t *b, uint16_t *out) {
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = o16_add(a[i], b[i]);

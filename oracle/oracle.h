@@ -87,6 +87,7 @@ uint16_t o16_mul(uint16_t a, uint16_t b);
 void o16_from_double_array(int64_t n, const double *x, uint16_t *h);
 void o16_to_double_array(int64_t n, const uint16_t *h, double *x);
 void o16_fma_array(int64_t n, const uint16_t *a, const uint16_t *b, const uint16_t *c, uint16_t *out);
+void o32_fma_array(int64_t n, const float *a, const float *b, const float *c, float *out); /* fmaf */
 void o16_add_array(int64_t n, const uint16_t *a, const uint16_t *b, uint16_t *out);
 void o16_mul_array(int64_t n, const uint16_t *a, const uint16_t *b, uint16_t *out);
 

@@ -191,3 +191,41 @@ def test_zero_signs_and_specials(orc):
     assert orc.mul16(0x7BFF, 0x7BFF) == INF  # overflow
     assert orc.mul16(0x0001, 0x3800) == 0x0000  # 2^-24 * 0.5 -> tie -> even (0)
     assert orc.mul16(0x0003, 0x3800) == 0x0002  # 1.5 quanta -> tie -> even (2)
+
+
+# ------------------------------------------------- fp32 fused multiply-add --
+def _rn32_fraction(F):
+    """Nearest-even fp32 to the rational F (finite, normal-range results here), by brute force over
+    the neighbours of numpy's float32 of float(F)."""
+    c = np.float32(float(F))
+    cands = {c, np.nextafter(c, np.float32(np.inf)), np.nextafter(c, np.float32(-np.inf))}
+    best = None
+    for x in cands:
+        d = abs(Fraction(float(x)) - F)
+        key = (d, int(np.array(x, np.float32).view(np.uint32)) & 1)  # ties: even significand
+        if best is None or key < best[0]:
+            best = (key, x)
+    return best[1]
+
+
+def test_fma32_matches_exact_rational(orc):
+    """o32_fma_array (the fp32 AXPY primitive of the classic-phase mirrors): one rounding of the
+    exact a*b + c; a single-rounding witness differs from round(round(a*b) + c)."""
+    rng = np.random.default_rng(5)
+    n = 6000
+    a = rng.uniform(-2, 2, n).astype(np.float32)
+    b = rng.uniform(-2, 2, n).astype(np.float32)
+    c = rng.uniform(-2, 2, n).astype(np.float32)
+    c[: n // 3] = (-(a[: n // 3].astype(np.float64) * b[: n // 3])).astype(np.float32)  # cancellation
+    got = orc.fma32_array(a, b, c)
+    unfused_differs = 0
+    for i in range(n):
+        F = Fraction(float(a[i])) * Fraction(float(b[i])) + Fraction(float(c[i]))
+        if F == 0:
+            assert got[i] == 0
+            continue
+        assert got[i] == _rn32_fraction(F), (a[i], b[i], c[i])
+        unfused_differs += got[i] != np.float32(np.float32(a[i] * b[i]) + c[i])
+    assert unfused_differs > 0
+    # scalar broadcasting, as the mirrors use it
+    assert np.array_equal(orc.fma32_array(np.float32(0.5), b[:8], c[:8]), orc.fma32_array(np.full(8, 0.5), b[:8], c[:8]))
