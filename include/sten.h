@@ -319,6 +319,27 @@ int sten_set_dot_precision(sten_stencil *st, int dots);
  * segments partition every (x, y) column into the pencils of
  * STEN_DOTS_HALF.  Errors: STEN_EINVAL (cap too small, NULL n). */
 int sten_sr_segments(sten_stencil *st, int precision, int *z0, int cap, int *n);
+/* The same for the classic kernels (H1, H2, apply): the first plane of every
+ * z chunk a CTA marches, per slab (the decomposed, overlapped schedule cuts
+ * each slab into plane 0, the interior in chunks from plane 1, plane nz-1). */
+int sten_classic_segments(sten_stencil *st, int precision, int *z0, int cap, int *n);
+
+/* One phase of the classic schedule (Alg. 1) on caller
+ * vectors, for parity tests, in the kernels and launch configuration a solve
+ * uses (slabs, halo exchange and its overlap included).  The scalars are
+ * rounded to fp32 (DevState), then to the working precision (R11):
+ *   phase 1 (H1): out0 = p' = r + beta (p - omega v) (as fma(beta,
+ *     fma(-omega, v, p), r)), out1 = v' = A p'; dots[0] = (rh, v');
+ *   phase 2 (H2): out0 = s = r - alpha v (as fma(-alpha, v, r)),
+ *     out1 = t = A s; dots[0] = (t, s), dots[1] = (t, t);
+ * the SpMV as R10's FMA chain.  Vectors: this rank's points, dense, storage
+ * type of `precision`, host or device; p and rh are read by H1 only (may be
+ * NULL for H2).  dots (host) receives the fp32 sums over all slabs and ranks.
+ * Synchronises cuda_stream.  Errors: STEN_EINVAL, STEN_ECUDA, STEN_ENCCL,
+ * STEN_EUNSUPPORTED (p2p-only communicator). */
+int sten_classic_phase(sten_stencil *st, int precision, int phase, double alpha, double omega, double beta,
+                       const void *r, const void *p, const void *v, const void *rh, void *out0, void *out1,
+                       float *dots, void *cuda_stream);
 
 /* One SR sweep on caller vectors, for parity tests (oracle/osr.c
  * o16_sr_sweep / o32_sr_sweep).  With the scalars (alpha, omega, beta) of
@@ -388,6 +409,12 @@ int sten_set_host_barrier(sten_stencil *st, void (*fn)(void *ctx), void *ctx);
  * (uniform chunks), pack bytes per thread vector (16, or 8 = twice the
  * threads per tile).  Errors: STEN_EINVAL for an unsupported combination. */
 int sten_set_sr_tiling(sten_stencil *st, int precision, int by, int stages, int cstages, int zc, int pack);
+/* SR chunk plan for tuning and tests: every CTA marches zc planes, except that
+ * the last tail_planes planes of each slab (plus any remainder) go in chunks of
+ * zc_tail (the default plan at config 3: 160, then 320 planes of 64-plane
+ * chunks).  tail_planes = 0, or >= the slab's planes: uniform zc chunks (the
+ * remainder in one zc_tail chunk).  Errors: STEN_EINVAL. */
+int sten_set_sr_chunks(sten_stencil *st, int precision, int zc, int tail_planes, int zc_tail);
 
 /* Tile geometry override for tuning (0 = library default).  bx: points per
  * tile in x (multiple of 8), by: rows per tile, zc: planes per CTA,

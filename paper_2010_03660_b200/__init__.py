@@ -94,6 +94,9 @@ def lib():
         L.sten_set_sr_exchange.argtypes = [P, I]
         L.sten_p2p_export.argtypes = [P, I, P, ctypes.POINTER(ctypes.c_size_t)]
         L.sten_p2p_import.argtypes = [P, I, P, ctypes.c_size_t]
+        L.sten_classic_phase.argtypes = [P, I, I, D, D, D, P, P, P, P, P, P, P, P]
+        L.sten_classic_segments.argtypes = [P, I, ctypes.POINTER(ctypes.c_int), I, ctypes.POINTER(ctypes.c_int)]
+        L.sten_set_sr_chunks.argtypes = [P, I, I, I, I]
         L.sten_sr_sweep.argtypes = [P, I, D, D, D, P, P, P, P, P, P, P, P, P]
         L.bicgstab_refine.argtypes = [P, P, P, D, I, D, I, P, ctypes.POINTER(I), ctypes.POINTER(I), P,
                                       ctypes.POINTER(I), P]
@@ -144,6 +147,8 @@ def _stream(stream):
 
 
 def _check_vec(a, precision, n, name):
+    if a is None:
+        raise StenError(f"{name} is required")
     want = 4 if precision == FP32 else 2
     if _itemsize(a) != want:
         raise StenError(f"{name}: element size {_itemsize(a)} does not match precision {precision}")
@@ -367,6 +372,20 @@ def set_dot_precision(st: Stencil, dots: int):
     _check(lib().sten_set_dot_precision(st.handle, int(dots)))
 
 
+def classic_segments(st: Stencil, precision: int):
+    """First planes of the classic kernels' z chunks on this rank (sten_classic_segments)."""
+    n = ctypes.c_int(0)
+    _check(lib().sten_classic_segments(st.handle, precision, None, 0, ctypes.byref(n)))
+    buf = (ctypes.c_int * max(n.value, 1))()
+    _check(lib().sten_classic_segments(st.handle, precision, buf, n.value, ctypes.byref(n)))
+    return [int(buf[i]) for i in range(n.value)]
+
+
+def set_sr_chunks(st: Stencil, precision: int, zc: int, tail_planes: int = 0, zc_tail: int = 0):
+    """sten_set_sr_chunks: zc-plane chunks, the last tail_planes planes in zc_tail-plane chunks."""
+    _check(lib().sten_set_sr_chunks(st.handle, precision, zc, tail_planes, zc_tail))
+
+
 def sr_segments(st: Stencil, precision: int):
     """First planes of the SR chunk plan's z segments on this rank (the pencils of DOTS_HALF)."""
     n = ctypes.c_int(0)
@@ -395,6 +414,21 @@ def sr_sweep(st: Stencil, precision: int, scalars, rh, x, r, p, v, q, y, stream=
     _check(lib().sten_sr_sweep(st.handle, precision, al, om, be, _ptr(rh), _ptr(x), _ptr(r), _ptr(p), _ptr(v),
                                _ptr(q), _ptr(y), dots.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
     return dots
+
+
+def classic_phase(st: Stencil, precision: int, phase: int, scalars, r, p, v, rh, out0, out1, stream=None):
+    """sten_classic_phase: one H1 (phase 1: out0 = p', out1 = v' = A p', returns [(rh, v')]) or
+    H2 (phase 2: out0 = s, out1 = t = A s, returns [(t, s), (t, t)]) on caller vectors.
+    scalars = (alpha, omega, beta)."""
+    for name, a in (("r", r), ("v", v), ("out0", out0), ("out1", out1)) + (
+            (("p", p), ("rh", rh)) if phase == 1 else ()):
+        _check_vec(a, precision, st.npoints, name)
+    dots = np.zeros(2, np.float32)
+    al, om, be = (float(t) for t in scalars)
+    _check(lib().sten_classic_phase(st.handle, precision, int(phase), al, om, be, _ptr(r), _ptr(p), _ptr(v),
+                                    _ptr(rh), _ptr(out0), _ptr(out1), dots.ctypes.data_as(ctypes.c_void_p),
+                                    _stream(stream)))
+    return dots[:1] if phase == 1 else dots
 
 
 def bicgstab_refine(st: Stencil, b, x0, tol: float, outer_maxit: int, inner_tol: float, inner_maxit: int, x_out,

@@ -387,7 +387,7 @@ static Reduce make_red(sten_stencil *st, int slab) {
 // second reduction scratch because it runs concurrently with the other two)
 enum { CLS_ALL = 0, CLS_INTERIOR = 1, CLS_BOTTOM = 2, CLS_TOP = 3 };
 static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int parity, cudaStream_t s,
-                          int part = CLS_ALL) {
+                          int part = CLS_ALL, bool capture = false) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   const Tiling &t = st->tiling[prec];
@@ -426,6 +426,7 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
   if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + t.zc - 1) / t.zc) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: stencil grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
+  if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;  // raw sums (sten_classic_phase)
   if (part != CLS_ALL) {
     a.red.slab_out = st->slab_sums + (3 * slab + part - 1) * kMaxDots;
     if (part == CLS_INTERIOR) {
@@ -593,7 +594,8 @@ static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s, int nslot
 // planes and then runs the two boundary planes; the three parts' sums meet in
 // the phase's reduction.
 template <typename Xchg>
-static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cudaStream_t s, Xchg xchg) {
+static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cudaStream_t s, Xchg xchg,
+                            bool finalize = true) {
   const int ns = (int)st->slabs.size();
   CUDA_TRY(cudaEventRecord(st->ev_fork, s));
   CUDA_TRY(cudaStreamWaitEvent(st->side, st->ev_fork, 0));
@@ -605,7 +607,7 @@ static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cu
   }
   CUDA_TRY(cudaEventRecord(st->ev_join, st->side));
   CUDA_TRY(cudaStreamWaitEvent(s, st->ev_join, 0));
-  return reduce_scalars(st, mode == MODE_H1 ? PH_H1 : PH_H2, s, 3 * ns);
+  return finalize ? reduce_scalars(st, mode == MODE_H1 ? PH_H1 : PH_H2, s, 3 * ns) : STEN_OK;
 }
 
 static bool cls_overlapped(const sten_stencil *st) {
@@ -2115,6 +2117,31 @@ int sten_set_dot_precision(sten_stencil *st, int dots) {
   return STEN_OK;
 }
 
+int sten_classic_segments(sten_stencil *st, int prec, int *z0, int cap, int *n) {
+  if (!st || !n) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (st->tiling[prec].bx == 0) default_tiling(st, prec);
+  const int zc = st->tiling[prec].zc;
+  int cnt = 0;
+  for (const Slab &sl : st->slabs) {
+    std::vector<int> starts;
+    if (cls_overlapped(st)) {  // plane 0, the interior in zc chunks from plane 1, plane nz-1
+      starts.push_back(0);
+      for (int z = 1; z < sl.nz - 1; z += zc) starts.push_back(z);
+      starts.push_back(sl.nz - 1);
+    } else {
+      for (int z = 0; z < sl.nz; z += zc) starts.push_back(z);
+    }
+    for (int z : starts) {
+      if (z0 && cnt < cap) z0[cnt] = (int)sl.z_first + z;
+      ++cnt;
+    }
+  }
+  *n = cnt;
+  if (z0 && cnt > cap) return set_err(STEN_EINVAL, "%d segments, room for %d", cnt, cap);
+  return STEN_OK;
+}
+
 int sten_sr_segments(sten_stencil *st, int prec, int *z0, int cap, int *n) {
   if (!st || !n) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
@@ -2247,6 +2274,19 @@ int sten_set_sr_exchange(sten_stencil *st, int mode) {
   return STEN_OK;
 }
 
+int sten_set_sr_chunks(sten_stencil *st, int prec, int zc, int tail_planes, int zc_tail) {
+  if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
+  if (zc < 1 || tail_planes < 0 || (tail_planes > 0 && zc_tail < 1))
+    return set_err(STEN_EINVAL, "bad SR chunk plan zc=%d tail_planes=%d zc_tail=%d", zc, tail_planes, zc_tail);
+  if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
+  SrTiling &t = st->srt[prec];
+  t.zc = zc;
+  t.tail = tail_planes;
+  t.zc_tail = tail_planes > 0 ? zc_tail : zc;
+  drop_graphs(st);
+  return ensure_bufs(st, prec) == STEN_OK ? ensure_sr(st, prec) : STEN_ECUDA;  // partial-sum capacity
+}
+
 int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstages, int zc, int pack) {
   if (!st || (prec != STEN_FP32 && prec != STEN_MIXED)) return set_err(STEN_EINVAL, "bad handle/precision");
   if (st->srt[prec].by == 0) default_sr_tiling(st, prec);
@@ -2266,6 +2306,71 @@ int sten_set_sr_tiling(sten_stencil *st, int prec, int by, int stages, int cstag
   st->srt[prec] = t;
   for (Slab &sl : st->slabs) sl.sr[prec].maps_ok = false;
   drop_graphs(st);
+  return STEN_OK;
+}
+
+int sten_classic_phase(sten_stencil *st, int prec, int phase, double alpha, double omega, double beta,
+                       const void *r, const void *p, const void *v, const void *rh, void *out0, void *out1,
+                       float *dots, void *cuda_stream) {
+  if (!st || !r || !v || !out0 || !out1 || !dots) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (phase != 1 && phase != 2) return set_err(STEN_EINVAL, "phase %d is not 1 (H1) or 2 (H2)", phase);
+  if (phase == 1 && (!p || !rh)) return set_err(STEN_EINVAL, "H1 needs p and rh");
+  if (p2p_only(st)) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: sten_classic_phase needs NCCL");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  RC_TRY(ensure_bufs(st, prec));
+  st->launches = 0;
+  DevState h;
+  memset(&h, 0, sizeof h);
+  h.alpha = (float)alpha;
+  h.omega = (float)omega;
+  h.beta = (float)beta;
+  h.maxit = 1;
+  h.ev = -1;
+  h.half = prec == STEN_MIXED;
+  *st->st_host = h;
+  CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
+  const int ns = (int)st->slabs.size();
+  const int mode = phase == 1 ? MODE_H1 : MODE_H2;
+  RC_TRY(copy_in(st, prec, [](PrecBufs &b) -> void * { return b.r; }, r, s));
+  if (phase == 1) {
+    RC_TRY(copy_in(st, prec, [](PrecBufs &b) -> void * { return b.p[0]; }, p, s));
+    RC_TRY(copy_in(st, prec, [](PrecBufs &b) -> void * { return b.v[0]; }, v, s));
+    RC_TRY(copy_in(st, prec, [](PrecBufs &b) -> void * { return b.rh; }, rh, s));
+  } else {
+    RC_TRY(copy_in(st, prec, [](PrecBufs &b) -> void * { return b.v[1]; }, v, s));
+  }
+  auto xchg = [&](cudaStream_t ss) {
+    if (phase == 1) {
+      RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, ss));
+      RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.p[0]; }, ss));
+      return exchange(st, prec, [](PrecBufs &b) { return b.v[0]; }, ss);
+    }
+    // H2 also reads r at the neighbours (s = r - alpha v); a solve exchanged it before H1
+    RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, ss));
+    return exchange(st, prec, [](PrecBufs &b) { return b.v[1]; }, ss);
+  };
+  int nslots = ns;
+  if (cls_overlapped(st)) {
+    RC_TRY(overlapped_phase(st, prec, mode, 0, s, xchg, false));
+    nslots = 3 * ns;
+  } else {
+    if (decomposed(st)) RC_TRY(xchg(s));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, mode, k, 0, s, CLS_ALL, true));
+  }
+  KLAUNCH(slabsum_launch(st->slab_sums, nslots, st->red_total, s));
+  if (nccl_ranks(st))
+    NCCL_TRY(g_nccl.AllReduce(st->red_total, st->red_total, kMaxDots, ncclFloat32, ncclSum, st->comm->comm, s));
+  if (phase == 1) {
+    RC_TRY(copy_out(st, prec, [](PrecBufs &b) -> void * { return b.p[1]; }, out0, s));
+    RC_TRY(copy_out(st, prec, [](PrecBufs &b) -> void * { return b.v[1]; }, out1, s));
+  } else {
+    RC_TRY(copy_out(st, prec, sel_s, out0, s));
+    RC_TRY(copy_out(st, prec, sel_t, out1, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(dots, st->red_total, sizeof(float) * (phase == 1 ? 1 : 2), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
   return STEN_OK;
 }
 

@@ -6,8 +6,12 @@ for each sampled point the oracle scales (o64_jacobi_scale) and applies
 (o16/o32 mirrors) the 3x3x3 window around it, clipped to the global mesh, built
 from the global generator (inputs.field_at) - the centre value of the window is
 exactly the full-mesh value.  Samples cover mesh corners and faces, tile edges
-(x = 127/128, y = 15/16), z-chunk edges (z = 63/64) and random interior points.
-The solve is checked through properties that hold at any size.
+(x = 127/128, y = 15/16), the z-chunk edges of the library's own chunk plan
+(sten_classic_segments: every chunk start and the plane before it) and random
+interior points.  The fused phases H1 and H2 (sten_classic_phase, the kernels a
+solve launches) are sampled the same way against the oracle's composition of
+pinned primitives on the window.  The solve is checked through properties that
+hold at any size.
 """
 import numpy as np
 import pytest
@@ -21,11 +25,18 @@ pytestmark = pytest.mark.gpu
 NX, NY, NZ = 600, 595, 1536
 
 
-def sample_points(rng, n_random=600):
+def chunk_edges(segs):
+    zs = {0, 1, NZ - 2, NZ - 1}
+    for z in segs:
+        zs.update(z2 for z2 in (z - 1, z) if 0 <= z2 < NZ)
+    return sorted(zs)
+
+
+def sample_points(rng, n_random=600, zs=(0, 1, 63, 64, 127, 128, 1534, 1535)):
     pts = set()
     for x in (0, 1, 127, 128, 255, 256, 511, 512, 598, 599):
         for y in (0, 1, 15, 16, 593, 594):
-            for z in (0, 1, 63, 64, 127, 128, 1534, 1535):
+            for z in zs:
                 pts.add((x, y, z))
     for _ in range(n_random):
         pts.add((int(rng.integers(NX)), int(rng.integers(NY)), int(rng.integers(NZ))))
@@ -82,7 +93,9 @@ def test_fullsize_spmv_sampled_bitwise(full_problem, prec):
         v = inputs.uniform(3, 7, idx, -1.0, 1.0).astype(np.float32)
         return v if prec == "fp32" else orc.f16_from_double(v.astype(np.float64))
 
-    pts = sample_points(np.random.default_rng(11))
+    segs = sten.classic_segments(st, sten.FP32 if prec == "fp32" else sten.MIXED)
+    assert len(segs) > 1 and segs == sorted(segs)
+    pts = sample_points(np.random.default_rng(11), zs=chunk_edges(segs))
     idx = torch.tensor([x + NX * (y + NY * z) for x, y, z in pts], device="cuda")
     got = yt.reshape(-1)[idx].cpu().numpy()
     if prec != "fp32":
@@ -92,6 +105,76 @@ def test_fullsize_spmv_sampled_bitwise(full_problem, prec):
         a = float(got[k]) if prec == "fp32" else orc.f16_to_double(np.array([got[k]]))[0]
         b = float(want) if prec == "fp32" else orc.f16_to_double(np.array([want]))[0]
         assert a == b, (pt, a, b)
+
+
+PH_STREAMS = dict(r=21, p=22, v=23, rh=24)
+PH_SCAL = (0.61, 0.93, -0.27)  # alpha, omega, beta
+
+
+def _w(x, prec):  # scalar rounded fp64 -> fp32 -> working precision (R11)
+    x32 = np.float32(x)
+    return x32 if prec == "fp32" else orc.f16_from_double(np.array([float(x32)]))[0]
+
+
+def window_phase(pt, phase, prec):
+    """Oracle (out0, out1) of one classic phase at a global point from its clipped 3x3x3 window:
+    out0 = p' (H1) or s (H2) element-wise, out1 = A out0 at the centre."""
+    x, y, z = pt
+    x0, x1 = max(x - 1, 0), min(x + 2, NX)
+    y0, y1 = max(y - 1, 0), min(y + 2, NY)
+    z0, z1 = max(z - 1, 0), min(z + 2, NZ)
+    kg, j, i = np.meshgrid(np.arange(z0, z1), np.arange(y0, y1), np.arange(x0, x1), indexing="ij")
+    diag, offs = inputs.field_at(inputs.KIND_CD, NX, NY, i, j, kg, seed=1, delta=0.1)
+    cq = orc.quantize_coeffs(orc.jacobi_scale(diag, offs), prec)
+    idx = (i + NX * (j + NY * kg)).astype(np.uint64)
+    V = {}
+    for n, s_ in PH_STREAMS.items():
+        v = inputs.uniform(9, s_, idx, -1.0, 1.0).astype(np.float32)
+        V[n] = v if prec == "fp32" else orc.f16_from_double(v.astype(np.float64))
+    al, om, be = (_w(t, prec) for t in PH_SCAL)
+    if prec == "fp32":
+        fma, neg = orc.fma32_array, (lambda a: np.float32(-a))
+        A = lambda u: orc.apply32_fma(cq, u)  # noqa: E731
+    else:
+        fma = lambda a, b, c: orc.fma16_array(np.full(b.shape, a, np.uint16), b, c)  # noqa: E731
+        neg = lambda a: np.uint16(int(a) ^ 0x8000)  # noqa: E731
+        A = lambda u: orc.apply16(cq, u)  # noqa: E731
+    out0 = fma(be, fma(neg(om), V["v"], V["p"]), V["r"]) if phase == 1 else fma(neg(al), V["v"], V["r"])
+    out1 = A(out0)
+    c = (z - z0, y - y0, x - x0)
+    return out0[c], out1[c]
+
+
+@pytest.mark.parametrize("prec", ["mixed", "fp32"])
+@pytest.mark.parametrize("phase", [1, 2])
+def test_fullsize_phase_sampled_bitwise(full_problem, prec, phase):
+    """H1 (p' = r + beta(p - omega v), v' = A p') and H2 (s = r - alpha v, t = A s) at 600x595x1536 in
+    the bench's launch configuration, sampled bitwise; their sums against fp64 reductions."""
+    torch = torch_cuda()
+    import inputs.cuda as ic
+    import paper_2010_03660_b200 as sten
+    st = full_problem
+    P = sten.FP32 if prec == "fp32" else sten.MIXED
+    t = {}
+    for n, s_ in PH_STREAMS.items():
+        v32 = ic.uniform_device(NX, NY, NZ, seed=9, stream=s_, dtype="f32")
+        t[n] = v32 if prec == "fp32" else v32.to(torch.float16)
+        del v32
+    o0, o1 = torch.empty_like(t["r"]), torch.empty_like(t["r"])
+    dots = sten.classic_phase(st, P, phase, PH_SCAL, t["r"], t["p"], t["v"], t["rh"], o0, o1)
+    torch.cuda.synchronize()
+    pts = sample_points(np.random.default_rng(23), n_random=300, zs=chunk_edges(sten.classic_segments(st, P)))
+    idx = torch.tensor([x + NX * (y + NY * z) for x, y, z in pts], device="cuda")
+    g0, g1 = (o.reshape(-1)[idx].cpu().numpy() for o in (o0, o1))
+    wid = (lambda a: float(a)) if prec == "fp32" else (lambda a: float(orc.f16_to_double(np.array([a]).view(np.uint16))[0]))
+    for k, pt in enumerate(pts):
+        w0, w1 = window_phase(pt, phase, prec)
+        assert wid(g0[k]) == wid(w0) and wid(g1[k]) == wid(w1), (pt, phase)
+    d0, d1 = o0.double().reshape(-1), o1.double().reshape(-1)
+    pairs = [(t["rh"].double().reshape(-1), d1)] if phase == 1 else [(d1, d0), (d1, d1)]
+    for got, (a, b) in zip(dots, pairs):
+        exact, scale = float(torch.dot(a, b)), float(torch.dot(a.abs(), b.abs()))
+        assert abs(float(got) - exact) <= 2e-5 * scale, (float(got), exact)
 
 
 def test_fullsize_mixed_solve_properties(full_problem):

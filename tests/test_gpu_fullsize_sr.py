@@ -1,13 +1,14 @@
 """SR-schedule parity at BASELINE.json's full size (600x595x1536, config 3) in the
-launch configuration bench.py times (the SR defaults: 320-plane chunks with
-64-plane tail chunks, 16-row tiles, unpadded rows).
+launch configuration bench.py times (the SR defaults: 160-plane chunks with
+64-plane tail chunks over the last 320 planes, 16-row tiles, unpadded rows).
 
 One sweep (sten_sr_sweep) on seeded full-mesh inputs is checked on SAMPLED
 outputs: the oracle runs o16_sr_sweep / o32_sr_sweep on the clipped 5x5x5 window
 around each sampled point (y' = A A p' reaches two points), built from the global
 generator; the window centre is exactly the full-mesh value.  Samples cover mesh
-corners and faces, tile edges (x = 127/128, y = 15/16), z-chunk edges of the SR
-chunk plan (z = 319/320, 1279/1280, 1343/1344) and random interior points.  The
+corners and faces, tile edges (x = 127/128, y = 15/16), every z-chunk edge of
+the library's own SR chunk plan (sten_sr_segments: each chunk start and the plane
+before it, including the long-to-tail transition) and random interior points.  The
 twelve sums are checked against fp64 reductions of the returned vectors; the
 solve through properties that hold at any size.
 """
@@ -25,11 +26,18 @@ STREAMS = dict(rh=7, x=8, r=9, p=10, v=11, q=12, y=13)
 SCAL = (0.61, 0.93, -0.27)
 
 
-def sample_points(rng, n_random=300):
+def chunk_edges(segs):
+    zs = {0, 1, NZ - 2, NZ - 1}
+    for z in segs:
+        zs.update(z2 for z2 in (z - 1, z) if 0 <= z2 < NZ)
+    return sorted(zs)
+
+
+def sample_points(rng, zs, n_random=300):
     pts = set()
     for x in (0, 1, 127, 128, 511, 512, 598, 599):
         for y in (0, 1, 15, 16, 593, 594):
-            for z in (0, 1, 319, 320, 1279, 1280, 1343, 1344, 1534, 1535):
+            for z in zs:
                 pts.add((x, y, z))
     for _ in range(n_random):
         pts.add((int(rng.integers(NX)), int(rng.integers(NY)), int(rng.integers(NZ))))
@@ -85,7 +93,11 @@ def test_fullsize_sr_sweep_sampled_bitwise(full_problem, prec):
     order = ["rh", "x", "r", "p", "v", "q", "y"]
     dots = sten.sr_sweep(st, P, SCAL, *[ts[n] for n in order])
     torch.cuda.synchronize()
-    pts = sample_points(np.random.default_rng(17))
+    segs = sten.sr_segments(st, P)
+    if prec == "mixed":  # the bench's plan: long chunks, then the short tail chunks
+        steps = [b - a for a, b in zip(segs, segs[1:])]
+        assert len(set(steps)) == 2 and steps == sorted(steps, reverse=True), segs
+    pts = sample_points(np.random.default_rng(17), chunk_edges(segs))
     idx = torch.tensor([x + NX * (y + NY * z) for x, y, z in pts], device="cuda")
     got = {n: ts[n].reshape(-1)[idx].cpu().numpy() for n in order[1:]}
     widen = (lambda a: a.astype(np.float64)) if prec == "fp32" else (lambda a: orc.f16_to_double(np.asarray(a)))

@@ -33,12 +33,14 @@ def _pairs(rh, r, v, q, y):
     return [(rh, v), (rh, r), (rh, q), (rh, y), (q, r), (q, v), (y, r), (y, v), (q, q), (q, y), (y, y), (r, r)]
 
 
-def _sweep_case(sten, prec, mesh, tiling=None, nslabs=1, scalars=(0.61, 0.93, -0.27), seed=1):
+def _sweep_case(sten, prec, mesh, tiling=None, nslabs=1, scalars=(0.61, 0.93, -0.27), seed=1, chunks=None):
     nx, ny, nz = mesh
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.0, seed=seed)
     st = gpu_stencil(diag, offs, nslabs=nslabs)
     if tiling:
         sten.set_sr_tiling(st, PREC[prec], *tiling)
+    if chunks:
+        sten.set_sr_chunks(st, PREC[prec], *chunks)
     cq = oracle_coeffs(diag, offs, prec)
     rng = np.random.default_rng(seed + 17)
     vec = lambda: quantize_vec(rng.uniform(-1, 1, (nz, ny, nx)), prec)
@@ -82,6 +84,36 @@ def test_sr_sweep_geometries(sten, prec, tiling):
     got, dots, ref, _ = _sweep_case(sten, prec, (141, 37, 23), tiling=tiling, seed=4)
     for g, w in zip(got, ref[:6]):
         assert np.array_equal(widen(g, prec), widen(w, prec))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("chunks,nslabs", [((16, 16, 4), 1), ((10, 20, 3), 1), ((7, 48, 5), 1), ((9, 12, 2), 2),
+                                           ((16, 0, 0), 1)])
+def test_sr_sweep_long_and_tail_chunks(sten, prec, chunks, nslabs):
+    """A long + tail chunk plan (the shape of the bench's: long chunks, then short ones over the
+    last planes, with a remainder) at a size the oracle runs whole: bitwise, and the segment list
+    is the plan."""
+    nx, ny, nz = 70, 19, 48
+    got, dots, ref, _ = _sweep_case(sten, prec, (nx, ny, nz), nslabs=nslabs, seed=8, chunks=chunks)
+    for g, w in zip(got, ref[:6]):
+        assert np.array_equal(widen(g, prec), widen(w, prec))
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.0, seed=8)
+    st = gpu_stencil(diag, offs, nslabs=nslabs)
+    sten.set_sr_chunks(st, PREC[prec], *chunks)
+    zc, tail, zct = chunks
+    want = []
+    for k in range(nslabs):
+        nzs = nz // nslabs
+        big = (nzs - (tail if tail < nzs else 0)) // zc  # a tail as long as the slab: no tail
+        z = [k * nzs + c * zc for c in range(big)]
+        zt = big * zc
+        step = zct if zt < nzs and tail else zc
+        while zt < nzs:
+            z.append(k * nzs + zt)
+            zt += step
+        want += z
+    assert sten.sr_segments(st, PREC[prec]) == want
+    st.close()
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
