@@ -270,6 +270,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     it = i;
     int code = -1;
     if (!isfinite(rr) || !isfinite(rhon)) code = ORC_NONFINITE;
+    else if (rr == 0.0f && rhon != 0.0f) code = ORC_BREAKDOWN; /* R23: (r,r) underflowed, r != 0 */
     else if (rr == 0.0f || (tol > 0.0 && hist[i] <= tol)) code = ORC_CONVERGED;
     else if (omega == 0.0f || rhon == 0.0f) code = ORC_BREAKDOWN;
     beta = (rhon / rho) * (alpha / omega);            /* l.183, fp32 */

@@ -213,6 +213,7 @@ int o64_bicgstab(int nx, int ny, int nz, const double *const c[6],
     it = i;
     int code = -1;
     if (!isfinite(rr) || !isfinite(rhon)) code = ORC_NONFINITE;
+    else if (rr == 0.0 && rhon != 0.0) code = ORC_BREAKDOWN; /* R23: (r,r) underflowed, r != 0 */
     else if (rr == 0.0 || (tol > 0.0 && hist[i] <= tol)) code = ORC_CONVERGED;
     else if (omega == 0.0 || rhon == 0.0) code = ORC_BREAKDOWN;
     beta = (rhon / rho) * (alpha / omega);          /* l.183 beta_i             */

@@ -113,6 +113,7 @@ int o64_sr_bicgstab(int nx, int ny, int nz, const double *const c[6],
     it = i;
     int code = -1;
     if (!isfinite(rr) || !isfinite(rho)) code = ORC_NONFINITE;
+    else if (rr == 0.0 && rho != 0.0) code = ORC_BREAKDOWN; /* R23: (r,r) underflowed, r != 0 */
     else if (rr == 0.0 || (tol > 0.0 && hist[i] <= tol)) code = ORC_CONVERGED;
     else if (i > 0 && (omega == 0.0 || rho == 0.0)) code = ORC_BREAKDOWN;
     if (code >= 0 && sr_on_event(code, i, tol, &ev, &ev_it)) break;
@@ -295,6 +296,7 @@ int o16h_sr_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     it = i;
     int code = -1;
     if (!isfinite(rr) || !isfinite(rho)) code = ORC_NONFINITE;
+    else if (rr == 0.0f && rho != 0.0f) code = ORC_BREAKDOWN; /* R23: (r,r) underflowed, r != 0 */
     else if (rr == 0.0f || (tol > 0.0 && hist[i] <= tol)) code = ORC_CONVERGED;
     else if (i > 0 && (omega == 0.0f || rho == 0.0f)) code = ORC_BREAKDOWN;
     if (code >= 0 && sr_on_event(code, i, tol, &ev, &ev_it)) break;

@@ -125,3 +125,26 @@ def test_half_dot_solve_tracks_mixed_early():
     half = orc.bicgstab16(c16, b16, tol=0.0, maxit=12, schedule="sr", segments=[0])
     assert half["hist"][0] == pytest.approx(mixed["hist"][0], rel=1e-3)
     assert np.all(np.abs(half["hist"][:5] - mixed["hist"][:5]) <= 5e-2 * mixed["hist"][:5])
+
+
+def test_half_dot_underflow_is_breakdown_not_convergence():
+    """R23: once ||r|| is ~6e-4 the squares of r's entries fall below fp16's smallest
+    subnormal and every half pencil of (r,r) is 0, while (rhat, r) - products of O(1)
+    entries with r - stays representable.  (r,r) = 0 with (rhat, r) != 0 is impossible
+    in exact arithmetic (r = 0 => (rhat, r) = 0), so the solve reports BREAKDOWN there,
+    never CONVERGED: with tol > 0 it stops with status BREAKDOWN (not a false
+    convergence); the mixed dots (fp32 sums of exact products) do not underflow."""
+    import inputs
+    n = 10
+    diag, offs = inputs.problem_fields(inputs.KIND_CD, n, n, n, seed=2, delta=0.1)
+    c16 = orc.quantize_coeffs(orc.jacobi_scale(diag, offs), "mixed")
+    b16 = orc.f16_from_double(inputs.rhs_uniform(n, n, n, seed=2))
+    half = orc.bicgstab16(c16, b16, tol=0.0, maxit=40, schedule="sr", segments=[0])
+    zero = np.flatnonzero(half["hist"] == 0.0)
+    assert zero.size > 0, "the half-dot (r,r) never underflowed"
+    k = int(zero[0])
+    assert half["status"] == orc.ORC_BREAKDOWN and half["event_it"] == k
+    stop = orc.bicgstab16(c16, b16, tol=1e-9, maxit=40, schedule="sr", segments=[0])
+    assert stop["status"] == orc.ORC_BREAKDOWN and stop["iters"] == k
+    mixed = orc.bicgstab16(c16, b16, tol=0.0, maxit=k, schedule="sr")
+    assert np.all(mixed["hist"] > 0.0)
