@@ -81,7 +81,9 @@ extern "C" {
 #define STEN_EUNSUPPORTED (-5)
 
 /* solve status (R6-R8) */
-#define STEN_CONVERGED 0 /* ||r_i||/||b|| <= tol, or r_i == 0 exactly        */
+#define STEN_CONVERGED 0 /* ||r_i||/||b|| <= tol, or r_i == 0 exactly (an
+                            (r,r) of 0 with (rhat,r) != 0 is an fp16
+                            underflow: BREAKDOWN, R23)                      */
 #define STEN_MAXIT 1     /* maxit iterations done without an event             */
 #define STEN_BREAKDOWN 2 /* (rhat, v) == 0, omega == 0 or (rhat, r_new) == 0   */
 #define STEN_NONFINITE 3 /* a dot product or scalar became Inf/NaN             */
@@ -249,7 +251,12 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
  *                              L2 prefetch distance in planes, 0..16 (default 0)
  *   STEN_OPT_SR_L2_PREFETCH    SR sweep: L2 prefetch distance, 0..16 (default 0)
  *   STEN_OPT_SR_LIGHT_LAST     SR on one slab: the last sweep of a solve
- *                              without its SpMVs (k_sr_last), 0 or 1 (default 1)
+ *                              without its SpMVs (k_sr_last), 0 or 1 (default 1).
+ *                              x and hist[0..maxit-1] are bitwise those of the
+ *                              full sweep; hist[maxit] (and so a status decided
+ *                              exactly at the tol boundary) may differ in the
+ *                              last fp32 bit of its sum; the SR work vectors
+ *                              (r, p, ...) are not valid after any solve
  *   STEN_OPT_CLASSIC_OVERLAP   classic schedule, decomposed (slabs >= 3
  *                              planes): the halo exchange before H1 / H2 runs
  *                              on a side stream with the two boundary planes,

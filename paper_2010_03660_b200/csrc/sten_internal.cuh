@@ -392,6 +392,7 @@ __device__ __forceinline__ void fin_h3(DevState *st, float rhon, float rr) {
   st->it = i;
   int code = -1;
   if (!isfinite(rr) || !isfinite(rhon)) code = STEN_NONFINITE;
+  else if (rr == 0.0f && rhon != 0.0f) code = STEN_BREAKDOWN;  // R23: (r,r) underflowed, r != 0
   else if (rr == 0.0f || (st->tol > 0.0 && h <= st->tol)) code = STEN_CONVERGED;
   else if (st->omega == 0.0f || rhon == 0.0f) code = STEN_BREAKDOWN;
   float beta = (rhon / st->rho) * (st->alpha / st->omega);
@@ -415,6 +416,7 @@ __device__ __forceinline__ void fin_sr(DevState *st, const float *d) {
   st->sweep = i + 1;
   int code = -1;
   if (!isfinite(rr) || !isfinite(rho)) code = STEN_NONFINITE;
+  else if (rr == 0.0f && rho != 0.0f) code = STEN_BREAKDOWN;  // R23: (r,r) underflowed, r != 0
   else if (rr == 0.0f || (st->tol > 0.0 && h <= st->tol)) code = STEN_CONVERGED;
   else if (i > 0 && (st->omega == 0.0f || rho == 0.0f)) code = STEN_BREAKDOWN;
   if (code >= 0) st_event(st, code, i, false);

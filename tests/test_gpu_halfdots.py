@@ -165,3 +165,33 @@ def test_half_dot_api_guards(sten):
     with pytest.raises(sten.StenError, match="constant"):
         sten.bicgstab_solve(cst, MIXED, b, None, 0.0, 3, x)
     cst.close()
+
+
+def test_half_dot_underflow_is_breakdown(sten):
+    """R23: when every fp16 pencil of (r,r) underflows to 0 while (rhat, r) does not,
+    the solve reports BREAKDOWN at that iteration - never a false CONVERGED - as the oracle does
+    (tests/test_oracle_halfdots.py); with tol > 0 it stops there with BREAKDOWN."""
+    torch = torch_cuda()
+    n = 10
+    diag, offs = fields(inputs.KIND_CD, n, n, n, delta=0.1, seed=2)
+    b = quantize_vec(inputs.rhs_uniform(n, n, n, seed=2), "mixed")
+    # the scaled system with b_hat = b (unit diagonal passed in): the RHS of the oracle pin
+    st = gpu_stencil(None, [o / diag for o in offs], unit_diag=True)
+    sten.set_schedule(st, sten.SCHED_SR)
+    sten.set_dot_precision(st, sten.DOTS_HALF)
+    seg = sten.sr_segments(st, MIXED)
+    bt = to_gpu_vec(b, "mixed")
+    xt = torch.empty_like(bt)
+    it, hist, status = sten.bicgstab_solve(st, MIXED, bt, None, 0.0, 40, xt)
+    zero = np.flatnonzero(hist == 0.0)
+    assert zero.size > 0
+    k = int(zero[0])
+    assert status == sten.BREAKDOWN and sten.get_stats(st)["event_iter"] == k
+    it2, hist2, status2 = sten.bicgstab_solve(st, MIXED, bt, None, 1e-9, 40, xt)
+    assert status2 == sten.BREAKDOWN and it2 == k and hist2[-1] == 0.0
+    # the oracle with the library's segments underflows at the same point within the
+    # fp32 reordering of the segment sums (its trajectory matches to 5e-2 until then)
+    cq = oracle_coeffs(diag, offs, "mixed")
+    ref = orc.bicgstab16(cq, b, tol=0.0, maxit=40, schedule="sr", segments=seg)
+    assert ref["status"] == orc.ORC_BREAKDOWN and abs(ref["event_it"] - k) <= 1
+    st.close()
