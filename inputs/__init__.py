@@ -28,4 +28,6 @@ from .gen import (  # noqa: F401
     problem_fields,
     rhs_uniform,
     field_at,
+    problem_fields_2d,
+    rhs_uniform_2d,
 )

@@ -46,6 +46,7 @@ def lib():
         L.sten_inputs_uniform.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong,
                                           ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_int, P, P]
+        L.sten_inputs_fields2d.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, P, P, P]
         _lib = L
     return _lib
 
@@ -73,6 +74,19 @@ def fields_device(kind: int, nx: int, ny: int, nz: int, z0: int = 0, seed: int =
                                   ctypes.c_void_p(diag.data_ptr()), arr, _stream())
     if rc != 0:
         raise RuntimeError(f"sten_inputs_fields failed ({rc})")
+    return diag, offs
+
+
+def fields2d_device(nx: int, ny: int, seed: int = SEED_DEFAULT, delta: float = 0.1):
+    """(diag, offs[8]) of the 2D 9-point stand-in as fp64 CUDA tensors (ny, nx) (gen.py problem_fields_2d)."""
+    import torch
+    diag = torch.empty((ny, nx), dtype=torch.float64, device="cuda")
+    offs = [torch.empty_like(diag) for _ in range(8)]
+    arr = (ctypes.c_void_p * 8)(*[o.data_ptr() for o in offs])
+    rc = lib().sten_inputs_fields2d(nx, ny, seed, 1.0 + float(delta), ctypes.c_void_p(diag.data_ptr()), arr,
+                                    _stream())
+    if rc != 0:
+        raise RuntimeError(f"sten_inputs_fields2d failed ({rc})")
     return diag, offs
 
 

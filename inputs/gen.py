@@ -23,6 +23,15 @@ Problem kinds (readings of BASELINE.json configs):
   computed here once on the host and handed to the CUDA twin, so no
   transcendental is evaluated on two different math libraries.
 
+* 2D (problem_fields_2d; the paper's 9-point SpMV / BiCG sketch, PAPER.md:362-373,
+  gives no test matrix): first-order upwinded convection-diffusion on an nx*ny
+  mesh with the 9-point Laplacian's corner couplings: per point k~U(0.5,2)
+  (stream 1), (ux,uy)~U(-1,1)^2 (streams 2-3); faces a_xm = k + max(ux,0),
+  a_xp = k + max(-ux,0), a_ym = k + max(uy,0), a_yp = k + max(-uy,0); corners
+  a_c = k/4 (the 4:1 face:corner ratio of the "Mehrstellen" 9-point Laplacian);
+  a_P = (1+delta) * sum(a_nb) summed in the o2d.c neighbour order; A[P,nb] = -a_nb.
+  Index i + nx*j.
+
 The right-hand side b ~ U(-1,1) (stream 0) is the right-hand side of the
 ORIGINAL (un-scaled) system A x = b.
 """
@@ -148,3 +157,27 @@ def rhs_uniform(nx: int, ny: int, nz: int, z0: int = 0, seed: int = SEED_DEFAULT
     kg, j, i = np.meshgrid(np.arange(z0, z0 + nz), np.arange(ny), np.arange(nx), indexing="ij")
     idx = (i + nx * (j + ny * kg)).astype(np.uint64)
     return uniform(seed, stream, idx, -1.0, 1.0)
+
+
+def problem_fields_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, delta: float = 0.1):
+    """(diag, offs[8]) of the 2D 9-point stand-in, arrays (ny, nx), offs in the o2d.c order
+    (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1)."""
+    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    idx = (i + nx * j).astype(np.uint64)
+    kd = uniform(seed, STREAM_K, idx, 0.5, 2.0)
+    ux = uniform(seed, STREAM_UX, idx, -1.0, 1.0)
+    uy = uniform(seed, STREAM_UY, idx, -1.0, 1.0)
+    corner = 0.25 * kd
+    a = [corner, kd + np.maximum(uy, 0.0), corner, kd + np.maximum(ux, 0.0), kd + np.maximum(-ux, 0.0),
+         corner, kd + np.maximum(-uy, 0.0), corner]
+    s = a[0] + a[1]
+    for d in range(2, 8):
+        s = s + a[d]
+    diag = (1.0 + float(delta)) * s
+    return np.ascontiguousarray(diag), [np.ascontiguousarray(-ad) for ad in a]
+
+
+def rhs_uniform_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, stream: int = STREAM_B) -> np.ndarray:
+    """b ~ U(-1,1) on the 2D mesh, shape (ny, nx)."""
+    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    return uniform(seed, stream, (i + nx * j).astype(np.uint64), -1.0, 1.0)

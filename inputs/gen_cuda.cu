@@ -65,6 +65,26 @@ __global__ void k_fields(int kind, int nx, int ny, int nz, long long z0, uint64_
   }
 }
 
+// the 2D 9-point stand-in (gen.py problem_fields_2d); offs in the o2d.c order
+__global__ void k_fields2d(int nx, int ny, uint64_t seed, double factor, double *diag, double *o0, double *o1,
+                           double *o2, double *o3, double *o4, double *o5, double *o6, double *o7) {
+  double *off[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+  const long long n = (long long)nx * ny;
+  const uint64_t kK = key(seed, 1), kX = key(seed, 2), kY = key(seed, 3);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const uint64_t idx = (uint64_t)q;
+    const double kd = uniform(kK, idx, 0.5, 2.0);
+    const double ux = uniform(kX, idx, -1.0, 1.0), uy = uniform(kY, idx, -1.0, 1.0);
+    const double c = __dmul_rn(0.25, kd);
+    double a[8] = {c, __dadd_rn(kd, fmax(uy, 0.0)), c, __dadd_rn(kd, fmax(ux, 0.0)), __dadd_rn(kd, fmax(-ux, 0.0)),
+                   c, __dadd_rn(kd, fmax(-uy, 0.0)), c};
+    double s = __dadd_rn(a[0], a[1]);
+    for (int d = 2; d < 8; ++d) s = __dadd_rn(s, a[d]);
+    diag[q] = __dmul_rn(factor, s);
+    for (int d = 0; d < 8; ++d) off[d][q] = -a[d];
+  }
+}
+
 __global__ void k_uniform(int nx, int ny, int nz, long long z0, uint64_t seed, uint64_t stream, double lo, double hi,
                           int out_dtype, void *out) {
   const long long n = (long long)nx * ny * nz;
@@ -92,6 +112,14 @@ int sten_inputs_fields(int kind, int nx, int ny, int nz, long long z0, unsigned 
   long long n = (long long)nx * ny * nz;
   k_fields<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(kind, nx, ny, nz, z0, seed, factor, kz_dev, diag, off[0],
                                                           off[1], off[2], off[3], off[4], off[5]);
+  return (int)cudaGetLastError();
+}
+// the 2D 9-point stand-in: dense (ny,nx) fp64 arrays, off[8] in the o2d.c order
+int sten_inputs_fields2d(int nx, int ny, unsigned long long seed, double factor, double *diag, double *const off[8],
+                         void *stream) {
+  long long n = (long long)nx * ny;
+  k_fields2d<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(nx, ny, seed, factor, diag, off[0], off[1], off[2],
+                                                            off[3], off[4], off[5], off[6], off[7]);
   return (int)cudaGetLastError();
 }
 // U(lo,hi) of `stream` on planes [z0, z0+nz); out_dtype 0: fp64, 1: fp32 (RN of the fp64 value)

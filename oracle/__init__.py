@@ -58,6 +58,11 @@ def _declare(L):
     L.o64_apply_raw.argtypes = [_I, _I, _I, _P, _P, _P, _P]
     L.o64_dot.argtypes = [_I64, _P, _P]
     L.oracle_set_threads.argtypes = [_I]
+    for f in ("o64_apply9_tiles", "o32_apply9_tiles", "o16_apply9_tiles"):
+        getattr(L, f).argtypes = [_I, _I, _I, _I, _P, _P, _P]
+    for f in ("o2d64_bicgstab", "o2d16_bicgstab"):
+        getattr(L, f).argtypes = [_I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
+        getattr(L, f).restype = _I
     L.o64_dot.restype = _D
     L.o64_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
     L.o64_bicgstab.restype = _I
@@ -447,6 +452,41 @@ def apply9_32(c32, v32):
     u = np.empty_like(v32)
     lib().o32_apply9(nx, ny, _arr8(c32), _ptr(v32), _ptr(u))
     return u
+
+
+def apply9_tiles(c, v, tiles, prec="fp64"):
+    """The paper's tiled 2D SpMV (o2d.c): tiles = (TX, TY); prec fp64 / fp32 /
+    mixed (binary16 bit patterns)."""
+    TX, TY = tiles
+    dt = {"fp64": np.float64, "fp32": np.float32, "mixed": np.uint16}[prec]
+    c = [_c(a, dt) for a in c]
+    v = _c(v, dt)
+    ny, nx = v.shape
+    u = np.empty_like(v)
+    fn = {"fp64": lib().o64_apply9_tiles, "fp32": lib().o32_apply9_tiles, "mixed": lib().o16_apply9_tiles}[prec]
+    fn(nx, ny, int(TX), int(TY), _arr8(c), _ptr(v), _ptr(u))
+    return u
+
+
+def bicgstab2d(c, b, x0=None, tol=0.0, maxit=50, prec="fp64"):
+    """BiCGStab on the 2D 9-point operator: prec fp64 (float64 arrays) or mixed
+    (binary16 bit patterns, the GPU's operation order).  Returns dict(x, hist, iters, status,
+    event_it, alpha, omega) like bicgstab64."""
+    dt = np.float64 if prec == "fp64" else np.uint16
+    c = [_c(a, dt) for a in c]
+    b = _c(b, dt)
+    ny, nx = b.shape
+    x = np.empty_like(b)
+    hist = np.zeros(maxit + 1)
+    ad = np.float64 if prec == "fp64" else np.float32
+    al, om = np.zeros(maxit + 1, ad), np.zeros(maxit + 1, ad)
+    st, ev = ctypes.c_int(0), ctypes.c_int(0)
+    x0c = None if x0 is None else _c(x0, dt)
+    fn = lib().o2d64_bicgstab if prec == "fp64" else lib().o2d16_bicgstab
+    it = fn(nx, ny, _arr8(c), _ptr(b), None if x0c is None else _ptr(x0c), float(tol), int(maxit), _ptr(x),
+            _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
+    return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value, alpha=al[: it + 1],
+                omega=om[: it + 1])
 
 
 # ---------------- fp32 mirror ----------------

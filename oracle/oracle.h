@@ -173,6 +173,17 @@ void o64_jacobi_scale9(int nx, int ny, const double *diag, const double *const o
 void o64_apply9(int nx, int ny, const double *const c[8], const double *v, double *u);
 void o16_apply9(int nx, int ny, const uint16_t *const c[8], const uint16_t *v, uint16_t *u);  /* mirror */
 void o32_apply9(int nx, int ny, const float *const c[8], const float *v, float *u);           /* mirror */
+/* the paper's tiled form: TX x TY tiles, local products of
+ * each tile's columns into its grown region, then the output-halo rounds x
+ * then y (see o2d.c); fp64, and the GPU's fp32 / binary16 orders */
+void o64_apply9_tiles(int nx, int ny, int TX, int TY, const double *const c[8], const double *v, double *u);
+void o32_apply9_tiles(int nx, int ny, int TX, int TY, const float *const c[8], const float *v, float *u);
+void o16_apply9_tiles(int nx, int ny, int TX, int TY, const uint16_t *const c[8], const uint16_t *v, uint16_t *u);
+/* BiCGStab (Alg. 1) on the 2D operator, readings as in 3D */
+int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, const double *x0, double tol,
+                   int maxit, double *x, double *hist, double *alpha, double *omega, int *status, int *event_it);
+int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b, const uint16_t *x0, double tol,
+                   int maxit, uint16_t *x, double *hist, float *alpha, float *omega, int *status, int *event_it);
 
 /* informational */
 int oracle_num_threads(void);
