@@ -446,9 +446,51 @@ int stencil2d_create(int nx, int ny, const void *const coeffs[9], int coeff_dtyp
  * (fp32, or fp16 for STEN_MIXED; oracle/o2d.c mirrors it).  x, y: dense
  * (ny, nx), host or device, must not overlap.  Synchronises cuda_stream. */
 int stencil2d_apply(sten_stencil2d *st, int precision, const void *x, void *y, void *cuda_stream);
-/* device time (ms) of the last apply's kernel (CUDA events around it) */
+/* device time (ms) of the last apply's kernels (CUDA events around them), or
+ * of the last bicgstab2d_solve from S1 to its last iteration (b already in) */
 int stencil2d_last_ms(sten_stencil2d *st, double *ms);
 void stencil2d_destroy(sten_stencil2d *st);
+
+/* The paper's tiled form of the 2D SpMV ("we map a
+ * rectangular region of the mesh of v to each core, and store all elements of
+ * the corresponding columns of A.  After multiplication of the local v with
+ * the local A we have generated products in an output halo that must be sent
+ * to neighboring tiles ... We complete a round of send and add in one
+ * direction, then a round for the other direction").  DESIGN.md R24 fixes
+ * what the paper leaves open: tile (a, b) of a tiles_x x tiles_y grid owns
+ * columns [floor(a nx / tiles_x), floor((a+1) nx / tiles_x)) and rows likewise;
+ * each tile forms, from ITS OWN v only, v_P + the products of its in-tile
+ * neighbours at its points and the products landing one point outside it (its
+ * output-halo ring); the x round adds the left, then the right neighbour's
+ * halo column into a tile's edge columns over its grown rows (corners ride
+ * along), then the y round adds the lower, then the upper neighbour's halo
+ * row.  The tiles are loopback partitions of one device (each reads only its
+ * own v and writes only its own u and ring; the rounds read the neighbours'
+ * rings, the data a multi-device layout would send).  Results are bitwise
+ * those of oracle/o2d.c o32/o16_apply9_tiles.  After this call
+ * stencil2d_apply uses the tiled form; 1 x 1 restores the gather.
+ * Errors: STEN_EINVAL (tiles_x not in 1..nx, tiles_y not in 1..ny),
+ * STEN_ENOMEM.  Synchronises the device. */
+int stencil2d_set_tiles(sten_stencil2d *st, int tiles_x, int tiles_y);
+
+/* BiCGStab on the 2D operator (each core holds "a matrix, halo,
+ * and vector (as well as all terms needed for BiCG)"; Alg. 1, PAPER.md:172-186,
+ * with the 9-point operator, R25).  Arguments, precisions, status,
+ * tol / maxit conventions and errors as bicgstab_solve; b, x0 (NULL: 0),
+ * x_out: dense (ny, nx) vectors of the precision's type, host or device;
+ * res_hist: host, maxit+1 doubles.  With a diagonal given at create, b_hat =
+ * b / A_P (R3) and the residuals refer to the scaled system.  Schedule: H1 =
+ * p' = r + beta (p - omega v), v' = A p', (rhat, v'); H2 = s = r - alpha v',
+ * t = A s, (t, s), (t, t); H3 = x, r updates, (rhat, r), (r, r) - fused
+ * kernels, 33 passes per iteration.  Tiles must be 1 x 1
+ * (STEN_EUNSUPPORTED otherwise).  Synchronises cuda_stream. */
+int bicgstab2d_solve(sten_stencil2d *st, int precision, const void *b, const void *x0, double tol, int maxit,
+                     void *x_out, int *iters, double *res_hist, int *status, void *cuda_stream);
+/* per-phase device timing of the 2D solve (CUDA events around H1, H2, H3 of
+ * every iteration; off by default): mean ms of each phase over the
+ * `iterations` iterations of the last timed solve */
+int stencil2d_set_timing(sten_stencil2d *st, int enable);
+int stencil2d_phase_ms(sten_stencil2d *st, double ms[3], long long *iterations);
 
 #ifdef __cplusplus
 }

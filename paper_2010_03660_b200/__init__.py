@@ -76,6 +76,10 @@ def lib():
         L.stencil2d_apply.argtypes = [P, I, P, P, P]
         L.stencil2d_last_ms.argtypes = [P, ctypes.POINTER(D)]
         L.stencil2d_destroy.argtypes = [P]
+        L.stencil2d_set_tiles.argtypes = [P, I, I]
+        L.stencil2d_set_timing.argtypes = [P, I]
+        L.stencil2d_phase_ms.argtypes = [P, P, ctypes.POINTER(ctypes.c_longlong)]
+        L.bicgstab2d_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
         L.stencil_apply.argtypes = [P, I, P, P, P]
         L.bicgstab_solve.argtypes = [P, I, P, P, D, I, P, ctypes.POINTER(I), P, ctypes.POINTER(I), P]
         L.bicgstab_solve_batch.argtypes = [P, I, I, P, P, D, I, P, P, P, P]
@@ -491,6 +495,42 @@ def stencil2d_apply(st: Stencil2D, precision: int, x, y, stream=None):
     ms = ctypes.c_double(0.0)
     _check(lib().stencil2d_last_ms(st.handle, ctypes.byref(ms)))
     return ms.value
+
+
+def stencil2d_set_tiles(st: Stencil2D, tiles_x: int, tiles_y: int):
+    """The paper's tiled output-halo SpMV (R24) for stencil2d_apply; (1, 1) = gather."""
+    _check(lib().stencil2d_set_tiles(st.handle, int(tiles_x), int(tiles_y)))
+
+
+def stencil2d_set_timing(st: Stencil2D, enable: bool):
+    _check(lib().stencil2d_set_timing(st.handle, 1 if enable else 0))
+
+
+def stencil2d_phase_ms(st: Stencil2D):
+    """(mean ms of H1, H2, H3 over the last timed 2D solve, iterations timed)"""
+    ms = np.zeros(3, np.float64)
+    n = ctypes.c_longlong(0)
+    _check(lib().stencil2d_phase_ms(st.handle, ms.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n)))
+    return ms, n.value
+
+
+def bicgstab2d_solve(st: Stencil2D, precision: int, b, x0, tol: float, maxit: int, x_out, stream=None):
+    """BiCGStab on the 2D 9-point operator (R25).  Returns (iters, res_hist, status)."""
+    n = st.nx * st.ny
+    _check_vec(b, precision, n, "b")
+    _check_vec(x_out, precision, n, "x_out")
+    if x0 is not None:
+        _check_vec(x0, precision, n, "x0")
+    hist = np.zeros(max(maxit, 0) + 1, dtype=np.float64)
+    it = ctypes.c_int(0)
+    status = ctypes.c_int(-1)
+    _check(lib().bicgstab2d_solve(st.handle, precision, _ptr(b), _ptr(x0), float(tol), int(maxit), _ptr(x_out),
+                                  ctypes.byref(it), hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(status),
+                                  _stream(stream)))
+    ms = ctypes.c_double(0.0)
+    _check(lib().stencil2d_last_ms(st.handle, ctypes.byref(ms)))
+    st.last_solve_ms = ms.value
+    return it.value, hist[: it.value + 1].copy(), status.value
 
 
 def p2p_export(st: Stencil, precision: int) -> bytes:

@@ -2422,17 +2422,46 @@ int sten_sr_sweep(sten_stencil *st, int prec, double alpha, double omega, double
 }  // extern "C"
 
 // ====================================================== 2D 9-point SpMV ==
-// NEXT-3 of SURVEY §8(f): the paper's second kernel.
+// NEXT-3 of SURVEY §8(f): the paper's second kernel, its
+// tiled output-halo form (R24) and BiCGStab around it (R25).
+struct Bufs2 {
+  bool ready = false;
+  void *x = nullptr, *r = nullptr, *rh = nullptr, *p[2] = {}, *v[2] = {}, *s = nullptr, *t = nullptr, *bw = nullptr;
+  CUtensorMap m_x, m_r, m_p[2], m_v[2];
+};
 struct sten_stencil2d {
   int nx = 0, ny = 0, pitch = 0;
+  int sm = 148;
+  bool has_diag = false;
   float *c32[8] = {};
   __half *c16[8] = {};
-  void *v[2] = {}, *u[2] = {};     // per precision: pitched input / output
+  double *aP = nullptr;            // a_P per point (padding 1) when a diagonal was given (R3)
+  void *v[2] = {}, *u[2] = {};     // stencil2d_apply, per precision: pitched input / output
   bool maps_ok[2] = {false, false};
   CUtensorMap m_v[2];
+  // tiled (output-halo) SpMV, R24
+  int TX = 1, TY = 1, HS = 0, WS = 0;
+  unsigned char *xm = nullptr, *ym = nullptr;
+  void *ring = nullptr;
+  // bicgstab2d_solve
+  Bufs2 sb[2];
+  DevState *st = nullptr, *st_host = nullptr;
+  float *partials = nullptr;
+  int partials_cap = 0;
+  unsigned *counter = nullptr;
+  double *hist = nullptr;
+  float *ahist = nullptr, *whist = nullptr;
+  int hist_cap = 0;
+  cudaStream_t cap = nullptr;
+  std::map<GraphKey, GraphRec> graphs;
+  bool timing = false;
+  double ph_ms[3] = {0, 0, 0};
+  long long ph_n = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   double last_ms = 0.0;
 };
+
+static int bx2d(int prec) { return prec == STEN_FP32 ? 64 : 128; }
 
 static int create2d_impl(int nx, int ny, const void *const coeffs[9], int dtype, cudaStream_t s,
                          sten_stencil2d **out) {
@@ -2444,7 +2473,9 @@ static int create2d_impl(int nx, int ny, const void *const coeffs[9], int dtype,
   sten_stencil2d *st = new sten_stencil2d;
   st->nx = nx;
   st->ny = ny;
-  st->pitch = (nx + 7) / 8 * 8;  // 16-B rows (TMA row strides are 16-B multiples)
+  st->pitch = (nx + 63) / 64 * 64;  // 128-B rows (fp16), like the 3D layout
+  st->has_diag = coeffs[0] != nullptr;
+  st->sm = device_sm_count();
   auto fail = [&](int rc) {
     stencil2d_destroy(st);
     return rc;
@@ -2474,8 +2505,10 @@ static int create2d_impl(int nx, int ny, const void *const coeffs[9], int dtype,
     co.c32[d] = st->c32[d];
     co.c16[d] = st->c16[d];
   }
+  if (rc == STEN_OK && st->has_diag && cudaMalloc(&st->aP, cells * 8) != cudaSuccess)
+    rc = set_err(STEN_ENOMEM, "2D a_P allocation failed");
   if (rc == STEN_OK) {
-    int e = create9_launch(dtype, dev[0], in, nx, ny, st->pitch, co, s);
+    int e = create9_launch(dtype, dev[0], in, nx, ny, st->pitch, co, st->aP, s);
     if (e) rc = set_err(STEN_ECUDA, "2D coefficient kernel: %s", cudaGetErrorString((cudaError_t)e));
   }
   if (rc == STEN_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = set_err(STEN_ECUDA, "stencil2d_create sync failed");
@@ -2484,6 +2517,222 @@ static int create2d_impl(int nx, int ny, const void *const coeffs[9], int dtype,
   if (cudaEventCreate(&st->e0) != cudaSuccess || cudaEventCreate(&st->e1) != cudaSuccess)
     return fail(set_err(STEN_ECUDA, "event creation failed"));
   *out = st;
+  return STEN_OK;
+}
+
+static void drop_graphs2d(sten_stencil2d *st) {
+  for (auto &kv : st->graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    for (auto e : kv.second.ev) cudaEventDestroy(e);
+  }
+  st->graphs.clear();
+}
+
+// one (nx, ny) map over a pitched plane, box (BX + 2H) x (BY + 2)
+static int map2d(const sten_stencil2d *st, CUtensorMap *m, void *base, int prec) {
+  const int e = esize(prec), H = 16 / e;
+  return make_map_p(m, base, e, st->nx, st->ny, 1, st->pitch, (long long)st->pitch * st->ny, 3, bx2d(prec) + 2 * H,
+                    kBicg9BY + 2);
+}
+
+// The apply path's SpMV: gather (1 x 1 tiles) or the tiled output-halo form.
+static int launch_apply2d(sten_stencil2d *st, int prec, const CUtensorMap &mv, const void *v, void *u,
+                          cudaStream_t s) {
+  Apply9Args a;
+  memset(&a, 0, sizeof a);
+  a.tm_v = mv;
+  for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
+  a.u = u;
+  a.nx = st->nx;
+  a.ny = st->ny;
+  a.pitch = st->pitch;
+  a.tiles_x = (st->nx + bx2d(prec) - 1) / bx2d(prec);
+  const bool tiled = st->TX * st->TY > 1;
+  if (tiled) {
+    a.xm = st->xm;
+    a.ym = st->ym;
+  }
+  if (prec == STEN_FP32) KLAUNCH(apply9_launch<float>(a, s));
+  else KLAUNCH(apply9_launch<__half>(a, s));
+  if (!tiled) return STEN_OK;
+  Ring9Args r;
+  memset(&r, 0, sizeof r);
+  for (int d = 0; d < 8; ++d) r.c[d] = a.c[d];
+  r.v = v;
+  r.u = u;
+  r.ring = st->ring;
+  r.nx = st->nx;
+  r.ny = st->ny;
+  r.pitch = st->pitch;
+  r.TX = st->TX;
+  r.TY = st->TY;
+  r.HS = st->HS;
+  r.WS = st->WS;
+  if (prec == STEN_FP32) KLAUNCH(ring9_launch<float>(r, s));
+  else KLAUNCH(ring9_launch<__half>(r, s));
+  for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 ? st->TX : st->TY) == 1) continue;
+    if (prec == STEN_FP32) KLAUNCH(round9_launch<float>(r, dir, s));
+    else KLAUNCH(round9_launch<__half>(r, dir, s));
+  }
+  return STEN_OK;
+}
+
+// ----------------------------------------------------- 2D solve plumbing --
+static int ensure2d(sten_stencil2d *st, int prec) {
+  Bufs2 &b = st->sb[prec];
+  const size_t bytes = (size_t)st->pitch * st->ny * esize(prec);
+  if (!b.ready) {
+    void **all[] = {&b.x, &b.r, &b.rh, &b.p[0], &b.p[1], &b.v[0], &b.v[1], &b.s, &b.t, &b.bw};
+    for (void **pp : all) {
+      if (!*pp) {
+        cudaError_t e = cudaMalloc(pp, bytes);
+        if (e != cudaSuccess) return set_err(STEN_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      }
+      CUDA_TRY(cudaMemset(*pp, 0, bytes));  // row padding stays zero (the element-wise kernels stream it)
+    }
+    RC_TRY(map2d(st, &b.m_x, b.x, prec));
+    RC_TRY(map2d(st, &b.m_r, b.r, prec));
+    for (int k = 0; k < 2; ++k) {
+      RC_TRY(map2d(st, &b.m_p[k], b.p[k], prec));
+      RC_TRY(map2d(st, &b.m_v[k], b.v[k], prec));
+    }
+    b.ready = true;
+  }
+  if (!st->st) {
+    CUDA_TRY(cudaMalloc(&st->st, sizeof(DevState)));
+    CUDA_TRY(cudaMallocHost(&st->st_host, sizeof(DevState)));
+    CUDA_TRY(cudaMalloc(&st->counter, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemset(st->counter, 0, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&st->cap, cudaStreamNonBlocking));
+  }
+  const int tiles = ((st->nx + bx2d(STEN_FP32) - 1) / bx2d(STEN_FP32)) * ((st->ny + kBicg9BY - 1) / kBicg9BY);
+  int need = tiles > st->sm * 64 ? tiles : st->sm * 64;  // the stencil grid and the element-wise grid
+  if (need > st->partials_cap) {
+    cudaFree(st->partials);
+    st->partials = nullptr;
+    CUDA_TRY(cudaMalloc(&st->partials, (size_t)need * kMaxDots * sizeof(float)));
+    st->partials_cap = need;
+    drop_graphs2d(st);
+  }
+  return STEN_OK;
+}
+
+static Reduce red2d(sten_stencil2d *st) {
+  Reduce r;
+  memset(&r, 0, sizeof r);
+  r.partials = st->partials;
+  r.counter = st->counter;
+  r.st = st->st;
+  return r;
+}
+
+static int ew_grid2d(const sten_stencil2d *st, long long nvec) {
+  long long need = (nvec + 511) / 512, g = (long long)st->sm * 64;
+  if (need < g) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
+static int ew2d(sten_stencil2d *st, int prec, EwArgs &a) {
+  a.rows = st->ny;
+  a.vpr = (st->nx + (prec == STEN_FP32 ? 4 : 8) - 1) / (prec == STEN_FP32 ? 4 : 8);
+  a.pitch = st->pitch;
+  a.nvec = (long long)st->pitch * st->ny / (prec == STEN_FP32 ? 4 : 8);
+  a.red = red2d(st);
+  return ew_grid2d(st, a.nvec);
+}
+
+// one iteration of Alg. 1: H1, H2 (k_bicg9), H3 (k_h3); p / v ping-pong on `parity`
+static int enqueue_iter2d(sten_stencil2d *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
+  Bufs2 &b = st->sb[prec];
+  const int cur = parity, nxt = parity ^ 1;
+  Bicg9Args a;
+  memset(&a, 0, sizeof a);
+  for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
+  a.nx = st->nx;
+  a.ny = st->ny;
+  a.pitch = st->pitch;
+  a.tiles_x = (st->nx + bx2d(prec) - 1) / bx2d(prec);
+  a.red = red2d(st);
+  // H1
+  a.tm_in[0] = b.m_r;
+  a.tm_in[1] = b.m_p[cur];
+  a.tm_in[2] = b.m_v[cur];
+  a.rh = b.rh;
+  a.out0 = b.v[nxt];
+  a.out1 = b.p[nxt];
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
+  if (prec == STEN_FP32) KLAUNCH(bicg9_launch<float>(MODE_H1, a, s));
+  else KLAUNCH(bicg9_launch<__half>(MODE_H1, a, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
+  // H2
+  a.tm_in[0] = b.m_r;
+  a.tm_in[1] = b.m_v[nxt];
+  a.rh = nullptr;
+  a.out0 = b.t;
+  a.out1 = b.s;
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
+  if (prec == STEN_FP32) KLAUNCH(bicg9_launch<float>(MODE_H2, a, s));
+  else KLAUNCH(bicg9_launch<__half>(MODE_H2, a, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
+  // H3
+  EwArgs e;
+  memset(&e, 0, sizeof e);
+  e.x = b.x;
+  e.p = b.p[nxt];
+  e.s = b.s;
+  e.t = b.t;
+  e.rhat = b.rh;
+  e.xo = b.x;
+  e.ro = b.r;
+  const int g = ew2d(st, prec, e);
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[4], s, cudaEventRecordExternal));
+  if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(e, g, 256, s));
+  else KLAUNCH(h3_launch<__half>(e, g, 256, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[5], s, cudaEventRecordExternal));
+  return STEN_OK;
+}
+
+static int graph2d(sten_stencil2d *st, int prec, int chunk, GraphRec **out) {
+  GraphKey key{prec, chunk, st->timing ? 1 : 0, 0};
+  auto it = st->graphs.find(key);
+  if (it != st->graphs.end()) {
+    *out = &it->second;
+    return STEN_OK;
+  }
+  GraphRec rec;
+  if (st->timing) {
+    rec.ev.resize((size_t)chunk * 6);
+    for (auto &e : rec.ev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  CUDA_TRY(cudaStreamBeginCapture(st->cap, cudaStreamCaptureModeThreadLocal));
+  int rc = STEN_OK;
+  for (int j = 0; j < chunk && rc == STEN_OK; ++j)
+    rc = enqueue_iter2d(st, prec, j & 1, st->cap, st->timing ? &rec.ev[(size_t)j * 6] : nullptr);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(st->cap, &g);
+  if (rc != STEN_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) return set_err(STEN_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&rec.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return set_err(STEN_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+  rec.kernels = 3LL * chunk;
+  auto ins = st->graphs.emplace(key, rec);
+  *out = &ins.first->second;
+  return STEN_OK;
+}
+
+static int copy2d_in(sten_stencil2d *st, int prec, void *dst, const void *src, cudaStream_t s) {
+  const size_t e = esize(prec);
+  CUDA_TRY(cudaMemcpy2DAsync(dst, st->pitch * e, src, st->nx * e, st->nx * e, st->ny, cudaMemcpyDefault, s));
+  return STEN_OK;
+}
+static int copy2d_out(sten_stencil2d *st, int prec, void *dst, const void *src, cudaStream_t s) {
+  const size_t e = esize(prec);
+  CUDA_TRY(cudaMemcpy2DAsync(dst, st->nx * e, src, st->pitch * e, st->nx * e, st->ny, cudaMemcpyDefault, s));
   return STEN_OK;
 }
 
@@ -2496,17 +2745,70 @@ int stencil2d_create(int nx, int ny, const void *const coeffs[9], int coeff_dtyp
 
 void stencil2d_destroy(sten_stencil2d *st) {
   if (!st) return;
+  if (st->st) cudaDeviceSynchronize();  // graphs / kernels of this handle may still run
+  drop_graphs2d(st);
   for (int d = 0; d < 8; ++d) {
     cudaFree(st->c32[d]);
     cudaFree(st->c16[d]);
   }
+  cudaFree(st->aP);
   for (int p = 0; p < 2; ++p) {
     cudaFree(st->v[p]);
     cudaFree(st->u[p]);
+    Bufs2 &b = st->sb[p];
+    for (void *q : {b.x, b.r, b.rh, b.p[0], b.p[1], b.v[0], b.v[1], b.s, b.t, b.bw}) cudaFree(q);
   }
+  cudaFree(st->xm);
+  cudaFree(st->ym);
+  cudaFree(st->ring);
+  cudaFree(st->st);
+  if (st->st_host) cudaFreeHost(st->st_host);
+  cudaFree(st->partials);
+  cudaFree(st->counter);
+  cudaFree(st->hist);
+  cudaFree(st->ahist);
+  cudaFree(st->whist);
+  if (st->cap) cudaStreamDestroy(st->cap);
   if (st->e0) cudaEventDestroy(st->e0);
   if (st->e1) cudaEventDestroy(st->e1);
   delete st;
+}
+
+int stencil2d_set_tiles(sten_stencil2d *st, int tiles_x, int tiles_y) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  if (tiles_x < 1 || tiles_y < 1 || tiles_x > st->nx || tiles_y > st->ny)
+    return set_err(STEN_EINVAL, "tiles %d x %d: need 1 <= tiles_x <= nx = %d, 1 <= tiles_y <= ny = %d", tiles_x, tiles_y,
+                   st->nx, st->ny);
+  CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(st->xm);
+  cudaFree(st->ym);
+  cudaFree(st->ring);
+  st->xm = st->ym = nullptr;
+  st->ring = nullptr;
+  st->TX = st->TY = 1;
+  if (tiles_x * (long long)tiles_y == 1) return STEN_OK;
+  // per column / row: is the -1 (bit 0) / +1 (bit 1) neighbour in the same tile (R24)
+  auto flags = [](int n, int t, int len) {
+    std::vector<unsigned char> f((size_t)len, 0);
+    for (int a = 0; a < t; ++a) {
+      const int lo = (int)((long long)a * n / t), hi = (int)((long long)(a + 1) * n / t);
+      for (int x = lo; x < hi; ++x) f[x] = (unsigned char)((x - 1 >= lo ? 1 : 0) | (x + 1 < hi ? 2 : 0));
+    }
+    return f;
+  };
+  const std::vector<unsigned char> fx = flags(st->nx, tiles_x, st->pitch), fy = flags(st->ny, tiles_y, st->ny);
+  const int HS = (st->ny + tiles_y - 1) / tiles_y + 2, WS = (st->nx + tiles_x - 1) / tiles_x;
+  const size_t ring_elems = (size_t)tiles_x * tiles_y * (2 * (size_t)HS + 2 * (size_t)WS);
+  if (cudaMalloc(&st->xm, fx.size()) != cudaSuccess || cudaMalloc(&st->ym, fy.size()) != cudaSuccess ||
+      cudaMalloc(&st->ring, ring_elems * 4) != cudaSuccess)
+    return set_err(STEN_ENOMEM, "tile masks / output-halo ring (%zu elements)", ring_elems);
+  CUDA_TRY(cudaMemcpy(st->xm, fx.data(), fx.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(st->ym, fy.data(), fy.size(), cudaMemcpyHostToDevice));
+  st->TX = tiles_x;
+  st->TY = tiles_y;
+  st->HS = HS;
+  st->WS = WS;
+  return STEN_OK;
 }
 
 int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *cuda_stream) {
@@ -2521,28 +2823,14 @@ int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *
     CUDA_TRY(cudaMemset(st->v[prec], 0, bytes));  // padding columns stay zero
   }
   if (!st->maps_ok[prec]) {
-    const int bx = prec == STEN_FP32 ? 64 : 128, H = 16 / e;
-    RC_TRY(make_map_p(&st->m_v[prec], st->v[prec], e, st->nx, st->ny, 1, st->pitch, (long long)st->pitch * st->ny, 3, bx + 2 * H, 32 + 2));
+    RC_TRY(map2d(st, &st->m_v[prec], st->v[prec], prec));
     st->maps_ok[prec] = true;
   }
-  CUDA_TRY(cudaMemcpy2DAsync(st->v[prec], (size_t)st->pitch * e, x, (size_t)st->nx * e, (size_t)st->nx * e, st->ny,
-                             cudaMemcpyDefault, s));
-  Apply9Args a;
-  memset(&a, 0, sizeof a);
-  a.tm_v = st->m_v[prec];
-  for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
-  a.u = st->u[prec];
-  a.nx = st->nx;
-  a.ny = st->ny;
-  a.pitch = st->pitch;
-  const int bx = prec == STEN_FP32 ? 64 : 128;
-  a.tiles_x = (st->nx + bx - 1) / bx;
+  RC_TRY(copy2d_in(st, prec, st->v[prec], x, s));
   CUDA_TRY(cudaEventRecord(st->e0, s));
-  if (prec == STEN_FP32) KLAUNCH(apply9_launch<float>(a, s));
-  else KLAUNCH(apply9_launch<__half>(a, s));
+  RC_TRY(launch_apply2d(st, prec, st->m_v[prec], st->v[prec], st->u[prec], s));
   CUDA_TRY(cudaEventRecord(st->e1, s));
-  CUDA_TRY(cudaMemcpy2DAsync(y, (size_t)st->nx * e, st->u[prec], (size_t)st->pitch * e, (size_t)st->nx * e, st->ny,
-                             cudaMemcpyDefault, s));
+  RC_TRY(copy2d_out(st, prec, y, st->u[prec], s));
   CUDA_TRY(cudaStreamSynchronize(s));
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, st->e0, st->e1));
@@ -2553,6 +2841,135 @@ int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *
 int stencil2d_last_ms(sten_stencil2d *st, double *ms) {
   if (!st || !ms) return set_err(STEN_EINVAL, "NULL argument");
   *ms = st->last_ms;
+  return STEN_OK;
+}
+
+int stencil2d_set_timing(sten_stencil2d *st, int enable) {
+  if (!st) return set_err(STEN_EINVAL, "NULL handle");
+  st->timing = enable != 0;
+  return STEN_OK;
+}
+
+int stencil2d_phase_ms(sten_stencil2d *st, double ms[3], long long *iterations) {
+  if (!st || !ms || !iterations) return set_err(STEN_EINVAL, "NULL argument");
+  for (int p = 0; p < 3; ++p) ms[p] = st->ph_n ? st->ph_ms[p] / (double)st->ph_n : 0.0;
+  *iterations = st->ph_n;
+  return STEN_OK;
+}
+
+int bicgstab2d_solve(sten_stencil2d *st, int prec, const void *b, const void *x0, double tol, int maxit, void *x_out,
+                     int *iters, double *res_hist, int *status, void *cuda_stream) {
+  if (!st || !b || !x_out || !iters || !res_hist || !status) return set_err(STEN_EINVAL, "NULL argument");
+  if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
+  if (!(tol >= 0.0) || !std::isfinite(tol) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
+  if (st->TX * st->TY > 1)
+    return set_err(STEN_EUNSUPPORTED, "bicgstab2d_solve runs the fused gather kernels: set 1 x 1 tiles "
+                                      "(the tiled output-halo SpMV is stencil2d_apply's)");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  RC_TRY(ensure2d(st, prec));
+  Bufs2 &bf = st->sb[prec];
+  if (maxit + 2 > st->hist_cap) {
+    cudaFree(st->hist);
+    cudaFree(st->ahist);
+    cudaFree(st->whist);
+    st->hist = nullptr;
+    st->ahist = st->whist = nullptr;
+    st->hist_cap = maxit + 2 < 64 ? 64 : maxit + 2;
+    CUDA_TRY(cudaMalloc(&st->hist, sizeof(double) * st->hist_cap));
+    CUDA_TRY(cudaMalloc(&st->ahist, sizeof(float) * st->hist_cap));
+    CUDA_TRY(cudaMalloc(&st->whist, sizeof(float) * st->hist_cap));
+  }
+  DevState h;
+  memset(&h, 0, sizeof h);
+  h.tol = tol;
+  h.maxit = maxit;
+  h.status = -1;
+  h.ev = -1;
+  h.half = prec == STEN_MIXED;
+  h.hist = st->hist;
+  h.ahist = st->ahist;
+  h.whist = st->whist;
+  *st->st_host = h;
+  CUDA_TRY(cudaMemcpyAsync(st->st, st->st_host, sizeof h, cudaMemcpyHostToDevice, s));
+  RC_TRY(copy2d_in(st, prec, bf.bw, b, s));
+  CUDA_TRY(cudaEventRecord(st->e0, s));
+  // S1 (Alg. 1 l.174, R1, R3): r0 = b_hat - A x0, rhat = p0 = r0, v0 = 0
+  if (x0) {
+    RC_TRY(copy2d_in(st, prec, bf.x, x0, s));
+    {  // A x0 by the gather SpMV into t
+      Apply9Args a;
+      memset(&a, 0, sizeof a);
+      a.tm_v = bf.m_x;
+      for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
+      a.u = bf.t;
+      a.nx = st->nx;
+      a.ny = st->ny;
+      a.pitch = st->pitch;
+      a.tiles_x = (st->nx + bx2d(prec) - 1) / bx2d(prec);
+      if (prec == STEN_FP32) KLAUNCH(apply9_launch<float>(a, s));
+      else KLAUNCH(apply9_launch<__half>(a, s));
+    }
+  } else {
+    CUDA_TRY(cudaMemsetAsync(bf.x, 0, (size_t)st->pitch * st->ny * esize(prec), s));
+  }
+  EwArgs e;
+  memset(&e, 0, sizeof e);
+  e.bw = bf.bw;
+  e.aP = st->aP;
+  e.ax = x0 ? bf.t : nullptr;
+  e.r = bf.r;
+  e.rh = bf.rh;
+  e.p0 = bf.p[0];
+  e.v0 = bf.v[0];
+  const int g = ew2d(st, prec, e);
+  if (g > st->partials_cap) return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
+  if (prec == STEN_FP32) KLAUNCH(init_launch<float>(e, g, 256, s));
+  else KLAUNCH(init_launch<__half>(e, g, 256, s));
+  // iterations: graphs of `chunk` iterations (even: the p / v parity repeats)
+  if (maxit > 0) {
+    int chunk = tol > 0.0 ? 8 : ((maxit + 1) / 2) * 2;
+    if (chunk > 2048) chunk = 2048;
+    GraphRec *gr = nullptr;
+    RC_TRY(graph2d(st, prec, chunk, &gr));
+    if (st->timing) {
+      st->ph_ms[0] = st->ph_ms[1] = st->ph_ms[2] = 0.0;
+      st->ph_n = 0;
+    }
+    const int nrep = (maxit + chunk - 1) / chunk;
+    for (int rep = 0; rep < nrep; ++rep) {
+      CUDA_TRY(cudaGraphLaunch(gr->exec, s));
+      if (tol > 0.0 || st->timing) {
+        CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (st->timing) {
+          const int done = st->st_host->it;
+          for (int j = 0; j < chunk && rep * chunk + j < done; ++j) {
+            for (int p = 0; p < 3; ++p) {
+              float ms = 0.f;
+              CUDA_TRY(cudaEventElapsedTime(&ms, gr->ev[(size_t)j * 6 + 2 * p], gr->ev[(size_t)j * 6 + 2 * p + 1]));
+              st->ph_ms[p] += ms;
+            }
+            st->ph_n += 1;
+          }
+        }
+        if (st->st_host->stop || st->st_host->it >= maxit) break;
+      }
+    }
+  }
+  CUDA_TRY(cudaEventRecord(st->e1, s));
+  CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const DevState fin = *st->st_host;
+  if (fin.zero_x) CUDA_TRY(cudaMemsetAsync(bf.x, 0, (size_t)st->pitch * st->ny * esize(prec), s));
+  RC_TRY(copy2d_out(st, prec, x_out, bf.x, s));
+  CUDA_TRY(cudaMemcpyAsync(res_hist, st->hist, sizeof(double) * (fin.it + 1), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  *iters = fin.it;
+  *status = fin.stop ? fin.status : (fin.ev >= 0 ? fin.ev : STEN_MAXIT);
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, st->e0, st->e1));
+  st->last_ms = ms;
   return STEN_OK;
 }
 

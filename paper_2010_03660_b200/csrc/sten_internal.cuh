@@ -601,18 +601,41 @@ int sr_launch(const SrArgs &a, int by, int stages, int cstages, int pack, bool c
 template <typename T> size_t sr_smem_bytes(int by, int stages, int cstages, int pack);
 template <typename T> int sr_threads(int by, int pack);
 
-// sten2d.cu: the 2D 9-point SpMV (NEXT-3)
+// sten2d.cu: the 2D 9-point SpMV and BiCGStab (NEXT-3)
 struct alignas(64) Apply9Args {
   CUtensorMap tm_v;       // v: box (BX + 2H) x (BY + 2), one plane
   const void *c[8];       // scaled couplings, rows of `pitch`
   void *u;
+  const unsigned char *xm, *ym;  // tiled product (R24): per column / row, bit 0 = the -1 neighbour
+                                 // is in the same tile, bit 1 = the +1 neighbour (null: gather)
   int nx, ny, pitch, tiles_x;
+};
+// the tiled SpMV's output-halo ring and its two rounds (TX x TY tiles)
+struct Ring9Args {
+  const void *c[8];
+  const void *v;          // ring: the input
+  void *u;                // rounds: the output being completed
+  void *ring;             // L[NT][HS] R[NT][HS] B[NT][WS] T[NT][WS]
+  int nx, ny, pitch, TX, TY, HS, WS;
+};
+// the fused 2D BiCGStab phases H1 (inputs r, p, v) and H2 (inputs r, v')
+constexpr int kBicg9BY = 32;
+struct alignas(64) Bicg9Args {
+  CUtensorMap tm_in[3];   // box (BX + 2H) x (BY + 2)
+  const void *c[8];
+  const void *rh;         // H1: rhat
+  void *out0, *out1;      // H1: v', p'   H2: t, s
+  int nx, ny, pitch, tiles_x;
+  Reduce red;
 };
 struct Coef9In { const void *off[8]; };
 struct Coef9Out { float *c32[8]; __half *c16[8]; };
 template <typename T> int apply9_launch(const Apply9Args &a, cudaStream_t s);
+template <typename T> int ring9_launch(const Ring9Args &a, cudaStream_t s);
+template <typename T> int round9_launch(const Ring9Args &a, int dir, cudaStream_t s);
+template <typename T> int bicg9_launch(int mode, const Bicg9Args &a, cudaStream_t s);
 int create9_launch(int in_dtype, const void *diag, const Coef9In &in, int nx, int ny, int pitch, const Coef9Out &out,
-                   cudaStream_t s);
+                   double *aP, cudaStream_t s);
 
 int create_coeffs_launch(int in_dtype, const void *diag, const void *const off[6], Geom g,
                          int has_below, int has_above, float *const c32[6], __half *const c16[6],

