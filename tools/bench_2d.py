@@ -11,7 +11,7 @@ against the HBM roofline, on the seeded 2D stand-in (inputs.fields2d_device, DES
 
 Kernel / phase times by CUDA events on the launching stream, median of repeats after warm-up;
 every array is > L2 (1.04 GB per fp16 vector), so no flush is needed.  Writes
-profiles/<tag>_2d.md and profiles/<tag>_2d.json."""
+gpurun_out/<tag>_2d.md and .json (copied to profiles/)."""
 import json
 import os
 import statistics
@@ -113,9 +113,11 @@ def main(tag="r2", n=22800, maxit=100):
                  "the SpMV input formed once per box element in shared memory) and the 3D k_h3.")
     out = "\n".join(lines) + "\n"
     print(out)
-    with open(os.path.join(ROOT, "profiles", f"{tag}_2d.md"), "w") as f:
+    outdir = os.path.join(ROOT, "gpurun_out")  # brought back by gpurun; copied into profiles/ by hand
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, f"{tag}_2d.md"), "w") as f:
         f.write(out)
-    with open(os.path.join(ROOT, "profiles", f"{tag}_2d.json"), "w") as f:
+    with open(os.path.join(outdir, f"{tag}_2d.json"), "w") as f:
         json.dump(rec, f, indent=1)
 
 
