@@ -1,8 +1,9 @@
 // kernels.cu - sm_100a kernels of the BiCGStab hot path.
 //
 //  (the fused stencil kernels k_stencil<T, MODE, BY, S> are in stencil.cu)
-//  k_h3<T>: x += alpha p + omega s (l.181), r = s - omega t (l.182),
-//           (rhat, r), (r, r) (l.183 and the stopping rule R4)
+//  k_h3<T>, k_h3_bulk<T>: x += alpha p + omega s (l.181), r = s - omega t (l.182),
+//           (rhat, r), (r, r) (l.183 and the stopping rule R4); the product runs
+//           k_h3_bulk (the five input streams through a cp.async.bulk ring)
 //  k_init<T>: b_hat = b / a_P (R3), r0 = b_hat - A x0 (R1), rhat = p = r0, v = 0
 //  k_create_coeffs: Jacobi scaling c_d = A_d / a_P in fp64, rounded to fp32 and
 //    fp16 (R3, R5).
@@ -56,8 +57,13 @@ __global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
     for (int u = 0; u < 4; ++u) {
       const long long o = vofs<VEC>(v + u * stride, a);
       P xn = P::fmas(ws, ss[u], P::fmas(as, ps[u], xs[u])), rn = P::fmas(mws, ts[u], ss[u]);
+#if STEN_H3_VARIANT == 1
+      __stcs(reinterpret_cast<uint4 *>(XO + o), *reinterpret_cast<const uint4 *>(&xn));
+      __stcs(reinterpret_cast<uint4 *>(RO + o), *reinterpret_cast<const uint4 *>(&rn));
+#else
       xn.st(XO + o);
       rn.st(RO + o);
+#endif
       rs[u].dot4(rn, d0);
       rn.dot4(rn, d1);
     }
@@ -92,9 +98,118 @@ __global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
   grid_reduce_finalize<2, PH_H3>(d, a.red, scratch);
 }
 
+// H3 implementation (tools/h3var.sh, config 3, paired runs at 1965 MHz): k_h3 1.24 ms; k_h3_bulk
+// 1.17-1.19 ms for 2-3 stages of 256-512 vectors at 2-4 CTAs/SM, best 3 x 384 at 2 CTAs/SM.
+#ifndef STEN_H3_VARIANT
+#define STEN_H3_VARIANT 2  // 0: k_h3 (register streams); 1: k_h3 with .cs stores; 2: k_h3_bulk
+#endif
+#ifndef STEN_H3_SEGV
+#define STEN_H3_SEGV 384   // k_h3_bulk: 16-B vectors per segment
+#endif
+#ifndef STEN_H3_NS
+#define STEN_H3_NS 3       // k_h3_bulk: ring stages (3 x 5 x 6 KB = 90 KB)
+#endif
+#ifndef STEN_H3_CPS
+#define STEN_H3_CPS 2      // k_h3_bulk: CTAs per SM
+#endif
+#ifndef STEN_H3_CSST
+#define STEN_H3_CSST 1  // k_h3_bulk: streaming (.cs) stores of x, r
+#endif
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// H3 through 1D bulk copies: a persistent CTA streams segments of SEGV 16-B vectors of the five
+// inputs (x, p, s, t, rhat) through an NS-stage shared ring (cp.async.bulk issued by one thread,
+// mbarrier complete_tx), computes from shared memory and stores x, r with streaming stores.
+template <typename T, int SEGV, int NS>
+__global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ float scratch[32 * kMaxDots];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  T *ring = reinterpret_cast<T *>(smem + 128);  // [NS][5][SEGV * VEC]
+  if (st_idle(a.red.st)) return;
+  const long long nseg = (a.nvec + SEGV - 1) / SEGV;
+  const long long nmine = blockIdx.x < nseg ? (nseg - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int tid = threadIdx.x;
+  const T *src[5] = {reinterpret_cast<const T *>(a.x), reinterpret_cast<const T *>(a.p),
+                     reinterpret_cast<const T *>(a.s), reinterpret_cast<const T *>(a.t),
+                     reinterpret_cast<const T *>(a.rhat)};
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long i) {
+    const int slot = (int)(i % NS);
+    const long long v0 = (blockIdx.x + i * gridDim.x) * (long long)SEGV;
+    const long long nv = min((long long)SEGV, a.nvec - v0);
+    const uint32_t bytes = (uint32_t)(nv * 16);
+    mbar_expect_tx(&bar[slot], 5u * bytes);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) bulk_g2s(ring + ((size_t)slot * 5 + k) * SEGV * VEC, src[k] + v0 * VEC, bytes, &bar[slot]);
+  };
+  if (tid == 0)
+    for (long long i = 0; i < NS && i < nmine; ++i) issue(i);
+  const typename P::S as = P::scalar(a.red.st->alpha);
+  const typename P::S ws = P::scalar(a.red.st->omega);
+  const typename P::S mws = P::neg(ws);
+  T *__restrict__ XO = reinterpret_cast<T *>(a.xo);
+  T *__restrict__ RO = reinterpret_cast<T *>(a.ro);
+  float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+  for (long long i = 0; i < nmine; ++i) {
+    const int slot = (int)(i % NS);
+    mbar_wait(&bar[slot], (uint32_t)((i / NS) & 1));
+    const long long v0 = (blockIdx.x + i * gridDim.x) * (long long)SEGV;
+    const int nv = (int)min((long long)SEGV, a.nvec - v0);
+    const T *rb = ring + (size_t)slot * 5 * SEGV * VEC;
+    for (int v = tid; v < nv; v += 256) {
+      const int e = v * VEC;
+      const P xs = P::ld(rb + e), ps = P::ld(rb + SEGV * VEC + e), ss = P::ld(rb + 2 * SEGV * VEC + e);
+      const P ts = P::ld(rb + 3 * SEGV * VEC + e), rs = P::ld(rb + 4 * SEGV * VEC + e);
+      const P xn = P::fmas(ws, ss, P::fmas(as, ps, xs)), rn = P::fmas(mws, ts, ss);
+      const long long o = (v0 + v) * VEC;
+      if (STEN_H3_CSST) {
+        __stcs(reinterpret_cast<uint4 *>(XO + o), *reinterpret_cast<const uint4 *>(&xn));
+        __stcs(reinterpret_cast<uint4 *>(RO + o), *reinterpret_cast<const uint4 *>(&rn));
+      } else {
+        xn.st(XO + o);
+        rn.st(RO + o);
+      }
+      rs.dot4(rn, d0);
+      rn.dot4(rn, d1);
+    }
+    __syncthreads();  // the slot is consumed
+    if (tid == 0 && i + NS < nmine) issue(i + NS);
+  }
+  float d[2] = {sum4(d0), sum4(d1)};
+  grid_reduce_finalize<2, PH_H3>(d, a.red, scratch);
+}
+
 template <typename T>
 int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
+#if STEN_H3_VARIANT == 2
+  (void)grid;
+  (void)threads;
+  constexpr size_t smem = 128 + (size_t)STEN_H3_NS * 5 * STEN_H3_SEGV * 16;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_h3_bulk<T, STEN_H3_SEGV, STEN_H3_NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  k_h3_bulk<T, STEN_H3_SEGV, STEN_H3_NS><<<device_sm_count() * STEN_H3_CPS, 256, smem, s>>>(a);
+#else
   k_h3<T><<<grid, threads, 0, s>>>(a);
+#endif
   return (int)cudaGetLastError();
 }
 
