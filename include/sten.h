@@ -327,7 +327,8 @@ int sten_set_dot_precision(sten_stencil *st, int dots);
  * STEN_DOTS_HALF.  Errors: STEN_EINVAL (cap too small, NULL n). */
 int sten_sr_segments(sten_stencil *st, int precision, int *z0, int cap, int *n);
 /* The same for the classic kernels (H1, H2, apply): the first plane of every
- * z chunk a CTA marches, per slab (the decomposed, overlapped schedule cuts
+ * z chunk a CTA of any of them marches (H2 may use longer chunks than H1 and
+ * the apply: the union), per slab (the decomposed, overlapped schedule cuts
  * each slab into plane 0, the interior in chunks from plane 1, plane nz-1). */
 int sten_classic_segments(sten_stencil *st, int precision, int *z0, int cap, int *n);
 

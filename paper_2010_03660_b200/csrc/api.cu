@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
@@ -134,7 +135,9 @@ struct Tiling {
   int rows = 0;  // 1: full-row strips (k_rows), 0: BX-wide tiles with an x halo (k_stencil)
   int bx = 0, by = 0, zc = 0, stages = 0, threads = 0;
   int cstages = 0;  // > 0: coefficient (+ rhat) tiles by TMA into a ring of this depth (k_stencil)
+  int zc2 = 0;      // z chunk of H2 (0: zc; H1 and the apply use zc)
 };
+static int zc_of(const Tiling &t, int mode) { return mode == MODE_H2 && t.zc2 > 0 ? t.zc2 : t.zc; }
 
 // SR schedule buffers (R19): two halo planes per side, because the
 // sweep's y' = A(A p') reaches two planes into the z-neighbour's data.
@@ -287,11 +290,17 @@ static int small_mesh_zc(const sten_stencil *st, int bx, int by, int nzs, int zc
 static void default_tiling(sten_stencil *st, int prec) {
   Tiling &t = st->tiling[prec];
   int nzs = st->slabs[0].nz;
-  t.zc = nzs < 64 ? nzs : 64;
+  // z chunks (config 3, paired runs, tools/zc_sweep.sh): H1 1.94 ms at 16-24 planes vs 2.07 at 64
+  // (2.15 at 128, 2.31 at 1536: neighbouring tiles march together for a shorter time, so fewer
+  // of their shared halo rows miss L2); H2 1.63 ms at 40-48 planes vs 1.66 at 16-20
+  t.zc = nzs < 20 ? nzs : 20;
+  t.zc2 = nzs < 40 ? nzs : 40;
   t.rows = 0;
   t.bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   t.by = 16;
-  t.zc = small_mesh_zc(st, t.bx, t.by, nzs, t.zc, 2);
+  const int zs = small_mesh_zc(st, t.bx, t.by, nzs, 64, 2);
+  if (zs < t.zc) t.zc = zs;
+  if (zs < t.zc2) t.zc2 = zs;
   // coefficient (+ rhat) tiles by TMA, 2 input + 2 coefficient stages (2 CTAs/SM): H1 2.12 ms vs
   // 2.31 ms with per-thread coefficient loads, which straddle sectors on unpadded rows
   t.stages = 2;
@@ -350,7 +359,8 @@ static int ensure_bufs(sten_stencil *st, int prec) {
   int need = 0;
   for (Slab &sl : st->slabs) {
     const Tiling &t = st->tiling[prec];
-    int g = ((st->nx + t.bx - 1) / t.bx) * ((st->ny + t.by - 1) / t.by) * ((sl.nz + t.zc - 1) / t.zc);
+    const int zmin = t.zc2 > 0 && t.zc2 < t.zc ? t.zc2 : t.zc;
+    int g = ((st->nx + t.bx - 1) / t.bx) * ((st->ny + t.by - 1) / t.by) * ((sl.nz + zmin - 1) / zmin);
     if (g > need) need = g;
     const int ge = ew_grid(st, (long long)st->plane * sl.nz / 4);  // vec = 4 gives the larger grid
     if (ge > need) need = ge;
@@ -416,14 +426,14 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     a.cptr[d] = prec == STEN_FP32 ? (const void *)sl.c32[d] : (const void *)sl.c16[d];
   }
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
-  a.zc = t.zc;
+  a.zc = zc_of(t, mode);
   a.zlo = part == CLS_INTERIOR ? 1 : (part == CLS_TOP ? sl.nz - 1 : 0);
   a.zhi = part == CLS_INTERIOR ? sl.nz - 1 : (part == CLS_BOTTOM ? 1 : sl.nz);
   if (part == CLS_BOTTOM || part == CLS_TOP) a.zc = 1;
   a.pf = st->coef_pf;
   a.tiles_x = t.rows ? 1 : (st->nx + t.bx - 1) / t.bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
-  if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + t.zc - 1) / t.zc) > st->partials_cap)
+  if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + a.zc - 1) / a.zc) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: stencil grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;  // raw sums (sten_classic_phase)
@@ -1509,7 +1519,7 @@ int sten_set_tiling(sten_stencil *st, int prec, int bx, int by, int zc, int stag
     return set_err(STEN_EINVAL, "bx must be 0, %d (tiles) or >= nx=%d (full-row strips)", tbx, st->nx);
   }
   if (by) t.by = by;
-  if (zc) t.zc = zc;
+  if (zc) t.zc = t.zc2 = zc;
   if (stages) {  // an explicit pipeline depth selects the per-thread coefficient loads (3 or 4 stages)
     t.stages = stages;
     t.cstages = 0;
@@ -2121,17 +2131,22 @@ int sten_classic_segments(sten_stencil *st, int prec, int *z0, int cap, int *n) 
   if (!st || !n) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
   if (st->tiling[prec].bx == 0) default_tiling(st, prec);
-  const int zc = st->tiling[prec].zc;
+  const Tiling &t = st->tiling[prec];
   int cnt = 0;
   for (const Slab &sl : st->slabs) {
     std::vector<int> starts;
-    if (cls_overlapped(st)) {  // plane 0, the interior in zc chunks from plane 1, plane nz-1
-      starts.push_back(0);
-      for (int z = 1; z < sl.nz - 1; z += zc) starts.push_back(z);
-      starts.push_back(sl.nz - 1);
-    } else {
-      for (int z = 0; z < sl.nz; z += zc) starts.push_back(z);
+    for (int mode : {MODE_H1, MODE_H2}) {  // the union of the H1 (= apply) and H2 plans
+      const int zc = zc_of(t, mode);
+      if (cls_overlapped(st)) {  // plane 0, the interior in zc chunks from plane 1, plane nz-1
+        starts.push_back(0);
+        for (int z = 1; z < sl.nz - 1; z += zc) starts.push_back(z);
+        starts.push_back(sl.nz - 1);
+      } else {
+        for (int z = 0; z < sl.nz; z += zc) starts.push_back(z);
+      }
     }
+    std::sort(starts.begin(), starts.end());
+    starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
     for (int z : starts) {
       if (z0 && cnt < cap) z0[cnt] = (int)sl.z_first + z;
       ++cnt;
