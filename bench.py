@@ -437,7 +437,7 @@ def run_sten(args):
         kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
         traffic, traffic_src = (None, None)
         if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
-            traffic, traffic_src = measured_traffic("k_sr<__half" if sr else "k_stencil<__half, 1")
+            traffic, traffic_src = measured_traffic("k_sr<__half, 16, 2, 2, 0" if sr else "k_stencil<__half, 1")
         passes = roofline.passes_per_iter(sch, const_op and sr)
         bpi = roofline.bytes_per_point_iter(pname, sch, const_op and sr)
         # whole step against the schedule's algorithmic bytes (classic: SURVEY 8(d)'s 29 passes)

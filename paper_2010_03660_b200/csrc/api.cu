@@ -2544,10 +2544,11 @@ static void drop_graphs2d(sten_stencil2d *st) {
 }
 
 // one (nx, ny) map over a pitched plane, box (BX + 2H) x (BY + 2)
-static int map2d(const sten_stencil2d *st, CUtensorMap *m, void *base, int prec) {
+static constexpr int kApply9BY = 32;  // rows per k_apply9 tile (apply9_launch)
+static int map2d(const sten_stencil2d *st, CUtensorMap *m, void *base, int prec, int by) {
   const int e = esize(prec), H = 16 / e;
   return make_map_p(m, base, e, st->nx, st->ny, 1, st->pitch, (long long)st->pitch * st->ny, 3, bx2d(prec) + 2 * H,
-                    kBicg9BY + 2);
+                    by + 2);
 }
 
 // The apply path's SpMV: gather (1 x 1 tiles) or the tiled output-halo form.
@@ -2606,11 +2607,11 @@ static int ensure2d(sten_stencil2d *st, int prec) {
       }
       CUDA_TRY(cudaMemset(*pp, 0, bytes));  // row padding stays zero (the element-wise kernels stream it)
     }
-    RC_TRY(map2d(st, &b.m_x, b.x, prec));
-    RC_TRY(map2d(st, &b.m_r, b.r, prec));
+    RC_TRY(map2d(st, &b.m_x, b.x, prec, kApply9BY));  // A x0 by k_apply9
+    RC_TRY(map2d(st, &b.m_r, b.r, prec, kBicg9BY));
     for (int k = 0; k < 2; ++k) {
-      RC_TRY(map2d(st, &b.m_p[k], b.p[k], prec));
-      RC_TRY(map2d(st, &b.m_v[k], b.v[k], prec));
+      RC_TRY(map2d(st, &b.m_p[k], b.p[k], prec, kBicg9BY));
+      RC_TRY(map2d(st, &b.m_v[k], b.v[k], prec, kBicg9BY));
     }
     b.ready = true;
   }
@@ -2838,7 +2839,7 @@ int stencil2d_apply(sten_stencil2d *st, int prec, const void *x, void *y, void *
     CUDA_TRY(cudaMemset(st->v[prec], 0, bytes));  // padding columns stay zero
   }
   if (!st->maps_ok[prec]) {
-    RC_TRY(map2d(st, &st->m_v[prec], st->v[prec], prec));
+    RC_TRY(map2d(st, &st->m_v[prec], st->v[prec], prec, kApply9BY));
     st->maps_ok[prec] = true;
   }
   RC_TRY(copy2d_in(st, prec, st->v[prec], x, s));

@@ -329,7 +329,10 @@ __global__ void k_round9(const Ring9Args a, int dir) {
 // loads issued before the TMA wait.  H3 and S1 are the 3D element-wise kernels
 // (k_h3, k_init) over the pitched plane.
 template <typename T, int MODE, int BY>
-__global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, 2) k_bicg9(const __grid_constant__ Bicg9Args a) {
+#ifndef STEN_BICG9_MINB
+#define STEN_BICG9_MINB 2
+#endif
+__global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, STEN_BICG9_MINB) k_bicg9(const __grid_constant__ Bicg9Args a) {
   using P = Pack<T>;
   constexpr int VEC = P::VEC, BX = Tile2<T>::BX, H = 16 / (int)sizeof(T), HW = BX + 2 * H, VPR = BX / VEC;
   constexpr int NT = VPR * BY, NIN = MODE == MODE_H1 ? 3 : 2, ND = MODE == MODE_H1 ? 1 : 2;
@@ -429,7 +432,7 @@ __global__ void k_create9(const TIN *diag, Coef9In in, int nx, int ny, int pitch
 
 template <typename T>
 int apply9_launch(const Apply9Args &a, cudaStream_t s) {
-  constexpr int BY = 32;
+  constexpr int BY = 32;  // = kApply9BY of the host's tensor maps
   const int ty = (a.ny + BY - 1) / BY;
   if (a.xm) k_apply9<T, BY, true><<<a.tiles_x * ty, (Tile2<T>::BX / Pack<T>::VEC) * BY, 0, s>>>(a);
   else k_apply9<T, BY, false><<<a.tiles_x * ty, (Tile2<T>::BX / Pack<T>::VEC) * BY, 0, s>>>(a);

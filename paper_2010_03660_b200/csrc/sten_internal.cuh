@@ -619,7 +619,10 @@ struct Ring9Args {
   int nx, ny, pitch, TX, TY, HS, WS;
 };
 // the fused 2D BiCGStab phases H1 (inputs r, p, v) and H2 (inputs r, v')
-constexpr int kBicg9BY = 32;
+#ifndef STEN_BICG9_BY
+#define STEN_BICG9_BY 32
+#endif
+constexpr int kBicg9BY = STEN_BICG9_BY;  // rows per k_bicg9 tile
 struct alignas(64) Bicg9Args {
   CUtensorMap tm_in[3];   // box (BX + 2H) x (BY + 2)
   const void *c[8];

@@ -18,11 +18,11 @@ ncu --metrics gpu__time_duration.sum $N -c 600 --csv --log-file gpurun_out/r2_la
 C="python bench.py --steps 1 --warmup 1 --maxit 2 --no-e2e --no-cpu --no-other --schedule classic"
 $C > gpurun_out/r2_c.log 2>&1 && ncu --set full $N --import-source on -k regex:'k_stencil|k_h3' -s 3 -c 3 -o gpurun_out/r2_classic_full $C > gpurun_out/r2_classic_full.log 2>&1 && reduce r2_classic_full src
 S="python bench.py --steps 1 --warmup 1 --maxit 2 --no-e2e --no-cpu --no-other --schedule sr"
-$S > gpurun_out/r2_s.log 2>&1 && ncu --set full $N --import-source on -k regex:'k_sr' -s 3 -c 1 -o gpurun_out/r2_sr_full $S > gpurun_out/r2_sr_full.log 2>&1 && reduce r2_sr_full
+$S > gpurun_out/r2_s.log 2>&1 && ncu --set full $N --import-source on -k regex:'^k_sr$' -s 0 -c 1 -o gpurun_out/r2_sr_full $S > gpurun_out/r2_sr_full.log 2>&1 && reduce r2_sr_full
 F="python bench.py --steps 1 --warmup 1 --maxit 2 --no-e2e --no-cpu --no-other --schedule sr --precision fp32"
-$F > gpurun_out/r2_f.log 2>&1 && ncu --set full $N -k regex:'k_sr' -s 3 -c 1 -o gpurun_out/r2_sr32_full $F > gpurun_out/r2_sr32_full.log 2>&1 && reduce r2_sr32_full
+$F > gpurun_out/r2_f.log 2>&1 && ncu --set full $N -k regex:'^k_sr$' -s 0 -c 1 -o gpurun_out/r2_sr32_full $F > gpurun_out/r2_sr32_full.log 2>&1 && reduce r2_sr32_full
 K="python bench.py --steps 1 --warmup 1 --maxit 2 --no-e2e --no-cpu --no-other --schedule sr --operator poisson-const"
-$K > gpurun_out/r2_k.log 2>&1 && ncu --set full $N -k regex:'k_sr' -s 3 -c 1 -o gpurun_out/r2_srcc_full $K > gpurun_out/r2_srcc_full.log 2>&1 && reduce r2_srcc_full
+$K > gpurun_out/r2_k.log 2>&1 && ncu --set full $N -k regex:'^k_sr$' -s 0 -c 1 -o gpurun_out/r2_srcc_full $K > gpurun_out/r2_srcc_full.log 2>&1 && reduce r2_srcc_full
 D="python tools/run_2d_once.py"
 $D > gpurun_out/r2_d.log 2>&1 && ncu --set full $N -k regex:'k_bicg9|k_apply9|k_ring9|k_round9' -c 8 -o gpurun_out/r2_2d_full $D > gpurun_out/r2_2d_full.log 2>&1 && reduce r2_2d_full
 du -sh gpurun_out; ls -la gpurun_out
