@@ -2669,6 +2669,7 @@ static int enqueue_iter2d(sten_stencil2d *st, int prec, int parity, cudaStream_t
   a.ny = st->ny;
   a.pitch = st->pitch;
   a.tiles_x = (st->nx + bx2d(prec) - 1) / bx2d(prec);
+  a.tiles_y = (st->ny + kBicg9BY - 1) / kBicg9BY;
   a.red = red2d(st);
   // H1
   a.tm_in[0] = b.m_r;

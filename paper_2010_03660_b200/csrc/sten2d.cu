@@ -323,15 +323,22 @@ __global__ void k_round9(const Ring9Args a, int dir) {
 //       (l.176), (rhat, v')  -> alpha (l.177)
 //   H2: s = r - alpha v' (l.178) on the whole box, t = A s (l.179),
 //       (t, s), (t, t)       -> omega (l.180)
-// A CTA owns a BX x BY tile: the NIN inputs arrive by TMA as (BX+2H) x (BY+2)
-// boxes (zero fill outside the mesh), the SpMV input is formed once per box
-// element into a fourth box, the eight couplings (and rhat) are streaming 16-B
-// loads issued before the TMA wait.  H3 and S1 are the 3D element-wise kernels
-// (k_h3, k_init) over the pitched plane.
-template <typename T, int MODE, int BY>
+// A persistent CTA (2 per SM) walks the BX x BY tiles b, b + G, b + 2G, ... (G = grid size; the G
+// tiles in flight are consecutive in row-major order, so y-neighbours run together and share halo
+// rows in L2).  Per tile the NIN inputs arrive by TMA as (BX+2H) x (BY+2) boxes (zero fill outside
+// the mesh) into a 2-stage ring - the next tile's boxes are in flight while this one is computed -
+// the SpMV input is formed once per box element into one of two shared boxes (ping-pong: one
+// barrier per tile), the eight couplings (and rhat) of the next tile are streaming 16-B loads
+// issued as soon as this tile's FMA chain has consumed its own.  The inner products accumulate
+// over all of a CTA's tiles: one deposit per CTA.  H3 and S1 are the 3D element-wise kernels
+// (k_h3_bulk, k_init) over the pitched plane.
 #ifndef STEN_BICG9_MINB
-#define STEN_BICG9_MINB 2
+#define STEN_BICG9_MINB 1  // CTAs per SM (measured: 1 per SM 5.44 ms per mixed iteration at 22800^2, 2 per SM 5.79)
 #endif
+#ifndef STEN_BICG9_NS
+#define STEN_BICG9_NS 2  // input stages
+#endif
+template <typename T, int MODE, int BY>
 __global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, STEN_BICG9_MINB) k_bicg9(const __grid_constant__ Bicg9Args a) {
   using P = Pack<T>;
   constexpr int VEC = P::VEC, BX = Tile2<T>::BX, H = 16 / (int)sizeof(T), HW = BX + 2 * H, VPR = BX / VEC;
@@ -339,29 +346,30 @@ __global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, STEN_BICG9
   constexpr int HSTR = a128_2d(HW * (BY + 2) * (int)sizeof(T)) / (int)sizeof(T);
   constexpr int NVB = (HW / VEC) * (BY + 2);  // 16-B vectors per box
   if (st_idle(a.red.st)) return;
-  __shared__ __align__(128) T box[(NIN + 1) * HSTR];
-  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(128) unsigned char smem2[];
+  constexpr int NS = STEN_BICG9_NS;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem2);  // [NS]
+  T *stage = reinterpret_cast<T *>(smem2 + 128);        // [NS][NIN][HSTR]
+  T *Ub = stage + NS * NIN * HSTR;                      // [2][HSTR]
   __shared__ float scratch[32 * kMaxDots];
-  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
-  const int x0 = tx * BX, y0 = ty * BY;
+  const int ntiles = a.tiles_x * a.tiles_y;
   const int tid = threadIdx.x, ry = tid / VPR, cx = tid - (tid / VPR) * VPR;
-  const int gx = x0 + cx * VEC, gy = y0 + ry;
-  const bool inside = gx < a.nx && gy < a.ny;
   if (tid == 0) {
-    mbar_init(&bar, 1);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    mbar_expect_tx(&bar, (uint32_t)(NIN * HW * (BY + 2) * sizeof(T)));
+  auto issue = [&](int tile, int slot) {  // one thread
+    const int x0 = (tile % a.tiles_x) * BX, y0 = (tile / a.tiles_x) * BY;
+    mbar_expect_tx(&bar[slot], (uint32_t)(NIN * HW * (BY + 2) * sizeof(T)));
 #pragma unroll
-    for (int i = 0; i < NIN; ++i) tma_load_3d(box + i * HSTR, &a.tm_in[i], x0 - H, y0 - 1, 0, &bar);
-  }
-  P c[8], rh = P::zero();
-  const long long o = (long long)gy * a.pitch + gx;
-#pragma unroll
-  for (int d = 0; d < 8; ++d) c[d] = inside ? P::ldg(reinterpret_cast<const T *>(a.c[d]) + o) : P::zero();
-  if (MODE == MODE_H1 && inside) rh = P::ldg(reinterpret_cast<const T *>(a.rh) + o);
+    for (int i = 0; i < NIN; ++i) tma_load_3d(stage + (slot * NIN + i) * HSTR, &a.tm_in[i], x0 - H, y0 - 1, 0, &bar[slot]);
+  };
+  const int t0 = blockIdx.x, G = gridDim.x;
+  if (tid == 0)
+    for (int q = 0; q < NS; ++q)
+      if (t0 + q * G < ntiles) issue(t0 + q * G, q);
   typename P::S s1{}, s2{};
   if (MODE == MODE_H1) {
     s1 = P::scalar(a.red.st->beta);
@@ -369,33 +377,57 @@ __global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, STEN_BICG9
   } else {
     s1 = P::neg(P::scalar(a.red.st->alpha));
   }
-  mbar_wait(&bar, 0);
-  T *U = box + NIN * HSTR;
-  for (int q = tid; q < NVB; q += NT) {  // the SpMV input on the whole box
-    const int h = q * VEC;
-    P f = P::ld(box + h);  // r
-    if (MODE == MODE_H1) f = P::fmas(s1, P::fmas(s2, P::ld(box + 2 * HSTR + h), P::ld(box + HSTR + h)), f);
-    else f = P::fmas(s1, P::ld(box + HSTR + h), f);
-    f.st(U + h);
-  }
-  __syncthreads();
-  const int e = (ry + 1) * HW + H + cx * VEC;
-  const P w = P::ld(U + e);  // p' (H1) / s (H2) at the own points
-  const P u = chain9<T, HW, false>(U, e, c, nullptr, nullptr, gx, gy, inside);
-  if (inside) {
-    u.st(reinterpret_cast<T *>(a.out0) + o);
-    w.st(reinterpret_cast<T *>(a.out1) + o);
-  }
+  P c[8], rh = P::zero();
+  auto load_own = [&](int tile, long long &o, bool &inside, int &gx, int &gy) {
+    gx = (tile % a.tiles_x) * BX + cx * VEC;
+    gy = (tile / a.tiles_x) * BY + ry;
+    inside = tile < ntiles && gx < a.nx && gy < a.ny;
+    o = (long long)gy * a.pitch + gx;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) c[d] = inside ? P::ldg(reinterpret_cast<const T *>(a.c[d]) + o) : P::zero();
+    if (MODE == MODE_H1) rh = inside ? P::ldg(reinterpret_cast<const T *>(a.rh) + o) : P::zero();
+  };
+  long long o;
+  bool inside;
+  int gx, gy;
+  load_own(t0, o, inside, gx, gy);
   float dacc[ND][4];
 #pragma unroll
   for (int d = 0; d < ND; ++d)
 #pragma unroll
     for (int i = 0; i < 4; ++i) dacc[d][i] = 0.0f;
-  if (MODE == MODE_H1) {
-    rh.dot4(u, dacc[0]);  // (rhat, v')
-  } else {
-    u.dot4(w, dacc[0]);          // (t, s)
-    u.dot4(u, dacc[ND - 1]);     // (t, t)
+  const int e = (ry + 1) * HW + H + cx * VEC;
+  int k = 0;
+  for (int tile = t0; tile < ntiles; tile += G, ++k) {
+    const int slot = k % NS;
+    mbar_wait(&bar[slot], (uint32_t)((k / NS) & 1));
+    const T *box = stage + slot * NIN * HSTR;
+    T *U = Ub + (k & 1) * HSTR;
+    for (int q = tid; q < NVB; q += NT) {  // the SpMV input on the whole box
+      const int h = q * VEC;
+      P f = P::ld(box + h);  // r
+      if (MODE == MODE_H1) f = P::fmas(s1, P::fmas(s2, P::ld(box + 2 * HSTR + h), P::ld(box + HSTR + h)), f);
+      else f = P::fmas(s1, P::ld(box + HSTR + h), f);
+      f.st(U + h);
+    }
+    __syncthreads();  // U complete, the stage consumed (and every thread is past the previous tile)
+    if (tid == 0 && tile + NS * G < ntiles) issue(tile + NS * G, slot);
+    const P w = P::ld(U + e);  // p' (H1) / s (H2) at the own points
+    const P u = chain9<T, HW, false>(U, e, c, nullptr, nullptr, gx, gy, inside);
+    const P rh_ = rh;
+    const long long o_ = o;
+    const bool in_ = inside;
+    load_own(tile + G, o, inside, gx, gy);  // the next tile's couplings in flight
+    if (in_) {
+      u.st(reinterpret_cast<T *>(a.out0) + o_);
+      w.st(reinterpret_cast<T *>(a.out1) + o_);
+      if (MODE == MODE_H1) {
+        rh_.dot4(u, dacc[0]);  // (rhat, v')
+      } else {
+        u.dot4(w, dacc[0]);       // (t, s)
+        u.dot4(u, dacc[ND - 1]);  // (t, t)
+      }
+    }
   }
   float v[ND];
 #pragma unroll
@@ -463,13 +495,27 @@ template int ring9_launch<__half>(const Ring9Args &, cudaStream_t);
 template int round9_launch<float>(const Ring9Args &, int, cudaStream_t);
 template int round9_launch<__half>(const Ring9Args &, int, cudaStream_t);
 
+template <typename T, int MODE, int BY>
+static int bicg9_one(const Bicg9Args &a, cudaStream_t s) {
+  constexpr int NIN = MODE == MODE_H1 ? 3 : 2, H = 16 / (int)sizeof(T), HW = Tile2<T>::BX + 2 * H;
+  constexpr size_t smem = 128 + (size_t)(STEN_BICG9_NS * NIN + 2) * (a128_2d(HW * (BY + 2) * (int)sizeof(T)));
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_bicg9<T, MODE, BY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  const int tiles = a.tiles_x * a.tiles_y, nt = (Tile2<T>::BX / Pack<T>::VEC) * BY;
+  int grid = device_sm_count() * STEN_BICG9_MINB;
+  if (grid > tiles) grid = tiles;
+  k_bicg9<T, MODE, BY><<<grid, nt, smem, s>>>(a);
+  return (int)cudaGetLastError();
+}
 template <typename T>
 int bicg9_launch(int mode, const Bicg9Args &a, cudaStream_t s) {
   constexpr int BY = kBicg9BY;
-  const int grid = a.tiles_x * ((a.ny + BY - 1) / BY), nt = (Tile2<T>::BX / Pack<T>::VEC) * BY;
-  if (mode == MODE_H1) k_bicg9<T, MODE_H1, BY><<<grid, nt, 0, s>>>(a);
-  else k_bicg9<T, MODE_H2, BY><<<grid, nt, 0, s>>>(a);
-  return (int)cudaGetLastError();
+  if (mode == MODE_H1) return bicg9_one<T, MODE_H1, BY>(a, s);
+  return bicg9_one<T, MODE_H2, BY>(a, s);
 }
 template int bicg9_launch<float>(int, const Bicg9Args &, cudaStream_t);
 template int bicg9_launch<__half>(int, const Bicg9Args &, cudaStream_t);

@@ -628,7 +628,7 @@ struct alignas(64) Bicg9Args {
   const void *c[8];
   const void *rh;         // H1: rhat
   void *out0, *out1;      // H1: v', p'   H2: t, s
-  int nx, ny, pitch, tiles_x;
+  int nx, ny, pitch, tiles_x, tiles_y;
   Reduce red;
 };
 struct Coef9In { const void *off[8]; };
