@@ -519,7 +519,10 @@ def run_sten(args):
         r = recs[sch]
         line[sch] = {"label": sched_names[sch], "value": r["value"], "unit": "Gpoint-iter/s",
                      "ms_per_step": r["t_ms"] / args.steps, "iters_per_solve": r["iters_done"] / args.steps,
-                     "gflops": r["value"] * roofline.FLOPS_PER_POINT_ITER,
+                     "gflops_alg1_equivalent": r["value"] * roofline.FLOPS_PER_POINT_ITER,
+                     "gflops_note": "Alg. 1's 44 flop per point-iteration (PAPER.md:399-417) credited per "
+                                    "iteration; the SR sweep itself performs more (three SpMVs, 12 dots)"
+                                    if sch == "sr" else "44 flop per point-iteration (PAPER.md:399-417)",
                      "status": r["status"], "final_rel_residual": r["final_rel_residual"],
                      "rel_residual_iter10": r["hist_10"], "events": r["events"],
                      "roofline": roofline_of(sch, r), "gpu_launches": int(r["launches"]),
