@@ -117,10 +117,12 @@ int sten_comm_unique_id(void *id_out);
  * built on the communicator must be created and used with that device current.
  *   unique_id != NULL: NCCL (loaded at run time, libnccl.so.2) carries the
  *     halo planes and the fp32 all-reduces of every schedule;
- *   unique_id == NULL: a peer-memory-only communicator (no NCCL): the only
- *     supported solve is the SR schedule with the fused exchange after
- *     sten_p2p_import (CUDA IPC peer stores and the one-shot peer all-reduce;
- *     x0 == NULL); everything else returns STEN_EUNSUPPORTED.
+ *   unique_id == NULL: a peer-memory-only communicator (no NCCL): after
+ *     sten_p2p_import, halos and all-reduces go through CUDA IPC peer memory:
+ *     the SR schedule with the fused exchange, or the classic schedule (halo
+ *     planes pushed into the neighbours' buffers, a one-shot peer all-reduce
+ *     per phase) in host lockstep (sten_set_host_barrier); x0 == NULL;
+ *     everything else returns STEN_EUNSUPPORTED.
  * Errors: STEN_EINVAL (bad rank/nranks/cuda_device), STEN_ECUDA, STEN_ENCCL
  * (NCCL missing or ncclCommInitRank failed). */
 int sten_comm_create(const void *unique_id, int nranks, int rank, int cuda_device, sten_comm **out);
@@ -381,8 +383,9 @@ int sten_sr_sweep(sten_stencil *st, int precision, double alpha, double omega, d
  * Default: FUSED.  SERIAL and FUSED add the slab sums in the same order: their
  * results are bitwise equal. */
 /* Peer memory across ranks (one node, NVLink/NVSwitch): export writes CUDA IPC
- * handles of this rank's boundary-slab SR buffers, its inbox and its boundary
- * slabs' coefficient arrays for `precision` (out == NULL: *bytes = the record
+ * handles of this rank's boundary-slab SR buffers, its inbox, its boundary
+ * slabs' coefficient arrays and their classic halo'd vectors (r, p, v) for
+ * `precision` (out == NULL: *bytes = the record
  * size); every rank passes all ranks' records, in rank order, to import, which
  * opens the z-neighbours' buffers and the other inboxes and selects
  * STEN_XCHG_FUSED across ranks.  With a peer-memory-only communicator
@@ -405,11 +408,14 @@ int sten_set_sr_exchange(sten_stencil *st, int mode);
  * written by another process's kernel are not guaranteed to make progress when
  * both processes share a GPU (a context-switch timeout, Xid 109, on B200), so
  * with a barrier set and a peer-memory-only communicator the solve runs sweep by
- * sweep without graphs and, before every peer-memory all-reduce's waiting
- * kernel, synchronises its stream and calls fn(ctx) - which must return only
- * after every rank has called it for the same reduction (e.g. a gloo barrier).
- * The waiting kernel then finds every peer's sums already deposited.  Results
- * are bitwise those of the unsynchronised path.  Errors: STEN_EINVAL. */
+ * sweep (classic: iteration by iteration) without graphs and, before every
+ * peer-memory all-reduce's waiting kernel, synchronises its stream and calls
+ * fn(ctx) - which must return only after every rank has called it for the same
+ * reduction (e.g. a gloo barrier).  The waiting kernel then finds every peer's
+ * sums already deposited.  The classic schedule also calls it after every halo
+ * push, so that the pushes have landed before any rank's stencil reads them; it
+ * needs the barrier on a peer-memory-only communicator.  Results are bitwise
+ * those of the unsynchronised path.  Errors: STEN_EINVAL. */
 int sten_set_host_barrier(sten_stencil *st, void (*fn)(void *ctx), void *ctx);
 
 /* SR kernel geometry for tuning (0 = default): by rows per tile (8 or 16),

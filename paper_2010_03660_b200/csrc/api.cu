@@ -237,6 +237,7 @@ struct sten_stencil {
   int p2p_slots = 0;
   std::vector<P2PBox> p2p_remote;           // other ranks' inboxes (IPC)
   void *p2p_lo[2][2][5] = {}, *p2p_hi[2][2][5] = {};  // [prec][set][vec]: the z-neighbour ranks' buffers (IPC)
+  void *cls_lo[2][5] = {}, *cls_hi[2][5] = {};  // [prec][r, p0, p1, v0, v1]: classic buffers of the z-neighbour ranks (IPC)
   std::vector<void *> ipc_opened;
   std::map<std::string, void *> ipc_map;  // IPC handle bytes -> mapped pointer
   cudaStream_t side = nullptr;  // capture side stream (exchange + boundary chunks)
@@ -534,6 +535,29 @@ static int exchange(sten_stencil *st, int prec, Pick pick, cudaStream_t s) {
     CUDA_TRY(cudaMemcpyAsync(hi, lo + (size_t)nzl * pb, pb, cudaMemcpyDeviceToDevice, s));        // top -> halo 0
     CUDA_TRY(cudaMemcpyAsync(lo + (size_t)(nzl + 1) * pb, hi + pb, pb, cudaMemcpyDeviceToDevice, s));  // bottom -> halo top
   }
+  if (p2p_only(st) && st->p2p_ranks) {
+    // peer memory (CUDA IPC): push this rank's boundary planes into the z-neighbour ranks' halo
+    // planes; the caller's host barrier then orders them before any rank's stencil reads them
+    const int R = st->comm->nranks, me = st->comm->rank;
+    PrecBufs &bb = st->slabs[0].pb[prec], &tb = st->slabs[ns - 1].pb[prec];
+    char *bot = (char *)pick(bb), *top = (char *)pick(tb);
+    int idx = -1;
+    const void *cand[5] = {bb.r, bb.p[0], bb.p[1], bb.v[0], bb.v[1]};
+    for (int i = 0; i < 5; ++i)
+      if (cand[i] == (void *)bot) idx = i;
+    if (idx < 0) return set_err(STEN_EUNSUPPORTED, "internal: peer-memory exchange of an unexported buffer");
+    const int nzt = st->slabs[ns - 1].nz;
+    if (me > 0) {  // our bottom interior plane -> the lower rank's top halo plane
+      if (!st->cls_lo[prec][idx]) return set_err(STEN_EUNSUPPORTED, "internal: classic peer buffers not imported");
+      CUDA_TRY(cudaMemcpyAsync((char *)st->cls_lo[prec][idx] + (size_t)(nzt + 1) * pb, bot + pb, pb,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    if (me + 1 < R) {  // our top interior plane -> the upper rank's bottom halo plane
+      if (!st->cls_hi[prec][idx]) return set_err(STEN_EUNSUPPORTED, "internal: classic peer buffers not imported");
+      CUDA_TRY(cudaMemcpyAsync((char *)st->cls_hi[prec][idx], top + (size_t)nzt * pb, pb, cudaMemcpyDeviceToDevice, s));
+    }
+    return STEN_OK;
+  }
   if (nccl_ranks(st)) {
     const int R = st->comm->nranks, me = st->comm->rank;
     char *bot = (char *)pick(st->slabs[0].pb[prec]);
@@ -574,14 +598,14 @@ static int reduce_scalars(sten_stencil *st, int phase, cudaStream_t s, int nslot
   if (!decomposed(st)) return STEN_OK;
   const int ns = nslots > 0 ? nslots : (int)st->slabs.size();
   if (p2p_only(st)) {  // peer-memory all-reduce: deposit this rank's slab sums, wait for every rank's
-    if (phase != PH_INIT || nslots > 0 || !st->p2p_ranks)
+    if (phase == PH_SR || nslots > 0 || !st->p2p_ranks)
       return set_err(STEN_EUNSUPPORTED, "internal: peer-memory reduction of phase %d", phase);
     std::vector<P2PBox> boxes{P2PBox{st->p2p_sums, st->p2p_flags}};
     for (const P2PBox &b : st->p2p_remote) boxes.push_back(b);
     KLAUNCH(p2p_put_launch(st->slab_sums, ns, st->comm->rank * ns, st->p2p_slots, boxes.data(), (int)boxes.size(),
                            st->p2p_seq, s));
     RC_TRY(host_barrier(st, s));
-    KLAUNCH(p2p_fin_launch(PH_INIT, P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
+    KLAUNCH(p2p_fin_launch(phase, P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
     st->launches += 2;
     return STEN_OK;
   }
@@ -621,7 +645,7 @@ static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cu
 }
 
 static bool cls_overlapped(const sten_stencil *st) {
-  if (!decomposed(st) || !st->cls_overlap) return false;
+  if (!decomposed(st) || !st->cls_overlap || p2p_only(st)) return false;
   for (const Slab &sl : st->slabs)
     if (sl.nz < 3) return false;
   return true;
@@ -655,13 +679,17 @@ static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_
     RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, s));
     RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.p[parity]; }, s));
     RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity]; }, s));
+    RC_TRY(host_barrier(st, s));  // peer memory: every rank's halo pushes have landed
   }
   for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H1, k, parity, s));
   RC_TRY(reduce_scalars(st, PH_H1, s));
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
   // H2: halo of the new v
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
-  if (dec) RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity ^ 1]; }, s));
+  if (dec) {
+    RC_TRY(exchange(st, prec, [parity](PrecBufs &b) { return b.v[parity ^ 1]; }, s));
+    RC_TRY(host_barrier(st, s));
+  }
   for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H2, k, parity, s));
   RC_TRY(reduce_scalars(st, PH_H2, s));
   if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
@@ -1651,11 +1679,14 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   const bool sr = st->schedule == STEN_SCHED_SR;
   if (!sr && prec == STEN_MIXED && st->half_dots)
     return set_err(STEN_EUNSUPPORTED, "half dots (STEN_DOTS_HALF) are built for the SR schedule only");
-  if (p2p_only(st)) {  // no NCCL: only the fused SR sweep moves data between ranks
-    if (!sr || !st->p2p_ranks || !st->sr_p2p)
-      return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: SR schedule with the fused exchange after "
-                                        "sten_p2p_import only");
+  if (p2p_only(st)) {  // no NCCL: peer memory moves the data between ranks (after sten_p2p_import)
+    if (!st->p2p_ranks || (sr && !st->sr_p2p))
+      return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: a solve needs sten_p2p_import (and, for the SR "
+                                        "schedule, the fused exchange)");
     if (with_x0) return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: x0 must be NULL");
+    if (!sr && !st->barrier_fn)
+      return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: the classic schedule runs in host lockstep "
+                                        "(sten_set_host_barrier)");
   }
   RC_TRY(ensure_bufs(st, prec));
   if (sr) RC_TRY(ensure_sr(st, prec));
@@ -1725,7 +1756,7 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
     // host lockstep (several ranks on one GPU): sweep by sweep, no graph; every
     // rank runs the same sweeps because every rank takes the same scalar decisions
     for (int i = 0; lockstep && i < nsteps; ++i) {
-      RC_TRY(enqueue_sr_sweep(st, prec, i & 1, s, nullptr));
+      RC_TRY(sr ? enqueue_sr_sweep(st, prec, i & 1, s, nullptr) : enqueue_iteration(st, prec, i & 1, s, nullptr));
       CUDA_TRY(cudaMemcpyAsync(st->st_host, st->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       if (st->st_host->stop || st->st_host->it >= maxit) break;
@@ -2191,7 +2222,7 @@ int sten_set_schedule(sten_stencil *st, int schedule) {
 // (2 sets x 5 vectors each), of its inbox (sums, flags) and of the bottom- and
 // top-slab coefficient arrays (6 fp32 + 6 fp16 each: a p2p-only communicator
 // fills the coefficient halo planes from them at import)
-constexpr int kIpcN = 46;
+constexpr int kIpcN = 56;  // SR vecs 2 x 10, inbox 2, coefficients 2 x 12, classic r p0 p1 v0 v1 2 x 5
 int sten_p2p_export(sten_stencil *st, int prec, void *out, size_t *bytes) {
   if (!st || !bytes) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
@@ -2213,6 +2244,10 @@ int sten_p2p_export(sten_stencil *st, int prec, void *out, size_t *bytes) {
   for (Slab *sl : {&st->slabs.front(), &st->slabs.back()}) {
     for (int d = 0; d < 6; ++d) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->c32b[d]));
     for (int d = 0; d < 6; ++d) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], sl->c16b[d]));
+  }
+  for (Slab *sl : {&st->slabs.front(), &st->slabs.back()}) {  // classic schedule: the halo'd vectors
+    PrecBufs &b = sl->pb[prec];
+    for (void *q : {b.r, b.p[0], b.p[1], b.v[0], b.v[1]}) CUDA_TRY(cudaIpcGetMemHandle(&h[n++], q));
   }
   *bytes = need;
   return STEN_OK;
@@ -2246,6 +2281,10 @@ int sten_p2p_import(sten_stencil *st, int prec, const void *all, size_t bytes_pe
       if (me > 0) RC_TRY(open(rec(me - 1)[10 + set * 5 + i], &st->p2p_lo[prec][set][i]));   // its top slab
       if (me + 1 < R) RC_TRY(open(rec(me + 1)[set * 5 + i], &st->p2p_hi[prec][set][i]));  // its bottom slab
     }
+  for (int i = 0; i < 5; ++i) {  // classic: the lower rank's top slab, the upper rank's bottom slab
+    if (me > 0) RC_TRY(open(rec(me - 1)[51 + i], &st->cls_lo[prec][i]));
+    if (me + 1 < R) RC_TRY(open(rec(me + 1)[46 + i], &st->cls_hi[prec][i]));
+  }
   st->p2p_remote.clear();
   for (int r = 0; r < R; ++r) {
     if (r == me) continue;

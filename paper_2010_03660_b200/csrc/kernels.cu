@@ -345,6 +345,7 @@ __global__ void k_slabsum(const float *__restrict__ slab_sums, int nslabs, float
 template <int PH>
 __global__ void k_p2p_fin(P2PBox inbox, int nslots, unsigned *seqp, DevState *st) {
   if (PH == PH_SR && sr_idle(st)) return;
+  if ((PH == PH_H1 || PH == PH_H2 || PH == PH_H3) && st_idle(st)) return;  // every rank idles alike
   const unsigned seq = *seqp + 1u;
   const int base = (int)(seq & 1u) * nslots;
   const long long t0 = clock64();
@@ -373,8 +374,13 @@ __global__ void k_p2p_fin(P2PBox inbox, int nslots, unsigned *seqp, DevState *st
 }
 
 int p2p_fin_launch(int phase, P2PBox inbox, int nslots, unsigned *seq, DevState *st, cudaStream_t s) {
-  if (phase == PH_INIT) k_p2p_fin<PH_INIT><<<1, 1, 0, s>>>(inbox, nslots, seq, st);
-  else k_p2p_fin<PH_SR><<<1, 1, 0, s>>>(inbox, nslots, seq, st);
+  switch (phase) {
+    case PH_INIT: k_p2p_fin<PH_INIT><<<1, 1, 0, s>>>(inbox, nslots, seq, st); break;
+    case PH_H1: k_p2p_fin<PH_H1><<<1, 1, 0, s>>>(inbox, nslots, seq, st); break;
+    case PH_H2: k_p2p_fin<PH_H2><<<1, 1, 0, s>>>(inbox, nslots, seq, st); break;
+    case PH_H3: k_p2p_fin<PH_H3><<<1, 1, 0, s>>>(inbox, nslots, seq, st); break;
+    default: k_p2p_fin<PH_SR><<<1, 1, 0, s>>>(inbox, nslots, seq, st); break;
+  }
   return (int)cudaGetLastError();
 }
 

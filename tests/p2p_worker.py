@@ -1,6 +1,7 @@
 """One rank of the cross-process peer-memory solve (tests/test_gpu_multiproc.py).
 
-Run as `python tests/p2p_worker.py RANK WORLD PORT OUTDIR PREC MAXIT TOL NX NY NZ SEED`.
+Run as `python tests/p2p_worker.py RANK WORLD PORT OUTDIR PREC MAXIT TOL NX NY NZ SEED [SCHEDULE]`
+(SCHEDULE sr, the default, or classic).
 Every rank uses cuda:0 (the one GPU here), owns planes [r nz/R, (r+1) nz/R) of the
 mesh, builds its handle on a peer-memory-only communicator (sten_comm_create with
 no NCCL id), exchanges the CUDA IPC records over gloo, and solves in host lockstep
@@ -21,6 +22,7 @@ def main():
     outdir, prec = sys.argv[4], sys.argv[5]
     maxit, tol = int(sys.argv[6]), float(sys.argv[7])
     nx, ny, nz, seed = (int(v) for v in sys.argv[8:12])
+    schedule = sys.argv[12] if len(sys.argv) > 12 else "sr"
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -41,7 +43,7 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()  # every rank's coefficients exist before anyone imports (sten.h)
     P = sten.FP32 if prec == "fp32" else sten.MIXED
-    sten.set_schedule(st, sten.SCHED_SR)
+    sten.set_schedule(st, sten.SCHED_SR if schedule == "sr" else sten.SCHED_CLASSIC)
     sten.p2p_setup(st, P)  # export, all_gather over gloo, import
     sten.set_host_barrier(st, lambda: dist.barrier())
     bt = to_gpu_vec(b, prec)

@@ -39,12 +39,12 @@ def _free_port():
         return so.getsockname()[1]
 
 
-def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed):
+def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed, schedule="sr"):
     port = _free_port()
     procs = []
     for r in range(world):
         cmd = [sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), str(world), str(port),
-               str(tmp_path), prec, str(maxit), repr(tol), str(nx), str(ny), str(nz), str(seed)]
+               str(tmp_path), prec, str(maxit), repr(tol), str(nx), str(ny), str(nz), str(seed), schedule]
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
     for p in procs:
@@ -60,14 +60,17 @@ def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed):
     return [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
 
 
-def _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, world):
+def _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, world, schedule="sr"):
     torch = torch_cuda()
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=seed)
     b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=seed), prec)
     coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
     st = sten.stencil_create(nx, ny, nz, coeffs, nslabs=world)
-    sten.set_schedule(st, sten.SCHED_SR)
-    sten.set_sr_exchange(st, sten.XCHG_FUSED)
+    if schedule == "sr":
+        sten.set_schedule(st, sten.SCHED_SR)
+        sten.set_sr_exchange(st, sten.XCHG_FUSED)
+    else:  # the serial classic exchange: slab sums in slab order, like the peer-memory reduction
+        sten.set_option(st, sten.OPT_CLASSIC_OVERLAP, 0)
     bt = to_gpu_vec(b, prec)
     xt = torch.empty_like(bt)
     it, hist, status = sten.bicgstab_solve(st, PREC[prec], bt, None, tol, maxit, xt)
@@ -98,9 +101,33 @@ def test_two_processes_fused_sr_equals_loopback_slabs(sten, tmp_path, prec, maxi
         assert s_ref == sten.CONVERGED and it_ref < maxit and h_ref[-1] <= tol
 
 
+@pytest.mark.parametrize("prec,maxit,tol,mesh", [
+    ("fp32", 10, 0.0, (40, 33, 24)),
+    ("mixed", 10, 0.0, (40, 33, 24)),
+    ("mixed", 40, 1e-3, (37, 29, 16)),
+])
+def test_two_processes_classic_equals_loopback_slabs(sten, tmp_path, prec, maxit, tol, mesh):
+    """The headline schedule (Alg. 1 as printed) across two PROCESSES: the halo
+    planes of r, p, v (before H1) and v' (before H2) pushed into the neighbour process's buffers
+    through CUDA IPC, the three per-iteration all-reduces through the peer-memory inboxes, host
+    lockstep; bitwise equal to the single-process solve on two loopback slabs with the serial
+    exchange (the same kernels, slab sums added in the same order)."""
+    nx, ny, nz = mesh
+    seed = 6
+    res = _run_ranks(tmp_path, 2, prec, maxit, tol, nx, ny, nz, seed, "classic")
+    x_ref, it_ref, h_ref, s_ref = _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, 2, "classic")
+    for r in res:
+        assert int(r["it"]) == it_ref and int(r["status"]) == s_ref
+        assert np.array_equal(r["hist"], h_ref)
+    x = np.concatenate([r["x"] for r in res], axis=0)
+    assert np.array_equal(x, x_ref)
+    if tol > 0:
+        assert s_ref == sten.CONVERGED and it_ref < maxit and h_ref[-1] <= tol
+
+
 def test_p2p_only_comm_refuses_what_needs_nccl(sten):
-    """A peer-memory-only communicator: create checks the slab convention; everything but the
-    imported fused SR solve is refused (no silent fallback)."""
+    """A peer-memory-only communicator: create checks the slab convention; a solve before
+    sten_p2p_import and the apply are refused (no silent fallback)."""
     torch = torch_cuda()
     nx, ny, nz = 16, 8, 8
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz // 2, seed=3)
@@ -113,7 +140,7 @@ def test_p2p_only_comm_refuses_what_needs_nccl(sten):
     b = torch.zeros(nz // 2, ny, nx, dtype=torch.float32, device="cuda")
     x = torch.empty_like(b)
     with pytest.raises(sten.StenError, match="p2p-only"):
-        sten.bicgstab_solve(st, sten.FP32, b, None, 0.0, 3, x)  # SR not imported / classic
+        sten.bicgstab_solve(st, sten.FP32, b, None, 0.0, 3, x)  # nothing imported
     with pytest.raises(sten.StenError, match="p2p-only"):
         sten.stencil_apply(st, sten.FP32, b, x)
     st.close()
