@@ -29,5 +29,6 @@ from .gen import (  # noqa: F401
     rhs_uniform,
     field_at,
     problem_fields_2d,
+    field_at_2d,
     rhs_uniform_2d,
 )

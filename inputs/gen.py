@@ -159,10 +159,13 @@ def rhs_uniform(nx: int, ny: int, nz: int, z0: int = 0, seed: int = SEED_DEFAULT
     return uniform(seed, stream, idx, -1.0, 1.0)
 
 
-def problem_fields_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, delta: float = 0.1):
-    """(diag, offs[8]) of the 2D 9-point stand-in, arrays (ny, nx), offs in the o2d.c order
-    (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1)."""
-    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+def field_at_2d(nx: int, i, j, seed: int = SEED_DEFAULT, delta: float = 0.1):
+    """(diag, offs[8]) of the 2D 9-point stand-in at global points (i, j) of an nx-wide mesh
+    (integer arrays), offs in the o2d.c order (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1)
+    (0,+1) (+1,+1).  fp64."""
+    i = np.asarray(i, dtype=np.int64)
+    j = np.asarray(j, dtype=np.int64)
+    i, j = np.broadcast_arrays(i, j)
     idx = (i + nx * j).astype(np.uint64)
     kd = uniform(seed, STREAM_K, idx, 0.5, 2.0)
     ux = uniform(seed, STREAM_UX, idx, -1.0, 1.0)
@@ -175,6 +178,13 @@ def problem_fields_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, delta: float =
         s = s + a[d]
     diag = (1.0 + float(delta)) * s
     return np.ascontiguousarray(diag), [np.ascontiguousarray(-ad) for ad in a]
+
+
+def problem_fields_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, delta: float = 0.1):
+    """(diag, offs[8]) of the 2D 9-point stand-in, arrays (ny, nx), offs in the o2d.c order
+    (-1,-1) (0,-1) (+1,-1) (-1,0) (+1,0) (-1,+1) (0,+1) (+1,+1)."""
+    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    return field_at_2d(nx, i, j, seed=seed, delta=delta)
 
 
 def rhs_uniform_2d(nx: int, ny: int, seed: int = SEED_DEFAULT, stream: int = STREAM_B) -> np.ndarray:
