@@ -210,3 +210,38 @@ def test_phase_timing(sten):
     ms, n = sten.stencil2d_phase_ms(st)
     assert n == it == 6 and np.all(ms > 0) and st.last_solve_ms > 0
     st.close()
+
+
+@pytest.mark.parametrize("prec,mesh", [("mixed", (1300, 1000)), ("fp32", (700, 1000))])
+def test_persistent_tile_walk_vs_oracle_and_deterministic(sten, prec, mesh):
+    """Meshes of 352 tiles: every persistent k_bicg9 CTA walks 2-3 tiles (TMA ring slots reused,
+    mbarrier phases flipped, the formed box ping-ponged) - the history against the oracle for 10
+    iterations and bitwise equal across repeated solves (no race between the tile walks)."""
+    torch = torch_cuda()
+    nx, ny = mesh
+    diag, offs, b64 = _problem(nx, ny, seed=9)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    P = sten.MIXED if prec == "mixed" else sten.FP32
+    if prec == "mixed":
+        c16 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "mixed")
+        bw = orc.f16_from_double(b64)
+        ref = orc.bicgstab2d(c16, bw, tol=0.0, maxit=10, prec="mixed")
+        rtol = 5e-2
+    else:
+        c32 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "fp32")
+        bw = b64.astype(np.float32)
+        ref = orc.bicgstab2d([a.astype(np.float64) for a in c32], bw.astype(np.float64), tol=0.0, maxit=10)
+        rtol = 1e-4
+    bt = _dev(torch, bw, prec)
+    outs = []
+    for _ in range(3):
+        x = torch.empty_like(bt)
+        it, hist, status = sten.bicgstab2d_solve(st, P, bt, None, 0.0, 10, x)
+        outs.append((x.clone(), hist))
+    assert it == 10
+    assert np.all(np.abs(hist - ref["hist"]) <= rtol * ref["hist"]), (hist, ref["hist"])
+    for xk, hk in outs[1:]:
+        assert torch.equal(xk.view(torch.int16 if prec == "mixed" else torch.int32),
+                           outs[0][0].view(torch.int16 if prec == "mixed" else torch.int32))
+        assert np.array_equal(hk, outs[0][1])
+    st.close()
