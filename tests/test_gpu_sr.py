@@ -353,7 +353,8 @@ def test_p2p_export_and_import_guards(sten):
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, seed=3)
     st = gpu_stencil(diag, offs, nslabs=2)
     rec = sten.p2p_export(st, PREC["mixed"])
-    assert len(rec) == 46 * 64  # 2 boundary slabs x (2 sets x 5 vectors + 12 coefficient arrays) + inbox sums, flags
+    # 2 boundary slabs x (2 sets x 5 SR vectors + 12 coefficient arrays + 5 classic halo'd vectors) + inbox sums, flags
+    assert len(rec) == 56 * 64
     with pytest.raises(sten.StenError):  # needs a multi-rank communicator
         sten.p2p_import(st, PREC["mixed"], [rec, rec])
     st.close()
