@@ -408,8 +408,10 @@ def run_sten(args):
     if args.dots == "half":
         sten.set_dot_precision(st, sten.DOTS_HALF)
     if world > 1 and os.environ.get("STEN_P2P", "0") == "1":
-        sten.set_schedule(st, sten.SCHED_SR)
-        sten.p2p_setup(st, prec)  # fused peer-memory halos + all-reduce across ranks (opt-in, SR)
+        # fused compute + collective over peer memory across ranks (opt-in): the SR sweep's and the
+        # classic phase kernels' own halo stores and inbox deposits (STEN_OPT_CLASSIC_FUSED)
+        sten.set_option(st, sten.OPT_CLASSIC_FUSED, 1)
+        sten.p2p_setup(st, prec)
     b = icuda.uniform_device(NX, NY, nzl, z0=z0, seed=1, stream=0).to(tdt)
     x = torch.empty_like(b)
     npts_local = NX * NY * nzl

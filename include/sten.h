@@ -264,13 +264,28 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
  *                              on a side stream with the two boundary planes,
  *                              concurrent with the interior planes, 0 or 1
  *                              (default 1).  Changes only the order in which
- *                              the phase sums are added. */
+ *                              the phase sums are added.
+ *   STEN_OPT_CLASSIC_FUSED     classic schedule, decomposed: 1 = fused compute +
+ *                              collective over peer memory - H1 stores its
+ *                              boundary planes of p', v' and H3 those of r
+ *                              straight into the z-neighbours' halo planes (the
+ *                              neighbour slab's buffers, or the neighbour rank's
+ *                              through CUDA IPC after sten_p2p_import), and the
+ *                              last CTA of every phase kernel writes the slab's
+ *                              sums into every participant's inbox (one-shot
+ *                              all-reduce, a 1-thread kernel per phase reads it);
+ *                              no separate exchange.  Loopback slabs and 1-rank
+ *                              communicators use it directly; across ranks it
+ *                              needs sten_p2p_import (else the handle keeps the
+ *                              NCCL exchange).  Bitwise equal to the serial
+ *                              exchange (same sum order).  0 or 1 (default 0). */
 #define STEN_OPT_TMA_L2_PROMOTION 1
 #define STEN_OPT_EW_CTAS_PER_SM 2
 #define STEN_OPT_COEF_PREFETCH 3
 #define STEN_OPT_SR_L2_PREFETCH 4
 #define STEN_OPT_SR_LIGHT_LAST 5
 #define STEN_OPT_CLASSIC_OVERLAP 6
+#define STEN_OPT_CLASSIC_FUSED 7
 int sten_set_option(sten_stencil *st, int option, int value);
 int sten_get_option(sten_stencil *st, int option, int *value);
 

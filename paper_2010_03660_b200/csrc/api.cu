@@ -217,6 +217,7 @@ struct sten_stencil {
   int ew_bps = 64;              // element-wise kernels: CTAs per SM (STEN_OPT_EW_CTAS_PER_SM)
   bool sr_light = true;         // SR, one slab: last sweep without its SpMVs (STEN_OPT_SR_LIGHT_LAST)
   bool cls_overlap = true;      // classic, decomposed: halo exchange overlapped with the interior (STEN_OPT_CLASSIC_OVERLAP)
+  bool cls_fuse = false;        // classic, decomposed: fused peer-memory exchange + all-reduce (STEN_OPT_CLASSIC_FUSED)
   void (*barrier_fn)(void *) = nullptr;  // host lockstep of several ranks on ONE GPU (sten_set_host_barrier)
   void *barrier_ctx = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -392,13 +393,45 @@ static Reduce make_red(sten_stencil *st, int slab) {
   return r;
 }
 
+// fused exchange: the slab's sums go straight into every participant's inbox (slot = global slab)
+static void fused_red(sten_stencil *st, int slab, Reduce &r) {
+  const int ns = (int)st->slabs.size();
+  r.slab_out = nullptr;
+  r.p2p_slot = (st->comm ? st->comm->rank : 0) * ns + slab;
+  r.p2p_nslots = st->p2p_slots;
+  r.p2p_seq = st->p2p_seq;
+  r.p2p[0] = P2PBox{st->p2p_sums, st->p2p_flags};
+  r.p2p_n = 1;
+  for (const P2PBox &b : st->p2p_remote) r.p2p[r.p2p_n++] = b;
+}
+// classic buffers in the IPC record order (r, p0, p1, v0, v1)
+static void *cls_buf(PrecBufs &b, int i) {
+  void *q[5] = {b.r, b.p[0], b.p[1], b.v[0], b.v[1]};
+  return q[i];
+}
+// the lower / upper z-neighbour's halo plane of classic buffer i for slab `slab` (null: none)
+static void *cls_peer(sten_stencil *st, int prec, int slab, int i, bool lower) {
+  const size_t pb = (size_t)st->plane * esize(prec);
+  const int ns = (int)st->slabs.size();
+  Slab &sl = st->slabs[slab];
+  if (lower) {
+    if (slab > 0) {
+      Slab &n = st->slabs[slab - 1];
+      return (char *)cls_buf(n.pb[prec], i) + (size_t)(n.nz + 1) * pb;
+    }
+    return st->cls_lo[prec][i] ? (char *)st->cls_lo[prec][i] + (size_t)(sl.nz + 1) * pb : nullptr;  // equal slabs
+  }
+  if (slab + 1 < ns) return cls_buf(st->slabs[slab + 1].pb[prec], i);
+  return st->cls_hi[prec][i];
+}
+
 // part: CLS_ALL planes [0, nz) of the slab; CLS_INTERIOR [1, nz-1) (no halo plane
 // read), CLS_BOTTOM plane 0, CLS_TOP plane nz-1 (decomposed, overlapped exchange:
 // each part deposits its sums in slot 3*slab + part - 1, CLS_INTERIOR with the
 // second reduction scratch because it runs concurrently with the other two)
 enum { CLS_ALL = 0, CLS_INTERIOR = 1, CLS_BOTTOM = 2, CLS_TOP = 3 };
 static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int parity, cudaStream_t s,
-                          int part = CLS_ALL, bool capture = false) {
+                          int part = CLS_ALL, bool capture = false, bool fused = false) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   const Tiling &t = st->tiling[prec];
@@ -445,7 +478,25 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
       a.red.counter = st->counter2;
     }
   }
+  if (fused) {
+    fused_red(st, slab, a.red);
+    if (mode == MODE_H1) {  // p', v' boundary planes into the neighbours' halo planes
+      const int nxt = parity ^ 1;
+      for (int i = 0; i < 2; ++i) {
+        const int idx = i == 0 ? 3 + nxt : 1 + nxt;  // out0 = v[nxt], out1 = p[nxt]
+        a.peer_lo[i] = cls_peer(st, prec, slab, idx, true);
+        a.peer_hi[i] = cls_peer(st, prec, slab, idx, false);
+      }
+    }
+  }
   if (a.zhi <= a.zlo) return STEN_OK;
+  if (fused && mode == MODE_H1 && (a.peer_lo[0] || a.peer_hi[0])) {
+    if (t.rows) return set_err(STEN_EUNSUPPORTED, "the fused classic exchange needs the tile kernels");
+    if (prec == STEN_FP32) KLAUNCH(stencil_launch_fused<float>(a, t.by, t.stages, t.cstages, s));
+    else KLAUNCH(stencil_launch_fused<__half>(a, t.by, t.stages, t.cstages, s));
+    st->launches++;
+    return STEN_OK;
+  }
   if (t.rows) {
     if (prec == STEN_FP32) KLAUNCH(rows_launch<float>(mode, a, t.by, t.stages, s));
     else KLAUNCH(rows_launch<__half>(mode, a, t.by, t.stages, s));
@@ -468,7 +519,7 @@ static int ew_grid(sten_stencil *st, long long nvec) {
   return (int)(g < 1 ? 1 : g);
 }
 
-static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStream_t s) {
+static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStream_t s, bool fused = false) {
   Slab &sl = st->slabs[slab];
   PrecBufs &b = sl.pb[prec];
   const int e = esize(prec), vec = prec == STEN_FP32 ? 4 : 8;
@@ -488,6 +539,13 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
   a.pitch = st->pitch;
   a.nvec = (long long)st->plane * sl.nz / vec;  // linear over whole planes (padding holds zeros)
   a.red = make_red(st, slab);
+  if (fused) {  // r's boundary planes into the neighbours' halo planes, sums into the inboxes
+    fused_red(st, slab, a.red);
+    a.peer_lo_r = cls_peer(st, prec, slab, 0, true);
+    a.peer_hi_r = cls_peer(st, prec, slab, 0, false);
+    a.plane_elems = st->plane;
+    a.nzp = sl.nz;
+  }
   if (ew_grid(st, a.nvec) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
   if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(a, ew_grid(st, a.nvec), 256, s));
@@ -644,16 +702,45 @@ static int overlapped_phase(sten_stencil *st, int prec, int mode, int parity, cu
   return finalize ? reduce_scalars(st, mode == MODE_H1 ? PH_H1 : PH_H2, s, 3 * ns) : STEN_OK;
 }
 
+// classic fused exchange (STEN_OPT_CLASSIC_FUSED): loopback slabs, 1-rank communicators, or
+// ranks whose classic buffers were imported (sten_p2p_import)
+static bool cls_fused(const sten_stencil *st) {
+  if (!decomposed(st) || !st->cls_fuse) return false;
+  return !st->comm || st->comm->nranks == 1 || st->p2p_ranks;
+}
 static bool cls_overlapped(const sten_stencil *st) {
-  if (!decomposed(st) || !st->cls_overlap || p2p_only(st)) return false;
+  if (!decomposed(st) || !st->cls_overlap || p2p_only(st) || cls_fused(st)) return false;
   for (const Slab &sl : st->slabs)
     if (sl.nz < 3) return false;
   return true;
 }
 
+// peer all-reduce wait of a fused phase: (host lockstep: all ranks' deposits first) the 1-thread kernel
+static int fused_fin(sten_stencil *st, int phase, cudaStream_t s) {
+  RC_TRY(host_barrier(st, s));
+  KLAUNCH(p2p_fin_launch(phase, P2PBox{st->p2p_sums, st->p2p_flags}, st->p2p_slots, st->p2p_seq, st->st, s));
+  st->launches++;
+  return STEN_OK;
+}
+
 static int enqueue_iteration(sten_stencil *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
   const int ns = (int)st->slabs.size();
   const bool dec = decomposed(st);
+  if (cls_fused(st)) {  // compute + collective in the phase kernels themselves (STEN_OPT_CLASSIC_FUSED)
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H1, k, parity, s, CLS_ALL, false, true));
+    RC_TRY(fused_fin(st, PH_H1, s));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_stencil(st, prec, MODE_H2, k, parity, s, CLS_ALL, false, true));
+    RC_TRY(fused_fin(st, PH_H2, s));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[4], s, cudaEventRecordExternal));
+    for (int k = 0; k < ns; ++k) RC_TRY(launch_h3(st, prec, k, parity, s, true));
+    RC_TRY(fused_fin(st, PH_H3, s));
+    if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[5], s, cudaEventRecordExternal));
+    return STEN_OK;
+  }
   if (cls_overlapped(st)) {
     if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
     RC_TRY(overlapped_phase(st, prec, MODE_H1, parity, s, [&](cudaStream_t ss) {
@@ -1613,6 +1700,10 @@ int sten_set_option(sten_stencil *st, int option, int value) {
       if (value != 0 && value != 1) return set_err(STEN_EINVAL, "classic overlap must be 0 or 1 (got %d)", value);
       st->cls_overlap = value != 0;
       break;
+    case STEN_OPT_CLASSIC_FUSED:
+      if (value != 0 && value != 1) return set_err(STEN_EINVAL, "classic fused exchange must be 0 or 1 (got %d)", value);
+      st->cls_fuse = value != 0;
+      break;
     default:
       return set_err(STEN_EINVAL, "unknown option %d", option);
   }
@@ -1629,6 +1720,7 @@ int sten_get_option(sten_stencil *st, int option, int *value) {
     case STEN_OPT_SR_L2_PREFETCH: *value = st->sr_l2pf; break;
     case STEN_OPT_SR_LIGHT_LAST: *value = st->sr_light ? 1 : 0; break;
     case STEN_OPT_CLASSIC_OVERLAP: *value = st->cls_overlap ? 1 : 0; break;
+    case STEN_OPT_CLASSIC_FUSED: *value = st->cls_fuse ? 1 : 0; break;
     default: return set_err(STEN_EINVAL, "unknown option %d", option);
   }
   return STEN_OK;
@@ -1744,6 +1836,14 @@ static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, 
   // fused SR: every sweep writes the halos of the set the next one reads; the
   // first sweep's (set 0, from the init) are exchanged here once
   if (sr && sr_fused(st)) RC_TRY(sr_exchange(st, prec, 0, s));
+  // fused classic: H1 and H3 write the halos the next phases read; the first H1's (r, p0, v0 from
+  // the init) are exchanged here once
+  if (!sr && cls_fused(st)) {
+    RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.r; }, s));
+    RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.p[0]; }, s));
+    RC_TRY(exchange(st, prec, [](PrecBufs &b) { return b.v[0]; }, s));
+    RC_TRY(host_barrier(st, s));
+  }
   // iterations: CUDA graphs of `chunk` iterations (even, so the ping-pong
   // parity of p/v is the same at every replay)
   const int nsteps = sr ? maxit + 1 : maxit;  // SR: sweep i computes x_i, r_i (i = 0..maxit)

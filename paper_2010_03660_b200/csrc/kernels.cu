@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
   const typename P::S mws = P::neg(ws);
   T *__restrict__ XO = reinterpret_cast<T *>(a.xo);
   T *__restrict__ RO = reinterpret_cast<T *>(a.ro);
+  T *const PLR = reinterpret_cast<T *>(a.peer_lo_r), *const PHR = reinterpret_cast<T *>(a.peer_hi_r);
+  const long long top0 = (long long)(a.nzp - 1) * a.plane_elems;  // first element of the last plane
   float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
   for (long long i = 0; i < nmine; ++i) {
     const int slot = (int)(i % NS);
@@ -183,6 +185,8 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
         xn.st(XO + o);
         rn.st(RO + o);
       }
+      if (PLR && o < a.plane_elems) rn.st(PLR + o);  // fused exchange: r's boundary planes (H1's halos)
+      if (PHR && o >= top0) rn.st(PHR + (o - top0));
       rs.dot4(rn, d0);
       rn.dot4(rn, d1);
     }

@@ -87,6 +87,9 @@ struct alignas(64) StencilArgs {
   int zc, tiles_x, tiles_y;
   int zlo, zhi;           // planes [zlo, zhi) of the slab, in chunks of zc from zlo
   int pf;                 // L2 prefetch distance of the coefficient tiles (planes; 0 = off)
+  // fused exchange (H1): interior plane 0 of out0 / out1 also to peer_lo[i] (the lower z-neighbour's
+  // top halo plane), plane nz-1 to peer_hi[i] (the upper one's bottom halo plane); null: none
+  void *peer_lo[2], *peer_hi[2];
   Reduce red;
 };
 
@@ -99,6 +102,11 @@ struct EwArgs {           // element-wise kernels (H3, INIT)
   long long rows;                      // ny * nz rows of the interior range
   int vpr;                             // vectors per row that hold points (ceil(nx/VEC))
   int pitch;                           // row pitch in elements (multiple of 64: 128-B rows)
+  // fused exchange (H3): r's interior plane 0 also to peer_lo_r (the lower z-neighbour's top halo
+  // plane), plane nz-1 to peer_hi_r; plane_elems = elements per plane, nzp = interior planes
+  void *peer_lo_r, *peer_hi_r;
+  long long plane_elems;
+  int nzp;
   Reduce red;
 };
 
@@ -521,6 +529,8 @@ template <typename T> constexpr int tile_bx() { return sizeof(T) == 2 ? 128 : 64
 bool stencil_config_ok(int by, int stages, int cstages = 0);
 template <typename T>
 int stencil_launch(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
+// the fused-exchange instance (MODE_H1 with peer stores), default geometry only
+template <typename T> int stencil_launch_fused(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
 template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
 template <typename T> int stencil_threads(int by);
 // row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits

@@ -99,7 +99,7 @@ template <> struct Shift<__half> {
 
 }  // namespace
 
-template <typename T, int MODE, int BY, int S, int SC>
+template <typename T, int MODE, int BY, int S, int SC, bool FU = false>
 __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __grid_constant__ StencilArgs a) {
   using P = Pack<T>;
   using G = Geo<T, MODE, BY>;
@@ -265,6 +265,16 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
       const long long o = (long long)(k + 1) * a.g.plane + gofs;
       acc.st(reinterpret_cast<T *>(a.out0) + o);
       if (MODE != MODE_APPLY) uc.st(reinterpret_cast<T *>(a.out1) + o);
+      if (FU) {  // fused exchange: the slab's boundary planes into the z-neighbours' halo planes
+        if (k == 0 && a.peer_lo[0]) {
+          acc.st(reinterpret_cast<T *>(a.peer_lo[0]) + gofs);
+          uc.st(reinterpret_cast<T *>(a.peer_lo[1]) + gofs);
+        }
+        if (k == a.g.nz - 1 && a.peer_hi[0]) {
+          acc.st(reinterpret_cast<T *>(a.peer_hi[0]) + gofs);
+          uc.st(reinterpret_cast<T *>(a.peer_hi[1]) + gofs);
+        }
+      }
     }
     if (MODE == MODE_H1) {
       rh.dot4(acc, dacc[0]);  // (rhat, v')
@@ -506,19 +516,19 @@ template int rows_threads<__half>(int, int);
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int MODE, int BY, int S, int SC = 0>
+template <typename T, int MODE, int BY, int S, int SC = 0, bool FU = false>
 int launch_one(const StencilArgs &a, cudaStream_t s) {
   using G = Geo<T, MODE, BY>;
   constexpr size_t smem = smem_bytes_c<T, MODE, BY, S, SC>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC, FU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc);
-  k_stencil<T, MODE, BY, S, SC><<<grid, G::NT, smem, s>>>(a);
+  k_stencil<T, MODE, BY, S, SC, FU><<<grid, G::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 template <typename T, int MODE>
@@ -573,6 +583,13 @@ int stencil_threads(int by) {
   return (tile_bx<T>() / Pack<T>::VEC) * by;
 }
 
+template <typename T>
+int stencil_launch_fused(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
+  if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE_H1, 16, 2, 2, true>(a, s);
+  return (int)cudaErrorNotSupported;
+}
+template int stencil_launch_fused<float>(const StencilArgs &, int, int, int, cudaStream_t);
+template int stencil_launch_fused<__half>(const StencilArgs &, int, int, int, cudaStream_t);
 template int stencil_launch<float>(int, const StencilArgs &, int, int, int, cudaStream_t);
 template int stencil_launch<__half>(int, const StencilArgs &, int, int, int, cudaStream_t);
 template size_t stencil_smem_bytes<float>(int, int, int);

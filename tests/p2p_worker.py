@@ -1,7 +1,7 @@
 """One rank of the cross-process peer-memory solve (tests/test_gpu_multiproc.py).
 
 Run as `python tests/p2p_worker.py RANK WORLD PORT OUTDIR PREC MAXIT TOL NX NY NZ SEED [SCHEDULE]`
-(SCHEDULE sr, the default, or classic).
+(SCHEDULE sr, the default, classic, or classic_fused).
 Every rank uses cuda:0 (the one GPU here), owns planes [r nz/R, (r+1) nz/R) of the
 mesh, builds its handle on a peer-memory-only communicator (sten_comm_create with
 no NCCL id), exchanges the CUDA IPC records over gloo, and solves in host lockstep
@@ -44,6 +44,8 @@ def main():
     dist.barrier()  # every rank's coefficients exist before anyone imports (sten.h)
     P = sten.FP32 if prec == "fp32" else sten.MIXED
     sten.set_schedule(st, sten.SCHED_SR if schedule == "sr" else sten.SCHED_CLASSIC)
+    if schedule == "classic_fused":  # halos and sums stored by the phase kernels themselves
+        sten.set_option(st, sten.OPT_CLASSIC_FUSED, 1)
     sten.p2p_setup(st, P)  # export, all_gather over gloo, import
     sten.set_host_barrier(st, lambda: dist.barrier())
     bt = to_gpu_vec(b, prec)

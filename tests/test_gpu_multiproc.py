@@ -101,20 +101,24 @@ def test_two_processes_fused_sr_equals_loopback_slabs(sten, tmp_path, prec, maxi
         assert s_ref == sten.CONVERGED and it_ref < maxit and h_ref[-1] <= tol
 
 
+@pytest.mark.parametrize("schedule", ["classic", "classic_fused"])
 @pytest.mark.parametrize("prec,maxit,tol,mesh", [
     ("fp32", 10, 0.0, (40, 33, 24)),
     ("mixed", 10, 0.0, (40, 33, 24)),
     ("mixed", 40, 1e-3, (37, 29, 16)),
 ])
-def test_two_processes_classic_equals_loopback_slabs(sten, tmp_path, prec, maxit, tol, mesh):
-    """The headline schedule (Alg. 1 as printed) across two PROCESSES: the halo
-    planes of r, p, v (before H1) and v' (before H2) pushed into the neighbour process's buffers
-    through CUDA IPC, the three per-iteration all-reduces through the peer-memory inboxes, host
-    lockstep; bitwise equal to the single-process solve on two loopback slabs with the serial
-    exchange (the same kernels, slab sums added in the same order)."""
+def test_two_processes_classic_equals_loopback_slabs(sten, tmp_path, prec, maxit, tol, mesh, schedule):
+    """The headline schedule (Alg. 1 as printed) across two PROCESSES, host
+    lockstep.  classic: the halo planes of r, p, v (before H1) and v' (before H2) pushed into the
+    neighbour process's buffers through CUDA IPC, the three per-iteration all-reduces through the
+    peer-memory inboxes.  classic_fused: no exchange at all - H1 stores its boundary planes of p', v'
+    and H3 those of r straight into the neighbour process's halo planes, and the last CTA of every
+    phase kernel deposits the slab's sums in both processes' inboxes (fused compute + collective).
+    Both bitwise equal to the single-process solve on two loopback slabs with the serial exchange
+    (the same kernels, slab sums added in the same order)."""
     nx, ny, nz = mesh
     seed = 6
-    res = _run_ranks(tmp_path, 2, prec, maxit, tol, nx, ny, nz, seed, "classic")
+    res = _run_ranks(tmp_path, 2, prec, maxit, tol, nx, ny, nz, seed, schedule)
     x_ref, it_ref, h_ref, s_ref = _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, 2, "classic")
     for r in res:
         assert int(r["it"]) == it_ref and int(r["status"]) == s_ref
@@ -123,6 +127,34 @@ def test_two_processes_classic_equals_loopback_slabs(sten, tmp_path, prec, maxit
     assert np.array_equal(x, x_ref)
     if tol > 0:
         assert s_ref == sten.CONVERGED and it_ref < maxit and h_ref[-1] <= tol
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("nslabs,mesh", [(2, (40, 33, 24)), (3, (29, 17, 15)), (4, (64, 20, 16))])
+def test_classic_fused_loopback_equals_serial(sten, prec, nslabs, mesh):
+    """STEN_OPT_CLASSIC_FUSED on loopback slabs (one process): the phase kernels store the boundary
+    planes into the neighbour slabs' halo planes and deposit their sums in the inbox slots; bitwise
+    equal to the serial exchange (and the fused state survives repeated solves)."""
+    torch = torch_cuda()
+    nx, ny, nz = mesh
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=8)
+    b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=8), prec)
+    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+    st = sten.stencil_create(nx, ny, nz, coeffs, nslabs=nslabs)
+    bt = to_gpu_vec(b, prec)
+    res = {}
+    for mode in ("serial", "fused", "fused2"):
+        sten.set_option(st, sten.OPT_CLASSIC_OVERLAP, 0)
+        sten.set_option(st, sten.OPT_CLASSIC_FUSED, 0 if mode == "serial" else 1)
+        xt = torch.empty_like(bt)
+        it, hist, status = sten.bicgstab_solve(st, PREC[prec], bt, None, 0.0, 12, xt)
+        res[mode] = (from_gpu_vec(xt, prec), it, hist, status)
+    for mode in ("fused", "fused2"):
+        assert res[mode][1] == res["serial"][1] and res[mode][3] == res["serial"][3]
+        assert np.array_equal(res[mode][2], res["serial"][2])
+        assert np.array_equal(res[mode][0], res["serial"][0])
+    assert sten.get_option(st, sten.OPT_CLASSIC_FUSED) == 1
+    st.close()
 
 
 def test_p2p_only_comm_refuses_what_needs_nccl(sten):
