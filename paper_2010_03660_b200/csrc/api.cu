@@ -467,7 +467,7 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
   a.pf = st->coef_pf;
   a.tiles_x = t.rows ? 1 : (st->nx + t.bx - 1) / t.bx;
   a.tiles_y = (st->ny + t.by - 1) / t.by;
-  if ((long long)a.tiles_x * a.tiles_y * ((sl.nz + a.zc - 1) / a.zc) > st->partials_cap)
+  if (a.zhi > a.zlo && (long long)a.tiles_x * a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: stencil grid exceeds the partial-sum buffer");
   a.red = make_red(st, slab);
   if (capture) a.red.slab_out = st->slab_sums + slab * kMaxDots;  // raw sums (sten_classic_phase)

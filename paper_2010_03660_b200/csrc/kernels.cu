@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
   T *__restrict__ RO = reinterpret_cast<T *>(a.ro);
   T *const PLR = reinterpret_cast<T *>(a.peer_lo_r), *const PHR = reinterpret_cast<T *>(a.peer_hi_r);
   const long long top0 = (long long)(a.nzp - 1) * a.plane_elems;  // first element of the last plane
+  bool peer = false;
   float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
   for (long long i = 0; i < nmine; ++i) {
     const int slot = (int)(i % NS);
@@ -185,8 +186,14 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
         xn.st(XO + o);
         rn.st(RO + o);
       }
-      if (PLR && o < a.plane_elems) rn.st(PLR + o);  // fused exchange: r's boundary planes (H1's halos)
-      if (PHR && o >= top0) rn.st(PHR + (o - top0));
+      if (PLR && o < a.plane_elems) {  // fused exchange: r's boundary planes (H1's halos)
+        rn.st(PLR + o);
+        peer = true;
+      }
+      if (PHR && o >= top0) {
+        rn.st(PHR + (o - top0));
+        peer = true;
+      }
       rs.dot4(rn, d0);
       rn.dot4(rn, d1);
     }
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
     if (tid == 0 && i + NS < nmine) issue(i + NS);
   }
   float d[2] = {sum4(d0), sum4(d1)};
-  grid_reduce_finalize<2, PH_H3>(d, a.red, scratch);
+  grid_reduce_finalize<2, PH_H3>(d, a.red, scratch, __syncthreads_or(peer) != 0);
 }
 
 template <typename T>

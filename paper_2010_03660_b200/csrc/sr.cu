@@ -715,7 +715,8 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
 #pragma unroll
     for (int d = 0; d < 12; ++d) dacc[d] = sr_lanesum(hacc[d]);
   }
-  grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch);
+  // only the chunks holding a slab's two boundary planes on either side stored to peers
+  grid_reduce_finalize<12, PH_SR>(dacc, a.red, scratch, FU && (z0 < 2 || z1 > nzl - 2));
 }
 
 // The last sweep of a solve (i = maxit, DevState::light): phase A of k_sr -- the

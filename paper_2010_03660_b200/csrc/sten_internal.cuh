@@ -472,11 +472,14 @@ __device__ __forceinline__ bool sr_idle(const DevState *st) {
 // Grid-level end of a reduction: every CTA deposits its block sum; the last
 // CTA to arrive sums the deposits in CTA order (deterministic) and either
 // finalizes the phase or writes the slab's sums for the cross-slab step.
+// peer_stores: this CTA may have stored into peer memory (halo planes of a z-neighbour); only then
+// does it need the system-scope fence before its ticket (the last CTA fences before its flags anyway)
 template <int ND, int PH>
-__device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduce &red, float *scratch) {
+__device__ __forceinline__ void grid_reduce_finalize(float (&v)[ND], const Reduce &red, float *scratch,
+                                                     bool peer_stores = true) {
   block_sum<ND>(v, scratch);
   __shared__ int am_last;
-  if (red.p2p_n > 0) {
+  if (red.p2p_n > 0 && peer_stores) {
     __syncthreads();
     __threadfence_system();  // this CTA's stores to peer memory (halo planes) are visible before its ticket
   }

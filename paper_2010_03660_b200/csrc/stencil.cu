@@ -290,8 +290,9 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
     float v[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) v[d] = sum4(dacc[d]);
-    if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(v, a.red, scratch);
-    else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch);
+    const bool peer = FU && (z0 == 0 || z1 == a.g.nz);  // only boundary-plane chunks stored to peers
+    if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(v, a.red, scratch, peer);
+    else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch, peer);
   }
 }
 

@@ -218,3 +218,33 @@ def test_fullsize_fp32_reaches_1e6(full_problem):
     del dg
     true_res = float(torch.linalg.vector_norm((bh - ax).double()) / torch.linalg.vector_norm(bh.double()))
     assert true_res <= 1e-5, true_res
+
+
+def test_fullsize_loopback_slab_exchange_modes():
+    """Config 3 on 2 loopback z-slabs (the multi-GPU decomposition's code on one GPU, at the size
+    the scaling runs use): every classic exchange mode runs - serial, overlapped (side stream),
+    fused (peer stores + inbox deposits) - and serial and fused agree bitwise, overlapped to the
+    rounding of its different sum order; the SR fused sweep runs too."""
+    torch = torch_cuda()
+    import inputs.cuda as icuda
+    import paper_2010_03660_b200 as sten
+    diag, offs = icuda.fields_device(inputs.KIND_CD, NX, NY, NZ, seed=1, delta=0.1)
+    st = sten.stencil_create(NX, NY, NZ, [diag] + offs, nslabs=2)
+    del diag, offs
+    b = icuda.uniform_device(NX, NY, NZ, seed=1, stream=0).half()
+    res = {}
+    for mode, ov, fu in (("serial", 0, 0), ("overlap", 1, 0), ("fused", 0, 1)):
+        sten.set_option(st, sten.OPT_CLASSIC_OVERLAP, ov)
+        sten.set_option(st, sten.OPT_CLASSIC_FUSED, fu)
+        x = torch.empty_like(b)
+        it, hist, status = sten.bicgstab_solve(st, sten.MIXED, b, None, 0.0, 4, x)
+        res[mode] = (x, hist)
+        assert it == 4 and np.all(np.isfinite(hist))
+    assert torch.equal(res["serial"][0].view(torch.int16), res["fused"][0].view(torch.int16))
+    assert np.array_equal(res["serial"][1], res["fused"][1])
+    assert np.allclose(res["overlap"][1], res["serial"][1], rtol=1e-3)
+    sten.set_schedule(st, sten.SCHED_SR)
+    x = torch.empty_like(b)
+    it, hist, status = sten.bicgstab_solve(st, sten.MIXED, b, None, 0.0, 4, x)
+    assert it == 4 and np.allclose(hist, res["serial"][1], rtol=5e-2)
+    st.close()
