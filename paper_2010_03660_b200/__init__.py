@@ -189,7 +189,8 @@ def comm_unique_id() -> bytes:
 
 def comm_create(unique_id: bytes | None, nranks: int, rank: int, cuda_device: int | None = None) -> Comm:
     """sten_comm_create on `cuda_device` (default: the current device).  unique_id None gives a
-    peer-memory-only communicator (no NCCL; SR schedule with the fused exchange only)."""
+    peer-memory-only communicator (no NCCL; after p2p_setup, halos and all-reduces through CUDA IPC:
+    the fused SR sweep, or the classic schedule in host lockstep)."""
     if cuda_device is None:
         import torch
         cuda_device = torch.cuda.current_device()
