@@ -224,7 +224,7 @@ def test_fullsize_loopback_slab_exchange_modes():
     """Config 3 on 2 loopback z-slabs (the multi-GPU decomposition's code on one GPU, at the size
     the scaling runs use): every classic exchange mode runs - serial, overlapped (side stream),
     fused (peer stores + inbox deposits) - and serial and fused agree bitwise, overlapped to the
-    rounding of its different sum order; the SR fused sweep runs too."""
+    rounding of its different sum order; the SR sweep in its three exchange modes too."""
     torch = torch_cuda()
     import inputs.cuda as icuda
     import paper_2010_03660_b200 as sten
@@ -244,7 +244,12 @@ def test_fullsize_loopback_slab_exchange_modes():
     assert np.array_equal(res["serial"][1], res["fused"][1])
     assert np.allclose(res["overlap"][1], res["serial"][1], rtol=1e-3)
     sten.set_schedule(st, sten.SCHED_SR)
-    x = torch.empty_like(b)
-    it, hist, status = sten.bicgstab_solve(st, sten.MIXED, b, None, 0.0, 4, x)
-    assert it == 4 and np.allclose(hist, res["serial"][1], rtol=5e-2)
+    srh = {}
+    for xm in (sten.XCHG_SERIAL, sten.XCHG_OVERLAP, sten.XCHG_FUSED):  # the SR exchange modes too
+        sten.set_sr_exchange(st, xm)
+        x = torch.empty_like(b)
+        it, hist, status = sten.bicgstab_solve(st, sten.MIXED, b, None, 0.0, 4, x)
+        assert it == 4 and np.allclose(hist, res["serial"][1], rtol=5e-2)
+        srh[xm] = hist
+    assert np.array_equal(srh[sten.XCHG_SERIAL], srh[sten.XCHG_FUSED])
     st.close()
