@@ -63,6 +63,9 @@ def _declare(L):
     for f in ("o2d64_bicgstab", "o2d16_bicgstab"):
         getattr(L, f).argtypes = [_I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
         getattr(L, f).restype = _I
+    for f in ("o2d64_bicgstab_tiles", "o2d16_bicgstab_tiles"):
+        getattr(L, f).argtypes = [_I, _I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
+        getattr(L, f).restype = _I
     L.o64_dot.restype = _D
     L.o64_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P]
     L.o64_bicgstab.restype = _I
@@ -468,10 +471,11 @@ def apply9_tiles(c, v, tiles, prec="fp64"):
     return u
 
 
-def bicgstab2d(c, b, x0=None, tol=0.0, maxit=50, prec="fp64"):
+def bicgstab2d(c, b, x0=None, tol=0.0, maxit=50, prec="fp64", tiles=(1, 1)):
     """BiCGStab on the 2D 9-point operator: prec fp64 (float64 arrays) or mixed
-    (binary16 bit patterns, the GPU's operation order).  Returns dict(x, hist, iters, status,
-    event_it, alpha, omega) like bicgstab64."""
+    (binary16 bit patterns, the GPU's operation order); tiles = (TX, TY) > (1, 1): the paper's tiled
+    output-halo SpMV (R24).  Returns dict(x, hist, iters, status, event_it, alpha, omega) like
+    bicgstab64."""
     dt = np.float64 if prec == "fp64" else np.uint16
     c = [_c(a, dt) for a in c]
     b = _c(b, dt)
@@ -482,9 +486,9 @@ def bicgstab2d(c, b, x0=None, tol=0.0, maxit=50, prec="fp64"):
     al, om = np.zeros(maxit + 1, ad), np.zeros(maxit + 1, ad)
     st, ev = ctypes.c_int(0), ctypes.c_int(0)
     x0c = None if x0 is None else _c(x0, dt)
-    fn = lib().o2d64_bicgstab if prec == "fp64" else lib().o2d16_bicgstab
-    it = fn(nx, ny, _arr8(c), _ptr(b), None if x0c is None else _ptr(x0c), float(tol), int(maxit), _ptr(x),
-            _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
+    fn = lib().o2d64_bicgstab_tiles if prec == "fp64" else lib().o2d16_bicgstab_tiles
+    it = fn(nx, ny, int(tiles[0]), int(tiles[1]), _arr8(c), _ptr(b), None if x0c is None else _ptr(x0c), float(tol),
+            int(maxit), _ptr(x), _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
     return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value, alpha=al[: it + 1],
                 omega=om[: it + 1])
 

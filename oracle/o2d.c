@@ -249,7 +249,9 @@ void o16_apply9_tiles(int nx, int ny, int TX, int TY, const uint16_t *const c[8]
  * each core holds "a matrix, halo, and vector (as well as all
  * terms needed for BiCG)" - Alg. 1 with the 9-point
  * operator in place of the 7-point one, under the readings of the 3D oracle
- * (R1-R8, R12, R23).  fp64 (o2d64_bicgstab) and the binary16 mixed
+ * (R1-R8, R12, R23).  The SpMV is the gather, or with TX x TY > 1 the paper's
+ * tiled output-halo form (apply9_tiles, R24: "all terms needed for BiCG" live with each tile's
+ * columns of A).  fp64 (o2d64_bicgstab) and the binary16 mixed
  * mode in the GPU's operation order (o2d16_bicgstab: FMA-chain SpMV
  * o16_apply9, fp16 FMAC AXPYs with fp32 scalars rounded to fp16, dots of exact
  * fp16 products summed in fp32 over each row, then over rows). */
@@ -267,9 +269,19 @@ static double dot64_9(int64_t n, const double *a, const double *b) {
   return s;
 }
 
-int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, const double *x0, double tol,
-                   int maxit, double *x, double *hist, double *alpha_out, double *omega_out, int *status,
-                   int *event_it) {
+/* the SpMV of the solve: the gather (one tile) or the paper's tiled output-halo form (R24) */
+static void spmv64_9(int nx, int ny, int TX, int TY, const double *const c[8], const double *v, double *u) {
+  if (TX * TY == 1) o64_apply9(nx, ny, c, v, u);
+  else o64_apply9_tiles(nx, ny, TX, TY, c, v, u);
+}
+static void spmv16_9(int nx, int ny, int TX, int TY, const uint16_t *const c[8], const uint16_t *v, uint16_t *u) {
+  if (TX * TY == 1) o16_apply9(nx, ny, c, v, u);
+  else o16_apply9_tiles(nx, ny, TX, TY, c, v, u);
+}
+
+int o2d64_bicgstab_tiles(int nx, int ny, int TX, int TY, const double *const c[8], const double *b, const double *x0,
+                         double tol, int maxit, double *x, double *hist, double *alpha_out, double *omega_out,
+                         int *status, int *event_it) {
   const int64_t n = (int64_t)nx * ny;
   const size_t bytes = sizeof(double) * (size_t)(n > 0 ? n : 1);
   double *r = (double *)malloc(bytes), *rh = (double *)malloc(bytes);
@@ -278,7 +290,7 @@ int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, co
   int ev = -1, ev_it = 0, it = 0;
   if (x0) { /* R1 */
     memcpy(x, x0, bytes);
-    o64_apply9(nx, ny, c, x, t);
+    spmv64_9(nx, ny, TX, TY, c, x, t);
     for (int64_t P = 0; P < n; ++P) r[P] = b[P] - t[P];
   } else { /* l.174 */
     for (int64_t P = 0; P < n; ++P) {
@@ -307,7 +319,7 @@ int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, co
   for (int i = 1; i <= maxit; ++i) {
     if (i > 1)
       for (int64_t P = 0; P < n; ++P) p[P] = r[P] + beta * (p[P] - omega * v[P]); /* l.184 */
-    o64_apply9(nx, ny, c, p, v);                                                  /* l.176 */
+    spmv64_9(nx, ny, TX, TY, c, p, v);                                                  /* l.176 */
     const double sigma = dot64_9(n, rh, v);                                       /* l.177 */
     alpha = rho / sigma;
     if (sigma == 0.0 || !isfinite(alpha)) {
@@ -318,7 +330,7 @@ int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, co
       }
     }
     for (int64_t P = 0; P < n; ++P) s[P] = r[P] - alpha * v[P]; /* l.178 */
-    o64_apply9(nx, ny, c, s, t);                                /* l.179 */
+    spmv64_9(nx, ny, TX, TY, c, s, t);                                /* l.179 */
     const double ts = dot64_9(n, t, s), tt = dot64_9(n, t, t);
     if (tt == 0.0) {
       omega = 0.0; /* R8 */
@@ -373,9 +385,9 @@ static float dot16_9(int nx, int ny, const uint16_t *a, const uint16_t *b) {
   return total;
 }
 
-int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b, const uint16_t *x0, double tol,
-                   int maxit, uint16_t *x, double *hist, float *alpha_out, float *omega_out, int *status,
-                   int *event_it) {
+int o2d16_bicgstab_tiles(int nx, int ny, int TX, int TY, const uint16_t *const c[8], const uint16_t *b,
+                         const uint16_t *x0, double tol, int maxit, uint16_t *x, double *hist, float *alpha_out,
+                         float *omega_out, int *status, int *event_it) {
   const int64_t n = (int64_t)nx * ny;
   const size_t bytes = sizeof(uint16_t) * (size_t)(n > 0 ? n : 1);
   uint16_t *r = (uint16_t *)malloc(bytes), *rh = (uint16_t *)malloc(bytes);
@@ -384,7 +396,7 @@ int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b
   int ev = -1, ev_it = 0, it = 0;
   if (x0) { /* R1 */
     memcpy(x, x0, bytes);
-    o16_apply9(nx, ny, c, x, t);
+    spmv16_9(nx, ny, TX, TY, c, x, t);
     for (int64_t P = 0; P < n; ++P) r[P] = o16_add(b[P], neg16_9(t[P]));
   } else {
     for (int64_t P = 0; P < n; ++P) {
@@ -415,7 +427,7 @@ int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b
       const uint16_t bh = rn16f_9(beta), mwh = neg16_9(rn16f_9(omega));
       for (int64_t P = 0; P < n; ++P) p[P] = o16_fma(bh, o16_fma(mwh, v[P], p[P]), r[P]);
     }
-    o16_apply9(nx, ny, c, p, v);                   /* l.176 */
+    spmv16_9(nx, ny, TX, TY, c, p, v);                   /* l.176 */
     const float sigma = dot16_9(nx, ny, rh, v);    /* l.177 */
     alpha = rho / sigma;
     if (sigma == 0.0f || !usable16_9(alpha)) {
@@ -427,7 +439,7 @@ int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b
     }
     const uint16_t ah = rn16f_9(alpha);
     for (int64_t P = 0; P < n; ++P) s[P] = o16_fma(neg16_9(ah), v[P], r[P]); /* l.178 */
-    o16_apply9(nx, ny, c, s, t);                                             /* l.179 */
+    spmv16_9(nx, ny, TX, TY, c, s, t);                                             /* l.179 */
     const float ts = dot16_9(nx, ny, t, s), tt = dot16_9(nx, ny, t, t);
     if (tt == 0.0f) {
       omega = 0.0f;
@@ -464,4 +476,16 @@ int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b
 done:
   free(r); free(rh); free(p); free(v); free(s); free(t);
   return it;
+}
+
+/* the solves on the gather SpMV (one tile) */
+int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, const double *x0, double tol,
+                   int maxit, double *x, double *hist, double *alpha_out, double *omega_out, int *status,
+                   int *event_it) {
+  return o2d64_bicgstab_tiles(nx, ny, 1, 1, c, b, x0, tol, maxit, x, hist, alpha_out, omega_out, status, event_it);
+}
+int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b, const uint16_t *x0, double tol,
+                   int maxit, uint16_t *x, double *hist, float *alpha_out, float *omega_out, int *status,
+                   int *event_it) {
+  return o2d16_bicgstab_tiles(nx, ny, 1, 1, c, b, x0, tol, maxit, x, hist, alpha_out, omega_out, status, event_it);
 }

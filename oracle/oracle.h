@@ -184,6 +184,13 @@ int o2d64_bicgstab(int nx, int ny, const double *const c[8], const double *b, co
                    int maxit, double *x, double *hist, double *alpha, double *omega, int *status, int *event_it);
 int o2d16_bicgstab(int nx, int ny, const uint16_t *const c[8], const uint16_t *b, const uint16_t *x0, double tol,
                    int maxit, uint16_t *x, double *hist, float *alpha, float *omega, int *status, int *event_it);
+/* the same with the paper's tiled output-halo SpMV (apply9_tiles, R24) on TX x TY tiles */
+int o2d64_bicgstab_tiles(int nx, int ny, int TX, int TY, const double *const c[8], const double *b, const double *x0,
+                         double tol, int maxit, double *x, double *hist, double *alpha_out, double *omega_out,
+                         int *status, int *event_it);
+int o2d16_bicgstab_tiles(int nx, int ny, int TX, int TY, const uint16_t *const c[8], const uint16_t *b,
+                         const uint16_t *x0, double tol, int maxit, uint16_t *x, double *hist, float *alpha_out,
+                         float *omega_out, int *status, int *event_it);
 
 /* informational */
 int oracle_num_threads(void);

@@ -267,3 +267,72 @@ def test_bicgstab2d_mixed_tracks_fp64_then_plateaus(orc):
     bb = orc.f16_to_double(b16)
     true = np.linalg.norm(bb - orc.apply9_64([orc.f16_to_double(a) for a in c16], x)) / np.linalg.norm(bb)
     assert 1e-4 < true < 1e-2
+
+
+# ------------------------------- 2D BiCGStab on the tiled SpMV (R24, R25) --
+@pytest.mark.parametrize("tiles", [(2, 1), (3, 2), (5, 4), (12, 9)])
+def test_bicgstab2d_tiled_matches_lapack_and_gather(orc, tiles):
+    """The solve on the paper's tiled output-halo SpMV is the same algorithm on the same operator:
+    it converges to LAPACK's solution, and its fp64 iterates follow the gather solve's to rounding
+    (the tiling only re-associates the nine products at tile edges)."""
+    nx, ny = 12, 9
+    diag, offs, c = _cd2d(orc, nx, ny, 0.1)
+    import inputs
+    b = inputs.rhs_uniform_2d(nx, ny, seed=2) / diag
+    x_ref = np.linalg.solve(dense9(diag, offs), b.ravel())
+    r = orc.bicgstab2d(c, b, tol=1e-13, maxit=500, tiles=tiles)
+    assert r["status"] == orc.ORC_CONVERGED
+    assert np.linalg.norm(r["x"].ravel() - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+    g = orc.bicgstab2d(c, b, tol=0.0, maxit=8)
+    t = orc.bicgstab2d(c, b, tol=0.0, maxit=8, tiles=tiles)
+    assert np.allclose(t["hist"], g["hist"], rtol=1e-12, atol=0)
+    assert np.allclose(t["alpha"], g["alpha"], rtol=1e-12) and np.allclose(t["omega"], g["omega"], rtol=1e-12)
+
+
+def test_bicgstab2d_tiled_one_tile_is_the_gather(orc):
+    """tiles (1, 1) is the gather solve bitwise, in both precisions (one tile: no output halo)."""
+    nx, ny = 20, 13
+    diag, offs, c = _cd2d(orc, nx, ny, 0.1, seed=5)
+    import inputs
+    b = inputs.rhs_uniform_2d(nx, ny, seed=5) / diag
+    a = orc.bicgstab2d(c, b, tol=0.0, maxit=10)
+    t = orc.bicgstab2d(c, b, tol=0.0, maxit=10, tiles=(1, 1))
+    assert np.array_equal(a["x"], t["x"]) and np.array_equal(a["hist"], t["hist"])
+    c16, b16 = orc.quantize_coeffs(c, "mixed"), orc.f16_from_double(b)
+    a = orc.bicgstab2d(c16, b16, tol=0.0, maxit=10, prec="mixed")
+    t = orc.bicgstab2d(c16, b16, tol=0.0, maxit=10, prec="mixed", tiles=(1, 1))
+    assert np.array_equal(a["x"], t["x"]) and np.array_equal(a["hist"], t["hist"])
+
+
+def test_bicgstab2d_tiled_mixed_first_step_composes_pinned_primitives(orc):
+    """One binary16 iteration on tiles, recomputed here from the pinned pieces (the tiled fp16
+    SpMV apply9_tiles, exact binary16 FMA, fp32 dots of exact products): x_1 and hist[1] equal."""
+    nx, ny, tiles = 17, 11, (3, 2)
+    diag, offs, c = _cd2d(orc, nx, ny, 0.1, seed=6)
+    import inputs
+    c16 = orc.quantize_coeffs(c, "mixed")
+    b16 = orc.f16_from_double(inputs.rhs_uniform_2d(nx, ny, seed=6))
+    r = orc.bicgstab2d(c16, b16, tol=0.0, maxit=1, prec="mixed", tiles=tiles)
+    f = lambda a: orc.f16_to_double(a).astype(np.float32)
+
+    def dot(a, b):  # per row in fp32, then over rows (o2d.c dot16_9)
+        tot = np.float32(0)
+        for j in range(ny):
+            row = np.float32(0)
+            for i in range(nx):
+                row = np.float32(row + f(a)[j, i] * f(b)[j, i])
+            tot = np.float32(tot + row)
+        return tot
+    rho = dot(b16, b16)
+    v = orc.apply9_tiles(c16, b16, tiles, "mixed")
+    alpha = np.float32(rho / dot(b16, v))
+    ah = orc.f16_from_double(np.float64(alpha))
+    neg = lambda h: np.uint16(h ^ 0x8000)
+    s = orc.fma16_array(np.full_like(v, neg(ah)), v, b16)
+    t = orc.apply9_tiles(c16, s, tiles, "mixed")
+    omega = np.float32(dot(t, s) / dot(t, t))
+    wh = orc.f16_from_double(np.float64(omega))
+    x = orc.fma16_array(np.full_like(s, wh), s, orc.fma16_array(np.full_like(b16, ah), b16, np.zeros_like(b16)))
+    assert np.array_equal(r["x"], x)
+    rr = orc.fma16_array(np.full_like(t, neg(wh)), t, s)
+    assert r["hist"][1] == np.sqrt(np.float64(dot(rr, rr))) / np.sqrt(np.float64(rho))
