@@ -504,8 +504,10 @@ int stencil2d_set_tiles(sten_stencil2d *st, int tiles_x, int tiles_y);
  * b / A_P (R3) and the residuals refer to the scaled system.  Schedule: H1 =
  * p' = r + beta (p - omega v), v' = A p', (rhat, v'); H2 = s = r - alpha v',
  * t = A s, (t, s), (t, t); H3 = x, r updates, (rhat, r), (r, r) - fused
- * kernels, 33 passes per iteration.  Tiles must be 1 x 1
- * (STEN_EUNSUPPORTED otherwise).  Synchronises cuda_stream. */
+ * kernels, 33 passes per iteration.  With tiles > 1 x 1 (stencil2d_set_tiles)
+ * the SpMV is the paper's tiled output-halo form and the phases run unfused
+ * around it (update, tiled SpMV, dots; oracle/o2d.c o2d16_bicgstab_tiles).
+ * Synchronises cuda_stream. */
 int bicgstab2d_solve(sten_stencil2d *st, int precision, const void *b, const void *x0, double tol, int maxit,
                      void *x_out, int *iters, double *res_hist, int *status, void *cuda_stream);
 /* per-phase device timing of the 2D solve (CUDA events around H1, H2, H3 of

@@ -2582,6 +2582,7 @@ struct Bufs2 {
   bool ready = false;
   void *x = nullptr, *r = nullptr, *rh = nullptr, *p[2] = {}, *v[2] = {}, *s = nullptr, *t = nullptr, *bw = nullptr;
   CUtensorMap m_x, m_r, m_p[2], m_v[2];
+  CUtensorMap m_pa[2], m_sa;  // the tiled solve's SpMV inputs p', s (k_apply9 boxes)
 };
 struct sten_stencil2d {
   int nx = 0, ny = 0, pitch = 0;
@@ -2751,7 +2752,9 @@ static int ensure2d(sten_stencil2d *st, int prec) {
     for (int k = 0; k < 2; ++k) {
       RC_TRY(map2d(st, &b.m_p[k], b.p[k], prec, kBicg9BY));
       RC_TRY(map2d(st, &b.m_v[k], b.v[k], prec, kBicg9BY));
+      RC_TRY(map2d(st, &b.m_pa[k], b.p[k], prec, kApply9BY));
     }
+    RC_TRY(map2d(st, &b.m_sa, b.s, prec, kApply9BY));
     b.ready = true;
   }
   if (!st->st) {
@@ -2798,7 +2801,66 @@ static int ew2d(sten_stencil2d *st, int prec, EwArgs &a) {
 }
 
 // one iteration of Alg. 1: H1, H2 (k_bicg9), H3 (k_h3); p / v ping-pong on `parity`
+// the tiled solve's iteration (TX x TY > 1): unfused updates and dots around the tiled SpMV
+static int enqueue_iter2d_tiled(sten_stencil2d *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
+  Bufs2 &b = st->sb[prec];
+  const int cur = parity, nxt = parity ^ 1;
+  const long long nvec = (long long)st->pitch * st->ny / (prec == STEN_FP32 ? 4 : 8);
+  const int g = ew_grid2d(st, nvec);
+  Upd9Args u;
+  Dot9Args d;
+  memset(&u, 0, sizeof u);
+  memset(&d, 0, sizeof d);
+  u.nvec = d.nvec = nvec;
+  u.st = st->st;
+  d.red = red2d(st);
+  // H1: p' = r + beta (p - omega v), v' = A p' (tiled), (rhat, v')
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[0], s, cudaEventRecordExternal));
+  u.r = b.r;
+  u.p = b.p[cur];
+  u.v = b.v[cur];
+  u.out = b.p[nxt];
+  if (prec == STEN_FP32) KLAUNCH(upd9_launch<float>(MODE_H1, u, g, s));
+  else KLAUNCH(upd9_launch<__half>(MODE_H1, u, g, s));
+  RC_TRY(launch_apply2d(st, prec, b.m_pa[nxt], b.p[nxt], b.v[nxt], s));
+  d.a0 = b.rh;
+  d.b0 = b.v[nxt];
+  if (prec == STEN_FP32) KLAUNCH(dot9_launch<float>(MODE_H1, d, g, s));
+  else KLAUNCH(dot9_launch<__half>(MODE_H1, d, g, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[1], s, cudaEventRecordExternal));
+  // H2: s = r - alpha v', t = A s (tiled), (t, s), (t, t)
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[2], s, cudaEventRecordExternal));
+  u.p = nullptr;
+  u.v = b.v[nxt];
+  u.out = b.s;
+  if (prec == STEN_FP32) KLAUNCH(upd9_launch<float>(MODE_H2, u, g, s));
+  else KLAUNCH(upd9_launch<__half>(MODE_H2, u, g, s));
+  RC_TRY(launch_apply2d(st, prec, b.m_sa, b.s, b.t, s));
+  d.a0 = b.t;
+  d.b0 = b.s;
+  if (prec == STEN_FP32) KLAUNCH(dot9_launch<float>(MODE_H2, d, g, s));
+  else KLAUNCH(dot9_launch<__half>(MODE_H2, d, g, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[3], s, cudaEventRecordExternal));
+  // H3: the element-wise x, r updates and (rhat, r), (r, r)
+  EwArgs e;
+  memset(&e, 0, sizeof e);
+  e.x = b.x;
+  e.p = b.p[nxt];
+  e.s = b.s;
+  e.t = b.t;
+  e.rhat = b.rh;
+  e.xo = b.x;
+  e.ro = b.r;
+  const int g3 = ew2d(st, prec, e);
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[4], s, cudaEventRecordExternal));
+  if (prec == STEN_FP32) KLAUNCH(h3_launch<float>(e, g3, 256, s));
+  else KLAUNCH(h3_launch<__half>(e, g3, 256, s));
+  if (evs) CUDA_TRY(cudaEventRecordWithFlags(evs[5], s, cudaEventRecordExternal));
+  return STEN_OK;
+}
+
 static int enqueue_iter2d(sten_stencil2d *st, int prec, int parity, cudaStream_t s, cudaEvent_t *evs) {
+  if (st->TX * st->TY > 1) return enqueue_iter2d_tiled(st, prec, parity, s, evs);
   Bufs2 &b = st->sb[prec];
   const int cur = parity, nxt = parity ^ 1;
   Bicg9Args a;
@@ -2850,7 +2912,7 @@ static int enqueue_iter2d(sten_stencil2d *st, int prec, int parity, cudaStream_t
 }
 
 static int graph2d(sten_stencil2d *st, int prec, int chunk, GraphRec **out) {
-  GraphKey key{prec, chunk, st->timing ? 1 : 0, 0};
+  GraphKey key{prec, chunk, st->timing ? 1 : 0, st->TX * st->TY > 1 ? 1 : 0};
   auto it = st->graphs.find(key);
   if (it != st->graphs.end()) {
     *out = &it->second;
@@ -2936,6 +2998,7 @@ int stencil2d_set_tiles(sten_stencil2d *st, int tiles_x, int tiles_y) {
     return set_err(STEN_EINVAL, "tiles %d x %d: need 1 <= tiles_x <= nx = %d, 1 <= tiles_y <= ny = %d", tiles_x, tiles_y,
                    st->nx, st->ny);
   CUDA_TRY(cudaDeviceSynchronize());
+  drop_graphs2d(st);  // captured solves hold the old tiling's pointers
   cudaFree(st->xm);
   cudaFree(st->ym);
   cudaFree(st->ring);
@@ -3018,9 +3081,6 @@ int bicgstab2d_solve(sten_stencil2d *st, int prec, const void *b, const void *x0
   if (!st || !b || !x_out || !iters || !res_hist || !status) return set_err(STEN_EINVAL, "NULL argument");
   if (prec != STEN_FP32 && prec != STEN_MIXED) return set_err(STEN_EINVAL, "bad precision %d", prec);
   if (!(tol >= 0.0) || !std::isfinite(tol) || maxit < 0) return set_err(STEN_EINVAL, "tol=%g maxit=%d invalid", tol, maxit);
-  if (st->TX * st->TY > 1)
-    return set_err(STEN_EUNSUPPORTED, "bicgstab2d_solve runs the fused gather kernels: set 1 x 1 tiles "
-                                      "(the tiled output-halo SpMV is stencil2d_apply's)");
   cudaStream_t s = (cudaStream_t)cuda_stream;
   RC_TRY(ensure2d(st, prec));
   Bufs2 &bf = st->sb[prec];
@@ -3052,19 +3112,7 @@ int bicgstab2d_solve(sten_stencil2d *st, int prec, const void *b, const void *x0
   // S1 (Alg. 1 l.174, R1, R3): r0 = b_hat - A x0, rhat = p0 = r0, v0 = 0
   if (x0) {
     RC_TRY(copy2d_in(st, prec, bf.x, x0, s));
-    {  // A x0 by the gather SpMV into t
-      Apply9Args a;
-      memset(&a, 0, sizeof a);
-      a.tm_v = bf.m_x;
-      for (int d = 0; d < 8; ++d) a.c[d] = prec == STEN_FP32 ? (const void *)st->c32[d] : (const void *)st->c16[d];
-      a.u = bf.t;
-      a.nx = st->nx;
-      a.ny = st->ny;
-      a.pitch = st->pitch;
-      a.tiles_x = (st->nx + bx2d(prec) - 1) / bx2d(prec);
-      if (prec == STEN_FP32) KLAUNCH(apply9_launch<float>(a, s));
-      else KLAUNCH(apply9_launch<__half>(a, s));
-    }
+    RC_TRY(launch_apply2d(st, prec, bf.m_x, bf.x, bf.t, s));  // A x0 into t (the handle's SpMV form)
   } else {
     CUDA_TRY(cudaMemsetAsync(bf.x, 0, (size_t)st->pitch * st->ny * esize(prec), s));
   }

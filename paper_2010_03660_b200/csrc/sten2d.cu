@@ -436,6 +436,74 @@ __global__ void __launch_bounds__((Tile2<T>::BX / Pack<T>::VEC) * BY, STEN_BICG9
   else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch);
 }
 
+// ------------------------------- BiCGStab on the tiled SpMV (R24, R25) --
+// With the paper's tiled output-halo SpMV the phases cannot fuse the update into the product (the
+// rounds complete a tile's edge values after its kernel), so a tiled solve runs them unfused over
+// the pitched plane (linear 16-B vectors; padding holds zeros): H1 = k_upd9<P> (p' = r + beta (p -
+// omega v), l.184), the tiled apply of p', k_dot9 (rhat, v'); H2 = k_upd9<S> (s = r - alpha v',
+// l.178), the tiled apply of s, k_dot9 (t, s), (t, t); H3 = k_h3_bulk.  Same roundings as the
+// fused kernels (oracle/o2d.c o2d16_bicgstab_tiles).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_upd9(const __grid_constant__ Upd9Args a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  if (st_idle(a.st)) return;
+  typename P::S s1{}, s2{};
+  if (MODE == MODE_H1) {
+    s1 = P::scalar(a.st->beta);
+    s2 = P::neg(P::scalar(a.st->omega));
+  } else {
+    s1 = P::neg(P::scalar(a.st->alpha));
+  }
+  const T *R = reinterpret_cast<const T *>(a.r), *V = reinterpret_cast<const T *>(a.v);
+  const T *Pp = reinterpret_cast<const T *>(a.p);
+  T *O = reinterpret_cast<T *>(a.out);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.nvec; i += (long long)gridDim.x * blockDim.x) {
+    const long long o = i * VEC;
+    P f = P::ldg(R + o);
+    if (MODE == MODE_H1) f = P::fmas(s1, P::fmas(s2, P::ldg(V + o), P::ldg(Pp + o)), f);
+    else f = P::fmas(s1, P::ldg(V + o), f);
+    f.st(O + o);
+  }
+}
+
+template <typename T, int ND, int PH>
+__global__ void __launch_bounds__(256) k_dot9(const __grid_constant__ Dot9Args a) {
+  using P = Pack<T>;
+  constexpr int VEC = P::VEC;
+  __shared__ float scratch[32 * kMaxDots];
+  if (st_idle(a.red.st)) return;
+  const T *A0 = reinterpret_cast<const T *>(a.a0), *B0 = reinterpret_cast<const T *>(a.b0);
+  float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.nvec; i += (long long)gridDim.x * blockDim.x) {
+    const long long o = i * VEC;
+    const P x = P::ldg(A0 + o), y = P::ldg(B0 + o);
+    x.dot4(y, d0);              // H1: (rhat, v')   H2: (t, s)
+    if (ND == 2) x.dot4(x, d1);  // H2: (t, t)
+  }
+  float v[ND];
+  v[0] = sum4(d0);
+  if (ND == 2) v[ND - 1] = sum4(d1);
+  grid_reduce_finalize<ND, PH>(v, a.red, scratch);
+}
+
+template <typename T>
+int upd9_launch(int mode, const Upd9Args &a, int grid, cudaStream_t s) {
+  if (mode == MODE_H1) k_upd9<T, MODE_H1><<<grid, 256, 0, s>>>(a);
+  else k_upd9<T, MODE_H2><<<grid, 256, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+template <typename T>
+int dot9_launch(int mode, const Dot9Args &a, int grid, cudaStream_t s) {
+  if (mode == MODE_H1) k_dot9<T, 1, PH_H1><<<grid, 256, 0, s>>>(a);
+  else k_dot9<T, 2, PH_H2><<<grid, 256, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+template int upd9_launch<float>(int, const Upd9Args &, int, cudaStream_t);
+template int upd9_launch<__half>(int, const Upd9Args &, int, cudaStream_t);
+template int dot9_launch<float>(int, const Dot9Args &, int, cudaStream_t);
+template int dot9_launch<__half>(int, const Dot9Args &, int, cudaStream_t);
+
 // Jacobi scaling of the 9-point operator (R3/R5 in 2D): c_d = A_d / A_P in
 // fp64, couplings leaving the mesh dropped, rounded RN to fp32 and fp16;
 // padding columns hold zero couplings

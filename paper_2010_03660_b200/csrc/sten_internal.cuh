@@ -644,6 +644,21 @@ struct alignas(64) Bicg9Args {
   int nx, ny, pitch, tiles_x, tiles_y;
   Reduce red;
 };
+// the tiled solve's unfused pieces: H1 p' = r + beta (p - omega v), H2 s = r - alpha v (k_upd9)
+// and the phase's inner products (k_dot9: H1 (a0, b0); H2 (a0, b0), (a0, a0))
+struct Upd9Args {
+  const void *r, *p, *v;
+  void *out;
+  long long nvec;
+  DevState *st;
+};
+struct Dot9Args {
+  const void *a0, *b0;
+  long long nvec;
+  Reduce red;
+};
+template <typename T> int upd9_launch(int mode, const Upd9Args &a, int grid, cudaStream_t s);
+template <typename T> int dot9_launch(int mode, const Dot9Args &a, int grid, cudaStream_t s);
 struct Coef9In { const void *off[8]; };
 struct Coef9Out { float *c32[8]; __half *c16[8]; };
 template <typename T> int apply9_launch(const Apply9Args &a, cudaStream_t s);

@@ -180,16 +180,12 @@ def test_degenerate(sten):
     st.close()
 
 
-def test_tiled_handle_refused_and_invalid(sten):
+def test_invalid_arguments(sten):
     nx, ny = 20, 10
     offs = [np.full((ny, nx), -0.1) for _ in range(8)]
     st = sten.stencil2d_create(nx, ny, [None] + offs)
     b = np.ones((ny, nx), np.float32)
     x = np.zeros_like(b)
-    sten.stencil2d_set_tiles(st, 2, 2)
-    with pytest.raises(sten.StenError):
-        sten.bicgstab2d_solve(st, sten.FP32, b, None, 0.0, 5, x)
-    sten.stencil2d_set_tiles(st, 1, 1)
     for tol, maxit in [(-1.0, 5), (float("nan"), 5), (0.0, -1)]:
         with pytest.raises(sten.StenError):
             sten.bicgstab2d_solve(st, sten.FP32, b, None, tol, maxit, x)
@@ -244,4 +240,65 @@ def test_persistent_tile_walk_vs_oracle_and_deterministic(sten, prec, mesh):
         assert torch.equal(xk.view(torch.int16 if prec == "mixed" else torch.int32),
                            outs[0][0].view(torch.int16 if prec == "mixed" else torch.int32))
         assert np.array_equal(hk, outs[0][1])
+    st.close()
+
+
+@pytest.mark.parametrize("tiles,mesh", [((3, 2), (64, 48)), ((7, 5), (130, 33)), ((40, 30), (200, 150)),
+                                        ((1, 6), (300, 100))])
+def test_tiled_solve_vs_oracle(sten, tiles, mesh):
+    """BiCGStab on the paper's tiled output-halo SpMV: every element-wise op and
+    the tiled SpMV are the oracle's bit for bit, only the fp32 dot order differs - the mixed history
+    within 5e-2 of o2d16_bicgstab_tiles for 20 iterations, x_1 within one fp16 ulp; the fp32 solve
+    within 1e-4 of o2d64_bicgstab_tiles after 30 iterations; back on 1 x 1 tiles the fused solve."""
+    torch = torch_cuda()
+    nx, ny = mesh
+    diag, offs, b64 = _problem(nx, ny, seed=nx + 3 * ny)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    sten.stencil2d_set_tiles(st, *tiles)
+    c64 = orc.jacobi_scale9(diag, offs)
+    c16 = orc.quantize_coeffs(c64, "mixed")
+    b16 = orc.f16_from_double(b64)
+    x = torch.empty((ny, nx), dtype=torch.float16, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 0.0, 20, x)
+    ref = orc.bicgstab2d(c16, b16, tol=0.0, maxit=20, prec="mixed", tiles=tiles)
+    assert it == ref["iters"] == 20
+    assert np.all(np.abs(hist - ref["hist"]) <= 5e-2 * ref["hist"]), (hist, ref["hist"])
+    sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 0.0, 1, x)
+    r1 = orc.bicgstab2d(c16, b16, tol=0.0, maxit=1, prec="mixed", tiles=tiles)
+    xg, xo = orc.f16_to_double(x.cpu().numpy().view(np.uint16)), orc.f16_to_double(r1["x"])
+    assert np.all(np.abs(xg - xo) <= np.spacing(np.abs(xo).astype(np.float16)).astype(np.float64) + 1e-12)
+    c32 = orc.quantize_coeffs(c64, "fp32")
+    b32 = b64.astype(np.float32)
+    x32 = torch.empty((ny, nx), dtype=torch.float32, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.FP32, _dev(torch, b32, "fp32"), None, 0.0, 30, x32)
+    ref = orc.bicgstab2d([a.astype(np.float64) for a in c32], b32.astype(np.float64), tol=0.0, maxit=30,
+                         tiles=tiles)
+    xr = ref["x"]
+    assert np.linalg.norm(x32.cpu().numpy().astype(np.float64) - xr) <= 1e-4 * np.linalg.norm(xr)
+    sten.stencil2d_set_tiles(st, 1, 1)  # the fused gather solve again on the same handle
+    it, hist1, status = sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 0.0, 5, x)
+    ref1 = orc.bicgstab2d(c16, b16, tol=0.0, maxit=5, prec="mixed")
+    assert np.all(np.abs(hist1 - ref1["hist"]) <= 5e-2 * ref1["hist"])
+    st.close()
+
+
+def test_tiled_solve_targets_and_x0(sten):
+    """The tiled solve reaches the mixed target with x0 = 0 and from an x0 (r0 = b - A x0 by the
+    tiled SpMV), like the fused one."""
+    torch = torch_cuda()
+    nx, ny = 160, 120
+    diag, offs, b64 = _problem(nx, ny, seed=21)
+    st = sten.stencil2d_create(nx, ny, [None] + [torch.from_numpy(o / diag).cuda() for o in offs])
+    sten.stencil2d_set_tiles(st, 8, 6)
+    b16 = orc.f16_from_double(b64)
+    x = torch.empty((ny, nx), dtype=torch.float16, device="cuda")
+    it, hist, status = sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), None, 1e-3, 100, x)
+    assert status == sten.CONVERGED and hist[-1] <= 1e-3
+    c16 = orc.quantize_coeffs(orc.jacobi_scale9(diag, offs), "mixed")
+    x0 = orc.f16_from_double(0.5 * orc.f16_to_double(x.cpu().numpy().view(np.uint16)))
+    x2 = torch.empty_like(x)
+    it2, hist2, status2 = sten.bicgstab2d_solve(st, sten.MIXED, _dev(torch, b16, "mixed"), _dev(torch, x0, "mixed"),
+                                                0.0, 3, x2)
+    ref = orc.bicgstab2d(c16, b16, x0=x0, tol=0.0, maxit=3, prec="mixed", tiles=(8, 6))
+    assert np.all(np.abs(hist2 - ref["hist"]) <= 5e-2 * ref["hist"])
     st.close()
