@@ -67,6 +67,8 @@ def parse():
     p.add_argument("--tiling", default="", help="bx,by,zc,stages override (classic)")
     p.add_argument("--sr-tiling", default="", help="by,stages,cstages,zc override (sr)")
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
+    p.add_argument("--no-2d", action="store_true", help="skip the labelled NEXT-3 field (2D 9-point BiCGStab at "
+                                                         "the paper's 22800 x 22800, PAPER.md:371-373)")
     return p.parse_args()
 
 
@@ -360,6 +362,45 @@ def run_schedule(sten, st, prec, schedule, b, x, args, world, sdist, npts, clock
             "hist_10": float(hist[min(10, len(hist) - 1)]), "clocks": clk}
 
 
+def run_2d(sten, icuda, peak, n=22800, maxit=100):
+    """The labelled NEXT-3 field: BiCGStab on the 2D 9-point operator at the paper's 22800 x 22800
+    (R25), mixed fp16, `maxit` iterations at tol = 0, on the seeded 2D
+    stand-in; per-phase CUDA events, roofline on its 33 passes (H1 14, H2 12, H3 7)."""
+    import torch
+    diag, offs = icuda.fields2d_device(n, n, seed=1, delta=0.1)
+    s2 = sten.stencil2d_create(n, n, [diag] + offs)
+    del diag, offs
+    torch.cuda.empty_cache()
+    b = icuda.uniform_device(n, n, 1, seed=1, stream=0).view(n, n).half()
+    x = torch.empty_like(b)
+    sten.stencil2d_set_timing(s2, True)
+    sten.bicgstab2d_solve(s2, sten.MIXED, b, None, 0.0, 4, x)
+    runs = []
+    for _ in range(3):
+        it, hist, status = sten.bicgstab2d_solve(s2, sten.MIXED, b, None, 0.0, maxit, x)
+        ph, nit = sten.stencil2d_phase_ms(s2)
+        runs.append((float(sum(ph)), [float(v) for v in ph]))
+    sten.stencil2d_set_timing(s2, False)
+    tot = []
+    for _ in range(3):
+        sten.bicgstab2d_solve(s2, sten.MIXED, b, None, 0.0, maxit, x)
+        tot.append(s2.last_solve_ms / maxit)
+    s2.close()
+    del b, x
+    torch.cuda.empty_cache()
+    per_it = float(np.median(tot))
+    ph = sorted(runs)[1][1]
+    npts = n * n
+    h1_gbs = 14 * 2 * npts / (ph[0] * 1e-3) / 1e9
+    return {"label": "2D 9-point BiCGStab (SURVEY 8(f) NEXT-3, PAPER.md:362-373), mixed fp16, 22800 x 22800, "
+                     f"{maxit} iterations at tol 0, seeded stand-in (DESIGN.md R25)",
+            "value": npts / (per_it * 1e-3) / 1e9, "unit": "Gpoint-iter/s", "ms_per_iter": per_it,
+            "whole_iteration_frac": 33 * 2 * npts / (per_it * 1e-3) / 1e9 / peak, "passes_per_iter": 33,
+            "phase_ms_per_iter": ph,
+            "roofline": {"bound": "hbm", "kernel": "k_bicg9<half,H1>", "achieved": h1_gbs, "peak": peak,
+                         "unit": "GB/s", "frac": h1_gbs / peak, "passes": 14}}
+
+
 def run_sten(args):
     import torch
     import torch.distributed as dist
@@ -529,6 +570,10 @@ def run_sten(args):
                      "rel_residual_iter10": r["hist_10"], "events": r["events"],
                      "roofline": roofline_of(sch, r), "gpu_launches": int(r["launches"]),
                      **({"e2e": e2e[sch]} if sch in e2e else {})}
+    if not args.no_2d and world == 1 and prec == sten.MIXED:
+        del st, b, x
+        torch.cuda.empty_cache()
+        line["next3_2d"] = run_2d(sten, icuda, peak)
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_auto(pname, workload, args.cpu_planes)
     print(json.dumps(line), flush=True)
