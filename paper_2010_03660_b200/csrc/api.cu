@@ -927,11 +927,15 @@ static int ensure_sr(sten_stencil *st, int prec) {
     if (!b.maps_ok) {
       for (int k = 0; k < 2; ++k)
         for (int i = 0; i < 5; ++i)
-          RC_TRY(make_map(st, &b.m_vec[k][i], b.vec[k][i], e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx + 2 * H,
-                          t.by + 4));
+#ifndef STEN_SR_DIAG
+#define STEN_SR_DIAG 0
+#endif
+          RC_TRY(make_map(st, &b.m_vec[k][i], b.vec[k][i], e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch,
+                          bx + ((STEN_SR_DIAG & 1) ? 0 : 2 * H), t.by + ((STEN_SR_DIAG & 2) ? 0 : 4)));
       for (int d = 0; d < 6; ++d) {
         void *c = prec == STEN_FP32 ? (void *)sl.c32b[d] : (void *)sl.c16b[d];
-        RC_TRY(make_map(st, &b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + 2 * H, t.by + 2));
+        RC_TRY(make_map(st, &b.m_c[d], c, e, st->nx, st->ny, sl.nz + 2, st->pitch, bx + ((STEN_SR_DIAG & 4) ? 0 : 2 * H),
+                        t.by + ((STEN_SR_DIAG & 4) ? 0 : 2)));
       }
       RC_TRY(make_map(st, &b.m_x, b.x, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));
       RC_TRY(make_map(st, &b.m_rh, b.rh, e, st->nx, st->ny, sl.nz + 2 * kSrHalo, st->pitch, bx, t.by));

@@ -47,6 +47,9 @@ constexpr int a128(int b) { return (b + 127) & ~127; }
 
 template <int V> struct IC { static constexpr int value = V; };
 
+#ifndef STEN_SR_DIAG
+#define STEN_SR_DIAG 0
+#endif
 #ifndef STEN_SR_XTMA
 #define STEN_SR_XTMA 1  // x arrives with the input stage by TMA (else a direct load three planes ahead)
 #endif
@@ -436,17 +439,21 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   }
   __syncthreads();
 
+  // STEN_SR_DIAG (traffic diagnostics only - wrong results): bit 0 input boxes without the x halo,
+  // bit 1 without the y halo, bit 2 coefficient boxes without halos (the host maps match)
+  constexpr int DXH = (STEN_SR_DIAG & 1) ? 0 : H, DYH = (STEN_SR_DIAG & 2) ? 0 : 2;
+  constexpr int CXH = (STEN_SR_DIAG & 4) ? 0 : H, CYH = (STEN_SR_DIAG & 4) ? 0 : 1;
   auto issue_in = [&](int qi) {  // plane z0-2+qi of r, p, v, q, y (vectors: 2 halo planes)
     const int slot = qi % S, m = z0 - 2 + qi;
     // x and r_hat only on the chunk's own planes (the four halo planes need neither)
     const bool own = m >= z0 && m < z1;
-    mbar_expect_tx(&mbar[slot], (5u * HW * G::RI + (own && STEN_SR_XTMA ? G::BX * BY : 0) +
+    mbar_expect_tx(&mbar[slot], (5u * (G::BX + 2 * DXH) * (BY + 2 * DYH) + (own && STEN_SR_XTMA ? G::BX * BY : 0) +
                                  (own && STEN_SR_RHTMA ? G::BX * BY : 0)) *
                                     (uint32_t)sizeof(T));
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      if (STEN_SR_EVF & 8) tma_load_3d_hint(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot], pol_in);
-      else tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - H, y0 - 2, m + 2, &mbar[slot]);
+      if (STEN_SR_EVF & 8) tma_load_3d_hint(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - DXH, y0 - DYH, m + 2, &mbar[slot], pol_in);
+      else tma_load_3d(IN + slot * G::SE + i * IE, &a.tm_in[i], x0 - DXH, y0 - DYH, m + 2, &mbar[slot]);
     }
     if (!own) {
     } else if (STEN_SR_EVF & 2) {
@@ -459,11 +466,11 @@ __global__ void __launch_bounds__(SrGeo<T, BY, NB>::NT, 1) k_sr(const __grid_con
   };
   auto issue_c = [&](int qc) {  // plane z0-1+qc of the six coefficient arrays (1 halo plane)
     const int slot = qc % SC, m = z0 - 1 + qc;
-    mbar_expect_tx(&mbar[S + slot], 6u * HW * G::RC * (uint32_t)sizeof(T));
+    mbar_expect_tx(&mbar[S + slot], 6u * (G::BX + 2 * CXH) * (BY + 2 * CYH) * (uint32_t)sizeof(T));
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
-      if (STEN_SR_EVF & 4) tma_load_3d_hint(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot], pol);
-      else tma_load_3d(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - H, y0 - 1, m + 1, &mbar[S + slot]);
+      if (STEN_SR_EVF & 4) tma_load_3d_hint(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - CXH, y0 - CYH, m + 1, &mbar[S + slot], pol);
+      else tma_load_3d(CF + (slot * 6 + d) * CE, &a.tm_c[d], x0 - CXH, y0 - CYH, m + 1, &mbar[S + slot]);
     }
   };
   // optional L2 prefetch (cp.async.bulk.prefetch.tensor) of input planes beyond
