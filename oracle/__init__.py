@@ -92,6 +92,8 @@ def _declare(L):
     L.o16_dot.argtypes = [_I, _I, _I, _P, _P]
     L.o16_dot.restype = ctypes.c_float
     L.o16_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _I, _P, _P, _P, _P, _P, _P]
+    L.o16h_bicgstab.argtypes = [_I, _I, _I, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]
+    L.o16h_bicgstab.restype = _I
     L.o16_bicgstab.restype = _I
     L.o32_apply_fma.argtypes = [_I, _I, _I, _P, _P, _P]
     L.oracle_num_threads.restype = _I
@@ -311,13 +313,12 @@ def bicgstab16(c16, b16, x0=None, tol=0.0, maxit=50, unfused=False, schedule="cl
                                     0 if segments is None else len(seg), _ptr(seg),
                                     _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
                                     ctypes.byref(st), ctypes.byref(ev))
-    else:
-        if segments is not None:
-            raise ValueError("half dots (segments=) are defined for the SR schedule")
-        it = lib().o16_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
-                                None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
-                                int(bool(unfused)), _ptr(x), _ptr(hist), _ptr(al), _ptr(om),
-                                ctypes.byref(st), ctypes.byref(ev))
+    else:  # Alg. 1; segments: the iteration's dots as half-mode pencils (R22, R28)
+        seg = np.zeros(1, np.int32) if segments is None else _segments(segments, nz)
+        it = lib().o16h_bicgstab(nx, ny, nz, _arr6(c16), _ptr(b16),
+                                 None if x0keep is None else _ptr(x0keep), float(tol), int(maxit),
+                                 int(bool(unfused)), 0 if segments is None else len(seg), _ptr(seg),
+                                 _ptr(x), _ptr(hist), _ptr(al), _ptr(om), ctypes.byref(st), ctypes.byref(ev))
     return dict(x=x, hist=hist[: it + 1], iters=it, status=st.value, event_it=ev.value,
                 alpha=al[1: it + 1], omega=om[1: it + 1])
 

@@ -188,10 +188,23 @@ static int on_event(int code, int i, double tol, int *ev, int *ev_it) {
  * unusable as an fp32 Inf/NaN. */
 static int usable16(float s) { return isfinite(s) && finite16(rn16f(s)); }
 
-int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
-                 const uint16_t *b, const uint16_t *x0, double tol, int maxit,
-                 int unfused, uint16_t *x, double *hist, float *alpha_out,
-                 float *omega_out, int *status, int *event_it) {
+/* The iteration's inner products: mixed (o16_dot: exact fp16 products summed in fp32)
+ * or, nseg > 0, the half mode's fp16 column pencils over the z segments seg[0..nseg) (o16h_dot,
+ * DESIGN.md R22), their exact sum rounded once to fp32. */
+static float dot_it(int nx, int ny, int nz, const uint16_t *a, const uint16_t *b, int nseg, const int *seg) {
+  if (nseg <= 0) return o16_dot(nx, ny, nz, a, b);
+  double sm;
+  o16h_dot(nx, ny, nz, a, b, nseg, seg, &sm, NULL);
+  return (float)sm;
+}
+
+/* O16 (Alg. 1, in binary16) with the iteration's five inner products as half
+ * pencils over seg[0..nseg) (nseg = 0: mixed dots, = o16_bicgstab); the setup's rho_0, ||b||,
+ * hist[0] stay mixed (R28). */
+int o16h_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                  const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                  int unfused, int nseg, const int *seg, uint16_t *x, double *hist, float *alpha_out,
+                  float *omega_out, int *status, int *event_it) {
   int64_t n = (int64_t)nx * ny * nz;
   size_t bytes = sizeof(uint16_t) * (size_t)(n > 0 ? n : 1);
   uint16_t *r = (uint16_t *)malloc(bytes), *rh = (uint16_t *)malloc(bytes);
@@ -235,7 +248,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
       for (int64_t P = 0; P < n; ++P) p[P] = o16_fma(bh, o16_fma(mwh, v[P], p[P]), r[P]);
     }
     apply(nx, ny, nz, c, p, v);                       /* l.176 */
-    float sigma = o16_dot(nx, ny, nz, rh, v);         /* l.177 */
+    float sigma = dot_it(nx, ny, nz, rh, v, nseg, seg); /* l.177 */
     alpha = rho / sigma;
     if (sigma == 0.0f || !usable16(alpha)) {
       alpha = 0.0f;
@@ -247,7 +260,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     uint16_t ah = rn16f(alpha);
     for (int64_t P = 0; P < n; ++P) s[P] = o16_fma(neg16(ah), v[P], r[P]); /* l.178 */
     apply(nx, ny, nz, c, s, t);                       /* l.179 */
-    float ts = o16_dot(nx, ny, nz, t, s), tt = o16_dot(nx, ny, nz, t, t);
+    float ts = dot_it(nx, ny, nz, t, s, nseg, seg), tt = dot_it(nx, ny, nz, t, t, nseg, seg);
     if (tt == 0.0f) {
       omega = 0.0f;
     } else {
@@ -263,7 +276,7 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
     uint16_t wh = rn16f(omega);
     for (int64_t P = 0; P < n; ++P) x[P] = o16_fma(wh, s[P], o16_fma(ah, p[P], x[P])); /* l.181 */
     for (int64_t P = 0; P < n; ++P) r[P] = o16_fma(neg16(wh), t[P], s[P]);            /* l.182 */
-    float rhon = o16_dot(nx, ny, nz, rh, r), rr = o16_dot(nx, ny, nz, r, r);
+    float rhon = dot_it(nx, ny, nz, rh, r, nseg, seg), rr = dot_it(nx, ny, nz, r, r, nseg, seg);
     hist[i] = sqrt((double)rr) / nb;
     if (alpha_out) alpha_out[i] = alpha;
     if (omega_out) omega_out[i] = omega;
@@ -283,6 +296,14 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
 done:
   free(r); free(rh); free(p); free(v); free(s); free(t);
   return it;
+}
+
+int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
+                 const uint16_t *b, const uint16_t *x0, double tol, int maxit,
+                 int unfused, uint16_t *x, double *hist, float *alpha_out,
+                 float *omega_out, int *status, int *event_it) {
+  return o16h_bicgstab(nx, ny, nz, c, b, x0, tol, maxit, unfused, 0, NULL, x, hist, alpha_out, omega_out, status,
+                       event_it);
 }
 
 /* ---- fp32 mirror of the GPU fp32 SpMV evaluation order ---- */

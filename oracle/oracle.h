@@ -115,6 +115,11 @@ int o16_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6],
                  const uint16_t *b, const uint16_t *x0, double tol, int maxit,
                  int unfused, uint16_t *x, double *hist, float *alpha,
                  float *omega, int *status, int *event_it);
+/* o16_bicgstab with the iteration's five inner products as half-mode fp16 pencils over the z
+ * segments seg[0..nseg) (o16h_dot, R22; nseg = 0: mixed); rho_0, ||b|| and hist[0] stay mixed (R28) */
+int o16h_bicgstab(int nx, int ny, int nz, const uint16_t *const c[6], const uint16_t *b, const uint16_t *x0,
+                  double tol, int maxit, int unfused, int nseg, const int *seg, uint16_t *x, double *hist,
+                  float *alpha_out, float *omega_out, int *status, int *event_it);
 
 /* ---------------- fp32 mirror of the GPU fp32 kernels ---------------- */
 /* u = v; u = fmaf(c_xm, v_xm, u); ... (same order as o16_apply_fused) */

@@ -148,3 +148,67 @@ def test_half_dot_underflow_is_breakdown_not_convergence():
     assert stop["status"] == orc.ORC_BREAKDOWN and stop["iters"] == k
     mixed = orc.bicgstab16(c16, b16, tol=0.0, maxit=k, schedule="sr")
     assert np.all(mixed["hist"] > 0.0)
+
+
+# ---------------- half dots in the classic schedule (Alg. 1 as printed; R22, R28) ----------------
+def test_classic_half_first_iteration_composes_pinned_primitives():
+    """One iteration of the classic half-dot solve recomputed from pinned pieces: the fused fp16
+    SpMV (apply16), exact binary16 FMA, the half pencils (o16h_dot, pinned above) rounded once to
+    fp32 for sigma, (t,s), (t,t), (r,r), and the mixed setup dots (R28) - x_1 and hist[1] equal."""
+    import inputs
+    nx, ny, nz, seg = 7, 6, 9, [0, 4]
+    diag, offs = inputs.problem_fields(inputs.KIND_CD, nx, ny, nz, seed=3, delta=0.1)
+    c16 = orc.quantize_coeffs(orc.jacobi_scale(diag, offs), "mixed")
+    b = orc.f16_from_double(inputs.rhs_uniform(nx, ny, nz, seed=3))
+    r = orc.bicgstab16(c16, b, tol=0.0, maxit=1, segments=seg)
+    hd = lambda a, c: np.float32(orc.dot16h(a, c, seg)[0])
+    rho = np.float32(orc.dot16(b, b))  # setup: mixed
+    v = orc.apply16(c16, b)
+    alpha = np.float32(rho / hd(b, v))
+    ah = orc.f16_from_double(np.float64(alpha))
+    neg = lambda h: np.uint16(h ^ 0x8000)
+    s = orc.fma16_array(np.full_like(v, neg(ah)), v, b)
+    t = orc.apply16(c16, s)
+    omega = np.float32(hd(t, s) / hd(t, t))
+    wh = orc.f16_from_double(np.float64(omega))
+    x = orc.fma16_array(np.full_like(s, wh), s, orc.fma16_array(np.full_like(b, ah), b, np.zeros_like(b)))
+    assert np.array_equal(r["x"], x)
+    rr = orc.fma16_array(np.full_like(t, neg(wh)), t, s)
+    assert r["hist"][1] == np.sqrt(np.float64(hd(rr, rr))) / np.sqrt(np.float64(rho))
+
+
+def test_classic_half_identity_and_tracking():
+    """A = I: one iteration, x = b; on a well-conditioned system the classic half-dot solve follows
+    the classic mixed one for the first iterations; with no segments it is the mixed solve."""
+    rng = np.random.default_rng(8)
+    nz, ny, nx = 5, 4, 3
+    z = [np.zeros((nz, ny, nx), np.uint16)] * 6
+    b = orc.f16_from_double(rng.uniform(-1, 1, (nz, ny, nx)))
+    ref = orc.bicgstab16(z, b, tol=1e-6, maxit=10, segments=[0, 2])
+    assert ref["iters"] == 1 and ref["status"] == orc.ORC_CONVERGED and np.array_equal(ref["x"], b)
+    import inputs
+    n = 8
+    diag, offs = inputs.problem_fields(inputs.KIND_CD, n, n, n, seed=1, delta=0.1)
+    c16 = orc.quantize_coeffs(orc.jacobi_scale(diag, offs), "mixed")
+    b16 = orc.f16_from_double(inputs.rhs_uniform(n, n, n, seed=1))
+    mixed = orc.bicgstab16(c16, b16, tol=0.0, maxit=12)
+    half = orc.bicgstab16(c16, b16, tol=0.0, maxit=12, segments=[0])
+    assert half["hist"][0] == mixed["hist"][0]  # the setup stays mixed (R28)
+    assert np.all(np.abs(half["hist"][:5] - mixed["hist"][:5]) <= 5e-2 * mixed["hist"][:5])
+
+
+def test_classic_half_underflow_is_breakdown():
+    """R23 in the classic schedule: the half pencils of (r,r) underflow before r is zero, and the
+    solve reports BREAKDOWN there (never CONVERGED)."""
+    import inputs
+    n = 8
+    diag, offs = inputs.problem_fields(inputs.KIND_CD, n, n, n, seed=1, delta=0.1)
+    c16 = orc.quantize_coeffs(orc.jacobi_scale(diag, offs), "mixed")
+    b16 = orc.f16_from_double(inputs.rhs_uniform(n, n, n, seed=1))
+    half = orc.bicgstab16(c16, b16, tol=0.0, maxit=40, segments=[0])
+    zero = np.flatnonzero(half["hist"] == 0.0)
+    assert zero.size > 0 and half["status"] == orc.ORC_BREAKDOWN and half["event_it"] == int(zero[0])
+    stop = orc.bicgstab16(c16, b16, tol=1e-9, maxit=40, segments=[0])
+    assert stop["status"] == orc.ORC_BREAKDOWN and stop["iters"] == int(zero[0])
+    mixed = orc.bicgstab16(c16, b16, tol=0.0, maxit=int(zero[0]))
+    assert np.all(mixed["hist"] > 0.0)
