@@ -59,7 +59,7 @@ def parse():
     p.add_argument("--no-other", action="store_true", help="do not measure the non-headline schedule")
     p.add_argument("--dots", default="mixed", choices=["mixed", "half"],
                    help="mixed precision only: inner products as fp16 products summed in fp32 (the paper's "
-                        "instruction), or half: fp16 column pencils (DESIGN.md R22, NEXT-4; SR schedule)")
+                        "instruction), or half: fp16 column pencils (DESIGN.md R22, R28, NEXT-4)")
     p.add_argument("--operator", default="fields", choices=["fields", "poisson-const"],
                    help="fields: the workload's per-point coefficient fields; poisson-const: the constant "
                         "7-point Poisson operator (config 1's) at the same mesh via stencil_create_const "
@@ -463,7 +463,7 @@ def run_sten(args):
     # the headline schedule first, then (unless --no-sr / it is the headline) the SR schedule
     head = args.schedule
     scheds = [head] + ([] if args.no_other else [s_ for s_ in ("classic", "sr") if s_ != head])
-    if const_op or args.dots == "half":
+    if const_op:
         scheds = [s_ for s_ in scheds if s_ == "sr"] or ["sr"]
         head = "sr"
     recs = {}

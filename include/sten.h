@@ -317,7 +317,7 @@ int sten_iter_ms(sten_stencil *st, int phase, float *out, int cap, int *n);
  * Errors: STEN_EINVAL. */
 int sten_set_schedule(sten_stencil *st, int schedule);
 
-/* Inner-product precision of STEN_MIXED SR sweeps (R22; SURVEY
+/* Inner-product precision of STEN_MIXED solves (R22, R28; SURVEY
  * §8(f) NEXT-4, the "half" mode the paper sized but did not publish,
  * PAPER.md:427-441 (commented-out performance model: "16-bit mode")):
  *   STEN_DOTS_MIXED (default): fp16 products summed in fp32 (the paper's
@@ -326,11 +326,14 @@ int sten_set_schedule(sten_stencil *st, int schedule);
  *     running fp16 sum of its (x, y) column over one z segment (the CS-1 PE's
  *     core-local dot over its z pencil, in 16-bit); the column-segment sums
  *     are then added in fp32 (the AllReduce stays 32-bit).
- *     The segments are the SR chunk plan, listed by sten_sr_segments.
+ *     The segments are the chunk plan: sten_sr_segments for the SR schedule,
+ *     sten_classic_segments for the classic one (one plan for H1, H2 and H3
+ *     in this mode; the setup's rho_0, ||b||, hist[0] stay mixed, R28).
  * Vector arithmetic and HBM traffic are identical in both modes.  FP32
- * solves ignore the setting.  Supported with the SR schedule, the
- * field-coefficient operator, 16-B packs and the SERIAL/OVERLAP exchanges;
- * otherwise the solve / sweep returns STEN_EUNSUPPORTED.
+ * solves ignore the setting.  Supported with the field-coefficient operator:
+ * SR with 16-B packs and the SERIAL/OVERLAP exchanges, classic on one slab
+ * with the tile kernels; otherwise the solve / sweep returns
+ * STEN_EUNSUPPORTED.
  * Errors: STEN_EINVAL. */
 #define STEN_DOTS_MIXED 0
 #define STEN_DOTS_HALF 1

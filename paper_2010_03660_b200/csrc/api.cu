@@ -460,7 +460,7 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     a.cptr[d] = prec == STEN_FP32 ? (const void *)sl.c32[d] : (const void *)sl.c16[d];
   }
   a.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
-  a.zc = zc_of(t, mode);
+  a.zc = (prec == STEN_MIXED && st->half_dots) ? t.zc : zc_of(t, mode);  // half dots: one plan for all phases
   a.zlo = part == CLS_INTERIOR ? 1 : (part == CLS_TOP ? sl.nz - 1 : 0);
   a.zhi = part == CLS_INTERIOR ? sl.nz - 1 : (part == CLS_BOTTOM ? 1 : sl.nz);
   if (part == CLS_BOTTOM || part == CLS_TOP) a.zc = 1;
@@ -490,6 +490,12 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     }
   }
   if (a.zhi <= a.zlo) return STEN_OK;
+  if (prec == STEN_MIXED && st->half_dots && mode != MODE_APPLY) {  // half dots (R22, R28): one chunk plan
+    if (t.rows || fused) return set_err(STEN_EUNSUPPORTED, "half dots: the tile kernels without the fused exchange");
+    KLAUNCH(stencil_launch_half(mode, a, t.by, t.stages, t.cstages, s));
+    st->launches++;
+    return STEN_OK;
+  }
   if (fused && mode == MODE_H1 && (a.peer_lo[0] || a.peer_hi[0])) {
     if (t.rows) return set_err(STEN_EUNSUPPORTED, "the fused classic exchange needs the tile kernels");
     if (prec == STEN_FP32) KLAUNCH(stencil_launch_fused<float>(a, t.by, t.stages, t.cstages, s));
@@ -545,6 +551,28 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
     a.peer_hi_r = cls_peer(st, prec, slab, 0, false);
     a.plane_elems = st->plane;
     a.nzp = sl.nz;
+  }
+  if (prec == STEN_MIXED && st->half_dots) {  // half dots (R28): H3 marches the H1 / H2 chunk plan
+    const Tiling &t = st->tiling[prec];
+    H3zArgs h;
+    memset(&h, 0, sizeof h);
+    h.x = a.x;
+    h.p = a.p;
+    h.s = a.s;
+    h.t = a.t;
+    h.rh = a.rhat;
+    h.xo = a.xo;
+    h.ro = a.ro;
+    h.g = Geom{st->nx, st->ny, sl.nz, st->pitch, st->plane};
+    h.zc = t.zc;
+    h.tiles_x = (st->nx + t.bx - 1) / t.bx;
+    h.tiles_y = (st->ny + t.by - 1) / t.by;
+    h.red = a.red;
+    if ((long long)h.tiles_x * h.tiles_y * ((sl.nz + h.zc - 1) / h.zc) > st->partials_cap)
+      return set_err(STEN_ECUDA, "internal: H3 grid exceeds the partial-sum buffer");
+    KLAUNCH(h3z_half_launch(h, t.by, s));
+    st->launches++;
+    return STEN_OK;
   }
   if (ew_grid(st, a.nvec) > st->partials_cap)
     return set_err(STEN_ECUDA, "internal: element-wise grid exceeds the partial-sum buffer");
@@ -1773,8 +1801,12 @@ struct SolveOut {
 static int solve_core(sten_stencil *st, int prec, bool with_x0, bool scale_rhs, double tol, int maxit, cudaStream_t s,
                       SolveOut *out) {
   const bool sr = st->schedule == STEN_SCHED_SR;
-  if (!sr && prec == STEN_MIXED && st->half_dots)
-    return set_err(STEN_EUNSUPPORTED, "half dots (STEN_DOTS_HALF) are built for the SR schedule only");
+  if (!sr && prec == STEN_MIXED && st->half_dots) {  // R28: one slab, the tile kernels, field operator
+    const Tiling &t = st->tiling[prec];
+    if (decomposed(st) || st->cc || (t.bx != 0 && (t.rows || !(t.by == 16 && t.stages == 2 && t.cstages == 2))))
+      return set_err(STEN_EUNSUPPORTED, "half dots in the classic schedule: one slab, field coefficients, the "
+                                        "default tile kernels");
+  }
   if (p2p_only(st)) {  // no NCCL: peer memory moves the data between ranks (after sten_p2p_import)
     if (!st->p2p_ranks || (sr && !st->sr_p2p))
       return set_err(STEN_EUNSUPPORTED, "p2p-only communicator: a solve needs sten_p2p_import (and, for the SR "
@@ -2271,7 +2303,7 @@ int sten_classic_segments(sten_stencil *st, int prec, int *z0, int cap, int *n) 
   for (const Slab &sl : st->slabs) {
     std::vector<int> starts;
     for (int mode : {MODE_H1, MODE_H2}) {  // the union of the H1 (= apply) and H2 plans
-      const int zc = zc_of(t, mode);
+      const int zc = (prec == STEN_MIXED && st->half_dots) ? t.zc : zc_of(t, mode);  // half dots: one plan
       if (cls_overlapped(st)) {  // plane 0, the interior in zc chunks from plane 1, plane nz-1
         starts.push_back(0);
         for (int z = 1; z < sl.nz - 1; z += zc) starts.push_back(z);

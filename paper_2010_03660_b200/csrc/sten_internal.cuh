@@ -534,6 +534,17 @@ template <typename T>
 int stencil_launch(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
 // the fused-exchange instance (MODE_H1 with peer stores), default geometry only
 template <typename T> int stencil_launch_fused(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
+// half dots (R22, R28): H1 / H2 with their inner products as fp16 column pencils over the chunk
+int stencil_launch_half(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s);
+// the classic H3 marching z over the same chunks, its two inner products as fp16 column pencils
+struct H3zArgs {
+  const void *x, *p, *s, *t, *rh;  // interior plane 0
+  void *xo, *ro;
+  Geom g;
+  int zc, tiles_x, tiles_y;
+  Reduce red;
+};
+int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s);
 template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
 template <typename T> int stencil_threads(int by);
 // row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits

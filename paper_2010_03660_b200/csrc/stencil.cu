@@ -99,7 +99,20 @@ template <> struct Shift<__half> {
 
 }  // namespace
 
-template <typename T, int MODE, int BY, int S, int SC, bool FU = false>
+// the lanes of an fp16 pencil pack widened and added in fp32, in lane order (half dots, R22)
+__device__ __forceinline__ float pencil_sum(const Pack<__half> &h) {
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(Pack<__half>::h2(h.w[i]));
+    s += f.x;
+    s += f.y;
+  }
+  return s;
+}
+__device__ __forceinline__ float pencil_sum(const Pack<float> &h) { return (h.v[0] + h.v[1]) + (h.v[2] + h.v[3]); }
+
+template <typename T, int MODE, int BY, int S, int SC, bool FU = false, bool HD = false>
 __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __grid_constant__ StencilArgs a) {
   using P = Pack<T>;
   using G = Geo<T, MODE, BY>;
@@ -225,6 +238,9 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   for (int d = 0; d < ND; ++d)
 #pragma unroll
     for (int i = 0; i < 4; ++i) dacc[d][i] = 0.0f;
+  P hacc[ND];  // HD: the column pencils, fp16 running sums from +0 (R22)
+#pragma unroll
+  for (int d = 0; d < ND; ++d) hacc[d] = P::zero();
 
   for (int k = z0; k < z1; ++k) {
     const int qc = k - z0 + 1, qn = qc + 1;
@@ -276,7 +292,14 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
         }
       }
     }
-    if (MODE == MODE_H1) {
+    if (HD) {  // one fp16 FMA per point into the lane's pencil (o16h_dot order: fma16(a, b, acc))
+      if (MODE == MODE_H1) {
+        hacc[0] = P::fma(rh, acc, hacc[0]);  // (rhat, v')
+      } else if (MODE == MODE_H2) {
+        hacc[0] = P::fma(acc, uc, hacc[0]);       // (t, s)
+        hacc[ND - 1] = P::fma(acc, acc, hacc[ND - 1]);  // (t, t)
+      }
+    } else if (MODE == MODE_H1) {
       rh.dot4(acc, dacc[0]);  // (rhat, v')
     } else if (MODE == MODE_H2) {
       acc.dot4(uc, dacc[0]);        // (t, s)
@@ -289,7 +312,7 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   if (MODE != MODE_APPLY) {
     float v[ND];
 #pragma unroll
-    for (int d = 0; d < ND; ++d) v[d] = sum4(dacc[d]);
+    for (int d = 0; d < ND; ++d) v[d] = HD ? pencil_sum(hacc[d]) : sum4(dacc[d]);
     const bool peer = FU && (z0 == 0 || z1 == a.g.nz);  // only boundary-plane chunks stored to peers
     if (MODE == MODE_H1) grid_reduce_finalize<ND, PH_H1>(v, a.red, scratch, peer);
     else grid_reduce_finalize<ND, PH_H2>(v, a.red, scratch, peer);
@@ -517,19 +540,19 @@ template int rows_threads<__half>(int, int);
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int MODE, int BY, int S, int SC = 0, bool FU = false>
+template <typename T, int MODE, int BY, int S, int SC = 0, bool FU = false, bool HD = false>
 int launch_one(const StencilArgs &a, cudaStream_t s) {
   using G = Geo<T, MODE, BY>;
   constexpr size_t smem = smem_bytes_c<T, MODE, BY, S, SC>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC, FU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC, FU, HD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc);
-  k_stencil<T, MODE, BY, S, SC, FU><<<grid, G::NT, smem, s>>>(a);
+  k_stencil<T, MODE, BY, S, SC, FU, HD><<<grid, G::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 template <typename T, int MODE>
@@ -589,6 +612,84 @@ int stencil_launch_fused(const StencilArgs &a, int by, int stages, int cstages, 
   if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE_H1, 16, 2, 2, true>(a, s);
   return (int)cudaErrorNotSupported;
 }
+int stencil_launch_half(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
+  if (!(by == 16 && stages == 2 && cstages == 2)) return (int)cudaErrorNotSupported;
+  if (mode == MODE_H1) return launch_one<__half, MODE_H1, 16, 2, 2, false, true>(a, s);
+  if (mode == MODE_H2) return launch_one<__half, MODE_H2, 16, 2, 2, false, true>(a, s);
+  return (int)cudaErrorNotSupported;
+}
+
+// ---------------------------------------------- H3 half (R28): a z-march --
+// x += alpha p + omega s, r = s - omega t (the k_h3 operation order), with (rhat, r) and (r, r) as
+// fp16 column pencils over the chunk (one fp16 FMA per point, z ascending from +0), so that the
+// classic half mode's pencils follow one z-chunk plan in all three phases.  A CTA owns a BX x BY
+// tile and marches its chunk; two planes per trip keep ten loads in flight.
+template <int BY>
+__global__ void __launch_bounds__((128 / 8) * BY) k_h3z_half(const __grid_constant__ H3zArgs a) {
+  using P = Pack<__half>;
+  constexpr int VEC = 8, BX = 128, VPR = BX / VEC;  // = tile_bx<__half>(): the classic tiles
+  __shared__ float scratch[32 * kMaxDots];
+  if (st_idle(a.red.st)) return;
+  int b = blockIdx.x;
+  const int tx = b % a.tiles_x;
+  b /= a.tiles_x;
+  const int ty = b % a.tiles_y;
+  const int ch = b / a.tiles_y;
+  const int z0 = ch * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+  const int ry = threadIdx.x / VPR, cx = threadIdx.x - ry * VPR;
+  const int gx = tx * BX + cx * VEC, gy = ty * BY + ry;
+  P h0 = P::zero(), h1 = P::zero();
+  if (gx < a.g.nx && gy < a.g.ny) {
+    const typename P::S as = P::scalar(a.red.st->alpha), ws = P::scalar(a.red.st->omega), mws = P::neg(ws);
+    const __half *X = reinterpret_cast<const __half *>(a.x), *Pp = reinterpret_cast<const __half *>(a.p);
+    const __half *Sv = reinterpret_cast<const __half *>(a.s), *Tv = reinterpret_cast<const __half *>(a.t);
+    const __half *Rh = reinterpret_cast<const __half *>(a.rh);
+    __half *XO = reinterpret_cast<__half *>(a.xo), *RO = reinterpret_cast<__half *>(a.ro);
+    const long long g0 = (long long)gy * a.g.pitch + gx;
+    int k = z0;
+    constexpr int U = 4;  // planes per trip: twenty 16-B loads in flight per thread
+    for (; k + U - 1 < z1; k += U) {
+      P xs[U], ps[U], ss[U], ts[U], rs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long o = (long long)(k + u) * a.g.plane + g0;
+        xs[u] = P::ldg(X + o);
+        ps[u] = P::ldg(Pp + o);
+        ss[u] = P::ldg(Sv + o);
+        ts[u] = P::ldg(Tv + o);
+        rs[u] = P::ldg(Rh + o);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // z ascending: the pencils' order
+        const long long o = (long long)(k + u) * a.g.plane + g0;
+        const P xn = P::fmas(ws, ss[u], P::fmas(as, ps[u], xs[u])), rn = P::fmas(mws, ts[u], ss[u]);
+        xn.st(XO + o);
+        rn.st(RO + o);
+        h0 = P::fma(rs[u], rn, h0);  // (rhat, r)
+        h1 = P::fma(rn, rn, h1);     // (r, r)
+      }
+    }
+    for (; k < z1; ++k) {
+      const long long o0 = (long long)k * a.g.plane + g0;
+      const P x0 = P::ldg(X + o0), p0 = P::ldg(Pp + o0), s0 = P::ldg(Sv + o0), t0 = P::ldg(Tv + o0), r0 = P::ldg(Rh + o0);
+      const P xn0 = P::fmas(ws, s0, P::fmas(as, p0, x0)), rn0 = P::fmas(mws, t0, s0);
+      xn0.st(XO + o0);
+      rn0.st(RO + o0);
+      h0 = P::fma(r0, rn0, h0);
+      h1 = P::fma(rn0, rn0, h1);
+    }
+  }
+  float v[2] = {pencil_sum(h0), pencil_sum(h1)};
+  grid_reduce_finalize<2, PH_H3>(v, a.red, scratch);
+}
+
+int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s) {
+  if (by != 16) return (int)cudaErrorNotSupported;
+  const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
+  k_h3z_half<16><<<grid, (tile_bx<__half>() / 8) * 16, 0, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
 template int stencil_launch_fused<float>(const StencilArgs &, int, int, int, cudaStream_t);
 template int stencil_launch_fused<__half>(const StencilArgs &, int, int, int, cudaStream_t);
 template int stencil_launch<float>(int, const StencilArgs &, int, int, int, cudaStream_t);

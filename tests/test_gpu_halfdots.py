@@ -143,9 +143,18 @@ def test_half_dot_api_guards(sten):
     torch = torch_cuda()
     b = torch.ones(6, 8, 16, dtype=torch.float16, device="cuda")
     x = torch.empty_like(b)
-    sten.set_schedule(st, sten.SCHED_CLASSIC)
-    with pytest.raises(sten.StenError, match="SR schedule"):
+    sten.set_schedule(st, sten.SCHED_CLASSIC)  # classic half (R28): the default tile kernels only
+    sten.set_tiling(st, MIXED, 0, 8, 0, 0)
+    with pytest.raises(sten.StenError, match="half dots"):
         sten.bicgstab_solve(st, MIXED, b, None, 0.0, 3, x)
+    st.close()
+    st = gpu_stencil(diag, offs)
+    sten.set_dot_precision(st, sten.DOTS_HALF)
+    st2 = gpu_stencil(diag, offs, nslabs=2)  # and one slab
+    sten.set_dot_precision(st2, sten.DOTS_HALF)
+    with pytest.raises(sten.StenError, match="half dots"):
+        sten.bicgstab_solve(st2, MIXED, b, None, 0.0, 3, x)
+    st2.close()
     sten.set_schedule(st, sten.SCHED_SR)
     sten.set_sr_tiling(st, MIXED, 16, 2, 2, 0, 8)  # 8-B packs: not built with half dots
     with pytest.raises(sten.StenError, match="half dots"):
@@ -194,4 +203,69 @@ def test_half_dot_underflow_is_breakdown(sten):
     cq = oracle_coeffs(diag, offs, "mixed")
     ref = orc.bicgstab16(cq, b, tol=0.0, maxit=40, schedule="sr", segments=seg)
     assert ref["status"] == orc.ORC_BREAKDOWN and abs(ref["event_it"] - k) <= 1
+    st.close()
+
+
+# ---------------- the classic schedule (Alg. 1 as printed) with half dots (R28) ----------------
+@pytest.mark.parametrize("mesh,delta,nhist", [((32, 32, 32), 0.1, 12), ((37, 29, 19), 0.0, 10),
+                                              ((130, 33, 45), 0.1, 12)])
+def test_classic_half_dot_solve_history(sten, mesh, delta, nhist):
+    """The classic schedule with half dots against o16h_bicgstab over the library's own chunk plan
+    (sten_classic_segments, one plan for H1, H2 and H3 in this mode): the history within 5e-2, and
+    the same vectors as the classic mixed solve after one iteration except through the scalars."""
+    torch = torch_cuda()
+    nx, ny, nz = mesh
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=delta, seed=1)
+    b16 = orc.f16_from_double(inputs.rhs_uniform(nx, ny, nz, seed=1))
+    st = gpu_stencil(diag, offs)
+    sten.set_dot_precision(st, sten.DOTS_HALF)
+    seg = sten.classic_segments(st, MIXED)
+    bt = to_gpu_vec(b16, "mixed")
+    xt = torch.empty_like(bt)
+    it, hist, status = sten.bicgstab_solve(st, MIXED, bt, None, 0.0, nhist, xt)
+    c16 = oracle_coeffs(diag, offs, "mixed")
+    bh = orc.scale_rhs(b16, diag, "mixed")
+    ref = orc.bicgstab16(c16, bh, tol=0.0, maxit=nhist, segments=seg)
+    assert len(hist) == len(ref["hist"]) == nhist + 1
+    assert np.all(np.abs(hist - ref["hist"]) <= 5e-2 * ref["hist"]), (hist, ref["hist"])
+    mixed = orc.bicgstab16(c16, bh, tol=0.0, maxit=nhist)
+    assert hist[0] == pytest.approx(mixed["hist"][0], rel=1e-6)  # the setup stays mixed
+    assert not np.array_equal(hist, mixed["hist"])
+    st.close()
+
+
+def test_classic_half_first_iteration_vectors(sten):
+    """x_1 of the classic half solve within one fp16 ulp of o16h_bicgstab's (every vector op is the
+    oracle's; alpha_1, omega_1 come from pencils whose fp32 sum order differs)."""
+    torch = torch_cuda()
+    nx, ny, nz = 70, 37, 50
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=4)
+    b16 = orc.f16_from_double(inputs.rhs_uniform(nx, ny, nz, seed=4))
+    st = gpu_stencil(diag, offs)
+    sten.set_dot_precision(st, sten.DOTS_HALF)
+    seg = sten.classic_segments(st, MIXED)
+    assert seg == list(range(0, nz, seg[1] if len(seg) > 1 else nz))
+    bt = to_gpu_vec(b16, "mixed")
+    xt = torch.empty_like(bt)
+    sten.bicgstab_solve(st, MIXED, bt, None, 0.0, 1, xt)
+    c16 = oracle_coeffs(diag, offs, "mixed")
+    ref = orc.bicgstab16(c16, orc.scale_rhs(b16, diag, "mixed"), tol=0.0, maxit=1, segments=seg)
+    xg, xo = widen(from_gpu_vec(xt, "mixed"), "mixed"), widen(ref["x"], "mixed")
+    assert np.all(np.abs(xg - xo) <= np.spacing(np.abs(xo).astype(np.float16)).astype(np.float64) + 1e-12)
+    st.close()
+
+
+def test_classic_half_underflow_is_breakdown(sten):
+    """R23 with the classic half dots: the solve reports BREAKDOWN, never CONVERGED, where the
+    pencils of (r,r) underflow (the oracle pin's system)."""
+    torch = torch_cuda()
+    n = 8
+    diag, offs = fields(inputs.KIND_CD, n, n, n, delta=0.1, seed=1)
+    b = quantize_vec(inputs.rhs_uniform(n, n, n, seed=1), "mixed")
+    st = gpu_stencil(None, [o / diag for o in offs], unit_diag=True)
+    sten.set_dot_precision(st, sten.DOTS_HALF)
+    bt = to_gpu_vec(b, "mixed")
+    xt = torch.empty_like(bt)
+    it, hist, status = sten.bicgstab_solve(st, MIXED, bt, None, 1e-9, 40, xt)
+    assert status == sten.BREAKDOWN and hist[-1] == 0.0
     st.close()
