@@ -116,13 +116,6 @@ __global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
 #define STEN_H3_CSST 1  // k_h3_bulk: streaming (.cs) stores of x, r
 #endif
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 // H3 through 1D bulk copies: a persistent CTA streams segments of SEGV 16-B vectors of the five
 // inputs (x, p, s, t, rhat) through an NS-stage shared ring (cp.async.bulk issued by one thread,
 // mbarrier complete_tx), computes from shared memory and stores x, r with streaming stores.

@@ -276,6 +276,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+// 1D bulk copy global -> shared, completion on an mbarrier (complete_tx)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
                                             uint64_t *bar) {
   asm volatile(
@@ -545,6 +553,7 @@ struct H3zArgs {
   Reduce red;
 };
 int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s);
+int h3z_half_grid(int sm_count, int tiles, int nz, int zc);  // CTAs of h3z_half_launch
 template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
 template <typename T> int stencil_threads(int by);
 // row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits

@@ -683,12 +683,128 @@ __global__ void __launch_bounds__((128 / 8) * BY) k_h3z_half(const __grid_consta
   grid_reduce_finalize<2, PH_H3>(v, a.red, scratch);
 }
 
+// The same operation and the same pencils through a 1D bulk-copy ring (the k_h3_bulk stream):
+// a work item is (segment j of a plane, z chunk c) - SEGV consecutive 16-B vectors of every
+// plane of the chunk; thread tid owns vector j*SEGV + tid, i.e. one (x, y) column over the
+// chunk, so its two fp16 pencils run z ascending from +0 exactly as in k_h3z_half (the pencil
+// values are identical; only the fp32 order in which pencils are added differs).  Persistent
+// CTAs; one thread issues the five 6-KB copies of the step NS ahead (crossing items).
+// Planes hold whole padded rows: padding is zero and stays zero (x += a 0 + w 0, r = 0 - w 0).
+template <int SEGV, int NS>
+__global__ void __launch_bounds__(SEGV) k_h3s_half(const __grid_constant__ H3zArgs a) {
+  using P = Pack<__half>;
+  constexpr int VEC = 8, SE = SEGV * VEC;  // elements per input per step
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ float scratch[32 * kMaxDots];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  __half *ring = reinterpret_cast<__half *>(smem + 128);  // [NS][5][SE]
+  if (st_idle(a.red.st)) return;
+  const long long pv = a.g.plane / VEC;           // vectors per plane
+  const int nsp = (int)((pv + SEGV - 1) / SEGV);  // segments per plane
+  const int nch = (a.g.nz + a.zc - 1) / a.zc;
+  const long long nitems = (long long)nsp * nch;
+  const int tid = threadIdx.x;
+  const __half *src[5] = {reinterpret_cast<const __half *>(a.x), reinterpret_cast<const __half *>(a.p),
+                          reinterpret_cast<const __half *>(a.s), reinterpret_cast<const __half *>(a.t),
+                          reinterpret_cast<const __half *>(a.rh)};
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // producer cursor (thread 0): the item and plane of the next step to issue
+  long long pit = blockIdx.x, pstep = 0;
+  int pz = 0;
+  auto issue_next = [&]() {
+    if (pit >= nitems) return;
+    const int c = (int)(pit / nsp), j = (int)(pit - (long long)c * nsp);
+    const int z0 = c * a.zc, nzc = min(a.zc, a.g.nz - z0);
+    const long long v0 = (long long)j * SEGV;
+    const uint32_t bytes = (uint32_t)(min((long long)SEGV, pv - v0) * 16);
+    const int slot = (int)(pstep % NS);
+    const long long o = (long long)(z0 + pz) * a.g.plane + v0 * VEC;
+    mbar_expect_tx(&bar[slot], 5u * bytes);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) bulk_g2s(ring + ((size_t)slot * 5 + k) * SE, src[k] + o, bytes, &bar[slot]);
+    ++pstep;
+    if (++pz == nzc) {
+      pz = 0;
+      pit += gridDim.x;
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < NS; ++k) issue_next();
+  const typename P::S as = P::scalar(a.red.st->alpha), ws = P::scalar(a.red.st->omega), mws = P::neg(ws);
+  __half *XO = reinterpret_cast<__half *>(a.xo), *RO = reinterpret_cast<__half *>(a.ro);
+  float acc0 = 0.0f, acc1 = 0.0f;
+  long long step = 0;
+  for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int c = (int)(it / nsp), j = (int)(it - (long long)c * nsp);
+    const int z0 = c * a.zc, z1 = min(z0 + a.zc, a.g.nz);
+    const long long v0 = (long long)j * SEGV;
+    const bool own = v0 + tid < pv;
+    P h0 = P::zero(), h1 = P::zero();
+    for (int z = z0; z < z1; ++z, ++step) {
+      const int slot = (int)(step % NS);
+      mbar_wait(&bar[slot], (uint32_t)((step / NS) & 1));
+      if (own) {
+        const __half *rb = ring + (size_t)slot * 5 * SE + tid * VEC;
+        const P xs = P::ld(rb), ps = P::ld(rb + SE), ss = P::ld(rb + 2 * SE), ts = P::ld(rb + 3 * SE),
+                rs = P::ld(rb + 4 * SE);
+        const P xn = P::fmas(ws, ss, P::fmas(as, ps, xs)), rn = P::fmas(mws, ts, ss);
+        const long long o = (long long)z * a.g.plane + (v0 + tid) * VEC;
+        __stcs(reinterpret_cast<uint4 *>(XO + o), *reinterpret_cast<const uint4 *>(&xn));
+        __stcs(reinterpret_cast<uint4 *>(RO + o), *reinterpret_cast<const uint4 *>(&rn));
+        h0 = P::fma(rs, rn, h0);  // (rhat, r)
+        h1 = P::fma(rn, rn, h1);  // (r, r)
+      }
+      __syncthreads();  // the slot is consumed
+      if (tid == 0) issue_next();
+    }
+    acc0 += pencil_sum(h0);
+    acc1 += pencil_sum(h1);
+  }
+  float v[2] = {acc0, acc1};
+  grid_reduce_finalize<2, PH_H3>(v, a.red, scratch);
+}
+
+#ifndef STEN_H3Z_VARIANT
+#define STEN_H3Z_VARIANT 1  // 0: k_h3z_half (tile z-march, direct loads); 1: k_h3s_half (bulk ring)
+#endif
+#ifndef STEN_H3S_SEGV
+#define STEN_H3S_SEGV 384  // k_h3s_half: 16-B vectors per segment (= threads)
+#endif
+#ifndef STEN_H3S_NS
+#define STEN_H3S_NS 3      // k_h3s_half: ring stages (3 x 5 x 6 KB = 90 KB)
+#endif
+#ifndef STEN_H3S_CPS
+#define STEN_H3S_CPS 2     // k_h3s_half: CTAs per SM
+#endif
+
+int h3z_half_grid(int sm_count, int tiles, int nz, int zc) {
+  return STEN_H3Z_VARIANT == 1 ? sm_count * STEN_H3S_CPS : tiles * ((nz + zc - 1) / zc);
+}
+
 int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s) {
   if (by != 16) return (int)cudaErrorNotSupported;
+#if STEN_H3Z_VARIANT == 1
+  constexpr size_t smem = 128 + (size_t)STEN_H3S_NS * 5 * STEN_H3S_SEGV * 16;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_h3s_half<STEN_H3S_SEGV, STEN_H3S_NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  k_h3s_half<STEN_H3S_SEGV, STEN_H3S_NS><<<device_sm_count() * STEN_H3S_CPS, STEN_H3S_SEGV, smem, s>>>(a);
+#else
   const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
   k_h3z_half<16><<<grid, (tile_bx<__half>() / 8) * 16, 0, s>>>(a);
+#endif
   return (int)cudaGetLastError();
 }
+
 
 template int stencil_launch_fused<float>(const StencilArgs &, int, int, int, cudaStream_t);
 template int stencil_launch_fused<__half>(const StencilArgs &, int, int, int, cudaStream_t);
