@@ -463,9 +463,6 @@ def run_sten(args):
     # the headline schedule first, then (unless --no-sr / it is the headline) the SR schedule
     head = args.schedule
     scheds = [head] + ([] if args.no_other else [s_ for s_ in ("classic", "sr") if s_ != head])
-    if const_op:
-        scheds = [s_ for s_ in scheds if s_ == "sr"] or ["sr"]
-        head = "sr"
     recs = {}
     for sch in scheds:
         recs[sch] = run_schedule(sten, st, prec, sch, b, x, args, world, sdist, npts,
@@ -474,15 +471,15 @@ def run_sten(args):
     def roofline_of(sch, r):
         sr = sch == "sr"
         kb = (roofline.sweep_bytes(pname, npts_local, const_op) if sr
-              else roofline.phase_bytes("H1", pname, npts_local))
+              else roofline.phase_bytes("H1", pname, npts_local, const_op))
         achieved = kb / (r["dom_ms"] / 1e3) / 1e9
         tname = "half" if prec == sten.MIXED else "float"
         kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
         traffic, traffic_src = (None, None)
         if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
             traffic, traffic_src = measured_traffic("k_sr<__half, 16, 2, 2, 0" if sr else "k_stencil<__half, 1")
-        passes = roofline.passes_per_iter(sch, const_op and sr)
-        bpi = roofline.bytes_per_point_iter(pname, sch, const_op and sr)
+        passes = roofline.passes_per_iter(sch, const_op)
+        bpi = roofline.bytes_per_point_iter(pname, sch, const_op)
         # whole step against the schedule's algorithmic bytes (classic: SURVEY 8(d)'s 29 passes)
         whole_gbs = npts_local * r["iters_done"] * bpi / (r["t_ms"] / 1e3) / 1e9
         whole_gbs_v = r["value"] / n * bpi  # Gpt-iter/s per GPU x B/pt-iter = GB/s
@@ -529,8 +526,10 @@ def run_sten(args):
         return 0
 
     h = recs[head]
-    sched_names = {"classic": "Alg. 1 as printed (PAPER.md:172-186): H1, H2, H3, 3 reductions, 29 passes",
-                   "sr": "single-reduction sweep (DESIGN.md R19, SURVEY 8(f) NEXT-1): 19 passes, 1 reduction"}
+    pc, ps = roofline.passes_per_iter("classic", const_op), roofline.passes_per_iter("sr", const_op)
+    cnote = " (constant couplings as scalars, NEXT-4)" if const_op else ""
+    sched_names = {"classic": f"Alg. 1 as printed (PAPER.md:172-186): H1, H2, H3, 3 reductions, {pc} passes{cnote}",
+                   "sr": f"single-reduction sweep (DESIGN.md R19, SURVEY 8(f) NEXT-1): {ps} passes, 1 reduction{cnote}"}
     line = {
         "metric": METRIC, "value": h["value"], "unit": "Gpoint-iter/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": h["t_ms"] / args.steps, "higher_is_better": True,

@@ -156,10 +156,11 @@ int stencil_create(int nx, int ny, int nz_global, const void *const coeffs[7], i
  * Poisson stencil of BASELINE config 1): coeffs[0..6] = a_P, A_xm, A_xp,
  * A_ym, A_yp, A_zm, A_zp, the same at every point, with Dirichlet zero outside
  * the global mesh (couplings leaving it dropped, a_P unchanged: R5).  The
- * coefficient arrays are still built (for the classic schedule and
- * stencil_apply), but the SR sweep then reads none of them: it takes the six
+ * coefficient arrays are still built (for non-default classic tilings and
+ * STEN_OPT_CLASSIC_CONST = 0), but the SR sweep reads none of them: it takes the six
  * scaled couplings (A_d / a_P in fp64, rounded once to fp32 / fp16) as
- * scalars and moves 13 instead of 19 arrays per iteration.  Results equal those
+ * scalars and moves 13 instead of 19 arrays per iteration, and so do the
+ * classic kernels (17 instead of 29; STEN_OPT_CLASSIC_CONST).  Results equal those
  * of stencil_create on the same constant fields (bitwise up to the sign of
  * zero).  Errors: STEN_EINVAL (non-finite coefficient, a_P == 0, sizes),
  * STEN_ENOMEM, STEN_ECUDA. */
@@ -278,7 +279,16 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
  *                              communicators use it directly; across ranks it
  *                              needs sten_p2p_import (else the handle keeps the
  *                              NCCL exchange).  Bitwise equal to the serial
- *                              exchange (same sum order).  0 or 1 (default 0). */
+ *                              exchange (same sum order).  0 or 1 (default 0).
+ *   STEN_OPT_CLASSIC_CONST     constant-coefficient handles (stencil_create_const),
+ *                              classic schedule and stencil_apply with the default
+ *                              tiling: 1 = the tile kernels take the six scaled
+ *                              couplings as scalars and read no coefficient
+ *                              tiles (H1 12 -> 6 passes, H2 10 -> 4: 17 per
+ *                              iteration instead of 29);
+ *                              0 = they read the coefficient arrays.  Results
+ *                              are equal up to the sign of zero.  0 or 1
+ *                              (default 1). */
 #define STEN_OPT_TMA_L2_PROMOTION 1
 #define STEN_OPT_EW_CTAS_PER_SM 2
 #define STEN_OPT_COEF_PREFETCH 3
@@ -286,6 +296,7 @@ int sten_scalar_history(sten_stencil *st, int n, double *alpha, double *omega);
 #define STEN_OPT_SR_LIGHT_LAST 5
 #define STEN_OPT_CLASSIC_OVERLAP 6
 #define STEN_OPT_CLASSIC_FUSED 7
+#define STEN_OPT_CLASSIC_CONST 8
 int sten_set_option(sten_stencil *st, int option, int value);
 int sten_get_option(sten_stencil *st, int option, int *value);
 

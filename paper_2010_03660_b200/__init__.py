@@ -25,7 +25,7 @@ SCHED_SR = 1
 DOTS_MIXED, DOTS_HALF = 0, 1
 XCHG_SERIAL, XCHG_OVERLAP, XCHG_FUSED = 0, 1, 2
 (OPT_TMA_L2_PROMOTION, OPT_EW_CTAS_PER_SM, OPT_COEF_PREFETCH, OPT_SR_L2_PREFETCH, OPT_SR_LIGHT_LAST,
- OPT_CLASSIC_OVERLAP, OPT_CLASSIC_FUSED) = 1, 2, 3, 4, 5, 6, 7
+ OPT_CLASSIC_OVERLAP, OPT_CLASSIC_FUSED, OPT_CLASSIC_CONST) = 1, 2, 3, 4, 5, 6, 7, 8
 DT_F64 = 0
 DT_F32 = 1
 

@@ -218,6 +218,7 @@ struct sten_stencil {
   bool sr_light = true;         // SR, one slab: last sweep without its SpMVs (STEN_OPT_SR_LIGHT_LAST)
   bool cls_overlap = true;      // classic, decomposed: halo exchange overlapped with the interior (STEN_OPT_CLASSIC_OVERLAP)
   bool cls_fuse = false;        // classic, decomposed: fused peer-memory exchange + all-reduce (STEN_OPT_CLASSIC_FUSED)
+  bool cls_const = true;        // constant operator: classic kernels with scalar couplings (STEN_OPT_CLASSIC_CONST)
   void (*barrier_fn)(void *) = nullptr;  // host lockstep of several ranks on ONE GPU (sten_set_host_barrier)
   void *barrier_ctx = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -490,6 +491,17 @@ static int launch_stencil(sten_stencil *st, int prec, int mode, int slab, int pa
     }
   }
   if (a.zhi <= a.zlo) return STEN_OK;
+  // constant operator (NEXT-4): the couplings as scalars, no coefficient tiles (17 instead of 29 passes
+  // per iteration); the default tile geometry only - any other tiling reads the coefficient arrays
+  if (st->cc && st->cls_const && !t.rows && t.by == 16 && t.stages == 2 && t.cstages == 2 &&
+      !(prec == STEN_MIXED && st->half_dots && mode != MODE_APPLY)) {
+    a.cc = 1;
+    for (int d = 0; d < 6; ++d) {  // the same roundings as k_create_coeffs: fp64 quotient, RN once
+      a.cf32[d] = (float)st->cscaled[d];
+      __half_raw hr = __half(__double2half(st->cscaled[d]));
+      a.cf16[d] = hr.x;
+    }
+  }
   if (prec == STEN_MIXED && st->half_dots && mode != MODE_APPLY) {  // half dots (R22, R28): one chunk plan
     if (t.rows || fused) return set_err(STEN_EUNSUPPORTED, "half dots: the tile kernels without the fused exchange");
     KLAUNCH(stencil_launch_half(mode, a, t.by, t.stages, t.cstages, s));
@@ -1736,6 +1748,10 @@ int sten_set_option(sten_stencil *st, int option, int value) {
       if (value != 0 && value != 1) return set_err(STEN_EINVAL, "classic fused exchange must be 0 or 1 (got %d)", value);
       st->cls_fuse = value != 0;
       break;
+    case STEN_OPT_CLASSIC_CONST:
+      if (value != 0 && value != 1) return set_err(STEN_EINVAL, "classic constant couplings must be 0 or 1 (got %d)", value);
+      st->cls_const = value != 0;
+      break;
     default:
       return set_err(STEN_EINVAL, "unknown option %d", option);
   }
@@ -1753,6 +1769,7 @@ int sten_get_option(sten_stencil *st, int option, int *value) {
     case STEN_OPT_SR_LIGHT_LAST: *value = st->sr_light ? 1 : 0; break;
     case STEN_OPT_CLASSIC_OVERLAP: *value = st->cls_overlap ? 1 : 0; break;
     case STEN_OPT_CLASSIC_FUSED: *value = st->cls_fuse ? 1 : 0; break;
+    case STEN_OPT_CLASSIC_CONST: *value = st->cls_const ? 1 : 0; break;
     default: return set_err(STEN_EINVAL, "unknown option %d", option);
   }
   return STEN_OK;

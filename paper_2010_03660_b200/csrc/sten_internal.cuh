@@ -90,6 +90,11 @@ struct alignas(64) StencilArgs {
   // fused exchange (H1): interior plane 0 of out0 / out1 also to peer_lo[i] (the lower z-neighbour's
   // top halo plane), plane nz-1 to peer_hi[i] (the upper one's bottom halo plane); null: none
   void *peer_lo[2], *peer_hi[2];
+  // constant-coefficient operator (stencil_create_const, NEXT-4): cc != 0 selects the kernels that
+  // take the six scaled couplings as scalars (fp32 / fp16 bits) and read no coefficient tiles
+  int cc;
+  float cf32[6];
+  uint16_t cf16[6];
   Reduce red;
 };
 

@@ -51,16 +51,18 @@ struct Geo {
 
 // SC > 0: the six coefficient tiles (and rhat for H1) of a plane arrive by TMA
 // into an SC-stage ring (no per-thread global loads on misaligned rows)
-template <typename T, int MODE, int BY>
+// (CC: constant couplings - only rhat's tile for H1, none for H2 / APPLY)
+template <typename T, int MODE, int BY, bool CC = false>
 struct CGeo {
-  static constexpr int NC = MODE == MODE_H1 ? 7 : 6;                                   // tiles per plane
+  static constexpr int NC = CC ? (MODE == MODE_H1 ? 1 : 0) : (MODE == MODE_H1 ? 7 : 6);  // tiles per plane
+  static constexpr int RH = CC ? 0 : 6;                                                 // rhat's tile index
   static constexpr int XE = align128c(tile_bx<T>() * BY * (int)sizeof(T)) / (int)sizeof(T);  // elements per tile
 };
 
-template <typename T, int MODE, int BY, int S, int SC = 0>
+template <typename T, int MODE, int BY, int S, int SC = 0, bool CC = false>
 constexpr size_t smem_bytes_c() {
   using G = Geo<T, MODE, BY>;
-  using C = CGeo<T, MODE, BY>;
+  using C = CGeo<T, MODE, BY, CC>;
   return 128 /* mbarriers */ + (size_t)S * G::NIN * G::HBYTES + 3 * (size_t)G::HBYTES +
          (size_t)SC * C::NC * C::XE * sizeof(T);
 }
@@ -112,14 +114,43 @@ __device__ __forceinline__ float pencil_sum(const Pack<__half> &h) {
 }
 __device__ __forceinline__ float pencil_sum(const Pack<float> &h) { return (h.v[0] + h.v[1]) + (h.v[2] + h.v[3]); }
 
-template <typename T, int MODE, int BY, int S, int SC, bool FU = false, bool HD = false>
+// constant couplings as packs, and "keep the first n lanes" (CC outputs outside the mesh are 0)
+template <typename T> struct CcPack;
+template <> struct CcPack<float> {
+  static __device__ __forceinline__ Pack<float> splat(const StencilArgs &a, int d) {
+    const float c = a.cf32[d];
+    return Pack<float>{{c, c, c, c}};
+  }
+  static __device__ __forceinline__ Pack<float> keep(const Pack<float> &v, int n) {
+    Pack<float> o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o.v[i] = i < n ? v.v[i] : 0.0f;
+    return o;
+  }
+};
+template <> struct CcPack<__half> {
+  static __device__ __forceinline__ Pack<__half> splat(const StencilArgs &a, int d) {
+    const uint32_t h = a.cf16[d];
+    return Pack<__half>{{h | (h << 16), h | (h << 16), h | (h << 16), h | (h << 16)}};
+  }
+  static __device__ __forceinline__ Pack<__half> keep(const Pack<__half> &v, int n) {
+    Pack<__half> o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o.w[i] = v.w[i] & ((2 * i < n ? 0x0000FFFFu : 0u) | (2 * i + 1 < n ? 0xFFFF0000u : 0u));
+    return o;
+  }
+};
+
+template <typename T, int MODE, int BY, int S, int SC, bool FU = false, bool HD = false, bool CC = false>
 __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __grid_constant__ StencilArgs a) {
   using P = Pack<T>;
   using G = Geo<T, MODE, BY>;
-  using CG = CGeo<T, MODE, BY>;
+  using CG = CGeo<T, MODE, BY, CC>;
   constexpr int VEC = G::VEC, BX = G::BX, H = G::H, HW = G::HW, NIN = G::NIN;
   constexpr int HSTR = G::HBYTES / (int)sizeof(T);  // elements between halo boxes
   constexpr int ND = MODE == MODE_H2 ? 2 : 1;
+  static_assert(!CC || SC > 0, "the constant-coefficient kernels take rhat through the tile ring");
 
   if (MODE != MODE_APPLY && st_idle(a.red.st)) return;
 
@@ -160,11 +191,13 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   __syncthreads();
 
   auto issue_c = [&](int k) {  // coefficient (+ rhat) tiles of plane k, one thread
+    if (CG::NC == 0) return;
     const int s = (k - z0) % (SC > 0 ? SC : 1);
     mbar_expect_tx(&mbar[S + s], CG::NC * BX * BY * (uint32_t)sizeof(T));
+    if (!CC)
 #pragma unroll
-    for (int d = 0; d < 6; ++d) tma_load_3d(CF + (s * CG::NC + d) * CG::XE, &a.tm_c[d], x0, y0, k, &mbar[S + s]);
-    if (MODE == MODE_H1) tma_load_3d(CF + (s * CG::NC + 6) * CG::XE, &a.tm_aux, x0, y0, k + 1, &mbar[S + s]);
+      for (int d = 0; d < 6; ++d) tma_load_3d(CF + (s * CG::NC + d) * CG::XE, &a.tm_c[d], x0, y0, k, &mbar[S + s]);
+    if (MODE == MODE_H1) tma_load_3d(CF + (s * CG::NC + CG::RH) * CG::XE, &a.tm_aux, x0, y0, k + 1, &mbar[S + s]);
   };
   auto issue = [&](int q) {  // planes z0-1+q of every halo'd operand, one thread
     const int s = q % S, p = z0 - 1 + q;
@@ -245,7 +278,15 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
   for (int k = z0; k < z1; ++k) {
     const int qc = k - z0 + 1, qn = qc + 1;
     P c[6], rh;
-    if (SC > 0) {  // this plane's tiles from the ring (slot refilled after the barrier below)
+    if (CC) {  // constant couplings; rhat (H1) from the ring
+#pragma unroll
+      for (int d = 0; d < 6; ++d) c[d] = CcPack<T>::splat(a, d);
+      if (MODE == MODE_H1) {
+        const int cs = (k - z0) % (SC > 0 ? SC : 1);
+        mbar_wait(&mbar[S + cs], (uint32_t)(((k - z0) / (SC > 0 ? SC : 1)) & 1));
+        rh = P::ld(CF + cs * CG::NC * CG::XE + ry * BX + cx * VEC);
+      }
+    } else if (SC > 0) {  // this plane's tiles from the ring (slot refilled after the barrier below)
       const int cs = (k - z0) % (SC > 0 ? SC : 1);
       mbar_wait(&mbar[S + cs], (uint32_t)(((k - z0) / (SC > 0 ? SC : 1)) & 1));
       const T *cf = CF + cs * CG::NC * CG::XE + ry * BX + cx * VEC;
@@ -277,6 +318,9 @@ __global__ void __launch_bounds__(Geo<T, MODE, BY>::NT, 2) k_stencil(const __gri
     acc = P::fma(c[3], P::ld(Uc + hown + HW), acc);
     acc = P::fma(c[4], um, acc);
     acc = P::fma(c[5], up, acc);
+    // CC: the couplings are not zero outside the mesh (the arrays' are), so points past nx / ny
+    // would see their in-mesh neighbours: they are 0 here, as the array kernels compute them
+    if (CC) acc = inside ? CcPack<T>::keep(acc, a.g.nx - gx) : P::zero();
     if (inside) {
       const long long o = (long long)(k + 1) * a.g.plane + gofs;
       acc.st(reinterpret_cast<T *>(a.out0) + o);
@@ -540,23 +584,27 @@ template int rows_threads<__half>(int, int);
 
 // ------------------------------------------------------------ host side --
 namespace {
-template <typename T, int MODE, int BY, int S, int SC = 0, bool FU = false, bool HD = false>
+template <typename T, int MODE, int BY, int S, int SC = 0, bool FU = false, bool HD = false, bool CC = false>
 int launch_one(const StencilArgs &a, cudaStream_t s) {
   using G = Geo<T, MODE, BY>;
-  constexpr size_t smem = smem_bytes_c<T, MODE, BY, S, SC>();
+  constexpr size_t smem = smem_bytes_c<T, MODE, BY, S, SC, CC>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC, FU, HD>,
+    cudaError_t e = cudaFuncSetAttribute(k_stencil<T, MODE, BY, S, SC, FU, HD, CC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
   const int grid = a.tiles_x * a.tiles_y * ((a.zhi - a.zlo + a.zc - 1) / a.zc);
-  k_stencil<T, MODE, BY, S, SC, FU, HD><<<grid, G::NT, smem, s>>>(a);
+  k_stencil<T, MODE, BY, S, SC, FU, HD, CC><<<grid, G::NT, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 template <typename T, int MODE>
 int launch_mode(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
+  if (a.cc) {  // constant couplings: the default tiling only
+    if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE, 16, 2, 2, false, false, true>(a, s);
+    return (int)cudaErrorNotSupported;
+  }
   if (cstages) {  // coefficient tiles by TMA
     if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE, 16, 2, 2>(a, s);
     if (by == 16 && stages == 3 && cstages == 1) return launch_one<T, MODE, 16, 3, 1>(a, s);
@@ -609,7 +657,8 @@ int stencil_threads(int by) {
 
 template <typename T>
 int stencil_launch_fused(const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {
-  if (by == 16 && stages == 2 && cstages == 2) return launch_one<T, MODE_H1, 16, 2, 2, true>(a, s);
+  if (by == 16 && stages == 2 && cstages == 2)
+    return a.cc ? launch_one<T, MODE_H1, 16, 2, 2, true, false, true>(a, s) : launch_one<T, MODE_H1, 16, 2, 2, true>(a, s);
   return (int)cudaErrorNotSupported;
 }
 int stencil_launch_half(int mode, const StencilArgs &a, int by, int stages, int cstages, cudaStream_t s) {

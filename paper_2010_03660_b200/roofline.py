@@ -28,14 +28,17 @@ ELEM_BYTES = {"fp32": 4, "mixed": 2}
 PASSES_SR = 19
 
 
-# constant-coefficient operator (stencil_create_const): the SR sweep reads no coefficient arrays
+# constant-coefficient operator (stencil_create_const): no coefficient
+# arrays are read - the SR sweep 13 passes, the classic phases H1 6, H2 4, H3 7 = 17
 PASSES_SR_CONST = PASSES_SR - 6
+PASSES_CONST = {"H1": PASSES["H1"] - 6, "H2": PASSES["H2"] - 6, "H3": PASSES["H3"]}
+PASSES_PER_ITER_CONST = sum(PASSES_CONST.values())  # 17
 
 
 def passes_per_iter(schedule: str = "classic", const_op: bool = False) -> int:
     if schedule == "sr":
         return PASSES_SR_CONST if const_op else PASSES_SR
-    return PASSES_PER_ITER
+    return PASSES_PER_ITER_CONST if const_op else PASSES_PER_ITER
 
 
 def bytes_per_point_iter(precision: str, schedule: str = "classic", const_op: bool = False) -> int:
@@ -46,5 +49,5 @@ def sweep_bytes(precision: str, npoints: int, const_op: bool = False) -> int:
     return (PASSES_SR_CONST if const_op else PASSES_SR) * ELEM_BYTES[precision] * npoints
 
 
-def phase_bytes(phase: str, precision: str, npoints: int) -> int:
-    return PASSES[phase] * ELEM_BYTES[precision] * npoints
+def phase_bytes(phase: str, precision: str, npoints: int, const_op: bool = False) -> int:
+    return (PASSES_CONST if const_op else PASSES)[phase] * ELEM_BYTES[precision] * npoints
