@@ -67,6 +67,8 @@ def parse():
     p.add_argument("--tiling", default="", help="bx,by,zc,stages override (classic)")
     p.add_argument("--sr-tiling", default="", help="by,stages,cstages,zc override (sr)")
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
+    p.add_argument("--set-option", action="append", default=[], metavar="NAME=V",
+                   help="sten_set_option before the run, e.g. TMA_L2_PROMOTION=0 (experiments)")
     p.add_argument("--no-2d", action="store_true", help="skip the labelled NEXT-3 field (2D 9-point BiCGStab at "
                                                          "the paper's 22800 x 22800, PAPER.md:371-373)")
     return p.parse_args()
@@ -448,6 +450,9 @@ def run_sten(args):
         sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
     if args.dots == "half":
         sten.set_dot_precision(st, sten.DOTS_HALF)
+    for kv in args.set_option:
+        name, val = kv.split("=")
+        sten.set_option(st, getattr(sten, "OPT_" + name), int(val))
     if world > 1 and os.environ.get("STEN_P2P", "0") == "1":
         # fused compute + collective over peer memory across ranks (opt-in): the SR sweep's and the
         # classic phase kernels' own halo stores and inbox deposits (STEN_OPT_CLASSIC_FUSED)
@@ -540,6 +545,7 @@ def run_sten(args):
                    "precision": pname, "schedule": head, "schedule_is": sched_names[head],
                    "operator": args.operator,
                    **({"dots": "half"} if args.dots == "half" and prec == sten.MIXED else {}),
+                   **({"options": args.set_option} if args.set_option else {}),
                    "maxit": args.maxit, "tol": args.tol,
                    "iters_per_solve": h["iters_done"] / args.steps,
                    "parallelism": f"zslab{n}",
