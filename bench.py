@@ -69,6 +69,8 @@ def parse():
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
     p.add_argument("--set-option", action="append", default=[], metavar="NAME=V",
                    help="sten_set_option before the run, e.g. TMA_L2_PROMOTION=0 (experiments)")
+    p.add_argument("--no-tts", action="store_true", help="skip the labelled time-to-solution field (1e-6: fp32 "
+                   "BiCGStab vs mixed refinement)")
     p.add_argument("--no-2d", action="store_true", help="skip the labelled NEXT-3 field (2D 9-point BiCGStab at "
                                                          "the paper's 22800 x 22800, PAPER.md:371-373)")
     return p.parse_args()
@@ -364,6 +366,37 @@ def run_schedule(sten, st, prec, schedule, b, x, args, world, sdist, npts, clock
             "hist_10": float(hist[min(10, len(hist) - 1)]), "clocks": clk}
 
 
+def run_tts(sten, st, b, tol=1e-6):
+    """Labelled field: time to ||r||/||b|| <= tol on the bench's system (cfg 3, delta = 0.1) - fp32
+    BiCGStab (Alg. 1) against the mixed iterative refinement (R21: fp32 residual and update, fp16
+    inner solves of Alg. 1 to 1e-2; NEXT-2): the fp16 bandwidth carried to an
+    fp32-accurate answer.  One warm-up call each (graph capture), then one timed call; the library
+    synchronises its stream before returning, so the host clock around the call is the device time
+    plus the call overhead."""
+    import torch
+    sten.set_schedule(st, sten.SCHED_CLASSIC)
+    b32 = b.float()
+    x32 = torch.empty_like(b32)
+    out = {"tol": tol, "schedule": "classic", "clock": "host wall clock around the (synchronising) call"}
+    sten.bicgstab_solve(st, sten.FP32, b32, None, tol, 500, x32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    it, hist, status = sten.bicgstab_solve(st, sten.FP32, b32, None, tol, 500, x32)
+    ms = (time.perf_counter() - t0) * 1e3
+    out["fp32_bicgstab"] = {"ms": ms, "iters": it, "rel_residual": float(hist[-1]), "status": int(status)}
+    sten.bicgstab_refine(st, b32, None, tol, 30, 1e-2, 200, x32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ko, ki, rh, status = sten.bicgstab_refine(st, b32, None, tol, 30, 1e-2, 200, x32)
+    ms = (time.perf_counter() - t0) * 1e3
+    out["mixed_refinement"] = {"ms": ms, "outer_steps": ko, "fp16_iters": ki, "true_rel_residual_fp32": float(rh[-1]),
+                               "status": int(status), "inner_tol": 1e-2}
+    out["speedup_vs_fp32"] = out["fp32_bicgstab"]["ms"] / ms
+    del b32, x32
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_2d(sten, icuda, peak, n=22800, maxit=100):
     """The labelled NEXT-3 field: BiCGStab on the 2D 9-point operator at the paper's 22800 x 22800
     (R25), mixed fp16, `maxit` iterations at tol = 0, on the seeded 2D
@@ -575,6 +608,8 @@ def run_sten(args):
                      "rel_residual_iter10": r["hist_10"], "events": r["events"],
                      "roofline": roofline_of(sch, r), "gpu_launches": int(r["launches"]),
                      **({"e2e": e2e[sch]} if sch in e2e else {})}
+    if not args.no_tts and world == 1 and prec == sten.MIXED and not const_op and workload == "cfg3":
+        line["time_to_solution"] = run_tts(sten, st, b)
     if not args.no_2d and world == 1 and prec == sten.MIXED:
         del st, b, x
         torch.cuda.empty_cache()
