@@ -66,6 +66,7 @@ def parse():
                         "(no coefficient streams in the SR sweep, NEXT-4)")
     p.add_argument("--tiling", default="", help="bx,by,zc,stages override (classic)")
     p.add_argument("--sr-tiling", default="", help="by,stages,cstages,zc override (sr)")
+    p.add_argument("--sr-chunks", default="", help="zc,tail_planes,zc_tail: SR chunk plan override (experiments)")
     p.add_argument("--cpu-planes", type=int, default=0, help="oracle sample planes (0 = auto)")
     p.add_argument("--set-option", action="append", default=[], metavar="NAME=V",
                    help="sten_set_option before the run, e.g. TMA_L2_PROMOTION=0 (experiments)")
@@ -481,6 +482,8 @@ def run_sten(args):
         sten.set_tiling(st, prec, bx, by, zc, stg)
     if args.sr_tiling:
         sten.set_sr_tiling(st, prec, *(int(v) for v in args.sr_tiling.split(",")))
+    if args.sr_chunks:
+        sten.set_sr_chunks(st, prec, *(int(v) for v in args.sr_chunks.split(",")))
     if args.dots == "half":
         sten.set_dot_precision(st, sten.DOTS_HALF)
     for kv in args.set_option:
@@ -514,7 +517,8 @@ def run_sten(args):
         tname = "half" if prec == sten.MIXED else "float"
         kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
         traffic, traffic_src = (None, None)
-        if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not const_op:
+        if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not args.sr_chunks \
+                and not const_op:
             traffic, traffic_src = measured_traffic("k_sr<__half, 16, 2, 2, 0" if sr else "k_stencil<__half, 1")
         passes = roofline.passes_per_iter(sch, const_op)
         bpi = roofline.bytes_per_point_iter(pname, sch, const_op)
@@ -579,6 +583,7 @@ def run_sten(args):
                    "operator": args.operator,
                    **({"dots": "half"} if args.dots == "half" and prec == sten.MIXED else {}),
                    **({"options": args.set_option} if args.set_option else {}),
+                   **({"sr_chunks": args.sr_chunks} if args.sr_chunks else {}),
                    "maxit": args.maxit, "tol": args.tol,
                    "iters_per_solve": h["iters_done"] / args.steps,
                    "parallelism": f"zslab{n}",
