@@ -12,6 +12,10 @@ NPTS3 = 600 * 595 * 1536
 NPTS2 = 22800 * 22800
 # kernel-name prefix -> (passes, element bytes, points)
 ALGO = [
+    # the constant-coefficient (scalar-coupling, CC = last template argument 1) classic kernels: 6 / 4 passes
+    ("k_stencil<__half, 1, 16, 2, 2, 0, 0, 1>", 6, 2, NPTS3), ("k_stencil<__half, 2, 16, 2, 2, 0, 0, 1>", 4, 2, NPTS3),
+    ("k_stencil<float, 1, 16, 2, 2, 0, 0, 1>", 6, 4, NPTS3), ("k_stencil<float, 2, 16, 2, 2, 0, 0, 1>", 4, 4, NPTS3),
+    ("k_h3s_half<", 7, 2, NPTS3),
     ("k_stencil<__half, 1,", 12, 2, NPTS3), ("k_stencil<__half, 2,", 10, 2, NPTS3),
     ("k_stencil<float, 1,", 12, 4, NPTS3), ("k_stencil<float, 2,", 10, 4, NPTS3),
     ("k_h3_bulk<__half", 7, 2, NPTS3), ("k_h3<__half", 7, 2, NPTS3),
@@ -31,7 +35,8 @@ def algo(name):
 
 
 def main(tag, files):
-    out = {"source": "ncu --set full --clock-control none, full-size launches (tools/profile_r2.sh)", "kernels": {}}
+    out = {"source": "ncu --set full --clock-control none, full-size launches (tools/profile_r2.sh, "
+                     "tools/profile_cc.sh)", "kernels": {}}
     for fn in files:
         rows = list(csv.reader(open(fn)))
         hdr, units, data = rows[0], rows[1], rows[2:]
