@@ -234,11 +234,13 @@ def test_classic_half_dot_solve_history(sten, mesh, delta, nhist):
     st.close()
 
 
-def test_classic_half_first_iteration_vectors(sten):
+@pytest.mark.parametrize("mesh", [(70, 37, 50), (130, 33, 45), (600, 7, 9)])
+def test_classic_half_first_iteration_vectors(sten, mesh):
     """x_1 of the classic half solve within one fp16 ulp of o16h_bicgstab's (every vector op is the
-    oracle's; alpha_1, omega_1 come from pencils whose fp32 sum order differs)."""
+    oracle's; alpha_1, omega_1 come from pencils whose fp32 sum order differs).  The two larger
+    planes span two of k_h3s_half's 384-vector segments (the second one partial)."""
     torch = torch_cuda()
-    nx, ny, nz = 70, 37, 50
+    nx, ny, nz = mesh
     diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=4)
     b16 = orc.f16_from_double(inputs.rhs_uniform(nx, ny, nz, seed=4))
     st = gpu_stencil(diag, offs)
@@ -247,11 +249,13 @@ def test_classic_half_first_iteration_vectors(sten):
     assert seg == list(range(0, nz, seg[1] if len(seg) > 1 else nz))
     bt = to_gpu_vec(b16, "mixed")
     xt = torch.empty_like(bt)
-    sten.bicgstab_solve(st, MIXED, bt, None, 0.0, 1, xt)
+    _, hist, _ = sten.bicgstab_solve(st, MIXED, bt, None, 0.0, 1, xt)
     c16 = oracle_coeffs(diag, offs, "mixed")
     ref = orc.bicgstab16(c16, orc.scale_rhs(b16, diag, "mixed"), tol=0.0, maxit=1, segments=seg)
     xg, xo = widen(from_gpu_vec(xt, "mixed"), "mixed"), widen(ref["x"], "mixed")
     assert np.all(np.abs(xg - xo) <= np.spacing(np.abs(xo).astype(np.float16)).astype(np.float64) + 1e-12)
+    # hist[1] = sqrt((r_1, r_1)) / ||b||: H3's (r,r) pencils over the same segments, summed in another order
+    assert abs(hist[1] - ref["hist"][1]) <= 1e-3 * ref["hist"][1], (hist[1], ref["hist"][1])
     st.close()
 
 
