@@ -162,9 +162,9 @@ template <int NB> struct SPack<float, NB> {
     return o;
   }
   static __device__ __forceinline__ SPack fma(const SPack &a, const SPack &b, const SPack &c) {
-    SPack o;
+    SPack o;  // FFMA2: two RN fp32 FMAs per instruction, lane for lane __fmaf_rn
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) o.v[i] = __fmaf_rn(a.v[i], b.v[i], c.v[i]);
+    for (int i = 0; i < VEC; i += 2) ffma2(o.v[i], o.v[i + 1], a.v[i], a.v[i + 1], b.v[i], b.v[i + 1], c.v[i], c.v[i + 1]);
     return o;
   }
   static __device__ __forceinline__ S scalar(float a) { return a; }
@@ -172,7 +172,7 @@ template <int NB> struct SPack<float, NB> {
   static __device__ __forceinline__ SPack fmas(S a, const SPack &b, const SPack &c) {
     SPack o;
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) o.v[i] = __fmaf_rn(a, b.v[i], c.v[i]);
+    for (int i = 0; i < VEC; i += 2) ffma2(o.v[i], o.v[i + 1], a, a, b.v[i], b.v[i + 1], c.v[i], c.v[i + 1]);
     return o;
   }
   __device__ __forceinline__ float mdot(const SPack &b, float acc) const {

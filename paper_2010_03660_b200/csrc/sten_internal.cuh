@@ -116,6 +116,26 @@ struct EwArgs {           // element-wise kernels (H3, INIT)
 };
 
 // ---------------------------------------------------------------- packs --
+// Two IEEE fp32 fused multiply-adds in one instruction (FFMA2, sm_100): d_i = rn(a_i * b_i + c_i),
+// lane for lane the result of __fmaf_rn - half the issue slots of the fp32 element-wise work.
+#ifndef STEN_FFMA2
+#define STEN_FFMA2 1  // 0: two scalar FFMA (the experiment baseline; bitwise the same results)
+#endif
+__device__ __forceinline__ void ffma2(float &d0, float &d1, float a0, float a1, float b0, float b1, float c0,
+                                      float c1) {
+  if (!STEN_FFMA2) {
+    d0 = __fmaf_rn(a0, b0, c0);
+    d1 = __fmaf_rn(a1, b1, c1);
+    return;
+  }
+  unsigned long long ra, rb, rc, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c0), "f"(c1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(rd));
+}
+
 template <typename T> struct Pack;
 
 template <> struct Pack<float> {
@@ -144,7 +164,7 @@ template <> struct Pack<float> {
   static __device__ __forceinline__ Pack fma(const Pack &a, const Pack &b, const Pack &c) {
     Pack o;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o.v[i] = __fmaf_rn(a.v[i], b.v[i], c.v[i]);
+    for (int i = 0; i < 4; i += 2) ffma2(o.v[i], o.v[i + 1], a.v[i], a.v[i + 1], b.v[i], b.v[i + 1], c.v[i], c.v[i + 1]);
     return o;
   }
   static __device__ __forceinline__ S scalar(float a) { return a; }
@@ -152,7 +172,7 @@ template <> struct Pack<float> {
   static __device__ __forceinline__ Pack fmas(S a, const Pack &b, const Pack &c) {
     Pack o;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o.v[i] = __fmaf_rn(a, b.v[i], c.v[i]);
+    for (int i = 0; i < 4; i += 2) ffma2(o.v[i], o.v[i + 1], a, a, b.v[i], b.v[i + 1], c.v[i], c.v[i + 1]);
     return o;
   }
   static __device__ __forceinline__ Pack sub(const Pack &a, const Pack &b) {
@@ -169,8 +189,8 @@ template <> struct Pack<float> {
   }
   // four independent partial sums (short dependency chains)
   __device__ __forceinline__ void dot4(const Pack &b, float (&acc)[4]) const {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = __fmaf_rn(v[i], b.v[i], acc[i]);
+    ffma2(acc[0], acc[1], v[0], v[1], b.v[0], b.v[1], acc[0], acc[1]);
+    ffma2(acc[2], acc[3], v[2], v[3], b.v[2], b.v[3], acc[2], acc[3]);
   }
   __device__ __forceinline__ float mdot(const Pack &b, float acc) const { return dot(b, acc); }
 };
