@@ -44,7 +44,8 @@ def main(tag="r1"):
         run(st, b1, sched, "1: 32^3 Poisson (fields)", rows)
     st.close()
     stc = sten.stencil_create_const(n, n, n, (6.0, -1, -1, -1, -1, -1, -1))
-    run(stc, b1, sten.SCHED_SR, "1: 32^3 Poisson (constant operator)", rows)
+    for sched in (sten.SCHED_SR, sten.SCHED_CLASSIC):
+        run(stc, b1, sched, "1: 32^3 Poisson (constant operator)", rows)
     stc.close()
     n = 128  # config 2: convection-diffusion, delta = 0.1
     diag, offs = inputs.problem_fields(inputs.KIND_CD, n, n, n, seed=1, delta=0.1)
