@@ -580,7 +580,7 @@ static int launch_h3(sten_stencil *st, int prec, int slab, int parity, cudaStrea
     h.tiles_x = (st->nx + t.bx - 1) / t.bx;
     h.tiles_y = (st->ny + t.by - 1) / t.by;
     h.red = a.red;
-    if (h3z_half_grid(st->sm, h.tiles_x * h.tiles_y, sl.nz, h.zc) > st->partials_cap)
+    if (h3z_half_grid(st->sm, h) > st->partials_cap)
       return set_err(STEN_ECUDA, "internal: H3 grid exceeds the partial-sum buffer");
     KLAUNCH(h3z_half_launch(h, t.by, s));
     st->launches++;

@@ -9,6 +9,8 @@
 //    fp16 (R3, R5).
 #include "sten_internal.cuh"
 
+#include <algorithm>
+
 namespace sten {
 
 // ------------------------------------------------------------------ H3 --
@@ -210,7 +212,11 @@ int h3_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  k_h3_bulk<T, STEN_H3_SEGV, STEN_H3_NS><<<device_sm_count() * STEN_H3_CPS, 256, smem, s>>>(a);
+  // persistent CTAs, but no more than there are segments (a small mesh would otherwise launch idle CTAs
+  // that still take part in the last-CTA reduction)
+  const long long nseg = (a.nvec + STEN_H3_SEGV - 1) / STEN_H3_SEGV;
+  const int g = (int)std::max(1LL, std::min((long long)device_sm_count() * STEN_H3_CPS, nseg));
+  k_h3_bulk<T, STEN_H3_SEGV, STEN_H3_NS><<<g, 256, smem, s>>>(a);
 #else
   k_h3<T><<<grid, threads, 0, s>>>(a);
 #endif

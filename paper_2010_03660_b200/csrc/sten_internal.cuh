@@ -578,7 +578,7 @@ struct H3zArgs {
   Reduce red;
 };
 int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s);
-int h3z_half_grid(int sm_count, int tiles, int nz, int zc);  // CTAs of h3z_half_launch
+int h3z_half_grid(int sm_count, const H3zArgs &a);  // CTAs of h3z_half_launch
 template <typename T> size_t stencil_smem_bytes(int mode, int by, int stages);
 template <typename T> int stencil_threads(int by);
 // row-strip kernel (no x halo): a CTA owns `by` full rows; used when a row fits

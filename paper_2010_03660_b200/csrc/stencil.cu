@@ -29,6 +29,8 @@
 //    registers and reduced by the deterministic last-CTA reduction.
 #include "sten_internal.cuh"
 
+#include <algorithm>
+
 namespace sten {
 
 namespace {
@@ -831,8 +833,11 @@ __global__ void __launch_bounds__(SEGV) k_h3s_half(const __grid_constant__ H3zAr
 #define STEN_H3S_CPS 2     // k_h3s_half: CTAs per SM
 #endif
 
-int h3z_half_grid(int sm_count, int tiles, int nz, int zc) {
-  return STEN_H3Z_VARIANT == 1 ? sm_count * STEN_H3S_CPS : tiles * ((nz + zc - 1) / zc);
+int h3z_half_grid(int sm_count, const H3zArgs &a) {
+  const int nch = (a.g.nz + a.zc - 1) / a.zc;
+  if (STEN_H3Z_VARIANT != 1) return a.tiles_x * a.tiles_y * nch;
+  const long long items = (a.g.plane / 8 + STEN_H3S_SEGV - 1) / STEN_H3S_SEGV * nch;  // (segment, chunk) items
+  return (int)std::max(1LL, std::min((long long)sm_count * STEN_H3S_CPS, items));
 }
 
 int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s) {
@@ -846,7 +851,7 @@ int h3z_half_launch(const H3zArgs &a, int by, cudaStream_t s) {
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  k_h3s_half<STEN_H3S_SEGV, STEN_H3S_NS><<<device_sm_count() * STEN_H3S_CPS, STEN_H3S_SEGV, smem, s>>>(a);
+  k_h3s_half<STEN_H3S_SEGV, STEN_H3S_NS><<<h3z_half_grid(device_sm_count(), a), STEN_H3S_SEGV, smem, s>>>(a);
 #else
   const int grid = a.tiles_x * a.tiles_y * ((a.g.nz + a.zc - 1) / a.zc);
   k_h3z_half<16><<<grid, (tile_bx<__half>() / 8) * 16, 0, s>>>(a);
