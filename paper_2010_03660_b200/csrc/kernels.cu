@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(256) k_h3(const __grid_constant__ EwArgs a) {
 #ifndef STEN_H3_CPS
 #define STEN_H3_CPS 2      // k_h3_bulk: CTAs per SM
 #endif
+#ifndef STEN_H3_LDHINT
+#define STEN_H3_LDHINT 0  // k_h3_bulk: the five input streams' bulk copies with an L2 evict-first hint
+#endif
 #ifndef STEN_H3_CSST
 #define STEN_H3_CSST 1  // k_h3_bulk: streaming (.cs) stores of x, r
 #endif
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
     fence_mbar_init();
   }
   __syncthreads();
+  uint64_t pol = 0;
+  if (STEN_H3_LDHINT) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   auto issue = [&](long long i) {
     const int slot = (int)(i % NS);
     const long long v0 = (blockIdx.x + i * gridDim.x) * (long long)SEGV;
@@ -149,7 +154,10 @@ __global__ void __launch_bounds__(256) k_h3_bulk(const __grid_constant__ EwArgs 
     const uint32_t bytes = (uint32_t)(nv * 16);
     mbar_expect_tx(&bar[slot], 5u * bytes);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) bulk_g2s(ring + ((size_t)slot * 5 + k) * SEGV * VEC, src[k] + v0 * VEC, bytes, &bar[slot]);
+    for (int k = 0; k < 5; ++k) {
+      if (STEN_H3_LDHINT) bulk_g2s_hint(ring + ((size_t)slot * 5 + k) * SEGV * VEC, src[k] + v0 * VEC, bytes, &bar[slot], pol);
+      else bulk_g2s(ring + ((size_t)slot * 5 + k) * SEGV * VEC, src[k] + v0 * VEC, bytes, &bar[slot]);
+    }
   };
   if (tid == 0)
     for (long long i = 0; i < NS && i < nmine; ++i) issue(i);
