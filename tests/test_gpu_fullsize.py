@@ -253,3 +253,37 @@ def test_fullsize_loopback_slab_exchange_modes():
         srh[xm] = hist
     assert np.array_equal(srh[sten.XCHG_SERIAL], srh[sten.XCHG_FUSED])
     st.close()
+
+
+@pytest.mark.parametrize("phase", [1, 2])
+def test_fullsize_half_dot_phase(full_problem, phase):
+    """Half dots (R22, R28; `bench.py --dots half`) at 600x595x1536: the phase's vectors bitwise those
+    of the mixed-dot phase (only the sums differ), and its sums within 2e-5 of the sum of |segment
+    sums| from the oracle's exact sum of the same fp16 column pencils (dot16h) over the library's
+    chunk plan (one plan for the three phases in this mode)."""
+    torch = torch_cuda()
+    import inputs.cuda as ic
+    import paper_2010_03660_b200 as sten
+    st = full_problem
+    t = {}
+    for n, s_ in PH_STREAMS.items():
+        t[n] = ic.uniform_device(NX, NY, NZ, seed=9, stream=s_, dtype="f32").to(torch.float16)
+    outs = {}
+    for mode in (sten.DOTS_MIXED, sten.DOTS_HALF):
+        sten.set_dot_precision(st, mode)
+        try:
+            o0, o1 = torch.empty_like(t["r"]), torch.empty_like(t["r"])
+            dots = sten.classic_phase(st, sten.MIXED, phase, PH_SCAL, t["r"], t["p"], t["v"], t["rh"], o0, o1)
+            segs = sten.classic_segments(st, sten.MIXED)
+        finally:
+            sten.set_dot_precision(st, sten.DOTS_MIXED)
+        outs[mode] = (o0, o1, dots, segs)
+    o0, o1, dots, segs = outs[sten.DOTS_HALF]
+    assert torch.equal(o0.view(torch.int16), outs[sten.DOTS_MIXED][0].view(torch.int16))
+    assert torch.equal(o1.view(torch.int16), outs[sten.DOTS_MIXED][1].view(torch.int16))
+    host = lambda a: a.cpu().numpy().view(np.uint16).reshape(NZ, NY, NX)  # noqa: E731
+    h1 = host(o1)
+    pairs = [(host(t["rh"]), h1)] if phase == 1 else [(h1, host(o0)), (h1, h1)]
+    for got, (a, b) in zip(dots, pairs):
+        want, absum = orc.dot16h(a, b, segs)
+        assert abs(float(got) - want) <= 2e-5 * absum, (float(got), want, absum)
