@@ -120,3 +120,31 @@ def test_tiled_600x600_fullsize_against_gather(setup, prec):
     assert checked == 800
     # and the edge values really are the output-halo sums, not the gather's chain (some differ)
     assert not torch.equal(ug[~interior], ut[~interior])
+
+
+def test_solve_fullsize_properties():
+    """BiCGStab on the 2D operator at 22800 x 22800 (the bench's `next3_2d` configuration), mixed: the
+    tol = 1e-3 run converges in a handful of iterations, deterministically, and x's true residual
+    of the scaled system - b_hat = b / a_P and A_hat x through the library's fp32 apply, the
+    difference and the norms in fp64 - is at the mixed level (as for the small meshes)."""
+    torch = torch_cuda()
+    import inputs.cuda as icuda
+    import paper_2010_03660_b200 as sten
+    diag, offs = icuda.fields2d_device(N, N, seed=1, delta=0.1)
+    st = sten.stencil2d_create(N, N, [diag] + offs)
+    del offs
+    b64 = icuda.uniform_device(N, N, 1, seed=1, stream=0).view(N, N)
+    b16 = b64.to(torch.float16)
+    x = torch.empty_like(b16)
+    it, hist, status = sten.bicgstab2d_solve(st, sten.MIXED, b16, None, 1e-3, 100, x)
+    assert status == sten.CONVERGED and hist[-1] <= 1e-3 and it <= 20, (it, hist, status)
+    x2 = torch.empty_like(b16)
+    it2, hist2, status2 = sten.bicgstab2d_solve(st, sten.MIXED, b16, None, 1e-3, 100, x2)
+    assert (it2, status2) == (it, status) and np.array_equal(hist2, hist) and torch.equal(x2.view(torch.int16),
+                                                                                          x.view(torch.int16))
+    y = torch.empty((N, N), dtype=torch.float32, device="cuda")
+    sten.stencil2d_apply(st, sten.FP32, x.float(), y)
+    bh = (b16.double() / diag.double().view(N, N)).half().double()  # b_hat = rn16(b / a_P) (R3)
+    true = float(torch.linalg.vector_norm(bh - y.double()) / torch.linalg.vector_norm(bh))
+    assert true <= 1e-2, true
+    st.close()
