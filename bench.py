@@ -523,7 +523,8 @@ def run_sten(args):
     clk = recs[head]["clocks"]
     bad = clk and (set(clk["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
                    or (not clk["reasons"] and clk["sm_mhz"] < 0.7 * clk["sm_max_mhz"]))
-    if bad:
+    # (every rank takes the same decision: the flag is all-reduced, MAX over ranks)
+    if sdist.max_over_ranks(1.0 if bad else 0.0, device="cuda") > 0.0:
         first = clk
         recs[head] = run_schedule(sten, st, prec, head, b, x, args, world, sdist, npts, clocks_gpu=local)
         if recs[head]["clocks"] is not None:
