@@ -39,12 +39,12 @@ def _free_port():
         return so.getsockname()[1]
 
 
-def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed, schedule="sr"):
+def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed, schedule="sr", op="fields"):
     port = _free_port()
     procs = []
     for r in range(world):
         cmd = [sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), str(world), str(port),
-               str(tmp_path), prec, str(maxit), repr(tol), str(nx), str(ny), str(nz), str(seed), schedule]
+               str(tmp_path), prec, str(maxit), repr(tol), str(nx), str(ny), str(nz), str(seed), schedule, op]
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
     for p in procs:
@@ -60,12 +60,16 @@ def _run_ranks(tmp_path, world, prec, maxit, tol, nx, ny, nz, seed, schedule="sr
     return [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
 
 
-def _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, world, schedule="sr"):
+def _loopback(sten, prec, maxit, tol, nx, ny, nz, seed, world, schedule="sr", op="fields"):
     torch = torch_cuda()
-    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=seed)
     b = quantize_vec(inputs.rhs_uniform(nx, ny, nz, seed=seed), prec)
-    coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
-    st = sten.stencil_create(nx, ny, nz, coeffs, nslabs=world)
+    if op == "const":
+        from p2p_worker import CONST_SKEW
+        st = sten.stencil_create_const(nx, ny, nz, CONST_SKEW, nslabs=world)
+    else:
+        diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=0.1, seed=seed)
+        coeffs = [torch.from_numpy(diag).cuda()] + [torch.from_numpy(o).cuda() for o in offs]
+        st = sten.stencil_create(nx, ny, nz, coeffs, nslabs=world)
     if schedule == "sr":
         sten.set_schedule(st, sten.SCHED_SR)
         sten.set_sr_exchange(st, sten.XCHG_FUSED)
@@ -179,3 +183,19 @@ def test_p2p_only_comm_refuses_what_needs_nccl(sten):
     comm.close()
     with pytest.raises(sten.StenError):
         sten.comm_create(None, 2, 0, 9999)  # no such device
+
+
+@pytest.mark.parametrize("schedule", ["sr", "classic_fused"])
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_two_processes_constant_operator(sten, tmp_path, schedule, prec):
+    """The constant-coefficient kernels (scalar couplings: k_sr<CC> with its fused halo stores, the classic
+    tile kernels' CC + fused instance) across two processes, bitwise the loopback-slab solve."""
+    nx, ny, nz = 45, 33, 20
+    seed = 7
+    res = _run_ranks(tmp_path, 2, prec, 12, 0.0, nx, ny, nz, seed, schedule, "const")
+    x_ref, it_ref, h_ref, s_ref = _loopback(sten, prec, 12, 0.0, nx, ny, nz, seed, 2,
+                                            "sr" if schedule == "sr" else "classic", "const")
+    for r in res:
+        assert int(r["it"]) == it_ref and int(r["status"]) == s_ref
+        assert np.array_equal(r["hist"], h_ref)
+    assert np.array_equal(np.concatenate([r["x"] for r in res], axis=0), x_ref)
