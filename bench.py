@@ -538,14 +538,20 @@ def run_sten(args):
         tname = "half" if prec == sten.MIXED else "float"
         kname = f"k_sr<{tname}>" if sr else f"k_stencil<{tname},H1>"
         traffic, traffic_src = (None, None)
-        if prec == sten.MIXED and nzl == NZ and not args.tiling and not args.sr_tiling and not args.sr_chunks \
-                and args.dots != "half":
+        if nzl == NZ and not args.tiling and not args.sr_tiling and not args.sr_chunks and args.dots != "half":
             # the exact instance the run launches (fields / constant couplings), from the latest capture
+            # (ncu prints the defaulted template arguments of k_stencil either elided or in full)
+            tn = "__half" if prec == sten.MIXED else "float"
             if sr:
-                kpre = "k_sr<__half, 8, 3, 2, 1" if const_op else "k_sr<__half, 16, 2, 2, 0"
+                kpre = ([f"k_sr<{tn}, 8, 3, 2, 1"] if const_op and prec == sten.MIXED else
+                        [f"k_sr<{tn}, 16, 2, 2, 1"] if const_op else [f"k_sr<{tn}, 16, 2, 2, 0"])
             else:
-                kpre = "k_stencil<__half, 1, 16, 2, 2, 0, 0, 1>" if const_op else "k_stencil<__half, 1, 16, 2, 2, 0>"
-            traffic, traffic_src = measured_traffic(kpre)
+                kpre = ([f"k_stencil<{tn}, 1, 16, 2, 2, 0, 0, 1>"] if const_op else
+                        [f"k_stencil<{tn}, 1, 16, 2, 2, 0>", f"k_stencil<{tn}, 1, 16, 2, 2, 0, 0, 0>"])
+            for kp in kpre:
+                traffic, traffic_src = measured_traffic(kp)
+                if traffic is not None:
+                    break
         passes = roofline.passes_per_iter(sch, const_op)
         bpi = roofline.bytes_per_point_iter(pname, sch, const_op)
         # whole step against the schedule's algorithmic bytes (classic: SURVEY 8(d)'s 29 passes)

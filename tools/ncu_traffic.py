@@ -18,6 +18,7 @@ ALGO = [
     ("k_h3s_half<", 7, 2, NPTS3),
     ("k_stencil<__half, 1,", 12, 2, NPTS3), ("k_stencil<__half, 2,", 10, 2, NPTS3),
     ("k_stencil<float, 1,", 12, 4, NPTS3), ("k_stencil<float, 2,", 10, 4, NPTS3),
+    ("k_h3_bulk<float", 7, 4, NPTS3),
     ("k_h3_bulk<__half", 7, 2, NPTS3), ("k_h3<__half", 7, 2, NPTS3),
     ("k_sr<__half, 16, 2, 2, 0", 19, 2, NPTS3), ("k_sr<__half, 8, 3, 2, 1", 13, 2, NPTS3),
     ("k_sr<float", 19, 4, NPTS3),
