@@ -296,11 +296,13 @@ static void default_tiling(sten_stencil *st, int prec) {
   // z chunks (config 3, paired runs, tools/zc_sweep.sh): H1 1.94 ms at 16-24 planes vs 2.07 at 64
   // (2.15 at 128, 2.31 at 1536: neighbouring tiles march together for a shorter time, so fewer
   // of their shared halo rows miss L2); H2 1.63 ms at 40-48 planes vs 1.66 at 16-20
-  // fp32 (planes twice the bytes): H1 4.05 ms at 32 planes vs 4.07-4.08 at 20 and 4.10-4.11 at 16
-  // (tools/fp32_zc.sh); H2 3.39-3.40 at 40-48
-  const int zc1 = prec == STEN_FP32 ? 32 : 20;
+  // fp32 fields (planes twice the bytes): H1 4.05 ms at 32 planes vs 4.07-4.08 at 20 and 4.10-4.11 at 16
+  // (tools/fp32_zc.sh); H2 3.39-3.40 at 40-48.  fp32 constant operator (scalar couplings,
+  // tools/fp32c_zc.sh): H1 2.075 ms at 20 vs 2.30 at 32; H2 1.48 at 64 vs 1.54 at 32
+  const bool f32 = prec == STEN_FP32;
+  const int zc1 = f32 && !st->cc ? 32 : 20, zc2 = f32 && st->cc ? 64 : 40;
   t.zc = nzs < zc1 ? nzs : zc1;
-  t.zc2 = nzs < 40 ? nzs : 40;
+  t.zc2 = nzs < zc2 ? nzs : zc2;
   t.rows = 0;
   t.bx = prec == STEN_FP32 ? tile_bx<float>() : tile_bx<__half>();
   t.by = 16;
