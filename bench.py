@@ -367,20 +367,11 @@ def run_schedule(sten, st, prec, schedule, b, x, args, world, sdist, npts, clock
             "hist_10": float(hist[min(10, len(hist) - 1)]), "clocks": clk}
 
 
-def run_tts(sten, st, b, tol=1e-6):
-    """Labelled field: the mixed solve to 1e-3 (BASELINE config 3's tol run), and the time to
-    ||r||/||b|| <= tol on the bench's system (cfg 3, delta = 0.1) - fp32
-    BiCGStab (Alg. 1) against the mixed iterative refinement (R21: fp32 residual and update, fp16
-    inner solves of Alg. 1 to 1e-2; NEXT-2, PAPER.md:586-601): the fp16 bandwidth carried to an
-    fp32-accurate answer.  One warm-up call each (graph capture), then one timed call; the library
-    synchronises its stream before returning, so the host clock around the call is the device time
-    plus the call overhead."""
+def _tts_one(sten, st, b, b32, x32, tol):
+    """The three timed solves of one schedule (the handle's current one)."""
     import torch
-    sten.set_schedule(st, sten.SCHED_CLASSIC)
-    b32 = b.float()
-    x32 = torch.empty_like(b32)
-    out = {"tol": tol, "schedule": "classic", "clock": "host wall clock around the (synchronising) call"}
-    # BASELINE config 3's "tol 1e-3 run": the mixed solve (Alg. 1) to the mixed-mode target
+    out = {}
+    # BASELINE config 3's "tol 1e-3 run": the mixed solve to the mixed-mode target
     xm = torch.empty_like(b)
     sten.bicgstab_solve(st, sten.MIXED, b, None, 1e-3, 100, xm)
     torch.cuda.synchronize()
@@ -403,6 +394,29 @@ def run_tts(sten, st, b, tol=1e-6):
     out["mixed_refinement"] = {"ms": ms, "outer_steps": ko, "fp16_iters": ki, "true_rel_residual_fp32": float(rh[-1]),
                                "status": int(status), "inner_tol": 1e-2}
     out["speedup_vs_fp32"] = out["fp32_bicgstab"]["ms"] / ms
+    return out
+
+
+def run_tts(sten, st, b, tol=1e-6):
+    """Labelled field: the mixed solve to 1e-3 (BASELINE config 3's tol run), and the time to
+    ||r||/||b|| <= tol on the bench's system (cfg 3, delta = 0.1) - fp32
+    BiCGStab (Alg. 1) against the mixed iterative refinement (R21: fp32 residual and update, fp16
+    inner solves of Alg. 1 to 1e-2; NEXT-2, PAPER.md:586-601): the fp16 bandwidth carried to an
+    fp32-accurate answer.  One warm-up call each (graph capture), then one timed call; the library
+    synchronises its stream before returning, so the host clock around the call is the device time
+    plus the call overhead.  The same three solves again on the single-reduction schedule (NEXT-1,
+    R19: fp32 solve and the refinement's fp16 inner solves as SR sweeps) in the "sr" sub-field; the
+    handle is left on the classic schedule."""
+    import torch
+    b32 = b.float()
+    x32 = torch.empty_like(b32)
+    out = {"tol": tol, "schedule": "classic", "clock": "host wall clock around the (synchronising) call"}
+    sten.set_schedule(st, sten.SCHED_CLASSIC)
+    out.update(_tts_one(sten, st, b, b32, x32, tol))
+    sten.set_schedule(st, sten.SCHED_SR)
+    out["sr"] = dict(schedule="sr", **_tts_one(sten, st, b, b32, x32, tol))
+    out["sr"]["speedup_vs_classic_fp32"] = out["fp32_bicgstab"]["ms"] / out["sr"]["mixed_refinement"]["ms"]
+    sten.set_schedule(st, sten.SCHED_CLASSIC)
     del b32, x32
     torch.cuda.empty_cache()
     return out

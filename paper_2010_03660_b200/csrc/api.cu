@@ -1289,6 +1289,11 @@ static cudaError_t copy3d(sten_stencil *st, void *dst, size_t dpitch, size_t dys
     if (e != cudaSuccess) return e;
     return cudaMemcpyAsync(dst, stg, wbytes * h * d, cudaMemcpyDeviceToHost, s);
   }
+  if (dev_src && dev_dst) {  // device <-> device: the row-copy stream (falls back for odd alignment)
+    const int e = copy_rows_launch(dst, dpitch, dysize, src, spitch, sysize, wbytes, h, d, st->sm, s);
+    if (e == (int)cudaSuccess) st->launches++;
+    if (e != (int)cudaErrorNotSupported) return (cudaError_t)e;
+  }
   cudaMemcpy3DParms p;
   memset(&p, 0, sizeof p);
   p.srcPtr = make_cudaPitchedPtr(const_cast<void *>(src), spitch, wbytes, sysize);
@@ -2154,12 +2159,14 @@ static int ir_grid(sten_stencil *st, long long n) {
 }
 
 // r = b_hat - A x (fp32) on every slab; returns ||r||^2 (all slabs / ranks) and
-// leaves max|r| in ir_amax
-static int ir_residual(sten_stencil *st, cudaStream_t s, double *rr) {
+// leaves max|r| in ir_amax.  x_zero: x = 0, so r = b_hat exactly and no SpMV runs.
+static int ir_residual(sten_stencil *st, cudaStream_t s, double *rr, bool x_zero = false) {
   const int F = STEN_FP32;
   const size_t vb = (size_t)st->plane * 4;
-  if (decomposed(st)) RC_TRY(exchange(st, F, [](PrecBufs &bb) { return bb.s; }, s));
-  for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, F, MODE_APPLY, k, 0, s));
+  if (!x_zero) {
+    if (decomposed(st)) RC_TRY(exchange(st, F, [](PrecBufs &bb) { return bb.s; }, s));
+    for (int k = 0; k < (int)st->slabs.size(); ++k) RC_TRY(launch_stencil(st, F, MODE_APPLY, k, 0, s));
+  }
   CUDA_TRY(cudaMemsetAsync(st->ir_amax, 0, sizeof(unsigned), s));
   for (int k = 0; k < (int)st->slabs.size(); ++k) {
     Slab &sl = st->slabs[k];
@@ -2167,7 +2174,7 @@ static int ir_residual(sten_stencil *st, cudaStream_t s, double *rr) {
     IrArgs a;
     memset(&a, 0, sizeof a);
     a.b = (const float *)((char *)b.rh + vb);  // b_hat
-    a.ax = (const float *)((char *)b.t + vb);
+    a.ax = x_zero ? nullptr : (const float *)((char *)b.t + vb);
     a.r = (float *)((char *)b.r + vb);
     a.amax = st->ir_amax;
     a.n = (long long)st->plane * sl.nz;
@@ -2227,7 +2234,7 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
     CUDA_TRY(cudaMemsetAsync((char *)pb.s + v4, 0, v4 * sl.nz, s));
   }
   double bb = 0.0;
-  RC_TRY(ir_residual(st, s, &bb));  // x = 0: r = b_hat
+  RC_TRY(ir_residual(st, s, &bb, true));  // x = 0: r = b_hat
   const double nb = sqrt(bb);
   const bool zero_b = nb == 0.0;  // b = 0: x = 0 is exact, whatever x0 is
   if (x0 && !zero_b) RC_TRY(copy_in(st, F, sel_s, x0, s));

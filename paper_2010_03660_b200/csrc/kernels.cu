@@ -281,21 +281,47 @@ int init_launch(const EwArgs &a, int grid, int threads, cudaStream_t s) {
 }
 
 // ------------------------------------------- iterative refinement (R21) --
+// The four streams run on 4-element vectors (the interior range is whole
+// planes, a multiple of 64 elements, at a 256-B-aligned start); the element
+// arithmetic is the scalar one, lane by lane.
 // b_hat = rn32(b / a_P) in fp64 (R3); the refinement's fp32 right-hand side
 __global__ void k_ir_bhat(const IrArgs a) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
-    a.r[i] = a.aP ? __double2float_rn((double)a.b[i] / a.aP[i]) : a.b[i];
+  const long long nv = a.n >> 2;
+  const float4 *B = reinterpret_cast<const float4 *>(a.b);
+  const double2 *D = reinterpret_cast<const double2 *>(a.aP);
+  float4 *R = reinterpret_cast<float4 *>(a.r);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    float4 v = __ldcs(B + i);
+    if (a.aP) {
+      const double2 d0 = __ldcs(D + 2 * i), d1 = __ldcs(D + 2 * i + 1);
+      v = make_float4(__double2float_rn((double)v.x / d0.x), __double2float_rn((double)v.y / d0.y),
+                      __double2float_rn((double)v.z / d1.x), __double2float_rn((double)v.w / d1.y));
+    }
+    R[i] = v;
+  }
 }
-// r = b_hat - A x in fp32; (r, r) by the deterministic grid reduction; max|r|
+// r = b_hat - A x in fp32 (ax null: x = 0, r = b_hat exactly); (r, r) by the
+// deterministic grid reduction; max|r|
 __global__ void __launch_bounds__(256) k_ir_resid(const IrArgs a) {
   __shared__ float scratch[32 * kMaxDots];
   float d[1] = {0.0f};
   float m = 0.0f;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
-    const float r = __fsub_rn(a.b[i], a.ax[i]);
-    a.r[i] = r;
-    d[0] = __fmaf_rn(r, r, d[0]);
-    m = fmaxf(m, fabsf(r));
+  const long long nv = a.n >> 2;
+  const float4 *B = reinterpret_cast<const float4 *>(a.b);
+  const float4 *AX = reinterpret_cast<const float4 *>(a.ax);
+  float4 *R = reinterpret_cast<float4 *>(a.r);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    float4 r = __ldcs(B + i);
+    if (AX) {
+      const float4 ax = __ldcs(AX + i);
+      r = make_float4(__fsub_rn(r.x, ax.x), __fsub_rn(r.y, ax.y), __fsub_rn(r.z, ax.z), __fsub_rn(r.w, ax.w));
+    }
+    R[i] = r;
+    d[0] = __fmaf_rn(r.x, r.x, d[0]);
+    d[0] = __fmaf_rn(r.y, r.y, d[0]);
+    d[0] = __fmaf_rn(r.z, r.z, d[0]);
+    d[0] = __fmaf_rn(r.w, r.w, d[0]);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -310,14 +336,68 @@ __global__ void k_ir_scale(const IrArgs a) {
   frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
   const float inv = ldexpf(1.0f, -e);
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.sigma = ldexpf(1.0f, e);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
-    a.r16[i] = __float2half_rn(a.r[i] * inv);
+  const long long nv = a.n >> 2;
+  const float4 *R = reinterpret_cast<const float4 *>(a.r);
+  uint2 *R16 = reinterpret_cast<uint2 *>(a.r16);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const float4 r = __ldcs(R + i);
+    const __half2 lo = __halves2half2(__float2half_rn(r.x * inv), __float2half_rn(r.y * inv));
+    const __half2 hi = __halves2half2(__float2half_rn(r.z * inv), __float2half_rn(r.w * inv));
+    R16[i] = make_uint2(*reinterpret_cast<const uint32_t *>(&lo), *reinterpret_cast<const uint32_t *>(&hi));
+  }
 }
 // x = fma(sigma, d, x) in fp32
 __global__ void k_ir_update(const IrArgs a) {
   const float sg = *a.sigma;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x)
-    a.x[i] = __fmaf_rn(sg, __half2float(a.d16[i]), a.x[i]);
+  const long long nv = a.n >> 2;
+  const uint2 *D = reinterpret_cast<const uint2 *>(a.d16);
+  float4 *X = reinterpret_cast<float4 *>(a.x);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    const uint2 u = __ldcs(D + i);
+    const float2 lo = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+    const float2 hi = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+    float4 x = X[i];
+    x = make_float4(__fmaf_rn(sg, lo.x, x.x), __fmaf_rn(sg, lo.y, x.y), __fmaf_rn(sg, hi.x, x.z), __fmaf_rn(sg, hi.y, x.w));
+    X[i] = x;
+  }
+}
+
+// ------------------------------------------------ pitched device copies --
+// dst rows (y, z) <- src rows: one warp per row, lanes over the row's W-byte
+// words (the layouts' host-side copies: user vectors <-> halo'd pitched
+// planes; cudaMemcpy3D moved them at ~2 TB/s, this stream at the copy peak)
+template <typename W>
+__global__ void __launch_bounds__(256) k_copy_rows(char *__restrict__ dst, long long dpitch, long long dysize,
+                                                   const char *__restrict__ src, long long spitch, long long sysize,
+                                                   int words, long long h, long long rows) {
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
+    const long long z = r / h, y = r - z * h;
+    const W *sp = reinterpret_cast<const W *>(src + (z * sysize + y) * spitch);
+    W *dp = reinterpret_cast<W *>(dst + (z * dysize + y) * dpitch);
+    for (int i = lane; i < words; i += 32) dp[i] = __ldcs(sp + i);
+  }
+}
+
+int copy_rows_launch(void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch, size_t sysize,
+                     size_t wbytes, size_t h, size_t d, int sms, cudaStream_t s) {
+  const long long rows = (long long)h * (long long)d;
+  if (rows == 0 || wbytes == 0) return (int)cudaSuccess;
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | dpitch | spitch | wbytes;
+  long long g = (rows + 7) / 8;
+  if (g > (long long)sms * 8) g = (long long)sms * 8;
+  char *D = static_cast<char *>(dst);
+  const char *S = static_cast<const char *>(src);
+  if (al % 16 == 0)
+    k_copy_rows<uint4><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 16), h, rows);
+  else if (al % 4 == 0)
+    k_copy_rows<uint32_t><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 4), h, rows);
+  else if (al % 2 == 0)
+    k_copy_rows<unsigned short><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 2), h, rows);
+  else
+    return (int)cudaErrorNotSupported;
+  return (int)cudaGetLastError();
 }
 
 int ir_launch(int which, const IrArgs &a, int grid, cudaStream_t s) {

@@ -621,6 +621,9 @@ struct IrArgs {
   Reduce red;            // ir_resid: (r, r) deposited in red.slab_out
 };
 int ir_launch(int which, const IrArgs &a, int grid, cudaStream_t s);
+// pitched device-to-device copy of h x d rows of wbytes (kernels.cu); cudaErrorNotSupported if odd-aligned
+int copy_rows_launch(void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch, size_t sysize,
+                     size_t wbytes, size_t h, size_t d, int sms, cudaStream_t s);
 enum { IR_BHAT = 0, IR_RESID = 1, IR_SCALE = 2, IR_UPDATE = 3 };
 
 // sr.cu: the single-reduction sweep kernel (one launch per iteration)
