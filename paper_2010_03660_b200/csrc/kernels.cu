@@ -363,40 +363,60 @@ __global__ void k_ir_update(const IrArgs a) {
 }
 
 // ------------------------------------------------ pitched device copies --
-// dst rows (y, z) <- src rows: one warp per row, lanes over the row's W-byte
-// words (the layouts' host-side copies: user vectors <-> halo'd pitched
-// planes; cudaMemcpy3D moved them at ~2 TB/s, this stream at the copy peak)
+// d planes of h rows of W-byte words, dst <- src (the layouts' host-side
+// copies: user vectors <-> halo'd pitched planes; cudaMemcpy3D moved them at
+// ~2 TB/s).  blockIdx.y walks the planes; inside a plane either one linear
+// stream (rows contiguous on both sides: the plane is one row of h*words) or
+// one warp per row with the lanes over its words.
 template <typename W>
-__global__ void __launch_bounds__(256) k_copy_rows(char *__restrict__ dst, long long dpitch, long long dysize,
-                                                   const char *__restrict__ src, long long spitch, long long sysize,
-                                                   int words, long long h, long long rows) {
-  const int lane = threadIdx.x & 31;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
-    const long long z = r / h, y = r - z * h;
-    const W *sp = reinterpret_cast<const W *>(src + (z * sysize + y) * spitch);
-    W *dp = reinterpret_cast<W *>(dst + (z * dysize + y) * dpitch);
-    for (int i = lane; i < words; i += 32) dp[i] = __ldcs(sp + i);
+__global__ void __launch_bounds__(256) k_copy_rows(char *__restrict__ dst, long long dplane, long long dpitch,
+                                                   const char *__restrict__ src, long long splane, long long spitch,
+                                                   int words, int h, long long d, int linear) {
+  for (long long z = blockIdx.y; z < d; z += gridDim.y) {
+    const char *sp0 = src + z * splane;
+    char *dp0 = dst + z * dplane;
+    if (linear) {
+      const W *sp = reinterpret_cast<const W *>(sp0);
+      W *dp = reinterpret_cast<W *>(dp0);
+      const long long n = (long long)words * h;
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dp[i] = __ldcs(sp + i);
+    } else {
+      const int lane = threadIdx.x & 31;
+      for (int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); y < h; y += gridDim.x * (blockDim.x >> 5)) {
+        const W *sp = reinterpret_cast<const W *>(sp0 + y * spitch);
+        W *dp = reinterpret_cast<W *>(dp0 + y * dpitch);
+        for (int i = lane; i < words; i += 32) dp[i] = __ldcs(sp + i);
+      }
+    }
   }
 }
 
 int copy_rows_launch(void *dst, size_t dpitch, size_t dysize, const void *src, size_t spitch, size_t sysize,
                      size_t wbytes, size_t h, size_t d, int sms, cudaStream_t s) {
-  const long long rows = (long long)h * (long long)d;
-  if (rows == 0 || wbytes == 0) return (int)cudaSuccess;
+  if (h == 0 || d == 0 || wbytes == 0) return (int)cudaSuccess;
+  if (h > 0x7fffffff) return (int)cudaErrorNotSupported;
   const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | dpitch | spitch | wbytes;
-  long long g = (rows + 7) / 8;
-  if (g > (long long)sms * 8) g = (long long)sms * 8;
+  const int ws = al % 16 == 0 ? 16 : al % 4 == 0 ? 4 : al % 2 == 0 ? 2 : 0;
+  if (ws == 0 || wbytes / ws > 0x7fffffff) return (int)cudaErrorNotSupported;
+  const int words = (int)(wbytes / ws);
+  const int linear = (dpitch == wbytes && spitch == wbytes) ? 1 : 0;
+  // about 8 resident 256-thread CTAs per SM in total, at least one per plane
+  const long long gy = d < 65535 ? (long long)d : 65535;
+  const long long per_plane = linear ? ((long long)words * (long long)h + 255) / 256 : ((long long)h + 7) / 8;
+  long long gx = ((long long)sms * 8 + gy - 1) / gy;
+  if (gx > per_plane) gx = per_plane;
+  if (gx < 1) gx = 1;
+  const dim3 grid((unsigned)gx, (unsigned)gy);
   char *D = static_cast<char *>(dst);
   const char *S = static_cast<const char *>(src);
-  if (al % 16 == 0)
-    k_copy_rows<uint4><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 16), h, rows);
-  else if (al % 4 == 0)
-    k_copy_rows<uint32_t><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 4), h, rows);
-  else if (al % 2 == 0)
-    k_copy_rows<unsigned short><<<(int)g, 256, 0, s>>>(D, dpitch, dysize, S, spitch, sysize, (int)(wbytes / 2), h, rows);
+  const long long dpl = (long long)(dpitch * dysize), spl = (long long)(spitch * sysize);
+  if (ws == 16)
+    k_copy_rows<uint4><<<grid, 256, 0, s>>>(D, dpl, (long long)dpitch, S, spl, (long long)spitch, words, (int)h, (long long)d, linear);
+  else if (ws == 4)
+    k_copy_rows<uint32_t><<<grid, 256, 0, s>>>(D, dpl, (long long)dpitch, S, spl, (long long)spitch, words, (int)h, (long long)d, linear);
   else
-    return (int)cudaErrorNotSupported;
+    k_copy_rows<unsigned short><<<grid, 256, 0, s>>>(D, dpl, (long long)dpitch, S, spl, (long long)spitch, words, (int)h, (long long)d, linear);
   return (int)cudaGetLastError();
 }
 
