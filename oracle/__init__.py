@@ -377,16 +377,19 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
     plateau).  Composes the pinned pieces: the fp32 FMA-chain SpMV mirror
     (apply32_fma), fp32 element-wise arithmetic (numpy float32), binary16
     rounding (f16_from_double) and the O16 solver (bicgstab16).
-    bhat32: the scaled right-hand side b_hat (float32).  Returns dict(x (float32),
-    hist (outer residuals), outer, inner, status)."""
+    bhat32: the scaled right-hand side b_hat (float32).  With schedule="sr" the
+    first stagnation (three outer steps without a 1% gain) switches the inner
+    solves to the classic schedule (Alg. 1 as printed) instead of stopping; the
+    second one stops (BREAKDOWN).  Returns dict(x (float32), hist (outer
+    residuals), outer, inner, status, handover (outer step of the switch, or -1))."""
     c32 = quantize_coeffs(c64, "fp32")
     c16 = quantize_coeffs(c64, "mixed")
     b = np.asarray(bhat32, np.float32)
     nb = float(np.sqrt(np.sum(b.astype(np.float64) ** 2)))
     x = np.zeros_like(b) if x0 is None else np.asarray(x0, np.float32).copy()
     if nb == 0.0:
-        return dict(x=np.zeros_like(b), hist=np.array([0.0]), outer=0, inner=0, status=ORC_CONVERGED)
-    hist, inner, status, best, stale = [], 0, ORC_MAXIT, None, 0
+        return dict(x=np.zeros_like(b), hist=np.array([0.0]), outer=0, inner=0, status=ORC_CONVERGED, handover=-1)
+    hist, inner, status, best, stale, handover = [], 0, ORC_MAXIT, None, 0, -1
     for k in range(outer_maxit + 1):
         r = b - apply32_fma(c32, x)                      # fp32: one rounding per element
         res = float(np.sqrt(np.sum(r.astype(np.float64) ** 2))) / nb
@@ -403,8 +406,11 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         else:
             stale += 1
             if stale >= 3:
-                status = ORC_BREAKDOWN
-                break
+                if schedule == "sr":  # R21: a stalled SR inner solve hands over to Alg. 1's schedule
+                    schedule, stale, handover = "classic", 0, k
+                else:
+                    status = ORC_BREAKDOWN
+                    break
         if k == outer_maxit:
             break
         sigma = 2.0 ** np.frexp(float(np.max(np.abs(r))))[1]  # power of two >= max|r|
@@ -412,7 +418,7 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         d = bicgstab16(c16, r16, tol=inner_tol, maxit=inner_maxit, schedule=schedule)
         inner += d["iters"]
         x = (x.astype(np.float64) + sigma * f16_to_double(d["x"])).astype(np.float32)
-    return dict(x=x, hist=np.array(hist), outer=len(hist) - 1, inner=inner, status=status)
+    return dict(x=x, hist=np.array(hist), outer=len(hist) - 1, inner=inner, status=status, handover=handover)
 
 
 # ---------------- 2D 9-point SpMV (o2d.c) ----------------
