@@ -377,10 +377,11 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
     plateau).  Composes the pinned pieces: the fp32 FMA-chain SpMV mirror
     (apply32_fma), fp32 element-wise arithmetic (numpy float32), binary16
     rounding (f16_from_double) and the O16 solver (bicgstab16).
-    bhat32: the scaled right-hand side b_hat (float32).  With schedule="sr" the
-    first stagnation (three outer steps without a 1% gain) switches the inner
-    solves to the classic schedule (Alg. 1 as printed) instead of stopping; the
-    second one stops (BREAKDOWN).  Returns dict(x (float32), hist (outer
+    bhat32: the scaled right-hand side b_hat (float32).  The first stagnation
+    (three outer steps without a 1% gain) switches the inner solves to the
+    other schedule (classic <-> sr: they round differently, and on weakly
+    dominant systems either fp16 iteration can stall where the other still
+    gains) instead of stopping; the second one stops (BREAKDOWN).  Returns dict(x (float32), hist (outer
     residuals), outer, inner, status, handover (outer step of the switch, or -1))."""
     c32 = quantize_coeffs(c64, "fp32")
     c16 = quantize_coeffs(c64, "mixed")
@@ -406,8 +407,8 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         else:
             stale += 1
             if stale >= 3:
-                if schedule == "sr":  # R21: a stalled SR inner solve hands over to Alg. 1's schedule
-                    schedule, stale, handover = "classic", 0, k
+                if handover < 0:  # R21: the first stagnation switches the inner schedule
+                    schedule, stale, handover = ("classic" if schedule == "sr" else "sr"), 0, k
                 else:
                     status = ORC_BREAKDOWN
                     break

@@ -63,25 +63,25 @@ def test_zero_rhs_and_x0(orc):
 @pytest.mark.parametrize("kind,delta", [(inputs.KIND_POISSON, 0.0), (inputs.KIND_CD, 0.1), (inputs.KIND_CD, 0.0)])
 def test_sr_inner_stagnation_hands_over_to_classic(orc, kind, delta):
     """R21: with an unreachable tol the outer residual settles on the fp32 floor of the system;
-    SR inner solves then hand over to the classic schedule (Alg. 1) at the first stagnation
-    instead of stopping, and the second stagnation stops (BREAKDOWN).  The classic schedule
-    never hands over.  The handover step is the first one ending three steps without a 1% gain
-    on the best residual before them; x stays at LAPACK accuracy (4 kappa 1e-6)."""
+    the first stagnation switches the inner schedule (SR -> classic, classic -> SR) instead of
+    stopping, and the second stagnation stops (BREAKDOWN).  The handover step is the first one
+    ending three steps without a 1% gain on the best residual before them; x stays at LAPACK
+    accuracy (4 kappa 1e-6)."""
     nx = ny = nz = 6
     diag, offs = inputs.problem_fields(kind, nx, ny, nz, seed=2, delta=delta)
     c = orc.jacobi_scale(diag, offs)
     b = inputs.rhs_uniform(nx, ny, nz, seed=2).astype(np.float32)
     M = dense_scaled(None, [a.astype(np.float32).astype(np.float64) for a in c])
     x_lu = np.linalg.solve(M, b.astype(np.float64).ravel())
-    cl = orc.refine16(c, b, tol=1e-12, outer_maxit=40, inner_tol=1e-2, inner_maxit=60, schedule="classic")
-    assert cl["status"] == orc.ORC_BREAKDOWN and cl["handover"] == -1
-    sr = orc.refine16(c, b, tol=1e-12, outer_maxit=40, inner_tol=1e-2, inner_maxit=60, schedule="sr")
-    assert sr["status"] == orc.ORC_BREAKDOWN
-    h, k = sr["hist"], sr["handover"]
-    assert 3 <= k <= sr["outer"] - 3
-    assert np.all(h[k - 2:k + 1] >= 0.99 * np.min(h[:k - 2]))   # three steps without a 1% gain ...
-    assert not any(np.all(h[j - 2:j + 1] >= 0.99 * np.min(h[:j - 2])) for j in range(3, k))  # ... first at k
-    for res in (cl, sr):
+    runs = [orc.refine16(c, b, tol=1e-12, outer_maxit=60, inner_tol=1e-2, inner_maxit=60, schedule=s)
+            for s in ("classic", "sr")]
+    for res in runs:
+        assert res["status"] == orc.ORC_BREAKDOWN
+        h, k = res["hist"], res["handover"]
+        assert 3 <= k <= res["outer"] - 3
+        assert np.all(h[k - 2:k + 1] >= 0.99 * np.min(h[:k - 2]))   # three steps without a 1% gain ...
+        assert not any(np.all(h[j - 2:j + 1] >= 0.99 * np.min(h[:j - 2])) for j in range(3, k))  # ... first at k
+    for res in runs:
         assert res["hist"][-1] <= 2e-7
         err = np.linalg.norm(res["x"].ravel() - x_lu) / np.linalg.norm(x_lu)
         assert err <= 4 * np.linalg.cond(M) * 1e-6
