@@ -101,6 +101,9 @@ typedef struct sten_stats {
   long long kernel_launches; /* kernels of this library launched by the solve  */
   int event_iter;         /* iteration of the first breakdown event (0: none) */
   int graph_chunk;        /* iterations per CUDA-graph replay                  */
+  int handover;           /* bicgstab_refine: outer step at which the inner
+                             solves switched schedule after a stagnation
+                             (-1: none; 0 after other calls)                  */
 } sten_stats;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -221,8 +224,14 @@ int bicgstab_solve_batch(sten_stencil *st, int precision, int n, const void *con
  *     res_hist[k] = ||r||_2 / ||b_hat||_2 (fp32 sums);
  *     stop: res <= tol -> STEN_CONVERGED; three consecutive steps without
  *           a 1% gain on the best residual so far -> STEN_BREAKDOWN
- *           (stagnation); k == outer_maxit -> STEN_MAXIT; non-finite ->
- *           STEN_NONFINITE;
+ *           (stagnation) - except the first time: the remaining inner
+ *           solves then run the other schedule (classic <-> SR; they round
+ *           differently, and on weakly dominant systems either fp16 iteration
+ *           can stall where the other still gains) and the count restarts
+ *           (sten_stats.handover = k; the handle's schedule is unchanged after
+ *           the call; a handle whose configuration has no SR sweep stops
+ *           instead); k == outer_maxit -> STEN_MAXIT;
+ *           non-finite -> STEN_NONFINITE;
  *     sigma = 2^e, the power of two with max|r| <= sigma; r16 = rn16(r / sigma);
  *     d = the mixed-precision solve of A_hat d = r16 (the handle's schedule,
  *         relative tolerance inner_tol, at most inner_maxit iterations, x0 = 0);

@@ -46,7 +46,7 @@ _BARRIER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
 class _Stats(ctypes.Structure):
     _fields_ = [("phase_ms", ctypes.c_double * 3), ("phase_launches", ctypes.c_longlong * 3),
                 ("solve_ms", ctypes.c_double), ("kernel_launches", ctypes.c_longlong),
-                ("event_iter", ctypes.c_int), ("graph_chunk", ctypes.c_int)]
+                ("event_iter", ctypes.c_int), ("graph_chunk", ctypes.c_int), ("handover", ctypes.c_int)]
 
 
 _lib = None
@@ -349,7 +349,8 @@ def get_stats(st: Stencil) -> dict:
     s = _Stats()
     _check(lib().sten_get_stats(st.handle, ctypes.byref(s)))
     return dict(phase_ms=list(s.phase_ms), phase_launches=list(s.phase_launches), solve_ms=s.solve_ms,
-                kernel_launches=s.kernel_launches, event_iter=s.event_iter, graph_chunk=s.graph_chunk)
+                kernel_launches=s.kernel_launches, event_iter=s.event_iter, graph_chunk=s.graph_chunk,
+                handover=s.handover)
 
 
 def iter_ms(st: Stencil, phase: int = -1) -> list:

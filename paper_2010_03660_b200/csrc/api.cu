@@ -2240,6 +2240,14 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
   if (x0 && !zero_b) RC_TRY(copy_in(st, F, sel_s, x0, s));
   int k = 0, inner = 0, stat = STEN_MAXIT, stale = 0;
   double best = 0.0;
+  // the first stagnation switches the inner schedule, classic <-> SR (R21);
+  // the handle's schedule is restored on every return
+  struct SchedRestore {
+    sten_stencil *st;
+    int sched;
+    ~SchedRestore() { st->schedule = sched; }
+  } restore{st, st->schedule};
+  st->stats.handover = -1;
   for (;; ++k) {
     if (zero_b) {
       res_hist[0] = 0.0;
@@ -2257,8 +2265,16 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
       best = (k == 0 || res < best) ? res : best;
       stale = 0;
     } else if (++stale >= 3) {
-      stat = STEN_BREAKDOWN;
-      break;
+      const int other = st->schedule == STEN_SCHED_SR ? STEN_SCHED_CLASSIC : STEN_SCHED_SR;
+      // (the classic buffers exist, ensure_bufs above; SR ones are made here - a handle
+      // whose configuration has no SR sweep stops instead)
+      if (st->stats.handover >= 0 || (other == STEN_SCHED_SR && ensure_sr(st, M) != STEN_OK)) {
+        stat = STEN_BREAKDOWN;
+        break;
+      }
+      st->schedule = other;
+      st->stats.handover = k;
+      stale = 0;
     }
     if (k == outer_maxit) { stat = STEN_MAXIT; break; }
     // inner right-hand side: r / sigma in fp16 (sigma = 2^e >= max|r|)

@@ -87,3 +87,28 @@ def test_refinement_slab_decomposed(sten, schedule):
     assert np.linalg.norm(x2 - x1) <= 1e-5 * np.linalg.norm(x1)
     st1.close()
     st2.close()
+
+
+@pytest.mark.parametrize("delta", [0.1, 0.0])
+def test_sr_inner_stagnation_hands_over_to_classic(sten, delta):
+    """R21 handover: with an unreachable tol the outer residual settles on the fp32 floor; the first
+    stagnation switches the inner schedule (SR <-> classic; sten_stats.handover = that outer step)
+    and the second stops with BREAKDOWN, as oracle.refine16 does."""
+    nx, ny, nz = 40, 24, 18
+    diag, offs = fields(inputs.KIND_CD, nx, ny, nz, delta=delta, seed=3)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=3).astype(np.float32)
+    st = gpu_stencil(diag, offs)
+    c64 = orc.jacobi_scale(diag, offs)
+    bh = orc.scale_rhs(b, diag, "fp32")
+    c32 = [a.astype(np.float32).astype(np.float64) for a in c64]
+    for schedule in (0, 1):
+        x, ko, ki, hist, status = _refine(sten, st, b, 1e-12, 60, 1e-2, 200, schedule=schedule)
+        ref = orc.refine16(c64, bh, tol=1e-12, outer_maxit=60, inner_tol=1e-2, inner_maxit=200,
+                           schedule="sr" if schedule else "classic")
+        k = sten.get_stats(st)["handover"]
+        assert status == sten.BREAKDOWN == ref["status"]
+        assert k >= 3 and ref["handover"] >= 3 and ko >= k + 3
+        assert np.all(hist[k - 2:k + 1] >= 0.99 * np.min(hist[:k - 2]))
+        assert hist[-1] <= 3e-7
+        assert orc.true_residual64(c32, bh.astype(np.float64), x.astype(np.float64)) <= 3e-7
+    st.close()
