@@ -381,7 +381,9 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
     (three outer steps without a 1% gain) switches the inner solves to the
     other schedule (classic <-> sr: they round differently, and on weakly
     dominant systems either fp16 iteration can stall where the other still
-    gains) instead of stopping; the second one stops (BREAKDOWN).  Returns dict(x (float32), hist (outer
+    gains) instead of stopping; the second one stops (BREAKDOWN).  An inner
+    solve that ends NONFINITE (fp16 overflow) adds no update to x and halves
+    the inner iteration cap for the rest of the call.  Returns dict(x (float32), hist (outer
     residuals), outer, inner, status, handover (outer step of the switch, or -1))."""
     c32 = quantize_coeffs(c64, "fp32")
     c16 = quantize_coeffs(c64, "mixed")
@@ -418,6 +420,9 @@ def refine16(c64, bhat32, x0=None, tol=1e-6, outer_maxit=20, inner_tol=1e-3, inn
         r16 = f16_from_double(r.astype(np.float64) / sigma)
         d = bicgstab16(c16, r16, tol=inner_tol, maxit=inner_maxit, schedule=schedule)
         inner += d["iters"]
+        if d["status"] == ORC_NONFINITE:  # R21: a diverged inner solve adds nothing; the cap halves
+            inner_maxit = max(1, inner_maxit // 2)
+            continue
         x = (x.astype(np.float64) + sigma * f16_to_double(d["x"])).astype(np.float32)
     return dict(x=x, hist=np.array(hist), outer=len(hist) - 1, inner=inner, status=status, handover=handover)
 

@@ -85,3 +85,27 @@ def test_sr_inner_stagnation_hands_over_to_classic(orc, kind, delta):
         assert res["hist"][-1] <= 2e-7
         err = np.linalg.norm(res["x"].ravel() - x_lu) / np.linalg.norm(x_lu)
         assert err <= 4 * np.linalg.cond(M) * 1e-6
+
+
+@pytest.mark.parametrize("schedule", ["classic", "sr"])
+def test_nonfinite_inner_solve_adds_no_update(orc, schedule):
+    """R21: an inner solve that ends NONFINITE (its fp16 scalars overflow, R7) adds nothing to x
+    and halves the inner cap.  On an indefinite 6^3 system (couplings about -1 against a unit
+    diagonal) the first inner solve, run here directly on r16 = rn16(b_hat / sigma), ends
+    NONFINITE; the refinement's second residual is then bitwise its first, x stays finite and
+    the call ends on stagnation, not NONFINITE."""
+    nx = ny = nz = 6
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        rng.uniform(0.5, 1.5, (nz, ny, nx))  # the draw order of the probe that found this system
+    diag = np.ones((nz, ny, nx))
+    offs = [-1.0 * rng.uniform(0.5, 1.5, (nz, ny, nx)) for _ in range(6)]
+    c = orc.jacobi_scale(diag, offs)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=2).astype(np.float32)
+    sigma = 2.0 ** np.frexp(float(np.max(np.abs(b))))[1]
+    d = orc.bicgstab16(orc.quantize_coeffs(c, "mixed"), orc.f16_from_double(b.astype(np.float64) / sigma),
+                       tol=1e-2, maxit=64, schedule=schedule)
+    assert d["status"] == orc.ORC_NONFINITE
+    res = orc.refine16(c, b, tol=1e-6, outer_maxit=20, inner_tol=1e-2, inner_maxit=64, schedule=schedule)
+    assert res["hist"][0] == 1.0 and res["hist"][1] == res["hist"][0]
+    assert res["status"] == orc.ORC_BREAKDOWN and np.all(np.isfinite(res["x"]))
