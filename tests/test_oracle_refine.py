@@ -90,16 +90,14 @@ def test_sr_inner_stagnation_hands_over_to_classic(orc, kind, delta):
 @pytest.mark.parametrize("schedule", ["classic", "sr"])
 def test_nonfinite_inner_solve_adds_no_update(orc, schedule):
     """R21: an inner solve that ends NONFINITE (its fp16 scalars overflow, R7) adds nothing to x
-    and halves the inner cap.  On an indefinite 6^3 system (couplings about -1 against a unit
+    and halves the inner cap.  On an indefinite 6^3 system (couplings about -30 against a unit
     diagonal) the first inner solve, run here directly on r16 = rn16(b_hat / sigma), ends
-    NONFINITE; the refinement's second residual is then bitwise its first, x stays finite and
+    NONFINITE within four iterations; the refinement's second residual is then bitwise its first, x stays finite and
     the call ends on stagnation, not NONFINITE."""
     nx = ny = nz = 6
     rng = np.random.default_rng(5)
-    for _ in range(6):
-        rng.uniform(0.5, 1.5, (nz, ny, nx))  # the draw order of the probe that found this system
     diag = np.ones((nz, ny, nx))
-    offs = [-1.0 * rng.uniform(0.5, 1.5, (nz, ny, nx)) for _ in range(6)]
+    offs = [-30.0 * rng.uniform(0.5, 1.5, (nz, ny, nx)) for _ in range(6)]
     c = orc.jacobi_scale(diag, offs)
     b = inputs.rhs_uniform(nx, ny, nz, seed=2).astype(np.float32)
     sigma = 2.0 ** np.frexp(float(np.max(np.abs(b))))[1]
