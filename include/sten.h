@@ -235,7 +235,9 @@ int bicgstab_solve_batch(sten_stencil *st, int precision, int n, const void *con
  *     sigma = 2^e, the power of two with max|r| <= sigma; r16 = rn16(r / sigma);
  *     d = the mixed-precision solve of A_hat d = r16 (the handle's schedule,
  *         relative tolerance inner_tol, at most inner_maxit iterations, x0 = 0);
- *     x = fma(sigma, d, x) in fp32.
+ *     x = fma(sigma, d, x) in fp32 - unless the inner solve ended
+ *         STEN_NONFINITE (its fp16 scalars overflowed, R7): then x is kept
+ *         and inner_maxit halves for the rest of the call.
  *   b, x0, x_out: fp32, this rank's points (dense layout, host or device);
  *   outer_iters: refinement steps taken (k at exit); inner_iters: total
  *   mixed iterations; res_hist: host array of >= outer_maxit + 1 doubles.

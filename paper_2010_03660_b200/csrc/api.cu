@@ -2293,6 +2293,11 @@ int bicgstab_refine(sten_stencil *st, const void *b, const void *x0, double tol,
     RC_TRY(solve_core(st, M, false, false, inner_tol, inner_maxit, s, &so));
     inner += so.fin.it;
     st->launches += so.kernels;
+    const int ist = so.fin.stop ? so.fin.status : (so.fin.ev >= 0 ? so.fin.ev : STEN_MAXIT);
+    if (ist == STEN_NONFINITE) {  // R21: a diverged inner solve adds nothing; the cap halves
+      inner_maxit = std::max(1, inner_maxit / 2);
+      continue;
+    }
     for (Slab &sl : st->slabs) {
       IrArgs a;
       memset(&a, 0, sizeof a);

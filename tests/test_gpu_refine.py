@@ -112,3 +112,24 @@ def test_sr_inner_stagnation_hands_over_to_classic(sten, delta):
         assert hist[-1] <= 3e-7
         assert orc.true_residual64(c32, bh.astype(np.float64), x.astype(np.float64)) <= 3e-7
     st.close()
+
+
+@pytest.mark.parametrize("schedule", [0, 1])
+def test_nonfinite_inner_solve_adds_no_update(sten, schedule):
+    """R21: an inner solve that ends NONFINITE adds nothing to x and halves the inner cap, as
+    oracle.refine16 does (tests/test_oracle_refine.py: the same indefinite 6^3 system, whose first
+    inner solve overflows within four iterations, early enough for both dot orders): the second outer residual is bitwise the first, x stays finite, the
+    call ends on stagnation (BREAKDOWN) like the oracle's."""
+    nx = ny = nz = 6
+    rng = np.random.default_rng(5)
+    diag = np.ones((nz, ny, nx))
+    offs = [-30.0 * rng.uniform(0.5, 1.5, (nz, ny, nx)) for _ in range(6)]
+    b = inputs.rhs_uniform(nx, ny, nz, seed=2).astype(np.float32)
+    st = gpu_stencil(diag, offs)
+    x, ko, ki, hist, status = _refine(sten, st, b, 1e-6, 20, 1e-2, 64, schedule=schedule)
+    ref = orc.refine16(orc.jacobi_scale(diag, offs), b, tol=1e-6, outer_maxit=20, inner_tol=1e-2, inner_maxit=64,
+                       schedule="sr" if schedule else "classic")
+    assert ref["hist"][1] == ref["hist"][0]
+    assert hist[0] == pytest.approx(1.0, rel=1e-6) and hist[1] == hist[0]
+    assert status == sten.BREAKDOWN == ref["status"] and np.all(np.isfinite(x))
+    st.close()
